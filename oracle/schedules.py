@@ -1,0 +1,259 @@
+"""The SpMV program DAG, tab:sync synchronisation insertion, a happens-before
+validator, and a brute-force schedule enumerator.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Sources
+-------
+* DAG vertices / vertex types: PAPER.md §III-A ``tab:vertices`` P:250-264 and
+  the SpMV description P:270-287 (Pack P:278, PostSends/PostRecvs P:279,
+  start/end P:286-287).  Fig. 3c itself is a ``[FIGURE]`` placeholder, so the
+  edge list is SPEC.md's inferred list plus, per the DESIGN.md reading
+  R-Q13, PostSend->WaitRecv and PostRecv->WaitSend (every rank runs the same P,
+  P:460, so a Wait before the matching Post on every rank can never finish).
+* Synchronisation: PAPER.md ``tab:sync`` P:436-451 --
+  CPU->*: none; GPU_i->CPU: cudaEventRecord -> cudaEventSynchronize;
+  GPU_i->GPU_i: none; GPU_i->GPU_j: cudaEventRecord -> cudaStreamWaitEvent.
+* Stream-bijection pruning: P:426-428 ("children that represent equivalent P_k
+  under a stream bijection are pruned") -- first-use relabelling.
+
+A schedule here is a list of tuples:
+  (name,)                    CPU vertex  (start, PostSend, PostRecv, WaitSend, WaitRecv, end)
+  (name, stream)             GPU vertex  (Pack, y_L, Unpack, y_R) bound to a stream
+  ("CER", stream, event)     cudaEventRecord on ``stream``
+  ("CES", event)             cudaEventSynchronize (host blocks)
+  ("CSWE", stream, event)    cudaStreamWaitEvent(stream, event)
+"""
+from __future__ import annotations
+
+import itertools
+
+VERTICES = ["start", "Pack", "y_L", "PostSend", "PostRecv", "WaitSend", "WaitRecv",
+            "Unpack", "y_R", "end"]
+GPU_VERTICES = {"Pack", "y_L", "Unpack", "y_R"}          # P:278, P:273 (GPU kernels)
+CPU_VERTICES = set(VERTICES) - GPU_VERTICES               # MPI calls, start/end are CPU
+
+# SPEC.md S:125 (Fig. 3c inferred)
+EDGES_A = [("start", "Pack"), ("start", "y_L"), ("start", "PostRecv"),
+           ("Pack", "PostSend"), ("PostSend", "WaitSend"), ("PostRecv", "WaitRecv"),
+           ("WaitRecv", "Unpack"), ("Unpack", "y_R"),
+           ("y_L", "end"), ("y_R", "end"), ("WaitSend", "end")]
+# DESIGN.md reading R-Q13: SPMD deadlock-freedom edges
+DEADLOCK_EDGES = [("PostSend", "WaitRecv"), ("PostRecv", "WaitSend")]
+EDGES = EDGES_A + DEADLOCK_EDGES
+
+
+def preds(v, edges=EDGES):
+    return [u for (u, w) in edges if w == v]
+
+
+# ------------------------------------------------------------------ topology
+def topological_orders(edges=EDGES, vertices=VERTICES):
+    """All topological orders of the DAG (plain recursive enumeration)."""
+    pred = {v: set(preds(v, edges)) for v in vertices}
+    out = []
+
+    def rec(prefix, done):
+        if len(prefix) == len(vertices):
+            out.append(list(prefix))
+            return
+        for v in vertices:  # declaration order
+            if v not in done and pred[v] <= done:
+                prefix.append(v)
+                done.add(v)
+                rec(prefix, done)
+                done.remove(v)
+                prefix.pop()
+
+    rec([], set())
+    return out
+
+
+# ----------------------------------------------------------- happens-before
+def _hb_graph(ops):
+    """Nodes: ('H', t) host point after op t; ('C', t) CPU vertex; ('G', t) GPU
+    op completion; ('R', e) event record; ('W', t) stream wait.  Returns
+    (succ dict, node-of-op dict)."""
+    succ = {}
+
+    def edge(a, b):
+        succ.setdefault(a, set()).add(b)
+        succ.setdefault(b, set())
+
+    prev_on_stream = {}
+    rec = {}
+    node_of = {}
+    hprev = ("H", -1)
+    succ[hprev] = set()
+    for t, op in enumerate(ops):
+        h = ("H", t)
+        edge(hprev, h)
+        name = op[0]
+        if name in CPU_VERTICES:
+            c = ("C", t)
+            edge(hprev, c)
+            edge(c, h)
+            node_of[t] = c
+        elif name in GPU_VERTICES:
+            g = ("G", t)
+            edge(hprev, g)
+            s = op[1]
+            if s in prev_on_stream:
+                edge(prev_on_stream[s], g)
+            prev_on_stream[s] = g
+            node_of[t] = g
+        elif name == "CER":
+            _, s, e = op
+            r = ("R", e)
+            edge(hprev, r)
+            if s in prev_on_stream:
+                edge(prev_on_stream[s], r)
+            prev_on_stream[s] = r
+            rec[e] = r
+            node_of[t] = r
+        elif name == "CES":
+            _, e = op
+            if e in rec:
+                edge(rec[e], h)
+            node_of[t] = h
+        elif name == "CSWE":
+            _, s, e = op
+            w = ("W", t)
+            edge(hprev, w)
+            if s in prev_on_stream:
+                edge(prev_on_stream[s], w)
+            if e in rec:
+                edge(rec[e], w)
+            prev_on_stream[s] = w
+            node_of[t] = w
+        else:
+            raise ValueError(f"unknown op {op!r}")
+        hprev = h
+    return succ, node_of
+
+
+def _reaches(succ, a, b):
+    seen = {a}
+    stack = [a]
+    while stack:
+        u = stack.pop()
+        if u == b:
+            return True
+        for w in succ.get(u, ()):
+            if w not in seen:
+                seen.add(w)
+                stack.append(w)
+    return False
+
+
+def edge_satisfied(ops, iu, iv):
+    """DAG edge ops[iu] -> ops[iv] is enforced by host order, stream order and
+    the inserted syncs (tab:sync P:444-448)."""
+    succ, node_of = _hb_graph(ops)
+    return _reaches(succ, node_of[iu], node_of[iv])
+
+
+def validate(ops, n_streams, edges=EDGES):
+    """Return (True, '') or (False, 'schedule'|'deadlock', reason)."""
+    pos = {}
+    recorded = set()
+    for t, op in enumerate(ops):
+        name = op[0]
+        if name in VERTICES:
+            if name in pos:
+                return (False, "schedule", f"duplicate vertex {name}")
+            pos[name] = t
+            if name in GPU_VERTICES and not (0 <= op[1] < n_streams):
+                return (False, "schedule", f"{name}: stream {op[1]} out of range")
+        elif name == "CER":
+            if not (0 <= op[1] < n_streams):
+                return (False, "schedule", "CER stream out of range")
+            if op[2] in recorded:
+                return (False, "schedule", f"event {op[2]} recorded twice")
+            recorded.add(op[2])
+        elif name in ("CES", "CSWE"):
+            e = op[-1]
+            if e not in recorded:
+                return (False, "schedule", f"event {e} used before record")
+            if name == "CSWE" and not (0 <= op[1] < n_streams):
+                return (False, "schedule", "CSWE stream out of range")
+        else:
+            return (False, "schedule", f"unknown op {name}")
+    for v in VERTICES:
+        if v not in pos:
+            return (False, "schedule", f"missing vertex {v}")
+    if pos["start"] != 0:
+        return (False, "schedule", "start is not first")
+    if pos["end"] != len(ops) - 1:
+        return (False, "schedule", "end is not last")
+    for (u, v) in edges:
+        if pos[u] > pos[v]:
+            kind = "deadlock" if (u, v) in DEADLOCK_EDGES else "schedule"
+            return (False, kind, f"{v} before {u}")
+    succ, node_of = _hb_graph(ops)
+    for (u, v) in edges:
+        if not _reaches(succ, node_of[pos[u]], node_of[pos[v]]):
+            return (False, "schedule", f"edge {u}->{v} not synchronised")
+    return (True, "", "")
+
+
+# ------------------------------------------------------------ sync insertion
+def derive(order, streams, edges=EDGES):
+    """Schedule from a vertex order and a {GPU vertex: stream} map, inserting
+    syncs per tab:sync immediately before the vertex that needs them
+    (already-satisfied edges insert nothing).  Events get
+    sequential ids in emission order."""
+    ops = []
+    ev = 0
+    for v in order:
+        vop = (v, streams[v]) if v in GPU_VERTICES else (v,)
+        for u in preds(v, edges):
+            iu = next(t for t, op in enumerate(ops) if op[0] == u)
+            trial = ops + [vop]
+            if edge_satisfied(trial, iu, len(ops)):
+                continue
+            su = ops[iu][1]
+            ops.append(("CER", su, ev))
+            if v in GPU_VERTICES:
+                ops.append(("CSWE", streams[v], ev))
+            else:
+                ops.append(("CES", ev))
+            ev += 1
+        ops.append(vop)
+    return ops
+
+
+def canonical(ops):
+    """First-use stream relabelling and sequential event ids."""
+    smap, emap = {}, {}
+    out = []
+    for op in ops:
+        name = op[0]
+        if name in GPU_VERTICES:
+            s = smap.setdefault(op[1], len(smap))
+            out.append((name, s))
+        elif name == "CER":
+            s = smap.setdefault(op[1], len(smap))
+            e = emap.setdefault(op[2], len(emap))
+            out.append(("CER", s, e))
+        elif name == "CSWE":
+            s = smap.setdefault(op[1], len(smap))
+            out.append(("CSWE", s, emap[op[2]]))
+        elif name == "CES":
+            out.append(("CES", emap[op[1]]))
+        else:
+            out.append(op)
+    return tuple(out)
+
+
+def enumerate_derived(n_streams=2, edges=EDGES):
+    """Brute force: every topological order x every stream assignment of the
+    four GPU vertices, syncs derived, deduplicated by canonical form."""
+    seen = {}
+    gpus = [v for v in VERTICES if v in GPU_VERTICES]
+    for order in topological_orders(edges):
+        for assign in itertools.product(range(n_streams), repeat=len(gpus)):
+            ops = derive(order, dict(zip(gpus, assign)), edges)
+            key = canonical(ops)
+            seen.setdefault(key, ops)
+    return list(seen.values())
