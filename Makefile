@@ -1,0 +1,36 @@
+# libdspmv (C ABI, sm_100a kernels) and the oracle's O1 library.
+PY        ?= python
+NCCL_HOME ?= $(shell $(PY) -c "import nvidia.nccl,os;print(list(nvidia.nccl.__path__)[0])")
+CUDA_HOME ?= /usr/local/cuda
+NVCC      := $(CUDA_HOME)/bin/nvcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+SRC       := paper_2203_02530_b200/csrc
+OUT       := paper_2203_02530_b200/lib
+BUILD     := build/obj
+
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+CXXFLAGS  := -O2 -g -fPIC -std=c++17 -Wall -Wno-unused-function -I$(CUDA_HOME)/include -I$(NCCL_HOME)/include
+
+OBJS := $(BUILD)/kernels.o $(BUILD)/api.o $(BUILD)/planner.o $(BUILD)/schedule.o
+
+all: $(OUT)/libdspmv.so oracle/libo1.so
+
+$(BUILD):
+	mkdir -p $(BUILD) $(OUT)
+
+$(BUILD)/kernels.o: $(SRC)/kernels.cu $(SRC)/runtime.h $(SRC)/internal.h include/dspmv.h | $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(BUILD)/ptxas_kernels.txt || (cat $(BUILD)/ptxas_kernels.txt; false)
+
+$(BUILD)/%.o: $(SRC)/%.cpp $(SRC)/runtime.h $(SRC)/internal.h include/dspmv.h | $(BUILD)
+	g++ $(CXXFLAGS) -c $< -o $@
+
+$(OUT)/libdspmv.so: $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_HOME)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_HOME)/lib
+
+oracle/libo1.so: oracle/o1.c
+	gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -o $@ $< -lm
+
+clean:
+	rm -rf $(BUILD) $(OUT)/libdspmv.so oracle/libo1.so
+
+.PHONY: all clean

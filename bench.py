@@ -1,0 +1,411 @@
+#!/usr/bin/env python
+"""Benchmark of the distributed SpMV hot path (arXiv 2203.02530).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c3|c4] [--schedule best|paper1]
+
+One "step" = one dspmv_apply of the whole hot path (Pack, NCCL exchange,
+Unpack, y_L, y_R + combine, all host syncs of the schedule) over the rank's
+rows, inputs resident in HBM.  N=1 runs BASELINE.json configs[1] (3D 7-point
+Laplacian 128^3, fp64, one B200).  N>1 (torchrun, one process per GPU) is weak
+scaling: a 128 x 128 x (128 N) 7-point grid row-partitioned over N ranks, so
+each rank owns exactly the C2 workload plus two halo planes exchanged with
+NCCL send/recv over NVLink.  The L2 is flushed between steps (flush kernel
+outside the per-step CUDA events); step time = sum of per-step event
+intervals on the caller stream, max over ranks.
+
+``--impl reference`` times the oracle (oracle/o1.c, serial CSR, 1 core) on the
+same workload -- the tier's reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SpMV GFLOP/s, HBM GB/s vs peak at 1/2/4/8 B200; schedule fast/slow ratio"
+BEST_ORDER = ["start", "PostRecv", "Pack", "y_L", "PostSend", "WaitRecv", "Unpack", "y_R",
+              "WaitSend", "end"]
+BEST_STREAMS = {"Pack": 0, "y_L": 1, "Unpack": 0, "y_R": 0}
+PAPER1_ORDER = ["start", "Pack", "y_L", "PostSend", "PostRecv", "WaitSend", "WaitRecv",
+                "Unpack", "y_R", "end"]
+VERTS = ["start", "Pack", "y_L", "PostSend", "PostRecv", "WaitSend", "WaitRecv", "Unpack",
+         "y_R", "end"]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"])
+    ap.add_argument("--schedule", default="best", choices=["best", "paper1"])
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- workload
+def workload(name, world, rank):
+    """(description, n_global, row range, rowptr, col, val) for this rank."""
+    import gen
+    from paper_2203_02530_b200 import dspmv as D
+    if name == "c2":
+        dims = (128, 128, 128 * world)
+        n = dims[0] * dims[1] * dims[2]
+        desc = (f"7pt-128x128x{128 * world} (BASELINE configs[1] per rank; "
+                f"{'weak-scaled, row-partitioned' if world > 1 else '1 GPU'})")
+        kind = "7pt"
+    elif name == "c3":
+        dims = (256, 256, 256)
+        n = 256 ** 3
+        desc = "27pt-256^3 (BASELINE configs[2], strong scaling)"
+        kind = "27pt"
+    else:
+        n = 1 << 23
+        dims = None
+        desc = "powerlaw-8M-avg16 (BASELINE configs[3], strong scaling)"
+        kind = "powerlaw"
+    rb = D.dspmv_partition(n, world)
+    lo, hi = int(rb[rank]), int(rb[rank + 1])
+    if kind == "powerlaw":
+        rp, col, val = gen.powerlaw(n, (lo, hi))
+    else:
+        rp, col, val = gen.stencil(kind, dims, (lo, hi))
+    return desc, n, (lo, hi), rp, col, val
+
+
+def alg_bytes_local(n_r, nnz_L, v):
+    """y_L bytes = (v+4)·nnz_L + 4(n_r+1) + v·n_r (x) + v·n_r (y)."""
+    return (v + 4) * nnz_L + 4 * (n_r + 1) + 2 * v * n_r
+
+
+def alg_bytes_rank(info, v):
+    """Per-rank distributed bytes B_r."""
+    n_r = info["row_end"] - info["row_begin"]
+    R, h, s = info["n_remote_rows"], info["n_halo"], info["n_send"]
+    nnz = info["nnz_local"] + info["nnz_remote"]
+    return ((v + 4) * nnz + 4 * (n_r + 1) + 2 * v * n_r + 8 * R + v * h + 2 * v * R
+            + (4 + 2 * v) * s + 2 * v * h)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload_key, world):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+        e = d.get(f"{workload_key}_n{world}")
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (recipe's clocks line)."""
+
+    def __init__(self, gpus):
+        self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", ",".join(map(str, gpus)),
+                                       f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [t.strip() for t in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------- ours
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    from paper_2203_02530_b200 import dspmv as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dt = D.DSPMV_F32 if a.dtype == "f32" else D.DSPMV_F64
+    v = 4 if dt == D.DSPMV_F32 else 8
+    npdt = np.float32 if dt == D.DSPMV_F32 else np.float64
+    tdt = torch.float32 if dt == D.DSPMV_F32 else torch.float64
+
+    desc, n, (lo, hi), rp, col, val = workload(a.workload, world, rank)
+    nnz_rank = int(rp[-1] - rp[0])
+    # library NCCL communicator (bootstrapped through torch.distributed)
+    uid = D.dspmv_comm_unique_id() if rank == 0 else None
+    if world > 1:
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    comm = D.dspmv_comm_create(uid, world, rank, local)
+    plan = D.dspmv_plan_create(comm, n, rp, col, val.astype(npdt), dtype=dt)
+    info = D.dspmv_plan_info_get(plan)
+    del col, val
+    order = BEST_ORDER if a.schedule == "best" else PAPER1_ORDER
+    streams = BEST_STREAMS if a.schedule == "best" else dict.fromkeys(BEST_STREAMS, 0)
+    ops = D.dspmv_schedule_derive([VERTS.index(x) for x in order],
+                                  [streams.get(x, 0) for x in order], 2)
+    sched = D.dspmv_schedule_create(plan, ops, 2)
+    D.dspmv_schedule_set_timing(sched, True)
+    iyl = [i for i, o in enumerate(ops) if o[0] == D.DSPMV_OP_SPMV_LOCAL][0]
+
+    import gen
+    x = torch.from_numpy(gen.x_values((lo, hi)).astype(npdt)).cuda()
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def allmax(t):
+        if world > 1:
+            tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            return float(tt.item())
+        return t
+
+    def allsum(t):
+        if world > 1:
+            tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+            return float(tt.item())
+        return t
+
+    # ---- warmup
+    for _ in range(a.warmup):
+        D.dspmv_l2_flush(local, stream)
+        D.dspmv_apply(sched, x, y, stream)
+    barrier()
+
+    # ---- timed region: K steps, flush between steps outside the per-step events
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(a.steps)]
+    clocks = Clocks(list(range(world))) if rank == 0 else None
+    launches0 = D.dspmv_launch_count()
+    yl_ms = 0.0
+    barrier()
+    t_wall0 = time.perf_counter()
+    for k in range(a.steps):
+        D.dspmv_l2_flush(local, stream)
+        evs[k][0].record(stream)
+        D.dspmv_apply(sched, x, y, stream)
+        evs[k][1].record(stream)
+        yl_ms += float(D.dspmv_schedule_op_times(sched)[iyl])
+    barrier()
+    t_wall = time.perf_counter() - t_wall0
+    launches = D.dspmv_launch_count() - launches0
+    clk = clocks.stop() if clocks else None
+    step_ms_rank = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+    total_ms = allmax(step_ms_rank)
+    ms_per_step = total_ms / a.steps
+    yl_ms_avg = yl_ms / a.steps
+    yl_ms_max = allmax(yl_ms_avg)
+    nnz_total = allsum(float(nnz_rank))
+    gflops = 2.0 * nnz_total / (ms_per_step * 1e-3) / 1e9
+    launches_total = int(allsum(float(launches)))
+
+    # ---- roofline of the dominant kernel (y_L: TMA row-block kernel)
+    n_r = hi - lo
+    yl_bytes = alg_bytes_local(n_r, info["nnz_local"], v)
+    achieved = yl_bytes / (yl_ms_avg * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    step_bytes = allsum(float(alg_bytes_rank(info, v)))
+    step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
+
+    # ---- e2e: the same apply through the C ABI with HOST buffers (pinned)
+    xh = torch.from_numpy(gen.x_values((lo, hi)).astype(npdt)).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    e2e_steps = max(3, min(a.steps, 100))
+    for _ in range(3):
+        D.dspmv_apply_host(sched, xh, yh, stream)
+    e2e_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(e2e_steps)]
+    barrier()
+    for k in range(e2e_steps):
+        D.dspmv_l2_flush(local, stream)
+        e2e_evs[k][0].record(stream)
+        D.dspmv_apply_host(sched, xh, yh, stream)
+        e2e_evs[k][1].record(stream)
+    barrier()
+    e2e_ms = allmax(sum(e0.elapsed_time(e1) for e0, e1 in e2e_evs)) / e2e_steps
+    e2e_gflops = 2.0 * nnz_total / (e2e_ms * 1e-3) / 1e9
+    n_total = allsum(float(n_r))
+
+    # ---- CPU oracle beside it (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(a.workload, budget_s=10.0)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(gflops, 3), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_per_step, 6),
+            "higher_is_better": True, "scaling": "weak" if a.workload == "c2" else "strong",
+            "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
+            "config": {
+                "workload": desc, "n_global": n, "nnz_global": int(nnz_total),
+                "ranks": world, "parallelism": f"row-partition x{world} (NCCL halo exchange)",
+                "schedule": a.schedule + ": " + " ".join(order) + f" streams={streams}",
+                "l2": "flushed between timed steps (flush kernel outside per-step CUDA events)",
+                "step_hbm_gbs_algorithmic": round(step_gbs, 1),
+                "wall_s_timed_region": round(t_wall, 3),
+            },
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": ncu_traffic(a.workload, world),
+                         "kernel": "spmv_block_kernel (y_L, SPMV_LOCAL op)",
+                         "alg_bytes_per_launch": int(yl_bytes),
+                         "avg_launch_ms": round(yl_ms_avg, 6), "max_rank_launch_ms": round(yl_ms_max, 6),
+                         "peak_source": peak_src},
+            "e2e": {"value": round(e2e_gflops, 3), "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": int(n_total * v), "d2h_bytes_per_step": int(n_total * v),
+                    "ms_per_step": round(e2e_ms, 6), "api": "dspmv_apply_host (pinned host x/y)"},
+            "gpu_launches": launches_total,
+            "clocks": clk,
+        }
+        if cpu is not None:
+            out["cpu_baseline"] = cpu
+        print(json.dumps(out), flush=True)
+
+    D.dspmv_schedule_destroy(sched)
+    D.dspmv_plan_destroy(plan)
+    D.dspmv_comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------- oracle legs
+def cpu_baseline(workload_name, budget_s=10.0, world=1):
+    """The oracle O1 (oracle/o1.c, serial, unmodified) on the same matrix and x
+    as the GPU run; repeats the full SpMV until `budget_s` of CPU work."""
+    from oracle import spmv as O1
+    desc, n, (lo, hi), rp, col, val = workload(workload_name, world, 0) if world == 1 else (None,) * 6
+    x = __import__("gen").x_values((0, n))
+    O1.o1_spmv(rp, col, val, x)  # warm
+    reps, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        O1.o1_spmv(rp, col, val, x)
+        reps += 1
+    dt = time.perf_counter() - t0
+    nnz = int(rp[-1])
+    return {"value": round(2.0 * nnz * reps / dt / 1e9, 4), "unit": "GFLOP/s", "cores": 1,
+            "kind": "oracle",
+            "sample": f"full {desc}: {reps} O1 SpMVs ({nnz} nnz each) in {dt:.2f} s, 1 thread",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(a):
+    """The oracle as the reference arm: rank 0 only; others exit 0."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import gen
+    from oracle import spmv as O1
+    # the whole job's matrix (N x C2 for weak scaling), bounded to ~20M nnz per step
+    if a.workload == "c2":
+        dims = (128, 128, 128 * world)
+        n = dims[0] * dims[1] * dims[2]
+        rows = min(n, 128 ** 3)   # bounded sample: the first 128^3 rows
+        rp, col, val = gen.stencil("7pt", dims, (0, rows))
+        desc = f"7pt-128x128x{128 * world}"
+    else:
+        desc, n, _, rp, col, val = workload(a.workload, 1, 0)
+        rows = n
+    x = gen.x_values((0, n))
+    for _ in range(a.warmup):
+        O1.o1_spmv(rp, col, val, x)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        O1.o1_spmv(rp, col, val, x)
+    dt = time.perf_counter() - t0
+    nnz = int(rp[-1])
+    gflops = 2.0 * nnz * a.steps / dt / 1e9
+    sample = f"rows [0,{rows}) of {desc} ({nnz} nnz) per step, O1 serial, 1 thread"
+    print(json.dumps({
+        "metric": METRIC, "value": round(gflops, 4), "unit": "GFLOP/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(dt / a.steps * 1e3, 4),
+        "higher_is_better": True, "scaling": "weak" if a.workload == "c2" else "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": desc, "sample": sample},
+        "cpu_baseline": {"value": round(gflops, 4), "unit": "GFLOP/s", "cores": 1,
+                         "kind": "oracle", "sample": sample, "cpu": _cpu_model()},
+        "e2e": {"value": round(gflops, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,277 @@
+/* dspmv.h -- C ABI of the B200-native distributed SpMV hot path of
+ * arXiv 2203.02530 (Pearson, Javeed, Devine, "Machine Learning for CUDA+MPI
+ * Design Rules").  Citations "P:n" are PAPER.md line numbers; "S:n" SPEC.md.
+ *
+ * What the library computes (§III-A "DAG Representation"):
+ *   "A common distributed memory implementation evenly divides contiguous rows
+ *    of A, x, and y evenly across MPI ranks.  A rank's y entries can then be
+ *    computed as the sum of a 'local' and 'remote' matrix-vector multiplication
+ *    y_L = A_L x_L and y_R = A_R x_R ... each rank must copy a subset of its x_L
+ *    entries into one buffer for each other rank (the Pack vertex).
+ *    Communication is done with point-to-point MPI_Isends (PostSends) and
+ *    MPI_Irecvs (PostRecvs)."
+ * The operations (Pack, PostSend, PostRecv, WaitSend, WaitRecv, Unpack, y_L,
+ * y_R, start, end) run in the order and on the CUDA streams given by a
+ * caller-supplied schedule -- one traversal P of the program DAG G_P
+ * (P:239-248), with the synchronisation operations of tab:sync
+ * (P:436-451).  MPI point-to-point is realised with NCCL grouped send/recv
+ * over NVLink; y = y_L + y_R is combined order-free (DESIGN.md R-Q9).
+ *
+ * Conventions
+ *  - Every call returns dspmv_status (0 = OK).  No exception crosses the ABI
+ *    and nothing aborts.  dspmv_last_error() returns a thread-local message
+ *    describing the last non-OK return on the calling thread.
+ *  - Handles are opaque.  Lifetime: comm >= plan >= schedule; destroying a
+ *    parent while children live returns DSPMV_ERR_STATE.
+ *  - Calls marked COLLECTIVE must be made by every rank of the communicator
+ *    with consistent arguments (same n_global, identical schedule ops).
+ *  - After a CUDA or NCCL error inside a collective the plan is poisoned and
+ *    every later apply returns DSPMV_ERR_STATE.
+ *  - Pointers: "host" pointers are ordinary CPU memory, read (or written)
+ *    only during the call; "device" pointers are CUDA global memory on the
+ *    plan's device.  The library never takes ownership of caller memory.
+ *  - Indices are int32 (per-rank nnz and n_global must be < 2^31,
+ *    DSPMV_ERR_RANGE otherwise; DESIGN.md R-Q1).
+ */
+#ifndef DSPMV_H
+#define DSPMV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSPMV_VERSION 1
+
+typedef enum {
+    DSPMV_OK = 0,
+    DSPMV_ERR_ARG = 1,       /* bad argument (NULL, out of range, inconsistent)  */
+    DSPMV_ERR_RANGE = 2,     /* sizes exceed int32 indexing                       */
+    DSPMV_ERR_SCHEDULE = 3,  /* not a valid traversal / missing tab:sync sync     */
+    DSPMV_ERR_DEADLOCK = 4,  /* a Wait precedes its matching Post (R-Q13)         */
+    DSPMV_ERR_STATE = 5,     /* wrong lifetime / not ready / poisoned             */
+    DSPMV_ERR_CUDA = 6,      /* CUDA runtime error                                */
+    DSPMV_ERR_NCCL = 7,      /* NCCL error (async error seen at a Wait)           */
+    DSPMV_ERR_OOM = 8        /* device or host allocation failed                  */
+} dspmv_status;
+
+typedef enum { DSPMV_F64 = 0, DSPMV_F32 = 1 } dspmv_dtype;
+
+typedef struct dspmv_comm_s* dspmv_comm_t;
+typedef struct dspmv_plan_s* dspmv_plan_t;
+typedef struct dspmv_schedule_s* dspmv_schedule_t;
+typedef struct dspmv_host_plan_s* dspmv_host_plan_t;
+/* a cudaStream_t passed through as an opaque pointer; NULL = legacy stream */
+typedef void* dspmv_stream_t;
+
+/* Thread-local description of the last failure on this thread ("" if none). */
+const char* dspmv_last_error(void);
+int dspmv_version(void);
+
+/* ------------------------------------------------------------ communicator
+ * The rank <-> GPU binding: one process per GPU (NCCL), or -- for tests on a
+ * single device -- an in-process group of nranks simulated ranks sharing one
+ * device whose exchange is a device-to-device copy (kind LOCAL).           */
+enum { DSPMV_COMM_NCCL = 0, DSPMV_COMM_LOCAL = 1 };
+
+/* Rank 0 obtains a 128-byte NCCL unique id; the caller broadcasts it (e.g.
+ * torch.distributed.broadcast_object_list) to every rank. */
+dspmv_status dspmv_comm_unique_id(unsigned char id[128]);
+/* COLLECTIVE.  ncclCommInitRank on cuda_device.  *out owned by the caller,
+ * release with dspmv_comm_destroy. */
+dspmv_status dspmv_comm_create(const unsigned char id[128], int nranks, int rank,
+                               int cuda_device, dspmv_comm_t* out);
+/* nranks in-process ranks on one device; out[r] is rank r's handle. */
+dspmv_status dspmv_comm_create_local(int nranks, int cuda_device, dspmv_comm_t* out);
+/* ERR_STATE if plans created on it are still alive. */
+dspmv_status dspmv_comm_destroy(dspmv_comm_t comm);
+dspmv_status dspmv_comm_info(dspmv_comm_t comm, int* nranks, int* rank, int* kind);
+
+/* ------------------------------------------------------------- partition
+ * P:271-272 "evenly divides contiguous rows": row_begin[r] =
+ * r*floor(n/P) + min(r, n mod P) for r = 0..P (host array of nranks+1
+ * int64, written by the call).  Ranks may own 0 rows when P > n (R-Q3). */
+dspmv_status dspmv_partition(int64_t n_global, int nranks, int64_t* row_begin);
+
+/* ------------------------------------------------------------------ plan */
+typedef struct {
+    int32_t dtype;             /* DSPMV_F64 (default) | DSPMV_F32                        */
+    int32_t vector_threshold;  /* rows with more nnz than this use the warp-per-row
+                                  kernel; the rest the TMA-staged row-block kernel.
+                                  -1 = default (32); valid 0..2048                       */
+    int32_t keep_host;         /* 1: keep host copies of A_L/A_R for dspmv_plan_export  */
+    int32_t comm_priority;     /* 1 (default): comm + stream 0 at the highest priority   */
+    int32_t reserved[4];
+} dspmv_plan_opts;
+
+void dspmv_plan_opts_default(dspmv_plan_opts* opts);
+
+/* COLLECTIVE (a1).  The caller passes ITS row block [row_begin,
+ * row_end) of A = dspmv_partition(n_global, nranks)[rank..rank+1] as host CSR:
+ *   rowptr     host int64[n_local+1] (offsets; rowptr[0] need not be 0),
+ *   col_global host int32[nnz], global column ids in [0, n_global), any order
+ *              (order is preserved inside A_L and A_R rows, R-Q5),
+ *   val        host dtype[nnz].
+ * Arrays are read during the call only.  The plan splits A_L / A_R, builds
+ * the halo list (ascending global id, R-Q4), exchanges request lists with the
+ * owners (NCCL; for LOCAL comms the exchange completes when the last rank of
+ * the group has called plan_create), builds pack maps, row blocks, uploads to
+ * the device and allocates the exchange buffers.  opts may be NULL. */
+dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_local,
+                               const int64_t* rowptr, const int32_t* col_global,
+                               const void* val, const dspmv_plan_opts* opts,
+                               dspmv_plan_t* out);
+dspmv_status dspmv_plan_destroy(dspmv_plan_t plan);
+
+typedef struct {
+    int64_t n_global, row_begin, row_end;
+    int64_t nnz_local, nnz_remote;   /* nnz of A_L, A_R                                */
+    int64_t n_remote_rows;           /* |R_r|: rows with >= 1 remote entry             */
+    int64_t n_halo, n_send;          /* h_r (entries received), s_r (entries sent)     */
+    int32_t n_recv_peers, n_send_peers;
+    int32_t n_blocks_local, n_vrows_local;    /* row blocks / warp-per-row rows, A_L   */
+    int32_t n_blocks_remote, n_vrows_remote;  /* same for A_R                          */
+    int32_t grid_local, grid_remote;          /* persistent grid of the block kernel   */
+    int32_t rank, nranks, dtype, ready;
+    int64_t device_bytes;
+} dspmv_plan_info;
+dspmv_status dspmv_plan_info_get(dspmv_plan_t plan, dspmv_plan_info* out);
+
+/* Bit-exact test hook: copy one plan array to host_dst (capacity `bytes`).
+ * *needed (may be NULL) receives the array's byte size.  Index arrays are
+ * int32; value arrays the plan dtype.  AL_* / AR_* need opts.keep_host = 1. */
+enum {
+    DSPMV_HALO_GID = 0,   /* int32[h]   global ids of x_R, ascending                  */
+    DSPMV_RECV_COUNTS,    /* int32[P]   halo entries owned by each rank                */
+    DSPMV_RECV_DISPL,     /* int32[P]   exclusive prefix of RECV_COUNTS               */
+    DSPMV_SEND_COUNTS,    /* int32[P]   entries each rank requests from this rank      */
+    DSPMV_SEND_DISPL,     /* int32[P]                                                  */
+    DSPMV_PACK_MAP,       /* int32[s]   local x index of each send-buffer entry (R-Q7) */
+    DSPMV_AL_ROWPTR,      /* int32[n_local+1]                                          */
+    DSPMV_AL_COL,         /* int32[nnz_L] local column (global - row_begin)            */
+    DSPMV_AR_ROWS,        /* int32[|R|] local row of each compressed A_R row           */
+    DSPMV_AR_ROWPTR,      /* int32[|R|+1]                                              */
+    DSPMV_AR_COL,         /* int32[nnz_R] position in HALO_GID                         */
+    DSPMV_AL_VAL,         /* dtype[nnz_L]                                              */
+    DSPMV_AR_VAL          /* dtype[nnz_R]                                              */
+};
+dspmv_status dspmv_plan_export(dspmv_plan_t plan, int what, void* host_dst, size_t bytes,
+                               size_t* needed);
+
+/* Host-only twin of plan_create for CPU tests and the oracle comparison:
+ * all ranks' plans from the global host CSR in one process (no device).
+ * val_global may be NULL (values then not exportable). */
+dspmv_status dspmv_plan_build_host(int nranks, int64_t n_global, const int64_t* rowptr_global,
+                                   const int32_t* col_global, const void* val_global,
+                                   int dtype, dspmv_host_plan_t* out);
+dspmv_status dspmv_host_plan_info(dspmv_host_plan_t hp, int rank, dspmv_plan_info* out);
+dspmv_status dspmv_host_plan_export(dspmv_host_plan_t hp, int rank, int what, void* host_dst,
+                                    size_t bytes, size_t* needed);
+dspmv_status dspmv_host_plan_destroy(dspmv_host_plan_t hp);
+
+/* ------------------------------------------------------------ schedules
+ * A schedule is a traversal of the program DAG with every GPU
+ * vertex bound to a stream (BoundGPU_s, tab:vertices P:250-264) and the
+ * synchronisation operations of tab:sync as explicit ops.
+ *
+ * DAG (SPEC S:125 + DESIGN.md R-Q13):  start->Pack, start->y_L,
+ * start->PostRecv, Pack->PostSend, PostSend->WaitSend, PostRecv->WaitRecv,
+ * WaitRecv->Unpack, Unpack->y_R, y_L->end, y_R->end, WaitSend->end,
+ * PostSend->WaitRecv, PostRecv->WaitSend.
+ * GPU vertices: PACK, SPMV_LOCAL (y_L), UNPACK, SPMV_REMOTE (y_R); all others
+ * are synchronous CPU operations. */
+typedef enum {
+    DSPMV_OP_START = 0,
+    DSPMV_OP_PACK = 1,         /* GPU: sendbuf[k] = x[pack_map[k]]                   */
+    DSPMV_OP_SPMV_LOCAL = 2,   /* GPU: y_L = A_L x_L (+ order-free combine)          */
+    DSPMV_OP_POST_SEND = 3,    /* CPU: MPI_Isend x peers -> NCCL (R-Q16)             */
+    DSPMV_OP_POST_RECV = 4,    /* CPU: MPI_Irecv x peers                             */
+    DSPMV_OP_WAIT_SEND = 5,    /* CPU: MPI_Wait on the sends                         */
+    DSPMV_OP_WAIT_RECV = 6,    /* CPU: MPI_Wait on the receives                      */
+    DSPMV_OP_UNPACK = 7,       /* GPU: x_halo = recvbuf (R-Q8)                       */
+    DSPMV_OP_SPMV_REMOTE = 8,  /* GPU: y_R = A_R x_R (+ order-free combine)          */
+    DSPMV_OP_END = 9,
+    DSPMV_OP_EVENT_RECORD = 10,      /* cudaEventRecord(event, stream)  "CER"       */
+    DSPMV_OP_EVENT_SYNC = 11,        /* cudaEventSynchronize(event)     "CES"       */
+    DSPMV_OP_STREAM_WAIT_EVENT = 12  /* cudaStreamWaitEvent(stream, event) "CSWE"   */
+} dspmv_op_kind;
+
+typedef struct {
+    int32_t kind;      /* dspmv_op_kind                                        */
+    int32_t stream;    /* GPU vertices, CER, CSWE: 0..n_streams-1; else ignored */
+    int32_t event;     /* CER, CES, CSWE: 0..DSPMV_MAX_EVENTS-1; else ignored   */
+    int32_t reserved;
+} dspmv_op;
+
+#define DSPMV_MAX_STREAMS 4
+#define DSPMV_MAX_EVENTS 64
+#define DSPMV_MAX_OPS 256
+
+/* Host-only.  DSPMV_OK if ops is a valid schedule: every DAG vertex exactly
+ * once, START first, END last, topological, every DAG edge u->v enforced by
+ * host order, stream order or the sync ops as tab:sync requires, each event
+ * recorded once before any CES/CSWE uses it.  ERR_DEADLOCK if a Wait precedes
+ * its matching Post; ERR_SCHEDULE otherwise. */
+dspmv_status dspmv_schedule_validate(const dspmv_op* ops, int n_ops, int n_streams);
+
+/* Host-only.  Build a schedule from the order of the 10 DAG vertices
+ * (order[i] = vertex kind) and a stream per GPU vertex (streams[i] for
+ * order[i]; ignored for CPU vertices), inserting syncs per tab:sync right
+ * before the vertex that needs them, predecessors in DAG edge order, already
+ * enforced edges inserting nothing, events numbered 0,1,2,....
+ * Writes up to cap ops to out; *n_out = count. */
+dspmv_status dspmv_schedule_derive(const int32_t* order, const int32_t* streams, int n_streams,
+                                   dspmv_op* out, int cap, int* n_out);
+
+/* Host-only.  External schedule text format: one op per line
+ * "<name> <kind> [stream=<i>] [event=<id>]", kind in {Cpu, BoundGpu,
+ * EventRecord, EventSync, StreamWaitEvent}; names start, Pack, y_L,
+ * PostSend, PostRecv, WaitSend, WaitRecv, Unpack, y_R, end (sync op names are
+ * free text, e.g. CER-after-Pack).  Blank lines and '#' comments ignored.
+ * *n_streams = 1 + highest stream used. */
+dspmv_status dspmv_schedule_parse(const char* text, dspmv_op* out, int cap, int* n_out,
+                                  int* n_streams);
+/* Host-only.  Inverse of parse (auto-named syncs CER-after-X / CES-b4-Y). */
+dspmv_status dspmv_schedule_format(const dspmv_op* ops, int n_ops, char* buf, size_t cap);
+
+/* Validate and compile a schedule for a plan (pre-creates its events).
+ * Not collective, but every rank must use identical ops in apply. */
+dspmv_status dspmv_schedule_create(dspmv_plan_t plan, const dspmv_op* ops, int n_ops,
+                                   int n_streams, dspmv_schedule_t* out);
+dspmv_status dspmv_schedule_destroy(dspmv_schedule_t sched);
+/* Per-op CUDA-event timing on the op's stream (adds 2 event records per GPU
+ * op).  After an apply, ms[i] = device time of ops[i] (0 for non-GPU ops). */
+dspmv_status dspmv_schedule_set_timing(dspmv_schedule_t sched, int enable);
+dspmv_status dspmv_schedule_op_times(dspmv_schedule_t sched, float* ms, int n);
+
+/* ----------------------------------------------------------------- apply
+ * COLLECTIVE for NCCL comms (every rank executes the same P).
+ * x_local, y_local: device arrays of n_local elements of the plan dtype, on
+ * the plan's device, 16-byte aligned, not aliasing.  Work is ordered after
+ * prior work on `stream`.  Returns after END, i.e. y is complete (END is a
+ * host synchronisation point).  Not re-entrant per plan. */
+dspmv_status dspmv_apply(dspmv_schedule_t sched, const void* x_local, void* y_local,
+                         dspmv_stream_t stream);
+/* Same with HOST x/y (pageable or pinned): H2D copy of x, apply, D2H copy of
+ * y, all inside the call (the end-to-end path). */
+dspmv_status dspmv_apply_host(dspmv_schedule_t sched, const void* x_host, void* y_host,
+                              dspmv_stream_t stream);
+/* LOCAL comms: all nranks ranks of one in-process group in lock-step (op k on
+ * every rank before op k+1).  scheds[r], x[r], y[r] belong to rank r. */
+dspmv_status dspmv_apply_group(const dspmv_schedule_t* scheds, int nranks,
+                               const void* const* x_local, void* const* y_local,
+                               dspmv_stream_t stream);
+
+/* ------------------------------------------------------------- utilities */
+/* Write a device scratch buffer of 2x the L2 size (allocated on first use)
+ * on `stream`, evicting the working set from L2 between timed iterations. */
+dspmv_status dspmv_l2_flush(int cuda_device, dspmv_stream_t stream);
+/* Number of kernels this library has launched since it was loaded. */
+dspmv_status dspmv_launch_count(uint64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSPMV_H */

@@ -1,0 +1,890 @@
+// api.cpp -- the C ABI (include/dspmv.h): communicators, plans, schedules,
+// the schedule executor and the NCCL / in-process halo exchange.
+//
+// Executor semantics (§III-A/§III-C): a schedule is walked op by op
+// on the host.  GPU vertices are asynchronous launches on their
+// bound stream; CPU vertices run synchronously; CER/CES/CSWE are
+// cudaEventRecord / cudaEventSynchronize / cudaStreamWaitEvent (tab:sync,
+// P:444-448).  PostSend / PostRecv set host flags; the later of the two
+// issues ONE NCCL group (ncclRecv from every owner, ncclSend to every
+// requester) on the high-priority comm stream -- NCCL requires sends and
+// receives that must progress together to be in one group (DESIGN.md R-Q16).
+// WaitSend / WaitRecv synchronise on the group's completion event while
+// polling ncclCommGetAsyncError.  END returns (all GPU work was
+// already host-synchronised by the schedule's own CES ops, R-Q17).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <mutex>
+#include <thread>
+
+#include "runtime.h"
+
+namespace dspmv {
+
+static thread_local std::string t_err;
+
+void set_error(const std::string& msg) { t_err = msg; }
+dspmv_status fail(dspmv_status st, const std::string& msg) {
+    t_err = msg;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+    do {                                                                                    \
+        cudaError_t _e = (expr);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            return fail(DSPMV_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+#define NCCL_TRY(expr)                                                                         \
+    do {                                                                                       \
+        ncclResult_t _r = (expr);                                                              \
+        if (_r != ncclSuccess)                                                                 \
+            return fail(DSPMV_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));   \
+    } while (0)
+
+int device_sm_count();
+
+namespace {
+
+ncclDataType_t nccl_type(int dtype) { return dtype == DSPMV_F32 ? ncclFloat32 : ncclFloat64; }
+
+template <typename T>
+dspmv_status dev_upload(Plan& p, T** dst, const T* src, size_t n) {
+    *dst = nullptr;
+    if (n == 0) return DSPMV_OK;
+    void* d = nullptr;
+    if (cudaMalloc(&d, n * sizeof(T)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DSPMV_ERR_OOM, "cudaMalloc of " + std::to_string(n * sizeof(T)) + " bytes failed");
+    }
+    p.allocs.push_back(d);
+    p.device_bytes += int64_t(n * sizeof(T));
+    if (src) CUDA_TRY(cudaMemcpy(d, src, n * sizeof(T), cudaMemcpyHostToDevice));
+    *dst = static_cast<T*>(d);
+    return DSPMV_OK;
+}
+
+dspmv_status dev_alloc(Plan& p, void** dst, size_t bytes, bool zero) {
+    *dst = nullptr;
+    if (bytes == 0) return DSPMV_OK;
+    if (cudaMalloc(dst, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(DSPMV_ERR_OOM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+    }
+    p.allocs.push_back(*dst);
+    p.device_bytes += int64_t(bytes);
+    if (zero) CUDA_TRY(cudaMemset(*dst, 0, bytes));
+    return DSPMV_OK;
+}
+
+#define ST_TRY(expr)                       \
+    do {                                   \
+        dspmv_status _s = (expr);          \
+        if (_s != DSPMV_OK) return _s;     \
+    } while (0)
+
+dspmv_status upload_layout(Plan& p, const Layout& L, DevLayout& D) {
+    D = DevLayout();
+    D.nS = L.nS;
+    D.nb = L.nb;
+    D.nV = L.nV;
+    const int sms = device_sm_count();
+    if (L.nb > 0) {
+        ST_TRY(dev_upload(p, &D.s_rowptr, L.s_rowptr.data(), L.s_rowptr.size()));
+        ST_TRY(dev_upload(p, &D.s_col, L.s_col.data(), L.s_col.size()));
+        ST_TRY(dev_upload(p, reinterpret_cast<uint8_t**>(&D.s_val), L.s_val.data(), L.s_val.size()));
+        ST_TRY(dev_upload(p, &D.s_blk, L.s_blk.data(), L.s_blk.size()));
+        if (L.s_has_slot) {
+            ST_TRY(dev_upload(p, &D.s_flag, L.s_flag.data(), L.s_flag.size()));
+            ST_TRY(dev_upload(p, &D.s_slot, L.s_slot.data(), L.s_slot.size()));
+        }
+        if (!L.s_identity) ST_TRY(dev_upload(p, &D.s_out, L.s_out.data(), L.s_out.size()));
+        const int per_sm = stream_kernel_ctas_per_sm(p.dtype);
+        D.grid_s = std::max(1, std::min(L.nb, per_sm * sms));
+    }
+    if (L.nV > 0) {
+        ST_TRY(dev_upload(p, &D.v_rowptr, L.v_rowptr.data(), L.v_rowptr.size()));
+        ST_TRY(dev_upload(p, &D.v_col, L.v_col.data(), L.v_col.size()));
+        ST_TRY(dev_upload(p, reinterpret_cast<uint8_t**>(&D.v_val), L.v_val.data(), L.v_val.size()));
+        ST_TRY(dev_upload(p, &D.v_out, L.v_out.data(), L.v_out.size()));
+        if (L.v_has_slot) ST_TRY(dev_upload(p, &D.v_slot, L.v_slot.data(), L.v_slot.size()));
+        D.grid_v = int(std::min<int64_t>((int64_t(L.nV) + 7) / 8, int64_t(sms) * 8));
+    }
+    D.combine = L.s_has_slot || L.v_has_slot;
+    return DSPMV_OK;
+}
+
+// Phase 2 on the device side: pack map + send buffer.
+dspmv_status finalize_send(Plan& p) {
+    const size_t s = p.host.pack_map.size();
+    ST_TRY(dev_upload(p, &p.d_pack_map, p.host.pack_map.data(), s));
+    ST_TRY(dev_alloc(p, &p.d_sendbuf, s * p.esize, true));
+    p.ready = true;
+    return DSPMV_OK;
+}
+
+dspmv_status finalize_local_group(LocalGroup& g) {
+    const int P = g.nranks;
+    for (int p = 0; p < P; ++p) {
+        std::vector<std::vector<int32_t>> req(P);
+        for (int r = 0; r < P; ++r) req[r] = halo_segment_for(g.plans[r]->host, p);
+        plan_phase2_from_requests(g.plans[p]->host, req);
+    }
+    for (int p = 0; p < P; ++p) {
+        CUDA_TRY(cudaSetDevice(g.plans[p]->device));
+        ST_TRY(finalize_send(*g.plans[p]));
+    }
+    return DSPMV_OK;
+}
+
+dspmv_status exchange_requests_nccl(Plan& p) {
+    RankPlan& h = p.host;
+    const int P = h.nranks, me = h.rank;
+    if (P == 1) {
+        std::vector<std::vector<int32_t>> req(1);
+        plan_phase2_from_requests(h, req);
+        return DSPMV_OK;
+    }
+    ncclComm_t comm = p.comm->nccl;
+    cudaStream_t s = p.comm_stream;
+    int32_t *d_cnt = nullptr, *d_scnt = nullptr;
+    CUDA_TRY(cudaMalloc(&d_cnt, sizeof(int32_t) * P));
+    CUDA_TRY(cudaMalloc(&d_scnt, sizeof(int32_t) * P));
+    CUDA_TRY(cudaMemcpy(d_cnt, h.recv_count.data(), sizeof(int32_t) * P, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemset(d_scnt, 0, sizeof(int32_t) * P));
+    NCCL_TRY(ncclGroupStart());
+    for (int q = 0; q < P; ++q) {
+        if (q == me) continue;
+        NCCL_TRY(ncclSend(d_cnt + q, 1, ncclInt32, q, comm, s));
+        NCCL_TRY(ncclRecv(d_scnt + q, 1, ncclInt32, q, comm, s));
+    }
+    NCCL_TRY(ncclGroupEnd());
+    CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<int32_t> scnt(P);
+    CUDA_TRY(cudaMemcpy(scnt.data(), d_scnt, sizeof(int32_t) * P, cudaMemcpyDeviceToHost));
+    int64_t tot = 0;
+    std::vector<int64_t> sdis(P, 0);
+    for (int q = 0; q < P; ++q) {
+        sdis[q] = tot;
+        tot += scnt[q];
+    }
+    int32_t *d_halo = nullptr, *d_req = nullptr;
+    if (!h.halo_gid.empty()) {
+        CUDA_TRY(cudaMalloc(&d_halo, sizeof(int32_t) * h.halo_gid.size()));
+        CUDA_TRY(cudaMemcpy(d_halo, h.halo_gid.data(), sizeof(int32_t) * h.halo_gid.size(), cudaMemcpyHostToDevice));
+    }
+    if (tot) CUDA_TRY(cudaMalloc(&d_req, sizeof(int32_t) * tot));
+    NCCL_TRY(ncclGroupStart());
+    for (int q = 0; q < P; ++q) {
+        if (q == me) continue;
+        if (h.recv_count[q] > 0) NCCL_TRY(ncclSend(d_halo + h.recv_displ[q], h.recv_count[q], ncclInt32, q, comm, s));
+        if (scnt[q] > 0) NCCL_TRY(ncclRecv(d_req + sdis[q], scnt[q], ncclInt32, q, comm, s));
+    }
+    NCCL_TRY(ncclGroupEnd());
+    CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<int32_t> all(tot);
+    if (tot) CUDA_TRY(cudaMemcpy(all.data(), d_req, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost));
+    std::vector<std::vector<int32_t>> req(P);
+    for (int q = 0; q < P; ++q) req[q].assign(all.begin() + sdis[q], all.begin() + sdis[q] + scnt[q]);
+    cudaFree(d_cnt);
+    cudaFree(d_scnt);
+    if (d_halo) cudaFree(d_halo);
+    if (d_req) cudaFree(d_req);
+    plan_phase2_from_requests(h, req);
+    return DSPMV_OK;
+}
+
+// ------------------------------------------------------------- executor
+dspmv_status wait_exchange(Plan& p) {
+    if (p.comm->kind == DSPMV_COMM_LOCAL || p.host.nranks == 1) {
+        CUDA_TRY(cudaEventSynchronize(p.ev_x));
+        return DSPMV_OK;
+    }
+    const auto t_start = std::chrono::steady_clock::now();
+    for (;;) {
+        cudaError_t q = cudaEventQuery(p.ev_x);
+        if (q == cudaSuccess) return DSPMV_OK;
+        if (q != cudaErrorNotReady) return fail(DSPMV_ERR_CUDA, std::string("exchange: ") + cudaGetErrorString(q));
+        ncclResult_t ar = ncclSuccess;
+        ncclCommGetAsyncError(p.comm->nccl, &ar);
+        if (ar != ncclSuccess && ar != ncclInProgress) {
+            ncclCommAbort(p.comm->nccl);
+            p.comm->nccl = nullptr;
+            p.comm->poisoned = true;
+            p.poisoned = true;
+            return fail(DSPMV_ERR_NCCL, std::string("NCCL async error at Wait: ") + ncclGetErrorString(ar));
+        }
+        if (std::chrono::steady_clock::now() - t_start > std::chrono::seconds(120)) {
+            p.poisoned = true;
+            return fail(DSPMV_ERR_NCCL, "exchange did not complete within 120 s");
+        }
+    }
+}
+
+dspmv_status issue_exchange_nccl(Plan& p) {
+    const RankPlan& h = p.host;
+    const int P = h.nranks;
+    bool any = false;
+    for (int q = 0; q < P; ++q) any |= (h.recv_count[q] > 0 || h.send_count[q] > 0);
+    if (any) {
+        const ncclDataType_t ty = nccl_type(p.dtype);
+        char* rb = static_cast<char*>(p.d_recvbuf);
+        char* sb = static_cast<char*>(p.d_sendbuf);
+        NCCL_TRY(ncclGroupStart());
+        for (int q = 0; q < P; ++q)
+            if (h.recv_count[q] > 0)
+                NCCL_TRY(ncclRecv(rb + size_t(h.recv_displ[q]) * p.esize, h.recv_count[q], ty, q, p.comm->nccl,
+                                  p.comm_stream));
+        for (int q = 0; q < P; ++q)
+            if (h.send_count[q] > 0)
+                NCCL_TRY(ncclSend(sb + size_t(h.send_displ[q]) * p.esize, h.send_count[q], ty, q, p.comm->nccl,
+                                  p.comm_stream));
+        NCCL_TRY(ncclGroupEnd());
+    }
+    CUDA_TRY(cudaEventRecord(p.ev_x, p.comm_stream));
+    p.issued = true;
+    return DSPMV_OK;
+}
+
+dspmv_status issue_exchange_local(const std::vector<Plan*>& ps) {
+    for (Plan* pr : ps) {
+        const RankPlan& h = pr->host;
+        for (int q = 0; q < h.nranks; ++q) {
+            const int32_t c = h.recv_count[q];
+            if (c <= 0) continue;
+            Plan* src = ps[q];
+            const size_t off_src = size_t(src->host.send_displ[h.rank]) * pr->esize;
+            CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(pr->d_recvbuf) + size_t(h.recv_displ[q]) * pr->esize,
+                                     static_cast<const char*>(src->d_sendbuf) + off_src, size_t(c) * pr->esize,
+                                     cudaMemcpyDeviceToDevice, pr->comm_stream));
+        }
+        CUDA_TRY(cudaEventRecord(pr->ev_x, pr->comm_stream));
+        pr->issued = true;
+    }
+    return DSPMV_OK;
+}
+
+dspmv_status begin_apply(Schedule& s, cudaStream_t caller) {
+    Plan& p = *s.plan;
+    if (p.poisoned) return fail(DSPMV_ERR_STATE, "plan is poisoned by an earlier error");
+    if (!p.ready) return fail(DSPMV_ERR_STATE, "plan not ready (LOCAL group: not every rank has called plan_create)");
+    CUDA_TRY(cudaSetDevice(p.device));
+    CUDA_TRY(cudaEventRecord(p.ev_start, caller));
+    for (int i = 0; i < s.n_streams; ++i) CUDA_TRY(cudaStreamWaitEvent(p.streams[i], p.ev_start, 0));
+    p.posted_send = p.posted_recv = p.issued = false;
+    return DSPMV_OK;
+}
+
+// Execute op t of schedule s. `defer` = LOCAL group (exchange issued by caller).
+dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
+    Plan& p = *s.plan;
+    const dspmv_op& o = s.ops[t];
+    const bool gpu = is_gpu_vertex(o.kind);
+    const bool on_stream = gpu || o.kind == DSPMV_OP_EVENT_RECORD || o.kind == DSPMV_OP_STREAM_WAIT_EVENT;
+    cudaStream_t st = on_stream ? p.streams[o.stream] : nullptr;
+    if (gpu && s.timing) CUDA_TRY(cudaEventRecord(s.t0[t], st));
+    cudaError_t e = cudaSuccess;
+    switch (o.kind) {
+        case DSPMV_OP_START:
+        case DSPMV_OP_END:
+            break;
+        case DSPMV_OP_PACK:
+            e = launch_pack(p.dtype, x, p.d_pack_map, p.d_sendbuf, int64_t(p.host.pack_map.size()), st);
+            break;
+        case DSPMV_OP_SPMV_LOCAL: {
+            SpmvOperands op{x, y, p.d_partL, p.d_partR, p.d_ticket};
+            e = launch_spmv(p.L, p.dtype, op, st);
+            break;
+        }
+        case DSPMV_OP_UNPACK:
+            e = launch_copy(p.dtype, p.d_recvbuf, p.d_xhalo, int64_t(p.host.halo_gid.size()), st);
+            break;
+        case DSPMV_OP_SPMV_REMOTE: {
+            SpmvOperands op{p.d_xhalo, y, p.d_partR, p.d_partL, p.d_ticket};
+            e = launch_spmv(p.R, p.dtype, op, st);
+            break;
+        }
+        case DSPMV_OP_POST_SEND:
+        case DSPMV_OP_POST_RECV:
+            if (o.kind == DSPMV_OP_POST_SEND) p.posted_send = true; else p.posted_recv = true;
+            if (!defer && p.posted_send && p.posted_recv && !p.issued) {
+                dspmv_status r = issue_exchange_nccl(p);
+                if (r != DSPMV_OK) {
+                    p.poisoned = true;
+                    return r;
+                }
+            }
+            break;
+        case DSPMV_OP_WAIT_SEND:
+        case DSPMV_OP_WAIT_RECV: {
+            if (!p.issued) return fail(DSPMV_ERR_STATE, "Wait before the exchange was issued");
+            dspmv_status r = wait_exchange(p);
+            if (r != DSPMV_OK) return r;
+            break;
+        }
+        case DSPMV_OP_EVENT_RECORD:
+            e = cudaEventRecord(s.ev[o.event], st);
+            break;
+        case DSPMV_OP_EVENT_SYNC:
+            e = cudaEventSynchronize(s.ev[o.event]);
+            break;
+        case DSPMV_OP_STREAM_WAIT_EVENT:
+            e = cudaStreamWaitEvent(st, s.ev[o.event], 0);
+            break;
+        default:
+            return fail(DSPMV_ERR_SCHEDULE, "bad op");
+    }
+    if (e != cudaSuccess) {
+        p.poisoned = true;
+        return fail(DSPMV_ERR_CUDA, std::string("op ") + std::to_string(t) + " (" + vertex_name(o.kind) +
+                                        "): " + cudaGetErrorString(e));
+    }
+    if (gpu && s.timing) CUDA_TRY(cudaEventRecord(s.t1[t], st));
+    return DSPMV_OK;
+}
+
+std::mutex g_flush_mu;
+void* g_flush_buf[64] = {};
+size_t g_flush_bytes[64] = {};
+
+}  // namespace
+}  // namespace dspmv
+
+using namespace dspmv;
+
+struct dspmv_comm_s : dspmv::Comm {};
+struct dspmv_plan_s : dspmv::Plan {};
+struct dspmv_schedule_s : dspmv::Schedule {};
+struct dspmv_host_plan_s {
+    std::vector<dspmv::RankPlan> ranks;
+    int esize = 8;
+    bool has_val = false;
+};
+
+extern "C" {
+
+const char* dspmv_last_error(void) { return t_err.c_str(); }
+int dspmv_version(void) { return DSPMV_VERSION; }
+
+dspmv_status dspmv_partition(int64_t n_global, int nranks, int64_t* row_begin) {
+    if (nranks < 1 || n_global < 0 || !row_begin) return fail(DSPMV_ERR_ARG, "bad partition arguments");
+    const auto rb = partition(n_global, nranks);
+    std::copy(rb.begin(), rb.end(), row_begin);
+    return DSPMV_OK;
+}
+
+// ---------------------------------------------------------------- comms
+dspmv_status dspmv_comm_unique_id(unsigned char id[128]) {
+    if (!id) return fail(DSPMV_ERR_ARG, "null id");
+    ncclUniqueId u;
+    NCCL_TRY(ncclGetUniqueId(&u));
+    static_assert(sizeof(u) == 128, "ncclUniqueId size");
+    std::memcpy(id, &u, 128);
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_comm_create(const unsigned char id[128], int nranks, int rank, int cuda_device,
+                               dspmv_comm_t* out) {
+    if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) return fail(DSPMV_ERR_ARG, "bad comm arguments");
+    CUDA_TRY(cudaSetDevice(cuda_device));
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    auto* c = new dspmv_comm_s();
+    c->kind = DSPMV_COMM_NCCL;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = cuda_device;
+    ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, u, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return fail(DSPMV_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    *out = c;
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_comm_create_local(int nranks, int cuda_device, dspmv_comm_t* out) {
+    if (!out || nranks < 1) return fail(DSPMV_ERR_ARG, "bad local comm arguments");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (cuda_device < 0 || cuda_device >= ndev) return fail(DSPMV_ERR_ARG, "no such device");
+    auto g = std::make_shared<LocalGroup>();
+    g->nranks = nranks;
+    g->device = cuda_device;
+    g->plans.assign(nranks, nullptr);
+    for (int r = 0; r < nranks; ++r) {
+        auto* c = new dspmv_comm_s();
+        c->kind = DSPMV_COMM_LOCAL;
+        c->nranks = nranks;
+        c->rank = r;
+        c->device = cuda_device;
+        c->group = g;
+        out[r] = c;
+    }
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_comm_destroy(dspmv_comm_t comm) {
+    if (!comm) return fail(DSPMV_ERR_ARG, "null comm");
+    if (comm->live_plans > 0) return fail(DSPMV_ERR_STATE, "comm still has live plans");
+    if (comm->nccl) ncclCommDestroy(comm->nccl);
+    delete comm;
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_comm_info(dspmv_comm_t comm, int* nranks, int* rank, int* kind) {
+    if (!comm) return fail(DSPMV_ERR_ARG, "null comm");
+    if (nranks) *nranks = comm->nranks;
+    if (rank) *rank = comm->rank;
+    if (kind) *kind = comm->kind;
+    return DSPMV_OK;
+}
+
+// ----------------------------------------------------------------- plans
+void dspmv_plan_opts_default(dspmv_plan_opts* o) {
+    if (!o) return;
+    std::memset(o, 0, sizeof(*o));
+    o->dtype = DSPMV_F64;
+    o->vector_threshold = -1;
+    o->keep_host = 0;
+    o->comm_priority = 1;
+}
+
+static void free_plan_device(Plan& p) {
+    for (void* a : p.allocs) cudaFree(a);
+    p.allocs.clear();
+    for (auto& s : p.streams)
+        if (s) cudaStreamDestroy(s), s = nullptr;
+    if (p.comm_stream) cudaStreamDestroy(p.comm_stream), p.comm_stream = nullptr;
+    if (p.ev_start) cudaEventDestroy(p.ev_start), p.ev_start = nullptr;
+    if (p.ev_x) cudaEventDestroy(p.ev_x), p.ev_x = nullptr;
+}
+
+dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_local, const int64_t* rowptr,
+                               const int32_t* col_global, const void* val, const dspmv_plan_opts* opts_in,
+                               dspmv_plan_t* out) {
+    if (!comm || !out) return fail(DSPMV_ERR_ARG, "null comm/out");
+    if (comm->poisoned) return fail(DSPMV_ERR_STATE, "comm poisoned");
+    dspmv_plan_opts opts;
+    dspmv_plan_opts_default(&opts);
+    if (opts_in) opts = *opts_in;
+    if (opts.dtype != DSPMV_F64 && opts.dtype != DSPMV_F32) return fail(DSPMV_ERR_ARG, "bad dtype");
+    int vthr = opts.vector_threshold < 0 ? kDefaultVectorThreshold : opts.vector_threshold;
+    if (vthr > kTile) return fail(DSPMV_ERR_ARG, "vector_threshold > 2048");
+    if (n_local > 0 && !val) return fail(DSPMV_ERR_ARG, "null val");
+    if (comm->kind == DSPMV_COMM_LOCAL && comm->group->plans[comm->rank])
+        return fail(DSPMV_ERR_STATE, "this LOCAL rank already has a plan");
+    CUDA_TRY(cudaSetDevice(comm->device));
+
+    auto* p = new dspmv_plan_s();
+    p->comm = comm;
+    p->device = comm->device;
+    p->dtype = opts.dtype;
+    p->esize = opts.dtype == DSPMV_F32 ? 4 : 8;
+    p->opts = opts;
+    auto bail = [&](dspmv_status st) {
+        std::string keep = t_err;
+        free_plan_device(*p);
+        delete p;
+        t_err = keep;
+        return st;
+    };
+    dspmv_status st = plan_phase1(n_global, comm->nranks, comm->rank, n_local, rowptr, col_global, val, p->esize,
+                                  p->host);
+    if (st != DSPMV_OK) return bail(st);
+    RankPlan& h = p->host;
+    p->nnz_L = int64_t(h.al_col.size());
+    p->nnz_R = int64_t(h.ar_col.size());
+
+    // streams: schedule streams + comm stream (highest priority if requested)
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    for (int i = 0; i < DSPMV_MAX_STREAMS; ++i) {
+        const int prio = (opts.comm_priority && i == 0) ? hi : lo;
+        if (cudaStreamCreateWithPriority(&p->streams[i], cudaStreamNonBlocking, prio) != cudaSuccess)
+            return bail(fail(DSPMV_ERR_CUDA, "cudaStreamCreateWithPriority failed"));
+    }
+    if (cudaStreamCreateWithPriority(&p->comm_stream, cudaStreamNonBlocking, opts.comm_priority ? hi : lo) !=
+            cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_x, cudaEventDisableTiming) != cudaSuccess)
+        return bail(fail(DSPMV_ERR_CUDA, "stream/event creation failed"));
+
+    // device layouts of A_L (slots = position of the row in ar_rows) and A_R
+    const int32_t nR = int32_t(h.ar_rows.size());
+    std::vector<int32_t> slotL;
+    if (nR > 0) {
+        slotL.assign(size_t(h.n_local()), -1);
+        for (int32_t k = 0; k < nR; ++k) slotL[h.ar_rows[k]] = k;
+    }
+    {
+        Layout L;
+        build_layout(h.al_rowptr.data(), int32_t(h.n_local()), h.al_col.data(), h.al_val.data(), p->esize, nullptr,
+                     nR > 0 ? slotL.data() : nullptr, vthr, L);
+        if ((st = upload_layout(*p, L, p->L)) != DSPMV_OK) return bail(st);
+    }
+    {
+        std::vector<int32_t> slotR(nR);
+        for (int32_t k = 0; k < nR; ++k) slotR[k] = k;
+        Layout R;
+        build_layout(h.ar_rowptr.data(), nR, h.ar_col.data(), h.ar_val.data(), p->esize, h.ar_rows.data(),
+                     slotR.data(), vthr, R);
+        if ((st = upload_layout(*p, R, p->R)) != DSPMV_OK) return bail(st);
+    }
+    const size_t hsz = h.halo_gid.size();
+    if ((st = dev_alloc(*p, &p->d_recvbuf, hsz * p->esize, true)) != DSPMV_OK) return bail(st);
+    if ((st = dev_alloc(*p, &p->d_xhalo, hsz * p->esize, true)) != DSPMV_OK) return bail(st);
+    if ((st = dev_alloc(*p, &p->d_partL, size_t(nR) * p->esize, true)) != DSPMV_OK) return bail(st);
+    if ((st = dev_alloc(*p, &p->d_partR, size_t(nR) * p->esize, true)) != DSPMV_OK) return bail(st);
+    if ((st = dev_alloc(*p, reinterpret_cast<void**>(&p->d_ticket), size_t(nR) * 4, true)) != DSPMV_OK)
+        return bail(st);
+    if (!opts.keep_host) {
+        std::vector<int32_t>().swap(h.al_rowptr);
+        std::vector<int32_t>().swap(h.al_col);
+        std::vector<uint8_t>().swap(h.al_val);
+        std::vector<int32_t>().swap(h.ar_rowptr);
+        std::vector<int32_t>().swap(h.ar_col);
+        std::vector<uint8_t>().swap(h.ar_val);
+    }
+
+    // phase 2: request lists -> send counts + pack maps
+    if (comm->kind == DSPMV_COMM_NCCL) {
+        if ((st = exchange_requests_nccl(*p)) != DSPMV_OK) return bail(st);
+        if ((st = finalize_send(*p)) != DSPMV_OK) return bail(st);
+    } else {
+        LocalGroup& g = *comm->group;
+        g.plans[comm->rank] = p;
+        g.registered++;
+        if (g.registered == g.nranks) {
+            if ((st = finalize_local_group(g)) != DSPMV_OK) {
+                g.plans[comm->rank] = nullptr;
+                g.registered--;
+                return bail(st);
+            }
+        }
+    }
+    CUDA_TRY(cudaDeviceSynchronize());
+    comm->live_plans++;
+    *out = p;
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_plan_destroy(dspmv_plan_t plan) {
+    if (!plan) return fail(DSPMV_ERR_ARG, "null plan");
+    if (plan->live_scheds > 0) return fail(DSPMV_ERR_STATE, "plan still has live schedules");
+    cudaSetDevice(plan->device);
+    cudaDeviceSynchronize();
+    free_plan_device(*plan);
+    if (plan->comm->kind == DSPMV_COMM_LOCAL) {
+        LocalGroup& g = *plan->comm->group;
+        if (g.plans[plan->comm->rank] == plan) {
+            g.plans[plan->comm->rank] = nullptr;
+            g.registered--;
+        }
+    }
+    plan->comm->live_plans--;
+    delete plan;
+    return DSPMV_OK;
+}
+
+static void fill_info(const RankPlan& h, dspmv_plan_info* o) {
+    std::memset(o, 0, sizeof(*o));
+    o->n_global = h.n_global;
+    o->row_begin = h.row_begin;
+    o->row_end = h.row_end;
+    o->n_remote_rows = int64_t(h.ar_rows.size());
+    o->n_halo = int64_t(h.halo_gid.size());
+    o->n_send = int64_t(h.pack_map.size());
+    for (int q = 0; q < h.nranks; ++q) {
+        o->n_recv_peers += h.recv_count[q] > 0;
+        if (!h.send_count.empty()) o->n_send_peers += h.send_count[q] > 0;
+    }
+    o->rank = h.rank;
+    o->nranks = h.nranks;
+    o->dtype = h.esize == 4 ? DSPMV_F32 : DSPMV_F64;
+}
+
+dspmv_status dspmv_plan_info_get(dspmv_plan_t plan, dspmv_plan_info* out) {
+    if (!plan || !out) return fail(DSPMV_ERR_ARG, "null argument");
+    fill_info(plan->host, out);
+    out->nnz_local = plan->nnz_L;
+    out->nnz_remote = plan->nnz_R;
+    out->n_blocks_local = plan->L.nb;
+    out->n_vrows_local = plan->L.nV;
+    out->n_blocks_remote = plan->R.nb;
+    out->n_vrows_remote = plan->R.nV;
+    out->grid_local = plan->L.grid_s;
+    out->grid_remote = plan->R.grid_s;
+    out->ready = plan->ready;
+    out->device_bytes = plan->device_bytes;
+    return DSPMV_OK;
+}
+
+static dspmv_status export_array(const RankPlan& h, int what, void* dst, size_t bytes, size_t* needed,
+                                 bool have_split) {
+    const void* src = nullptr;
+    size_t n = 0;
+    auto pick = [&](const auto& v) {
+        src = v.data();
+        n = v.size() * sizeof(v[0]);
+    };
+    switch (what) {
+        case DSPMV_HALO_GID: pick(h.halo_gid); break;
+        case DSPMV_RECV_COUNTS: pick(h.recv_count); break;
+        case DSPMV_RECV_DISPL: pick(h.recv_displ); break;
+        case DSPMV_SEND_COUNTS: pick(h.send_count); break;
+        case DSPMV_SEND_DISPL: pick(h.send_displ); break;
+        case DSPMV_PACK_MAP: pick(h.pack_map); break;
+        case DSPMV_AR_ROWS: pick(h.ar_rows); break;
+        case DSPMV_AL_ROWPTR: case DSPMV_AL_COL: case DSPMV_AR_ROWPTR: case DSPMV_AR_COL:
+        case DSPMV_AL_VAL: case DSPMV_AR_VAL:
+            if (!have_split) return fail(DSPMV_ERR_STATE, "split arrays not kept (opts.keep_host = 0)");
+            if (what == DSPMV_AL_ROWPTR) pick(h.al_rowptr);
+            else if (what == DSPMV_AL_COL) pick(h.al_col);
+            else if (what == DSPMV_AR_ROWPTR) pick(h.ar_rowptr);
+            else if (what == DSPMV_AR_COL) pick(h.ar_col);
+            else if (what == DSPMV_AL_VAL) pick(h.al_val);
+            else pick(h.ar_val);
+            break;
+        default:
+            return fail(DSPMV_ERR_ARG, "unknown export id");
+    }
+    if (needed) *needed = n;
+    if (!dst) return DSPMV_OK;
+    if (bytes < n) return fail(DSPMV_ERR_ARG, "destination too small");
+    if (n) std::memcpy(dst, src, n);
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_plan_export(dspmv_plan_t plan, int what, void* host_dst, size_t bytes, size_t* needed) {
+    if (!plan) return fail(DSPMV_ERR_ARG, "null plan");
+    if (!plan->ready && (what == DSPMV_SEND_COUNTS || what == DSPMV_SEND_DISPL || what == DSPMV_PACK_MAP))
+        return fail(DSPMV_ERR_STATE, "plan not ready");
+    return export_array(plan->host, what, host_dst, bytes, needed, plan->opts.keep_host != 0);
+}
+
+dspmv_status dspmv_plan_build_host(int nranks, int64_t n_global, const int64_t* rowptr_global,
+                                   const int32_t* col_global, const void* val_global, int dtype,
+                                   dspmv_host_plan_t* out) {
+    if (!out || nranks < 1 || n_global < 0 || (n_global > 0 && !rowptr_global))
+        return fail(DSPMV_ERR_ARG, "bad arguments");
+    if (dtype != DSPMV_F64 && dtype != DSPMV_F32) return fail(DSPMV_ERR_ARG, "bad dtype");
+    auto* hp = new dspmv_host_plan_s();
+    hp->esize = dtype == DSPMV_F32 ? 4 : 8;
+    hp->has_val = val_global != nullptr;
+    hp->ranks.resize(nranks);
+    const auto rb = partition(n_global, nranks);
+    for (int r = 0; r < nranks; ++r) {
+        const uint8_t* v = val_global ? static_cast<const uint8_t*>(val_global) : nullptr;
+        // the rank's rows: rowptr slice; col/val are addressed relative to rowptr[0]
+        const int64_t b = rb[r], nl = rb[r + 1] - rb[r];
+        const int64_t off = n_global > 0 ? rowptr_global[b] : 0;
+        dspmv_status st = plan_phase1(n_global, nranks, r, nl, n_global > 0 ? rowptr_global + b : nullptr,
+                                      col_global ? col_global + off : nullptr,
+                                      v ? v + size_t(off) * hp->esize : nullptr, hp->esize, hp->ranks[r]);
+        if (st != DSPMV_OK) {
+            delete hp;
+            return st;
+        }
+    }
+    for (int p = 0; p < nranks; ++p) {
+        std::vector<std::vector<int32_t>> req(nranks);
+        for (int r = 0; r < nranks; ++r) req[r] = halo_segment_for(hp->ranks[r], p);
+        plan_phase2_from_requests(hp->ranks[p], req);
+    }
+    *out = hp;
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_host_plan_info(dspmv_host_plan_t hp, int rank, dspmv_plan_info* out) {
+    if (!hp || !out || rank < 0 || rank >= int(hp->ranks.size())) return fail(DSPMV_ERR_ARG, "bad arguments");
+    const RankPlan& h = hp->ranks[rank];
+    fill_info(h, out);
+    out->nnz_local = int64_t(h.al_col.size());
+    out->nnz_remote = int64_t(h.ar_col.size());
+    out->ready = 1;
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_host_plan_export(dspmv_host_plan_t hp, int rank, int what, void* dst, size_t bytes,
+                                    size_t* needed) {
+    if (!hp || rank < 0 || rank >= int(hp->ranks.size())) return fail(DSPMV_ERR_ARG, "bad arguments");
+    if ((what == DSPMV_AL_VAL || what == DSPMV_AR_VAL) && !hp->has_val)
+        return fail(DSPMV_ERR_STATE, "host plan built without values");
+    return export_array(hp->ranks[rank], what, dst, bytes, needed, true);
+}
+
+dspmv_status dspmv_host_plan_destroy(dspmv_host_plan_t hp) {
+    if (!hp) return fail(DSPMV_ERR_ARG, "null host plan");
+    delete hp;
+    return DSPMV_OK;
+}
+
+// ------------------------------------------------------------- schedules
+dspmv_status dspmv_schedule_create(dspmv_plan_t plan, const dspmv_op* ops, int n_ops, int n_streams,
+                                   dspmv_schedule_t* out) {
+    if (!plan || !out) return fail(DSPMV_ERR_ARG, "null plan/out");
+    SchedCheck c = validate_schedule(ops, n_ops, n_streams);
+    if (c.st != DSPMV_OK) return fail(c.st, c.why);
+    CUDA_TRY(cudaSetDevice(plan->device));
+    auto* s = new dspmv_schedule_s();
+    s->plan = plan;
+    s->ops.assign(ops, ops + n_ops);
+    s->n_streams = n_streams;
+    for (const dspmv_op& o : s->ops) {
+        if (o.kind == DSPMV_OP_EVENT_RECORD && !s->ev[o.event]) {
+            if (cudaEventCreateWithFlags(&s->ev[o.event], cudaEventDisableTiming) != cudaSuccess) {
+                for (auto& e : s->ev)
+                    if (e) cudaEventDestroy(e);
+                delete s;
+                return fail(DSPMV_ERR_CUDA, "cudaEventCreate failed");
+            }
+        }
+    }
+    plan->live_scheds++;
+    *out = s;
+    return DSPMV_OK;
+}
+
+static void destroy_timing(Schedule& s) {
+    for (auto e : s.t0)
+        if (e) cudaEventDestroy(e);
+    for (auto e : s.t1)
+        if (e) cudaEventDestroy(e);
+    s.t0.clear();
+    s.t1.clear();
+}
+
+dspmv_status dspmv_schedule_destroy(dspmv_schedule_t s) {
+    if (!s) return fail(DSPMV_ERR_ARG, "null schedule");
+    cudaSetDevice(s->plan->device);
+    for (auto& e : s->ev)
+        if (e) cudaEventDestroy(e);
+    destroy_timing(*s);
+    s->plan->live_scheds--;
+    delete s;
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_schedule_set_timing(dspmv_schedule_t s, int enable) {
+    if (!s) return fail(DSPMV_ERR_ARG, "null schedule");
+    CUDA_TRY(cudaSetDevice(s->plan->device));
+    destroy_timing(*s);
+    s->timing = enable != 0;
+    s->timed_valid = false;
+    if (s->timing) {
+        s->t0.assign(s->ops.size(), nullptr);
+        s->t1.assign(s->ops.size(), nullptr);
+        for (size_t t = 0; t < s->ops.size(); ++t) {
+            if (!is_gpu_vertex(s->ops[t].kind)) continue;
+            CUDA_TRY(cudaEventCreate(&s->t0[t]));
+            CUDA_TRY(cudaEventCreate(&s->t1[t]));
+        }
+    }
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_schedule_op_times(dspmv_schedule_t s, float* ms, int n) {
+    if (!s || !ms) return fail(DSPMV_ERR_ARG, "null argument");
+    if (!s->timing || !s->timed_valid) return fail(DSPMV_ERR_STATE, "timing not enabled or no apply yet");
+    for (int t = 0; t < n && t < int(s->ops.size()); ++t) {
+        ms[t] = 0.f;
+        if (s->t0[t]) CUDA_TRY(cudaEventElapsedTime(&ms[t], s->t0[t], s->t1[t]));
+    }
+    return DSPMV_OK;
+}
+
+// ----------------------------------------------------------------- apply
+dspmv_status dspmv_apply(dspmv_schedule_t s, const void* x, void* y, dspmv_stream_t stream) {
+    if (!s) return fail(DSPMV_ERR_ARG, "null schedule");
+    Plan& p = *s->plan;
+    if (p.comm->kind == DSPMV_COMM_LOCAL && p.host.nranks > 1)
+        return fail(DSPMV_ERR_ARG, "LOCAL groups with >1 rank use dspmv_apply_group");
+    if (p.host.n_local() > 0 && (!x || !y)) return fail(DSPMV_ERR_ARG, "null x/y");
+    ST_TRY(begin_apply(*s, static_cast<cudaStream_t>(stream)));
+    const bool local = p.comm->kind == DSPMV_COMM_LOCAL;
+    for (int t = 0; t < int(s->ops.size()); ++t) {
+        ST_TRY(exec_op(*s, t, x, y, local));
+        if (local && p.posted_send && p.posted_recv && !p.issued) {
+            std::vector<Plan*> one{&p};
+            ST_TRY(issue_exchange_local(one));
+        }
+    }
+    s->timed_valid = s->timing;
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_apply_host(dspmv_schedule_t s, const void* x_host, void* y_host, dspmv_stream_t stream) {
+    if (!s) return fail(DSPMV_ERR_ARG, "null schedule");
+    Plan& p = *s->plan;
+    const size_t bytes = size_t(p.host.n_local()) * p.esize;
+    if (bytes && (!x_host || !y_host)) return fail(DSPMV_ERR_ARG, "null x/y");
+    CUDA_TRY(cudaSetDevice(p.device));
+    if (bytes && !p.d_xin) {
+        ST_TRY(dev_alloc(p, &p.d_xin, bytes, false));
+        ST_TRY(dev_alloc(p, &p.d_yout, bytes, false));
+    }
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    if (bytes) CUDA_TRY(cudaMemcpyAsync(p.d_xin, x_host, bytes, cudaMemcpyHostToDevice, cs));
+    ST_TRY(dspmv_apply(s, p.d_xin, p.d_yout, stream));
+    if (bytes) CUDA_TRY(cudaMemcpyAsync(y_host, p.d_yout, bytes, cudaMemcpyDeviceToHost, cs));
+    CUDA_TRY(cudaStreamSynchronize(cs));
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_apply_group(const dspmv_schedule_t* scheds, int nranks, const void* const* x, void* const* y,
+                               dspmv_stream_t stream) {
+    if (!scheds || nranks < 1 || !x || !y) return fail(DSPMV_ERR_ARG, "null argument");
+    std::vector<Plan*> plans(nranks);
+    for (int r = 0; r < nranks; ++r) {
+        if (!scheds[r]) return fail(DSPMV_ERR_ARG, "null schedule");
+        Plan* p = scheds[r]->plan;
+        if (p->comm->kind != DSPMV_COMM_LOCAL || p->comm->nranks != nranks || p->comm->rank != r)
+            return fail(DSPMV_ERR_ARG, "schedules must be ranks 0..n-1 of one LOCAL group");
+        if (r > 0 && p->comm->group != plans[0]->comm->group) return fail(DSPMV_ERR_ARG, "mixed groups");
+        if (scheds[r]->ops.size() != scheds[0]->ops.size() ||
+            std::memcmp(scheds[r]->ops.data(), scheds[0]->ops.data(), sizeof(dspmv_op) * scheds[0]->ops.size()))
+            return fail(DSPMV_ERR_ARG, "every rank must run the same schedule (P:460)");
+        plans[r] = p;
+    }
+    for (int r = 0; r < nranks; ++r) ST_TRY(begin_apply(*scheds[r], static_cast<cudaStream_t>(stream)));
+    const int n_ops = int(scheds[0]->ops.size());
+    for (int t = 0; t < n_ops; ++t) {
+        for (int r = 0; r < nranks; ++r) ST_TRY(exec_op(*scheds[r], t, x[r], y[r], true));
+        if (plans[0]->posted_send && plans[0]->posted_recv && !plans[0]->issued) ST_TRY(issue_exchange_local(plans));
+    }
+    for (int r = 0; r < nranks; ++r) scheds[r]->timed_valid = scheds[r]->timing;
+    return DSPMV_OK;
+}
+
+// -------------------------------------------------------------- utilities
+dspmv_status dspmv_l2_flush(int dev, dspmv_stream_t stream) {
+    if (dev < 0 || dev >= 64) return fail(DSPMV_ERR_ARG, "bad device");
+    std::lock_guard<std::mutex> lk(g_flush_mu);
+    CUDA_TRY(cudaSetDevice(dev));
+    if (!g_flush_buf[dev]) {
+        int l2 = 0;
+        CUDA_TRY(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+        size_t bytes = size_t(std::max(l2, 64 << 20)) * 2;
+        bytes = (bytes + 4095) & ~size_t(4095);
+        if (cudaMalloc(&g_flush_buf[dev], bytes) != cudaSuccess) {
+            cudaGetLastError();
+            g_flush_buf[dev] = nullptr;
+            return fail(DSPMV_ERR_OOM, "flush buffer allocation failed");
+        }
+        g_flush_bytes[dev] = bytes;
+    }
+    CUDA_TRY(launch_flush(g_flush_buf[dev], g_flush_bytes[dev], static_cast<cudaStream_t>(stream)));
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_launch_count(uint64_t* count) {
+    if (!count) return fail(DSPMV_ERR_ARG, "null count");
+    *count = g_launches.load();
+    return DSPMV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// internal.h -- shared internals of libdspmv (not part of the ABI).
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dspmv.h"
+
+namespace dspmv {
+
+// ----------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+dspmv_status fail(dspmv_status st, const std::string& msg);
+
+// ------------------------------------------------------- row-block kernel
+// Geometry of the TMA-staged row-block ("stream") kernel (kernels.cu):
+// a block is a run of consecutive rows with <= kTile nonzeros and
+// <= kRowMax rows; the whole block's val/col/rowptr are bulk-copied to
+// shared memory.
+constexpr int kTile = 2048;
+constexpr int kRowMax = 512;
+constexpr int kPad = 8;            // device arrays padded (aligned over-read)
+constexpr int kDefaultVectorThreshold = 32;
+
+// ----------------------------------------------------------- host planner
+// One rank's split of its rows (a1): A_L, A_R, halo, pack map.
+struct RankPlan {
+    int rank = 0, nranks = 1;
+    int64_t n_global = 0, row_begin = 0, row_end = 0;
+    int esize = 8;                    // bytes per value
+    std::vector<int32_t> al_rowptr, al_col;
+    std::vector<uint8_t> al_val;
+    std::vector<int32_t> ar_rows, ar_rowptr, ar_col;
+    std::vector<uint8_t> ar_val;
+    std::vector<int32_t> halo_gid;
+    std::vector<int32_t> recv_count, recv_displ;   // [P]
+    std::vector<int32_t> send_count, send_displ;   // [P] (phase 2)
+    std::vector<int32_t> pack_map;                 // [s]  (phase 2)
+    int64_t n_local() const { return row_end - row_begin; }
+};
+
+std::vector<int64_t> partition(int64_t n, int P);
+// Phase 1: split + halo of rank r (needs only its own rows).  val may be null.
+dspmv_status plan_phase1(int64_t n_global, int nranks, int rank, int64_t n_local,
+                         const int64_t* rowptr, const int32_t* col, const void* val,
+                         int esize, RankPlan& out);
+// Phase 2 given every rank's halo: send counts/displ + pack map of rank p.
+void plan_phase2_from_requests(RankPlan& p, const std::vector<std::vector<int32_t>>& requests);
+// requests[r] = global ids rank p must send to rank r (ascending)
+std::vector<int32_t> halo_segment_for(const RankPlan& r, int owner);
+
+// Row layout for one matrix (A_L or A_R) in device order.
+struct Layout {
+    int32_t nrows = 0;                 // matrix rows
+    // S group: rows with len <= vthr, in ascending matrix-row order
+    int32_t nS = 0, nb = 0;
+    std::vector<int32_t> s_rowptr, s_col, s_blk, s_out, s_slot;
+    std::vector<uint8_t> s_val, s_flag;
+    bool s_identity = true;            // s_out[i] == i
+    bool s_has_slot = false;
+    // V group: rows with len > vthr (warp-per-row)
+    int32_t nV = 0;
+    std::vector<int32_t> v_rowptr, v_col, v_out, v_slot;
+    std::vector<uint8_t> v_val;
+    bool v_has_slot = false;
+};
+// out_row / slot nullable: identity / no combine.
+void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, const uint8_t* val,
+                  int esize, const int32_t* out_row, const int32_t* slot, int vthr, Layout& L);
+
+// -------------------------------------------------------------- schedules
+struct SchedCheck {
+    dspmv_status st = DSPMV_OK;
+    std::string why;
+};
+bool is_gpu_vertex(int kind);
+bool is_dag_vertex(int kind);
+SchedCheck validate_schedule(const dspmv_op* ops, int n_ops, int n_streams);
+const char* vertex_name(int kind);
+
+}  // namespace dspmv

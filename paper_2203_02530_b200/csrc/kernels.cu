@@ -1,0 +1,397 @@
+// kernels.cu -- the sm_100a kernels of the distributed SpMV hot path.
+//
+//   spmv_block_kernel  y_L / y_R rows with <= vector_threshold nnz: a
+//                      persistent grid walks precomputed row blocks (<= kTile
+//                      nonzeros, <= kRowMax rows).  One elected thread stages
+//                      each block's val/col/rowptr slices into shared memory
+//                      with 1-D TMA bulk copies (cp.async.bulk, L2 evict_first)
+//                      into a 2-stage mbarrier pipeline, so the next block's
+//                      bytes are in flight while this one is computed.  Threads
+//                      then gather x (read-only path), form the products in
+//                      place, and each thread sums its rows sequentially in
+//                      stored order (the same rounding as the oracle's O1 loop).
+//   spmv_vector_kernel rows with > vector_threshold nnz: one warp per row,
+//                      unrolled coalesced loads, warp-shuffle reduction.
+//   pack_kernel        sendbuf[k] = x[pack_map[k]]
+//   copy_kernel        x_halo = recvbuf (Unpack, DESIGN.md R-Q8)
+//   flush_kernel       L2 eviction between timed iterations
+//
+// y = y_L + y_R on rows with remote entries is combined without an extra DAG
+// vertex (DESIGN.md R-Q9): each op stores its partial in its own slot, then
+// bumps a per-row ticket with acq_rel; the second arriver adds the two slots.
+// fl(a+b) = fl(b+a), so y is bitwise identical for every schedule.
+// SpMV is not a dense contraction: no tensor cores (north_star).
+#include <cuda/atomic>
+#include <cuda_runtime.h>
+
+#include "runtime.h"
+
+namespace dspmv {
+
+std::atomic<uint64_t> g_launches{0};
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kPerThread = kTile / kThreads;      // products per thread per block
+constexpr int kValCap = kTile + kPad;             // aligned over-read slack
+constexpr int kRpCap = kRowMax + kPad;
+constexpr int kStages = 2;
+
+template <typename T>
+struct __align__(16) Stage {
+    T val[kValCap];
+    int32_t col[kValCap];
+    int32_t rp[kRpCap];
+    int32_t hdr[4];  // r0, r1, a0 (aligned first nz), ra0 (aligned first row)
+};
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// 1-D TMA bulk copy global -> shared, completion counted on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+        : "memory");
+}
+
+template <typename T> __device__ __forceinline__ T mul_rn(T a, T b);
+template <> __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+template <> __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+template <typename T> __device__ __forceinline__ T add_rn(T a, T b);
+template <> __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+template <> __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+
+struct BlockArgs {
+    const int32_t* rowptr;
+    const int32_t* col;
+    const void* val;
+    const int32_t* blk;
+    const uint8_t* flag;
+    const int32_t* out;
+    const int32_t* slot;
+    int32_t nb;
+};
+
+struct VecArgs {
+    const int32_t* rowptr;
+    const int32_t* col;
+    const void* val;
+    const int32_t* out;
+    const int32_t* slot;
+    int32_t nV;
+};
+
+// Deposit a partial of a combined row; the second arriver writes y (R-Q9).
+template <typename T>
+__device__ __forceinline__ void combine(T acc, int32_t k, int32_t orow, const SpmvOperands& o) {
+    static_cast<T*>(o.my_part)[k] = acc;
+    cuda::atomic_ref<unsigned, cuda::thread_scope_device> tk(o.ticket[k]);
+    const unsigned old = tk.fetch_add(1u, cuda::memory_order_acq_rel);
+    if (old & 1u) {
+        const T other = *reinterpret_cast<const volatile T*>(static_cast<const T*>(o.other_part) + k);
+        static_cast<T*>(o.y)[orow] = add_rn(acc, other);
+    }
+}
+
+// Thread 0: stage block b into `st`, arming `bar` with the byte count.
+template <typename T>
+__device__ __forceinline__ void issue_block(const BlockArgs& a, Stage<T>& st, uint64_t* bar, int b,
+                                            uint64_t pol) {
+    const int32_t r0 = a.blk[b], r1 = a.blk[b + 1];
+    const int32_t p0 = a.rowptr[r0], p1 = a.rowptr[r1];
+    const int32_t a0 = p0 & ~3, a1 = (p1 + 3) & ~3;
+    const int32_t ra0 = r0 & ~3, ra1 = (r1 + 1 + 3) & ~3;
+    st.hdr[0] = r0;
+    st.hdr[1] = r1;
+    st.hdr[2] = a0;
+    st.hdr[3] = ra0;
+    const uint32_t nz = uint32_t(a1 - a0);
+    const uint32_t bv = nz * sizeof(T), bc = nz * 4u, br = uint32_t(ra1 - ra0) * 4u;
+    fence_proxy_async();  // generic smem accesses of the last use -> async-proxy writes
+    mbar_arrive_expect_tx(bar, bv + bc + br);
+    if (nz) {
+        bulk_g2s(st.val, static_cast<const T*>(a.val) + a0, bv, bar, pol);
+        bulk_g2s(st.col, a.col + a0, bc, bar, pol);
+    }
+    bulk_g2s(st.rp, a.rowptr + ra0, br, bar, pol);
+}
+
+template <typename T, bool kCombine, bool kIdentity>
+__global__ void __launch_bounds__(kThreads) spmv_block_kernel(BlockArgs a, SpmvOperands o) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Stage<T>* st = reinterpret_cast<Stage<T>*>(smem_raw);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + kStages * sizeof(Stage<T>));
+    const int tid = threadIdx.x;
+    const T* __restrict__ x = static_cast<const T*>(o.x);
+    T* __restrict__ y = static_cast<T*>(o.y);
+
+    uint64_t pol = 0;
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+        pol = policy_evict_first();
+        if (int(blockIdx.x) < a.nb) issue_block<T>(a, st[0], &bar[0], blockIdx.x, pol);
+    }
+    __syncthreads();
+
+    int it = 0;
+    for (int b = blockIdx.x; b < a.nb; b += gridDim.x, ++it) {
+        const int s = it & 1;
+        const uint32_t parity = (it >> 1) & 1;
+        const int bn = b + gridDim.x;
+        if (tid == 0 && bn < a.nb) issue_block<T>(a, st[s ^ 1], &bar[s ^ 1], bn, pol);
+        mbar_wait(&bar[s], parity);
+        Stage<T>& S = st[s];
+        const int32_t r0 = S.hdr[0], r1 = S.hdr[1], a0 = S.hdr[2], ra0 = S.hdr[3];
+        const int32_t q0 = S.rp[r0 - ra0] - a0, q1 = S.rp[r1 - ra0] - a0;
+
+        // products in place: val[q] <- val[q] * x[col[q]]
+        T xv[kPerThread];
+#pragma unroll
+        for (int k = 0; k < kPerThread; ++k) {
+            const int q = q0 + tid + k * kThreads;
+            if (q < q1) xv[k] = __ldg(x + S.col[q]);
+        }
+#pragma unroll
+        for (int k = 0; k < kPerThread; ++k) {
+            const int q = q0 + tid + k * kThreads;
+            if (q < q1) S.val[q] = mul_rn(S.val[q], xv[k]);
+        }
+        __syncthreads();
+
+        // row sums in stored order, one thread per row
+        const bool blk_combine = kCombine && a.flag[b] != 0;
+        for (int r = r0 + tid; r < r1; r += kThreads) {
+            const int32_t e0 = S.rp[r - ra0] - a0, e1 = S.rp[r + 1 - ra0] - a0;
+            T acc = T(0);
+            for (int q = e0; q < e1; ++q) acc = add_rn(acc, S.val[q]);
+            const int32_t orow = kIdentity ? r : a.out[r];
+            if (blk_combine) {
+                const int32_t k = a.slot[r];
+                if (k >= 0) {
+                    combine<T>(acc, k, orow, o);
+                    continue;
+                }
+            }
+            __stcs(y + orow, acc);
+        }
+        __syncthreads();  // stage s is free for reuse
+    }
+}
+
+template <typename T, bool kCombine>
+__global__ void __launch_bounds__(kThreads) spmv_vector_kernel(VecArgs a, SpmvOperands o) {
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * kThreads) >> 5;
+    const T* __restrict__ val = static_cast<const T*>(a.val);
+    const T* __restrict__ x = static_cast<const T*>(o.x);
+    for (int i = w; i < a.nV; i += nw) {
+        const int32_t p0 = __ldg(a.rowptr + i), p1 = __ldg(a.rowptr + i + 1);
+        T acc = T(0);
+        int p = p0 + lane;
+        for (; p + 96 < p1; p += 128) {
+            int32_t c[4];
+            T v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                c[u] = __ldcs(a.col + p + 32 * u);
+                v[u] = __ldcs(val + p + 32 * u);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc += v[u] * __ldg(x + c[u]);
+        }
+        for (; p < p1; p += 32) acc += __ldcs(val + p) * __ldg(x + __ldcs(a.col + p));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (lane == 0) {
+            const int32_t orow = a.out[i];
+            if (kCombine) {
+                const int32_t k = a.slot[i];
+                if (k >= 0) {
+                    combine<T>(acc, k, orow, o);
+                    continue;
+                }
+            }
+            static_cast<T*>(o.y)[orow] = acc;
+        }
+    }
+}
+
+template <typename T>
+__global__ void pack_kernel(const T* __restrict__ x, const int32_t* __restrict__ map, T* __restrict__ out,
+                            int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = __ldg(x + __ldg(map + i));
+}
+
+__global__ void copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int64_t n16,
+                            const unsigned char* __restrict__ s8, unsigned char* __restrict__ d8,
+                            int64_t tail_from, int64_t tail_to) {
+    const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = tid; i < n16; i += stride) dst[i] = __ldcs(src + i);
+    for (int64_t i = tail_from + tid; i < tail_to; i += stride) d8[i] = s8[i];
+}
+
+__global__ void flush_kernel(uint4* buf, int64_t n16, unsigned salt) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n16; i += int64_t(gridDim.x) * blockDim.x)
+        buf[i] = make_uint4(unsigned(i), salt, unsigned(i >> 32), salt ^ 0x5bd1e995u);
+}
+
+int g_num_sms = 0;
+
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+template <typename T, bool C, bool I>
+cudaError_t prep_block_kernel() {
+    static bool done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && done[dev]) return cudaSuccess;
+    const int smem = kStages * sizeof(Stage<T>) + kStages * 8;
+    cudaError_t e = cudaFuncSetAttribute(spmv_block_kernel<T, C, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(spmv_block_kernel<T, C, I>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e == cudaSuccess && dev < 64) done[dev] = true;
+    return e;
+}
+
+template <typename T, bool C, bool I>
+cudaError_t launch_block(const DevLayout& L, const SpmvOperands& o, cudaStream_t s) {
+    cudaError_t e = prep_block_kernel<T, C, I>();
+    if (e != cudaSuccess) return e;
+    BlockArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_blk, L.s_flag, L.s_out, L.s_slot, L.nb};
+    const int smem = kStages * sizeof(Stage<T>) + kStages * 8;
+    spmv_block_kernel<T, C, I><<<L.grid_s, kThreads, smem, s>>>(a, o);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_all(const DevLayout& L, const SpmvOperands& o, cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    if (L.nb > 0) {
+        const bool c = L.s_flag != nullptr, id = L.s_out == nullptr;
+        if (c && id) e = launch_block<T, true, true>(L, o, s);
+        else if (c) e = launch_block<T, true, false>(L, o, s);
+        else if (id) e = launch_block<T, false, true>(L, o, s);
+        else e = launch_block<T, false, false>(L, o, s);
+        if (e != cudaSuccess) return e;
+    }
+    if (L.nV > 0) {
+        VecArgs a{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, L.nV};
+        if (L.v_slot) spmv_vector_kernel<T, true><<<L.grid_v, kThreads, 0, s>>>(a, o);
+        else spmv_vector_kernel<T, false><<<L.grid_v, kThreads, 0, s>>>(a, o);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        e = cudaGetLastError();
+    }
+    return e;
+}
+
+}  // namespace
+
+int stream_kernel_smem_bytes(int dtype) {
+    return dtype == DSPMV_F32 ? int(kStages * sizeof(Stage<float>) + kStages * 8)
+                              : int(kStages * sizeof(Stage<double>) + kStages * 8);
+}
+
+int stream_kernel_ctas_per_sm(int dtype) {
+    int n = 0;
+    if (dtype == DSPMV_F32) {
+        if (prep_block_kernel<float, true, false>() != cudaSuccess) return 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_block_kernel<float, true, false>, kThreads,
+                                                      stream_kernel_smem_bytes(dtype));
+    } else {
+        if (prep_block_kernel<double, true, false>() != cudaSuccess) return 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_block_kernel<double, true, false>, kThreads,
+                                                      stream_kernel_smem_bytes(dtype));
+    }
+    return n > 0 ? n : 1;
+}
+
+int device_sm_count() { return num_sms(); }
+
+cudaError_t launch_spmv(const DevLayout& L, int dtype, const SpmvOperands& o, cudaStream_t s) {
+    return dtype == DSPMV_F32 ? launch_all<float>(L, o, s) : launch_all<double>(L, o, s);
+}
+
+cudaError_t launch_pack(int dtype, const void* x, const int32_t* map, void* out, int64_t n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
+    if (dtype == DSPMV_F32)
+        pack_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), map, static_cast<float*>(out), n);
+    else
+        pack_kernel<double><<<grid, 256, 0, s>>>(static_cast<const double*>(x), map, static_cast<double*>(out), n);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_copy(int dtype, const void* src, void* dst, int64_t n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t bytes = n * (dtype == DSPMV_F32 ? 4 : 8);
+    const int64_t n16 = bytes / 16;
+    const int grid = int(std::min<int64_t>((n16 + 255) / 256 + 1, int64_t(num_sms()) * 8));
+    copy_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst), n16,
+                                     static_cast<const unsigned char*>(src), static_cast<unsigned char*>(dst),
+                                     n16 * 16, bytes);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_flush(void* buf, size_t bytes, cudaStream_t s) {
+    static unsigned salt = 1;
+    const int64_t n16 = int64_t(bytes / 16);
+    flush_kernel<<<num_sms() * 4, 512, 0, s>>>(static_cast<uint4*>(buf), n16, salt++);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+
+}  // namespace dspmv

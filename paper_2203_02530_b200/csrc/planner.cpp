@@ -1,0 +1,200 @@
+// planner.cpp -- host planner: row partition (a0), local/remote split, halo
+// list and pack maps (a1), and the device row layout of A_L / A_R.
+//
+// PAPER.md §III-A: "evenly divides contiguous rows of A, x, and y
+// ... A_L has the column entries of A that correspond to x_L ... A_R has the
+// rest ... A is considered to be static, so the entries that make up x_R are
+// fixed ... each rank must copy a subset of its x_L entries into one buffer
+// for each other rank (the Pack vertex)".  Readings: DESIGN.md R-Q3 (uneven
+// partition), R-Q4 (halo ascending by global id => grouped by owner), R-Q5
+// (stored order kept), R-Q6 (compressed A_R rows), R-Q7 (pack-map order).
+#include <algorithm>
+#include <numeric>
+
+#include "internal.h"
+
+namespace dspmv {
+
+std::vector<int64_t> partition(int64_t n, int P) {
+    std::vector<int64_t> rb(P + 1);
+    const int64_t q = n / P, rem = n % P;
+    for (int r = 0; r <= P; ++r) rb[r] = r * q + std::min<int64_t>(r, rem);
+    return rb;
+}
+
+dspmv_status plan_phase1(int64_t n_global, int nranks, int rank, int64_t n_local,
+                         const int64_t* rowptr, const int32_t* col, const void* val,
+                         int esize, RankPlan& out) {
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(DSPMV_ERR_ARG, "bad rank/nranks");
+    if (n_global < 0) return fail(DSPMV_ERR_ARG, "n_global < 0");
+    if (n_global >= (int64_t(1) << 31)) return fail(DSPMV_ERR_RANGE, "n_global >= 2^31");
+    const std::vector<int64_t> rb = partition(n_global, nranks);
+    const int64_t b = rb[rank], e = rb[rank + 1];
+    if (n_local != e - b)
+        return fail(DSPMV_ERR_ARG, "n_local " + std::to_string(n_local) + " != partition size " +
+                                       std::to_string(e - b));
+    if (n_local > 0 && (!rowptr || (!col && rowptr[n_local] != rowptr[0])))
+        return fail(DSPMV_ERR_ARG, "null CSR array");
+    const int64_t base = n_local > 0 ? rowptr[0] : 0;
+    const int64_t nnz = n_local > 0 ? rowptr[n_local] - base : 0;
+    for (int64_t i = 0; i < n_local; ++i)
+        if (rowptr[i + 1] < rowptr[i]) return fail(DSPMV_ERR_ARG, "rowptr not monotone");
+    if (nnz >= (int64_t(1) << 31)) return fail(DSPMV_ERR_RANGE, "per-rank nnz >= 2^31");
+    for (int64_t p = 0; p < nnz; ++p)
+        if (col[p] < 0 || col[p] >= n_global)
+            return fail(DSPMV_ERR_ARG, "column id out of range at nz " + std::to_string(p));
+
+    out = RankPlan();
+    out.rank = rank;
+    out.nranks = nranks;
+    out.n_global = n_global;
+    out.row_begin = b;
+    out.row_end = e;
+    out.esize = esize;
+    const uint8_t* v = static_cast<const uint8_t*>(val);
+
+    // count local / remote per row
+    int64_t nL = 0, nR = 0, nRrows = 0;
+    for (int64_t i = 0; i < n_local; ++i) {
+        int64_t r_here = 0;
+        for (int64_t p = rowptr[i] - base; p < rowptr[i + 1] - base; ++p) {
+            const int32_t j = col[p];
+            if (j >= b && j < e) ++nL; else ++r_here;
+        }
+        nR += r_here;
+        nRrows += r_here > 0;
+    }
+    out.al_rowptr.resize(n_local + 1);
+    out.al_col.resize(nL);
+    if (v) out.al_val.resize(size_t(nL) * esize);
+    out.ar_rows.reserve(nRrows);
+    out.ar_rowptr.reserve(nRrows + 1);
+    out.ar_rowptr.push_back(0);
+    std::vector<int32_t> ar_gcol;
+    ar_gcol.reserve(nR);
+    if (v) out.ar_val.resize(size_t(nR) * esize);
+
+    int64_t qL = 0, qR = 0;
+    out.al_rowptr[0] = 0;
+    for (int64_t i = 0; i < n_local; ++i) {
+        bool had = false;
+        for (int64_t p = rowptr[i] - base; p < rowptr[i + 1] - base; ++p) {
+            const int32_t j = col[p];
+            if (j >= b && j < e) {
+                out.al_col[qL] = int32_t(j - b);
+                if (v) std::memcpy(&out.al_val[size_t(qL) * esize], v + size_t(p) * esize, esize);
+                ++qL;
+            } else {
+                ar_gcol.push_back(j);
+                if (v) std::memcpy(&out.ar_val[size_t(qR) * esize], v + size_t(p) * esize, esize);
+                ++qR;
+                had = true;
+            }
+        }
+        out.al_rowptr[i + 1] = int32_t(qL);
+        if (had) {
+            out.ar_rows.push_back(int32_t(i));
+            out.ar_rowptr.push_back(int32_t(qR));
+        }
+    }
+    // halo: sorted unique remote columns
+    out.halo_gid = ar_gcol;
+    std::sort(out.halo_gid.begin(), out.halo_gid.end());
+    out.halo_gid.erase(std::unique(out.halo_gid.begin(), out.halo_gid.end()), out.halo_gid.end());
+    out.ar_col.resize(ar_gcol.size());
+    for (size_t p = 0; p < ar_gcol.size(); ++p)
+        out.ar_col[p] = int32_t(std::lower_bound(out.halo_gid.begin(), out.halo_gid.end(),
+                                                 ar_gcol[p]) - out.halo_gid.begin());
+    // owner segments
+    out.recv_count.assign(nranks, 0);
+    out.recv_displ.assign(nranks, 0);
+    for (int32_t j : out.halo_gid) {
+        const int owner = int(std::upper_bound(rb.begin(), rb.end(), int64_t(j)) - rb.begin()) - 1;
+        out.recv_count[owner]++;
+    }
+    for (int p = 1; p < nranks; ++p) out.recv_displ[p] = out.recv_displ[p - 1] + out.recv_count[p - 1];
+    out.send_count.assign(nranks, 0);
+    out.send_displ.assign(nranks, 0);
+    return DSPMV_OK;
+}
+
+std::vector<int32_t> halo_segment_for(const RankPlan& r, int owner) {
+    const int32_t o = r.recv_displ[owner], c = r.recv_count[owner];
+    return std::vector<int32_t>(r.halo_gid.begin() + o, r.halo_gid.begin() + o + c);
+}
+
+void plan_phase2_from_requests(RankPlan& p, const std::vector<std::vector<int32_t>>& requests) {
+    const int P = p.nranks;
+    p.send_count.assign(P, 0);
+    p.send_displ.assign(P, 0);
+    p.pack_map.clear();
+    for (int r = 0; r < P; ++r) {
+        p.send_count[r] = int32_t(requests[r].size());
+        if (r > 0) p.send_displ[r] = p.send_displ[r - 1] + p.send_count[r - 1];
+        for (int32_t g : requests[r]) p.pack_map.push_back(int32_t(g - p.row_begin));
+    }
+}
+
+// ---------------------------------------------------------------- layout
+void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, const uint8_t* val,
+                  int esize, const int32_t* out_row, const int32_t* slot, int vthr, Layout& L) {
+    L = Layout();
+    L.nrows = nrows;
+    std::vector<int32_t> srows, vrows;
+    srows.reserve(nrows);
+    for (int32_t i = 0; i < nrows; ++i) {
+        if (rowptr[i + 1] - rowptr[i] > vthr) vrows.push_back(i); else srows.push_back(i);
+    }
+    L.nS = int32_t(srows.size());
+    L.nV = int32_t(vrows.size());
+    auto gather = [&](const std::vector<int32_t>& rows, std::vector<int32_t>& rp,
+                      std::vector<int32_t>& c, std::vector<uint8_t>& v, std::vector<int32_t>& out,
+                      std::vector<int32_t>& sl, bool& has_slot, bool& ident) {
+        const size_t n = rows.size();
+        int64_t tot = 0;
+        for (int32_t i : rows) tot += rowptr[i + 1] - rowptr[i];
+        rp.assign(n + 1 + kPad, 0);
+        c.assign(size_t(tot) + kPad, 0);
+        v.assign((size_t(tot) + kPad) * esize, 0);
+        out.resize(n);
+        sl.resize(n);
+        has_slot = false;
+        ident = true;
+        int64_t q = 0;
+        for (size_t k = 0; k < n; ++k) {
+            const int32_t i = rows[k];
+            const int32_t len = rowptr[i + 1] - rowptr[i];
+            std::memcpy(&c[q], col + rowptr[i], size_t(len) * 4);
+            if (val) std::memcpy(&v[size_t(q) * esize], val + size_t(rowptr[i]) * esize, size_t(len) * esize);
+            q += len;
+            rp[k + 1] = int32_t(q);
+            out[k] = out_row ? out_row[i] : i;
+            sl[k] = slot ? slot[i] : -1;
+            if (sl[k] >= 0) has_slot = true;
+            if (out[k] != int32_t(k)) ident = false;
+        }
+        for (size_t k = n + 1; k < rp.size(); ++k) rp[k] = int32_t(q);  // padded tail
+    };
+    bool dummy = true;
+    gather(srows, L.s_rowptr, L.s_col, L.s_val, L.s_out, L.s_slot, L.s_has_slot, L.s_identity);
+    gather(vrows, L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, L.v_has_slot, dummy);
+    // row blocks of the S group: greedy, <= kTile nnz and <= kRowMax rows
+    L.s_blk.clear();
+    L.s_flag.clear();
+    int32_t r = 0;
+    while (r < L.nS) {
+        const int32_t r0 = r;
+        const int32_t p0 = L.s_rowptr[r0];
+        bool flag = false;
+        while (r < L.nS && r - r0 < kRowMax && L.s_rowptr[r + 1] - p0 <= kTile) {
+            flag |= L.s_slot[r] >= 0;
+            ++r;
+        }
+        L.s_blk.push_back(r0);
+        L.s_flag.push_back(flag ? 1 : 0);
+    }
+    L.s_blk.push_back(L.nS);
+    L.nb = int32_t(L.s_flag.size());
+}
+
+}  // namespace dspmv

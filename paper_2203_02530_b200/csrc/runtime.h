@@ -1,0 +1,113 @@
+// runtime.h -- device-side objects of libdspmv (plans, schedules, comms) and
+// the kernel launchers of kernels.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <memory>
+#include <vector>
+
+#include "internal.h"
+
+typedef struct ncclComm* ncclComm_t;
+
+namespace dspmv {
+
+// ---------------------------------------------------------- launch counter
+extern std::atomic<uint64_t> g_launches;
+
+// Device copy of one Layout (A_L or A_R), see planner.cpp / kernels.cu.
+struct DevLayout {
+    int32_t nS = 0, nb = 0, nV = 0;
+    int grid_s = 0, grid_v = 0;
+    bool combine = false;              // any row of this matrix needs the ticket combine
+    int32_t* s_rowptr = nullptr;
+    int32_t* s_col = nullptr;
+    void* s_val = nullptr;
+    int32_t* s_blk = nullptr;
+    uint8_t* s_flag = nullptr;         // null when no block combines
+    int32_t* s_out = nullptr;          // null when identity
+    int32_t* s_slot = nullptr;         // null when no combine
+    int32_t* v_rowptr = nullptr;
+    int32_t* v_col = nullptr;
+    void* v_val = nullptr;
+    int32_t* v_out = nullptr;
+    int32_t* v_slot = nullptr;
+};
+
+// Operands of one SpMV op (y_L or y_R) for the kernels.
+struct SpmvOperands {
+    const void* x = nullptr;           // x_L (caller) or x_halo
+    void* y = nullptr;                 // caller's y
+    void* my_part = nullptr;           // this op's partial for combined rows
+    const void* other_part = nullptr;  // the other op's partial
+    unsigned* ticket = nullptr;        // per combined row, epoch counter
+};
+
+// kernels.cu
+int stream_kernel_smem_bytes(int dtype);
+int stream_kernel_ctas_per_sm(int dtype);
+cudaError_t launch_spmv(const DevLayout& L, int dtype, const SpmvOperands& o, cudaStream_t s);
+cudaError_t launch_pack(int dtype, const void* x, const int32_t* map, void* out, int64_t n,
+                        cudaStream_t s);
+cudaError_t launch_copy(int dtype, const void* src, void* dst, int64_t n, cudaStream_t s);
+cudaError_t launch_flush(void* buf, size_t bytes, cudaStream_t s);
+
+struct Plan;
+
+struct LocalGroup {
+    int nranks = 0;
+    int device = 0;
+    std::vector<Plan*> plans;          // by rank, once registered
+    int registered = 0;
+};
+
+struct Comm {
+    int kind = DSPMV_COMM_NCCL;
+    int nranks = 1, rank = 0, device = 0;
+    ncclComm_t nccl = nullptr;
+    std::shared_ptr<LocalGroup> group;
+    int live_plans = 0;
+    bool poisoned = false;
+};
+
+struct Plan {
+    Comm* comm = nullptr;
+    int device = 0, dtype = DSPMV_F64, esize = 8;
+    dspmv_plan_opts opts{};
+    RankPlan host;                     // split arrays (AL/AR freed unless keep_host)
+    int64_t nnz_L = 0, nnz_R = 0;
+    DevLayout L, R;
+    int32_t* d_pack_map = nullptr;
+    void* d_sendbuf = nullptr;
+    void* d_recvbuf = nullptr;
+    void* d_xhalo = nullptr;
+    void* d_partL = nullptr;
+    void* d_partR = nullptr;
+    unsigned* d_ticket = nullptr;
+    void* d_xin = nullptr;             // apply_host staging (lazy)
+    void* d_yout = nullptr;
+    cudaStream_t streams[DSPMV_MAX_STREAMS] = {};
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_x = nullptr;
+    std::vector<void*> allocs;
+    int64_t device_bytes = 0;
+    bool ready = false;                // phase 2 done (send lists, pack map)
+    bool poisoned = false;
+    int live_scheds = 0;
+    // per-apply exchange state
+    bool posted_send = false, posted_recv = false, issued = false;
+};
+
+struct Schedule {
+    Plan* plan = nullptr;
+    std::vector<dspmv_op> ops;
+    int n_streams = 1;
+    cudaEvent_t ev[DSPMV_MAX_EVENTS] = {};
+    bool timing = false;
+    std::vector<cudaEvent_t> t0, t1;   // per op (GPU vertices only)
+    bool timed_valid = false;
+};
+
+}  // namespace dspmv

@@ -1,0 +1,350 @@
+"""ctypes binding of include/dspmv.h -- same names as the C ABI.
+
+Argument marshalling only: numpy arrays / ints / torch tensors (anything with
+``data_ptr()``) are turned into pointers and sizes; statuses become
+``DspmvError``.  Device work, planning, scheduling and exchange all happen in
+``libdspmv.so``.  The library MUST be present (built by ``make`` /
+``__graft_entry__.build()``); there is no fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libdspmv.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libdspmv.so not built ({LIB_PATH}); run `make` or __graft_entry__.build()")
+lib = ctypes.CDLL(LIB_PATH)
+
+# ----------------------------------------------------------------- enums
+DSPMV_OK, DSPMV_ERR_ARG, DSPMV_ERR_RANGE, DSPMV_ERR_SCHEDULE, DSPMV_ERR_DEADLOCK, \
+    DSPMV_ERR_STATE, DSPMV_ERR_CUDA, DSPMV_ERR_NCCL, DSPMV_ERR_OOM = range(9)
+STATUS_NAMES = ["OK", "ERR_ARG", "ERR_RANGE", "ERR_SCHEDULE", "ERR_DEADLOCK", "ERR_STATE",
+                "ERR_CUDA", "ERR_NCCL", "ERR_OOM"]
+DSPMV_F64, DSPMV_F32 = 0, 1
+DSPMV_COMM_NCCL, DSPMV_COMM_LOCAL = 0, 1
+(DSPMV_OP_START, DSPMV_OP_PACK, DSPMV_OP_SPMV_LOCAL, DSPMV_OP_POST_SEND, DSPMV_OP_POST_RECV,
+ DSPMV_OP_WAIT_SEND, DSPMV_OP_WAIT_RECV, DSPMV_OP_UNPACK, DSPMV_OP_SPMV_REMOTE, DSPMV_OP_END,
+ DSPMV_OP_EVENT_RECORD, DSPMV_OP_EVENT_SYNC, DSPMV_OP_STREAM_WAIT_EVENT) = range(13)
+(DSPMV_HALO_GID, DSPMV_RECV_COUNTS, DSPMV_RECV_DISPL, DSPMV_SEND_COUNTS, DSPMV_SEND_DISPL,
+ DSPMV_PACK_MAP, DSPMV_AL_ROWPTR, DSPMV_AL_COL, DSPMV_AR_ROWS, DSPMV_AR_ROWPTR, DSPMV_AR_COL,
+ DSPMV_AL_VAL, DSPMV_AR_VAL) = range(13)
+DSPMV_MAX_STREAMS, DSPMV_MAX_EVENTS, DSPMV_MAX_OPS = 4, 64, 256
+GPU_VERTICES = (DSPMV_OP_PACK, DSPMV_OP_SPMV_LOCAL, DSPMV_OP_UNPACK, DSPMV_OP_SPMV_REMOTE)
+VERTEX_NAMES = ["start", "Pack", "y_L", "PostSend", "PostRecv", "WaitSend", "WaitRecv",
+                "Unpack", "y_R", "end"]
+
+
+class DspmvError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 9 else status}: {msg}")
+
+
+class dspmv_plan_opts(ctypes.Structure):
+    _fields_ = [("dtype", ctypes.c_int32), ("vector_threshold", ctypes.c_int32),
+                ("keep_host", ctypes.c_int32), ("comm_priority", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 4)]
+
+
+class dspmv_plan_info(ctypes.Structure):
+    _fields_ = [("n_global", ctypes.c_int64), ("row_begin", ctypes.c_int64),
+                ("row_end", ctypes.c_int64), ("nnz_local", ctypes.c_int64),
+                ("nnz_remote", ctypes.c_int64), ("n_remote_rows", ctypes.c_int64),
+                ("n_halo", ctypes.c_int64), ("n_send", ctypes.c_int64),
+                ("n_recv_peers", ctypes.c_int32), ("n_send_peers", ctypes.c_int32),
+                ("n_blocks_local", ctypes.c_int32), ("n_vrows_local", ctypes.c_int32),
+                ("n_blocks_remote", ctypes.c_int32), ("n_vrows_remote", ctypes.c_int32),
+                ("grid_local", ctypes.c_int32), ("grid_remote", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
+                ("dtype", ctypes.c_int32), ("ready", ctypes.c_int32),
+                ("device_bytes", ctypes.c_int64)]
+
+
+class dspmv_op(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("stream", ctypes.c_int32),
+                ("event", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_I64 = ctypes.c_int64
+_S = ctypes.c_int  # status
+
+
+def _sig(name, args, res=_S):
+    f = getattr(lib, name)
+    f.argtypes = args
+    f.restype = res
+    return f
+
+
+_sig("dspmv_last_error", [], ctypes.c_char_p)
+_sig("dspmv_version", [], _I)
+_sig("dspmv_comm_unique_id", [_P])
+_sig("dspmv_comm_create", [_P, _I, _I, _I, _P])
+_sig("dspmv_comm_create_local", [_I, _I, _P])
+_sig("dspmv_comm_destroy", [_P])
+_sig("dspmv_comm_info", [_P, _P, _P, _P])
+_sig("dspmv_partition", [_I64, _I, _P])
+_sig("dspmv_plan_opts_default", [_P], None)
+_sig("dspmv_plan_create", [_P, _I64, _I64, _P, _P, _P, _P, _P])
+_sig("dspmv_plan_destroy", [_P])
+_sig("dspmv_plan_info_get", [_P, _P])
+_sig("dspmv_plan_export", [_P, _I, _P, ctypes.c_size_t, _P])
+_sig("dspmv_plan_build_host", [_I, _I64, _P, _P, _P, _I, _P])
+_sig("dspmv_host_plan_info", [_P, _I, _P])
+_sig("dspmv_host_plan_export", [_P, _I, _I, _P, ctypes.c_size_t, _P])
+_sig("dspmv_host_plan_destroy", [_P])
+_sig("dspmv_schedule_validate", [_P, _I, _I])
+_sig("dspmv_schedule_derive", [_P, _P, _I, _P, _I, _P])
+_sig("dspmv_schedule_parse", [ctypes.c_char_p, _P, _I, _P, _P])
+_sig("dspmv_schedule_format", [_P, _I, _P, ctypes.c_size_t])
+_sig("dspmv_schedule_create", [_P, _P, _I, _I, _P])
+_sig("dspmv_schedule_destroy", [_P])
+_sig("dspmv_schedule_set_timing", [_P, _I])
+_sig("dspmv_schedule_op_times", [_P, _P, _I])
+_sig("dspmv_apply", [_P, _P, _P, _P])
+_sig("dspmv_apply_host", [_P, _P, _P, _P])
+_sig("dspmv_apply_group", [_P, _I, _P, _P, _P])
+_sig("dspmv_l2_flush", [_I, _P])
+_sig("dspmv_launch_count", [_P])
+
+
+def _check(st: int):
+    if st != DSPMV_OK:
+        raise DspmvError(st, lib.dspmv_last_error().decode(errors="replace"))
+
+
+def _ptr(a) -> int | None:
+    """Pointer of a numpy array, a torch tensor (data_ptr), an int, or None."""
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return a
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    raise TypeError(f"cannot take a pointer of {type(a)}")
+
+
+def _stream(s) -> int | None:
+    if s is None or isinstance(s, int):
+        return s
+    return s.cuda_stream  # torch.cuda.Stream
+
+
+def _ops_array(ops) -> np.ndarray:
+    a = np.zeros((len(ops), 4), np.int32)
+    for i, o in enumerate(ops):
+        o = tuple(o)
+        a[i, :len(o)] = o
+    return a
+
+
+# ------------------------------------------------------------------- API
+def dspmv_last_error() -> str:
+    return lib.dspmv_last_error().decode(errors="replace")
+
+
+def dspmv_version() -> int:
+    return lib.dspmv_version()
+
+
+def dspmv_partition(n_global: int, nranks: int) -> np.ndarray:
+    out = np.zeros(nranks + 1, np.int64)
+    _check(lib.dspmv_partition(n_global, nranks, out.ctypes.data))
+    return out
+
+
+def dspmv_comm_unique_id() -> bytes:
+    buf = (ctypes.c_ubyte * 128)()
+    _check(lib.dspmv_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def dspmv_comm_create(uid: bytes, nranks: int, rank: int, device: int):
+    buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
+    h = _P()
+    _check(lib.dspmv_comm_create(buf, nranks, rank, device, ctypes.byref(h)))
+    return h
+
+
+def dspmv_comm_create_local(nranks: int, device: int):
+    hs = (_P * nranks)()
+    _check(lib.dspmv_comm_create_local(nranks, device, hs))
+    return [_P(h) for h in hs]
+
+
+def dspmv_comm_destroy(comm):
+    _check(lib.dspmv_comm_destroy(comm))
+
+
+def dspmv_comm_info(comm):
+    n, r, k = _I(), _I(), _I()
+    _check(lib.dspmv_comm_info(comm, ctypes.byref(n), ctypes.byref(r), ctypes.byref(k)))
+    return n.value, r.value, k.value
+
+
+def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_F64,
+                      vector_threshold: int = -1, keep_host: bool = False,
+                      comm_priority: bool = True):
+    """rowptr int64[n_local+1], col int32[nnz] (global ids), val float64/32."""
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    col = np.ascontiguousarray(col, np.int32)
+    val = np.ascontiguousarray(val, np.float32 if dtype == DSPMV_F32 else np.float64)
+    o = dspmv_plan_opts()
+    lib.dspmv_plan_opts_default(ctypes.byref(o))
+    o.dtype = dtype
+    o.vector_threshold = vector_threshold
+    o.keep_host = int(keep_host)
+    o.comm_priority = int(comm_priority)
+    h = _P()
+    _check(lib.dspmv_plan_create(comm, n_global, len(rowptr) - 1, rowptr.ctypes.data,
+                                 col.ctypes.data, val.ctypes.data, ctypes.byref(o),
+                                 ctypes.byref(h)))
+    return h
+
+
+def dspmv_plan_destroy(plan):
+    _check(lib.dspmv_plan_destroy(plan))
+
+
+def _info_dict(i: dspmv_plan_info) -> dict:
+    return {f: getattr(i, f) for f, _ in dspmv_plan_info._fields_}
+
+
+def dspmv_plan_info_get(plan) -> dict:
+    i = dspmv_plan_info()
+    _check(lib.dspmv_plan_info_get(plan, ctypes.byref(i)))
+    return _info_dict(i)
+
+
+_VAL_IDS = (DSPMV_AL_VAL, DSPMV_AR_VAL)
+
+
+def _export(fn, args, what, dtype):
+    need = ctypes.c_size_t()
+    _check(fn(*args, what, None, 0, ctypes.byref(need)))
+    dt = (np.float32 if dtype == DSPMV_F32 else np.float64) if what in _VAL_IDS else np.int32
+    out = np.zeros(need.value // np.dtype(dt).itemsize, dt)
+    _check(fn(*args, what, out.ctypes.data, need.value, None))
+    return out
+
+
+def dspmv_plan_export(plan, what: int) -> np.ndarray:
+    return _export(lib.dspmv_plan_export, (plan,), what, dspmv_plan_info_get(plan)["dtype"])
+
+
+def dspmv_plan_build_host(nranks: int, n_global: int, rowptr, col, val=None, dtype=DSPMV_F64):
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    col = np.ascontiguousarray(col, np.int32)
+    vp = None
+    if val is not None:
+        val = np.ascontiguousarray(val, np.float32 if dtype == DSPMV_F32 else np.float64)
+        vp = val.ctypes.data
+    h = _P()
+    _check(lib.dspmv_plan_build_host(nranks, n_global, rowptr.ctypes.data, col.ctypes.data, vp,
+                                     dtype, ctypes.byref(h)))
+    h._dtype = dtype
+    return h
+
+
+def dspmv_host_plan_info(hp, rank: int) -> dict:
+    i = dspmv_plan_info()
+    _check(lib.dspmv_host_plan_info(hp, rank, ctypes.byref(i)))
+    return _info_dict(i)
+
+
+def dspmv_host_plan_export(hp, rank: int, what: int) -> np.ndarray:
+    return _export(lib.dspmv_host_plan_export, (hp, rank), what, getattr(hp, "_dtype", DSPMV_F64))
+
+
+def dspmv_host_plan_destroy(hp):
+    _check(lib.dspmv_host_plan_destroy(hp))
+
+
+def dspmv_schedule_validate(ops, n_streams: int):
+    a = _ops_array(ops)
+    _check(lib.dspmv_schedule_validate(a.ctypes.data, len(a), n_streams))
+
+
+def dspmv_schedule_derive(order, streams, n_streams: int) -> np.ndarray:
+    order = np.ascontiguousarray(order, np.int32)
+    streams = np.ascontiguousarray(streams, np.int32)
+    out = np.zeros((DSPMV_MAX_OPS, 4), np.int32)
+    n = _I()
+    _check(lib.dspmv_schedule_derive(order.ctypes.data, streams.ctypes.data, n_streams,
+                                     out.ctypes.data, DSPMV_MAX_OPS, ctypes.byref(n)))
+    return out[:n.value].copy()
+
+
+def dspmv_schedule_parse(text: str):
+    out = np.zeros((DSPMV_MAX_OPS, 4), np.int32)
+    n, ns = _I(), _I()
+    _check(lib.dspmv_schedule_parse(text.encode(), out.ctypes.data, DSPMV_MAX_OPS,
+                                    ctypes.byref(n), ctypes.byref(ns)))
+    return out[:n.value].copy(), ns.value
+
+
+def dspmv_schedule_format(ops) -> str:
+    a = _ops_array(ops)
+    buf = ctypes.create_string_buffer(64 * len(a) + 64)
+    _check(lib.dspmv_schedule_format(a.ctypes.data, len(a), buf, len(buf)))
+    return buf.value.decode()
+
+
+def dspmv_schedule_create(plan, ops, n_streams: int):
+    a = _ops_array(ops)
+    h = _P()
+    _check(lib.dspmv_schedule_create(plan, a.ctypes.data, len(a), n_streams, ctypes.byref(h)))
+    h._n_ops = len(a)
+    return h
+
+
+def dspmv_schedule_destroy(sched):
+    _check(lib.dspmv_schedule_destroy(sched))
+
+
+def dspmv_schedule_set_timing(sched, enable: bool):
+    _check(lib.dspmv_schedule_set_timing(sched, int(enable)))
+
+
+def dspmv_schedule_op_times(sched, n: int | None = None) -> np.ndarray:
+    n = getattr(sched, "_n_ops", 0) if n is None else n
+    out = np.zeros(n, np.float32)
+    _check(lib.dspmv_schedule_op_times(sched, out.ctypes.data, n))
+    return out
+
+
+def dspmv_apply(sched, x, y, stream=None):
+    """x, y: device buffers (torch tensors or raw pointers)."""
+    _check(lib.dspmv_apply(sched, _ptr(x), _ptr(y), _stream(stream)))
+
+
+def dspmv_apply_host(sched, x_host, y_host, stream=None):
+    """x_host, y_host: host buffers (numpy or pinned torch CPU tensors)."""
+    _check(lib.dspmv_apply_host(sched, _ptr(x_host), _ptr(y_host), _stream(stream)))
+
+
+def dspmv_apply_group(scheds, xs, ys, stream=None):
+    n = len(scheds)
+    sa = (_P * n)(*[s.value for s in scheds])
+    xa = (_P * n)(*[_ptr(x) for x in xs])
+    ya = (_P * n)(*[_ptr(y) for y in ys])
+    _check(lib.dspmv_apply_group(sa, n, xa, ya, _stream(stream)))
+
+
+def dspmv_l2_flush(device: int = 0, stream=None):
+    _check(lib.dspmv_l2_flush(device, _stream(stream)))
+
+
+def dspmv_launch_count() -> int:
+    c = ctypes.c_uint64()
+    _check(lib.dspmv_launch_count(ctypes.byref(c)))
+    return c.value

@@ -1,0 +1,270 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by
+element on the same seeded inputs.  Tolerance (BASELINE.json north_star):
+|y_gpu - y_ref| <= 1e-12 * sum_j |a_ij x_j| (fp64), 1e-5 (fp32, R-Q12); exact
+mode (integer values, R-Q23) and the row-block kernel (stored-order sums,
+DESIGN.md K1) are compared bitwise."""
+import numpy as np
+import pytest
+import torch
+
+import gen
+from oracle import plan as O2
+from oracle import schedules as S
+from oracle import spmv as O1
+from paper_2203_02530_b200 import dspmv as D
+from tests.gpu_helpers import LocalRun, derive_ops, oracle_ops_to_lib, within_tol
+
+pytestmark = pytest.mark.gpu
+
+
+def _mat(name, exact=False):
+    if name == "7pt32":
+        return 32 ** 3, gen.stencil("7pt", (32, 32, 32))
+    if name == "27pt20":
+        return 20 ** 3, gen.stencil("27pt", (20, 20, 20))
+    if name == "5pt64":
+        return gen.config_matrix("c1")
+    if name == "pl20k":
+        return 20000, gen.powerlaw(20000, exact=exact)
+    if name == "rand300":
+        return 300, gen.random_csr(300, 0.05, seed=11, exact=exact, empty_rows=(0, 1, 150, 299),
+                                   dense_rows=(7, 200))
+    raise KeyError(name)
+
+
+@pytest.mark.parametrize("name", ["7pt32", "27pt20", "5pt64"])
+def test_single_rank_stencil_bitwise_vs_o1(name):
+    """All stencil rows go through the TMA row-block kernel, which sums in
+    stored order with separate rounding: bitwise equal to O1."""
+    n, (rp, col, val) = _mat(name)
+    x = gen.x_values((0, n))
+    run = LocalRun(n, rp, col, val, 1)
+    try:
+        y = run.apply(run.schedule(derive_ops()), x)
+        assert np.array_equal(y, O1.o1_spmv(rp, col, val, x))
+    finally:
+        run.close()
+
+
+@pytest.mark.parametrize("name", ["pl20k", "rand300"])
+@pytest.mark.parametrize("vthr", [-1, 0, 2048])
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_irregular_multi_rank_vs_oracle(name, vthr, P):
+    for exact in (False, True):
+        n, (rp, col, val) = _mat(name, exact)
+        x = gen.x_values((0, n), exact=exact)
+        run = LocalRun(n, rp, col, val, P, vector_threshold=vthr)
+        try:
+            y = run.apply(run.schedule(derive_ops()), x)
+        finally:
+            run.close()
+        plans = O2.plan_all(rp, col, n, P)
+        yref = O2.simulate(plans, val, x, [(v,) for v in S.topological_orders(S.EDGES)[0]])
+        if exact:
+            assert np.array_equal(y, yref)
+        else:
+            assert within_tol(y, yref, O1.o1_absdot(rp, col, val, x), 1e-12)
+
+
+def test_row_length_bins():
+    """Rows of every length class: 0, 1, 2, ..., 33, 64, ..., 2048, 2049, 4096."""
+    lens = list(range(0, 34)) + [63, 64, 65, 255, 256, 1000, 2047, 2048, 2049, 4095, 4096]
+    n = 5000
+    rps, cols, vals = [0], [], []
+    for i in range(n):
+        L = lens[i % len(lens)]
+        c = (np.arange(L) * 7919 + i) % n
+        c = np.unique(c)
+        bits = gen.counter_u64(5, 9, np.uint64(i), np.arange(len(c), dtype=np.uint64))
+        cols.append(c)
+        vals.append(2.0 * gen.u01(bits) - 1.0)
+        rps.append(rps[-1] + len(c))
+    rp = np.array(rps, np.int64)
+    col = np.concatenate(cols).astype(np.int32)
+    val = np.concatenate(vals)
+    x = gen.x_values((0, n))
+    yref = O1.o1_spmv(rp, col, val, x)
+    s = O1.o1_absdot(rp, col, val, x)
+    for vthr in (-1, 0, 1, 32, 2048):
+        for P in (1, 4):
+            run = LocalRun(n, rp, col, val, P, vector_threshold=vthr)
+            try:
+                y = run.apply(run.schedule(derive_ops()), x)
+            finally:
+                run.close()
+            assert within_tol(y, yref, s, 1e-12), (vthr, P)
+
+
+def test_every_schedule_same_bits_c1():
+    """C1 (BASELINE configs[0]): 5-pt 64^2 over 2 ranks, every one of the 768
+    derived schedules, 1 and 2 streams: y bitwise identical across schedules
+    (R-Q9 ticket combine) and equal to the oracle (exact mode bitwise)."""
+    for exact in (True, False):
+        n, (rp, col, val) = gen.config_matrix("c1")
+        x = gen.x_values((0, n), exact=exact)
+        plans = O2.plan_all(rp, col, n, 2)
+        yref = O2.simulate(plans, val, x, [(v,) for v in S.topological_orders(S.EDGES)[0]])
+        run = LocalRun(n, rp, col, val, 2)
+        try:
+            first = None
+            for ops in S.enumerate_derived(2, S.EDGES):
+                ss = run.schedule(oracle_ops_to_lib(ops))
+                y = run.apply(ss, x)
+                for s in ss:
+                    D.dspmv_schedule_destroy(s)
+                run.scheds.pop()
+                if first is None:
+                    first = y
+                    if exact:
+                        assert np.array_equal(y, yref)
+                    else:
+                        assert within_tol(y, yref, O1.o1_absdot(rp, col, val, x), 1e-12)
+                assert np.array_equal(y.view(np.uint64), first.view(np.uint64))
+        finally:
+            run.close()
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_rank_count_invariance_27pt(P):
+    n, (rp, col, val) = _mat("27pt20", exact=True)
+    for exact in (True, False):
+        x = gen.x_values((0, n), exact=exact)
+        y1 = O1.o1_spmv(rp, col, val, x)
+        run = LocalRun(n, rp, col, val, P)
+        try:
+            y = run.apply(run.schedule(derive_ops()), x, reps=3)   # ticket epochs
+        finally:
+            run.close()
+        if exact:
+            assert np.array_equal(y, y1)
+        else:
+            assert within_tol(y, y1, O1.o1_absdot(rp, col, val, x), 1e-12)
+
+
+def test_fp32_tolerance():
+    n, (rp, col, val) = _mat("pl20k")
+    x = gen.x_values((0, n))
+    v32, x32 = val.astype(np.float32), x.astype(np.float32)
+    yref = O1.o1_spmv(rp, col, v32.astype(np.float64), x32.astype(np.float64))
+    s = O1.o1_absdot(rp, col, v32.astype(np.float64), x32.astype(np.float64))
+    for P in (1, 4):
+        run = LocalRun(n, rp, col, v32, P, dtype=D.DSPMV_F32)
+        try:
+            y = run.apply(run.schedule(derive_ops()), x32)
+        finally:
+            run.close()
+        assert within_tol(y, yref, s, 1e-5)
+    # exact mode: fp32 bitwise (partial sums < 2^24)
+    n, (rp, col, val) = _mat("pl20k", exact=True)
+    x = gen.x_values((0, n), exact=True)
+    run = LocalRun(n, rp, col, val.astype(np.float32), 4, dtype=D.DSPMV_F32)
+    try:
+        y = run.apply(run.schedule(derive_ops()), x.astype(np.float32))
+    finally:
+        run.close()
+    assert np.array_equal(y, O1.o1_spmv(rp, col, val, x))
+
+
+def test_more_ranks_than_rows_and_empty_matrix():
+    n, (rp, col, val) = 5, gen.random_csr(5, 0.6, seed=9)
+    x = gen.x_values((0, n))
+    run = LocalRun(n, rp, col, val, 8)
+    try:
+        y = run.apply(run.schedule(derive_ops()), x)
+    finally:
+        run.close()
+    assert within_tol(y, O1.o1_spmv(rp, col, val, x), O1.o1_absdot(rp, col, val, x), 1e-12)
+    n = 1000
+    rp = np.zeros(n + 1, np.int64)
+    run = LocalRun(n, rp, np.zeros(0, np.int32), np.zeros(0), 2)
+    try:
+        y = run.apply(run.schedule(derive_ops()), gen.x_values((0, n)))
+    finally:
+        run.close()
+    assert np.all(y == 0.0) and not np.any(np.signbit(y))
+
+
+def test_nccl_single_rank_apply_and_apply_host():
+    n, (rp, col, val) = _mat("27pt20")
+    x = gen.x_values((0, n))
+    uid = D.dspmv_comm_unique_id()
+    comm = D.dspmv_comm_create(uid, 1, 0, 0)
+    plan = D.dspmv_plan_create(comm, n, rp, col, val, keep_host=True)
+    ops = derive_ops()
+    s = D.dspmv_schedule_create(plan, ops, 2)
+    try:
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.empty_like(xd)
+        D.dspmv_schedule_set_timing(s, True)
+        D.dspmv_apply(s, xd, yd)
+        t = D.dspmv_schedule_op_times(s)
+        yL = [i for i, o in enumerate(ops) if o[0] == D.DSPMV_OP_SPMV_LOCAL][0]
+        assert t[yL] > 0
+        yref = O1.o1_spmv(rp, col, val, x)
+        assert np.array_equal(yd.cpu().numpy(), yref)
+        yh = np.empty(n)
+        D.dspmv_apply_host(s, x, yh)
+        assert np.array_equal(yh, yref)
+        assert np.array_equal(D.dspmv_plan_export(plan, D.DSPMV_AL_COL), col)
+        info = D.dspmv_plan_info_get(plan)
+        assert info["ready"] == 1 and info["nnz_remote"] == 0 and info["n_blocks_local"] > 0
+    finally:
+        D.dspmv_schedule_destroy(s)
+        D.dspmv_plan_destroy(plan)
+        D.dspmv_comm_destroy(comm)
+
+
+def test_lifetime_errors():
+    n, (rp, col, val) = _mat("5pt64")
+    comms = D.dspmv_comm_create_local(2, 0)
+    p0 = D.dspmv_plan_create(comms[0], n, rp[:2049], col[:rp[2048]], val[:rp[2048]])
+    s0 = D.dspmv_schedule_create(p0, derive_ops(), 2)
+    with pytest.raises(D.DspmvError) as e:     # group incomplete -> not ready
+        D.dspmv_apply_group([s0], [0], [0])
+    with pytest.raises(D.DspmvError) as e:
+        D.dspmv_plan_destroy(p0)               # live schedule
+    assert e.value.status == D.DSPMV_ERR_STATE
+    with pytest.raises(D.DspmvError) as e:
+        D.dspmv_comm_destroy(comms[0])         # live plan
+    assert e.value.status == D.DSPMV_ERR_STATE
+    bad = [tuple(o) for o in derive_ops() if o[0] < 10]
+    with pytest.raises(D.DspmvError) as e:
+        D.dspmv_schedule_create(p0, bad, 2)
+    assert e.value.status == D.DSPMV_ERR_SCHEDULE
+    D.dspmv_schedule_destroy(s0)
+    D.dspmv_plan_destroy(p0)
+    for c in comms:
+        D.dspmv_comm_destroy(c)
+
+
+def test_launch_count_increases():
+    n, (rp, col, val) = _mat("7pt32")
+    before = D.dspmv_launch_count()
+    run = LocalRun(n, rp, col, val, 2)
+    try:
+        run.apply(run.schedule(derive_ops()), gen.x_values((0, n)))
+    finally:
+        run.close()
+    assert D.dspmv_launch_count() - before >= 5   # pack, y_L, unpack, y_R (+ per rank)
+
+
+def test_full_size_c2_bench_config():
+    """BASELINE configs[1] (7-pt 128^3, 1 B200) in the launch configuration
+    bench.py times: the whole y against O1, bitwise."""
+    n, (rp, col, val) = gen.config_matrix("c2")
+    x = gen.x_values((0, n))
+    uid = D.dspmv_comm_unique_id()
+    comm = D.dspmv_comm_create(uid, 1, 0, 0)
+    plan = D.dspmv_plan_create(comm, n, rp, col, val)
+    s = D.dspmv_schedule_create(plan, derive_ops(), 2)
+    try:
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.empty_like(xd)
+        for _ in range(3):
+            D.dspmv_l2_flush(0)
+            D.dspmv_apply(s, xd, yd)
+        assert np.array_equal(yd.cpu().numpy(), O1.o1_spmv(rp, col, val, x))
+    finally:
+        D.dspmv_schedule_destroy(s)
+        D.dspmv_plan_destroy(plan)
+        D.dspmv_comm_destroy(comm)

@@ -1,0 +1,164 @@
+"""The library's schedule layer (vector-clock validator, tab:sync derivation,
+S:197 text format) against the oracle's happens-before graph enumerator."""
+import itertools
+import random
+
+import pytest
+
+from oracle import schedules as S
+from paper_2203_02530_b200 import dspmv as D
+
+KIND = {v: i for i, v in enumerate(S.VERTICES)}
+GPUS = ["Pack", "y_L", "Unpack", "y_R"]
+
+
+def to_lib(ops):
+    out = []
+    for op in ops:
+        n = op[0]
+        if n in KIND:
+            out.append((KIND[n], op[1] if n in S.GPU_VERTICES else 0, 0, 0))
+        elif n == "CER":
+            out.append((D.DSPMV_OP_EVENT_RECORD, op[1], op[2], 0))
+        elif n == "CES":
+            out.append((D.DSPMV_OP_EVENT_SYNC, 0, op[1], 0))
+        else:
+            out.append((D.DSPMV_OP_STREAM_WAIT_EVENT, op[1], op[2], 0))
+    return out
+
+
+def lib_status(ops, n_streams=2):
+    try:
+        D.dspmv_schedule_validate(to_lib(ops), n_streams)
+        return "ok"
+    except D.DspmvError as e:
+        return {D.DSPMV_ERR_SCHEDULE: "schedule", D.DSPMV_ERR_DEADLOCK: "deadlock"}[e.status]
+
+
+def oracle_status(ops, n_streams=2):
+    ok, kind, _ = S.validate(ops, n_streams)
+    return "ok" if ok else kind
+
+
+def test_derive_matches_oracle_for_every_order_and_stream_assignment():
+    for edges in (S.EDGES,):
+        for order in S.topological_orders(edges):
+            for assign in itertools.product(range(2), repeat=4):
+                streams = dict(zip(GPUS, assign))
+                want = to_lib(S.derive(order, streams, edges))
+                got = D.dspmv_schedule_derive([KIND[v] for v in order],
+                                              [streams.get(v, 0) for v in order], 2)
+                assert [tuple(r) for r in got] == want, order
+
+
+def test_validator_agrees_with_oracle_on_all_derived_schedules():
+    for ops in S.enumerate_derived(2, S.EDGES):
+        assert lib_status(ops) == "ok"
+    for ops in S.enumerate_derived(2, S.EDGES_A):      # 1408 of 2240 deadlock (R-Q13)
+        assert lib_status(ops) == oracle_status(ops)
+
+
+def _mutations(ops, rng):
+    ops = list(ops)
+    yield ops[:]                                         # identity
+    for t in range(len(ops)):                            # drop one op
+        yield ops[:t] + ops[t + 1:]
+    for t in range(len(ops) - 1):                        # swap neighbours
+        m = ops[:]
+        m[t], m[t + 1] = m[t + 1], m[t]
+        yield m
+    for t, op in enumerate(ops):                         # re-stream one op
+        if op[0] in S.GPU_VERTICES:
+            yield ops[:t] + [(op[0], 1 - op[1])] + ops[t + 1:]
+        if op[0] in ("CER", "CSWE"):
+            yield ops[:t] + [(op[0], 1 - op[1], op[2])] + ops[t + 1:]
+    for _ in range(5):                                   # move a sync op
+        syncs = [t for t, o in enumerate(ops) if o[0] in ("CER", "CES", "CSWE")]
+        if not syncs:
+            break
+        t = rng.choice(syncs)
+        m = ops[:t] + ops[t + 1:]
+        m.insert(rng.randrange(1, len(m)), ops[t])
+        yield m
+
+
+def test_validator_agrees_with_oracle_on_mutations():
+    rng = random.Random(2203)
+    scheds = S.enumerate_derived(2, S.EDGES)
+    rng.shuffle(scheds)
+    n = 0
+    for ops in scheds[:250]:
+        for m in _mutations(ops, rng):
+            assert lib_status(m) == oracle_status(m), m
+            n += 1
+    assert n > 5000
+
+
+def test_paper_sequences_and_parse_roundtrip():
+    seq2 = ["start", "PostRecv", "y_L", "Pack", "PostSend", "WaitRecv", "WaitSend",
+            "Unpack", "y_R", "end"]
+    ops = D.dspmv_schedule_derive([KIND[v] for v in seq2], [0, 0, 1, 0, 0, 0, 0, 0, 1, 0], 2)
+    D.dspmv_schedule_validate(ops, 2)
+    text = D.dspmv_schedule_format(ops)
+    assert "CES-b4-PostSend EventSync" in text
+    back, ns = D.dspmv_schedule_parse(text)
+    assert ns == 2 and (back == ops).all()
+
+
+def test_parse_spec_format_example():
+    text = """# S:197 external schedule format
+start Cpu
+Pack BoundGpu stream=0
+CER-after-Pack EventRecord stream=0 event=0
+CES-b4-PostSend EventSync event=0
+PostSend PostSend
+PostRecv PostRecv
+WaitSend WaitSend
+WaitRecv WaitRecv
+y_L BoundGpu stream=1
+Unpack BoundGpu stream=0
+y_R BoundGpu stream=0
+CER-after-y_R EventRecord stream=0 event=1
+CES-b4-end EventSync event=1
+CER-after-y_L EventRecord stream=1 event=2
+CES-b4-end EventSync event=2
+end Cpu
+"""
+    ops, ns = D.dspmv_schedule_parse(text)
+    assert ns == 2 and len(ops) == 16
+    D.dspmv_schedule_validate(ops, ns)
+    with pytest.raises(D.DspmvError):
+        D.dspmv_schedule_parse("Pack Cpu\n")             # kind/vertex mismatch
+    with pytest.raises(D.DspmvError):
+        D.dspmv_schedule_parse("foo BoundGpu stream=0\n")
+
+
+def test_error_cases_of_the_boundary_table():
+    good = D.dspmv_schedule_derive(list(range(10)), [0] * 10, 2)
+    D.dspmv_schedule_validate(good, 2)
+
+    def status(ops, ns=2):
+        try:
+            D.dspmv_schedule_validate(ops, ns)
+            return D.DSPMV_OK
+        except D.DspmvError as e:
+            return e.status
+
+    dup = list(map(tuple, good)) + [(D.DSPMV_OP_PACK, 0, 0, 0)]
+    assert status(dup) == D.DSPMV_ERR_SCHEDULE                  # duplicated DAG op
+    missing = [tuple(o) for o in good if o[0] != D.DSPMV_OP_UNPACK]
+    assert status(missing) == D.DSPMV_ERR_SCHEDULE              # missing DAG op
+    bad_stream = [tuple(o) for o in good]
+    i = [o[0] for o in bad_stream].index(D.DSPMV_OP_PACK)
+    bad_stream[i] = (D.DSPMV_OP_PACK, 3, 0, 0)
+    assert status(bad_stream) == D.DSPMV_ERR_SCHEDULE           # stream >= n_streams
+    unrec = [tuple(o) for o in good]
+    j = [o[0] for o in unrec].index(D.DSPMV_OP_EVENT_SYNC)
+    unrec[j] = (D.DSPMV_OP_EVENT_SYNC, 0, 33, 0)
+    assert status(unrec) == D.DSPMV_ERR_SCHEDULE                # CES on unrecorded event
+    nosync = [tuple(o) for o in good if o[0] < 10]
+    assert status(nosync) == D.DSPMV_ERR_SCHEDULE               # missing tab:sync sync
+    order = ["start", "PostRecv", "WaitRecv", "Pack", "PostSend", "WaitSend", "Unpack",
+             "y_L", "y_R", "end"]
+    dead = to_lib(S.derive(order, dict.fromkeys(GPUS, 0), S.EDGES_A))
+    assert status(dead) == D.DSPMV_ERR_DEADLOCK                 # WaitRecv before PostSend
