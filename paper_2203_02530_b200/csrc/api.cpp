@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <mutex>
 #include <thread>
 
@@ -86,7 +87,7 @@ dspmv_status dev_alloc(Plan& p, void** dst, size_t bytes, bool zero) {
         if (_s != DSPMV_OK) return _s;     \
     } while (0)
 
-dspmv_status upload_layout(Plan& p, const Layout& L, DevLayout& D) {
+dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
     D = DevLayout();
     D.nS = L.nS;
     D.nb = L.nb;
@@ -96,13 +97,11 @@ dspmv_status upload_layout(Plan& p, const Layout& L, DevLayout& D) {
         ST_TRY(dev_upload(p, &D.s_rowptr, L.s_rowptr.data(), L.s_rowptr.size()));
         ST_TRY(dev_upload(p, &D.s_col, L.s_col.data(), L.s_col.size()));
         ST_TRY(dev_upload(p, reinterpret_cast<uint8_t**>(&D.s_val), L.s_val.data(), L.s_val.size()));
-        ST_TRY(dev_upload(p, &D.s_blk, L.s_blk.data(), L.s_blk.size()));
-        if (L.s_has_slot) {
-            ST_TRY(dev_upload(p, &D.s_flag, L.s_flag.data(), L.s_flag.size()));
-            ST_TRY(dev_upload(p, &D.s_slot, L.s_slot.data(), L.s_slot.size()));
-        }
+        ST_TRY(dev_upload(p, &D.s_desc, L.s_desc.data(), L.s_desc.size()));
+        if (L.s_has_slot) ST_TRY(dev_upload(p, &D.s_slot, L.s_slot.data(), L.s_slot.size()));
         if (!L.s_identity) ST_TRY(dev_upload(p, &D.s_out, L.s_out.data(), L.s_out.size()));
-        const int per_sm = stream_kernel_ctas_per_sm(p.dtype);
+        D.cfg = cfg;
+        const int per_sm = block_kernel_ctas_per_sm(p.dtype, cfg);
         D.grid_s = std::max(1, std::min(L.nb, per_sm * sms));
     }
     if (L.nV > 0) {
@@ -473,7 +472,12 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
     if (opts_in) opts = *opts_in;
     if (opts.dtype != DSPMV_F64 && opts.dtype != DSPMV_F32) return fail(DSPMV_ERR_ARG, "bad dtype");
     int vthr = opts.vector_threshold < 0 ? kDefaultVectorThreshold : opts.vector_threshold;
-    if (vthr > kTile) return fail(DSPMV_ERR_ARG, "vector_threshold > 2048");
+    int cfg = opts.block_cfg < 0 ? kDefaultBlockCfg : opts.block_cfg;
+    if (const char* ev = std::getenv("DSPMV_BLOCK_CFG")) cfg = std::atoi(ev);  // tuning sweeps
+    if (cfg < 0 || cfg >= kNumBlockCfgs) return fail(DSPMV_ERR_ARG, "block_cfg out of range");
+    if (vthr > kBlockCfgs[cfg].tile)
+        return fail(DSPMV_ERR_ARG, "vector_threshold > tile of block_cfg (" +
+                                       std::to_string(kBlockCfgs[cfg].tile) + ")");
     if (n_local > 0 && !val) return fail(DSPMV_ERR_ARG, "null val");
     if (comm->kind == DSPMV_COMM_LOCAL && comm->group->plans[comm->rank])
         return fail(DSPMV_ERR_STATE, "this LOCAL rank already has a plan");
@@ -523,16 +527,16 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
     {
         Layout L;
         build_layout(h.al_rowptr.data(), int32_t(h.n_local()), h.al_col.data(), h.al_val.data(), p->esize, nullptr,
-                     nR > 0 ? slotL.data() : nullptr, vthr, L);
-        if ((st = upload_layout(*p, L, p->L)) != DSPMV_OK) return bail(st);
+                     nR > 0 ? slotL.data() : nullptr, vthr, kBlockCfgs[cfg], L);
+        if ((st = upload_layout(*p, L, cfg, p->L)) != DSPMV_OK) return bail(st);
     }
     {
         std::vector<int32_t> slotR(nR);
         for (int32_t k = 0; k < nR; ++k) slotR[k] = k;
         Layout R;
         build_layout(h.ar_rowptr.data(), nR, h.ar_col.data(), h.ar_val.data(), p->esize, h.ar_rows.data(),
-                     slotR.data(), vthr, R);
-        if ((st = upload_layout(*p, R, p->R)) != DSPMV_OK) return bail(st);
+                     slotR.data(), vthr, kBlockCfgs[cfg], R);
+        if ((st = upload_layout(*p, R, cfg, p->R)) != DSPMV_OK) return bail(st);
     }
     const size_t hsz = h.halo_gid.size();
     if ((st = dev_alloc(*p, &p->d_recvbuf, hsz * p->esize, true)) != DSPMV_OK) return bail(st);

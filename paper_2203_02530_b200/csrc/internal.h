@@ -15,13 +15,27 @@ void set_error(const std::string& msg);
 dspmv_status fail(dspmv_status st, const std::string& msg);
 
 // ------------------------------------------------------- row-block kernel
-// Geometry of the TMA-staged row-block ("stream") kernel (kernels.cu):
-// a block is a run of consecutive rows with <= kTile nonzeros and
-// <= kRowMax rows; the whole block's val/col/rowptr are bulk-copied to
-// shared memory.
-constexpr int kTile = 2048;
-constexpr int kRowMax = 512;
+// Geometry of the TMA-staged row-block kernel (kernels.cu): a block is a run
+// of consecutive rows with <= tile nonzeros and <= rowmax rows, split at plan
+// time into `warps` consumer-warp sub-ranges; one producer warp stages whole
+// blocks into a ring of `stages` shared-memory slots with 1-D TMA copies.
+struct BlockCfg {
+    int tile, rowmax, warps, stages, min_ctas;  // min_ctas: __launch_bounds__ occupancy
+};
+constexpr BlockCfg kBlockCfgs[] = {
+    // tile  rowmax warps stages min_ctas   (rowmax = 32 x warps: one row per lane)
+    {2048, 256, 8, 2, 4},   // 0
+    {1024, 128, 4, 2, 8},   // 1
+    {2048, 256, 8, 3, 2},   // 2
+    {1024, 128, 4, 3, 5},   // 3
+    {1024, 256, 8, 2, 5},   // 4
+    {512, 128, 4, 4, 6},    // 5
+};
+constexpr int kNumBlockCfgs = sizeof(kBlockCfgs) / sizeof(kBlockCfgs[0]);
+constexpr int kDefaultBlockCfg = 3;
+constexpr int kTileMax = 2048;     // vector_threshold upper bound (a row fits a block)
 constexpr int kPad = 8;            // device arrays padded (aligned over-read)
+constexpr int kDescInts = 16;      // per-block descriptor: r0 r1 p0 p1 flag wb[0..warps]
 constexpr int kDefaultVectorThreshold = 32;
 
 // ----------------------------------------------------------- host planner
@@ -56,8 +70,8 @@ struct Layout {
     int32_t nrows = 0;                 // matrix rows
     // S group: rows with len <= vthr, in ascending matrix-row order
     int32_t nS = 0, nb = 0;
-    std::vector<int32_t> s_rowptr, s_col, s_blk, s_out, s_slot;
-    std::vector<uint8_t> s_val, s_flag;
+    std::vector<int32_t> s_rowptr, s_col, s_desc, s_out, s_slot;
+    std::vector<uint8_t> s_val;
     bool s_identity = true;            // s_out[i] == i
     bool s_has_slot = false;
     // V group: rows with len > vthr (warp-per-row)
@@ -68,7 +82,8 @@ struct Layout {
 };
 // out_row / slot nullable: identity / no combine.
 void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, const uint8_t* val,
-                  int esize, const int32_t* out_row, const int32_t* slot, int vthr, Layout& L);
+                  int esize, const int32_t* out_row, const int32_t* slot, int vthr,
+                  const BlockCfg& cfg, Layout& L);
 
 // -------------------------------------------------------------- schedules
 struct SchedCheck {

@@ -1,15 +1,19 @@
 // kernels.cu -- the sm_100a kernels of the distributed SpMV hot path.
 //
-//   spmv_block_kernel  y_L / y_R rows with <= vector_threshold nnz: a
-//                      persistent grid walks precomputed row blocks (<= kTile
-//                      nonzeros, <= kRowMax rows).  One elected thread stages
-//                      each block's val/col/rowptr slices into shared memory
-//                      with 1-D TMA bulk copies (cp.async.bulk, L2 evict_first)
-//                      into a 2-stage mbarrier pipeline, so the next block's
-//                      bytes are in flight while this one is computed.  Threads
-//                      then gather x (read-only path), form the products in
-//                      place, and each thread sums its rows sequentially in
-//                      stored order (the same rounding as the oracle's O1 loop).
+//   spmv_block_kernel  y_L / y_R rows with <= vector_threshold nnz.  A
+//                      persistent grid walks plan-time row blocks (<= tile
+//                      nonzeros, <= rowmax rows).  Warp-specialised: one
+//                      producer warp stages each whole block (val, col, rowptr
+//                      slices) into a ring of shared-memory slots with 1-D TMA
+//                      bulk copies (cp.async.bulk, L2 evict_first) signalled on
+//                      per-slot "full" mbarriers, running up to `stages` blocks
+//                      ahead; `warps` consumer warps each own a plan-time
+//                      sub-range of the block's rows: they gather x (read-only
+//                      path) one lane per row -- coalesced for banded rows --
+//                      and sum each row sequentially in stored order with
+//                      products and sums rounded separately (the rounding of
+//                      the oracle's O1 loop), then release the slot on its
+//                      "empty" mbarrier.  No CTA-wide barrier in the loop.
 //   spmv_vector_kernel rows with > vector_threshold nnz: one warp per row,
 //                      unrolled coalesced loads, warp-shuffle reduction.
 //   pack_kernel        sendbuf[k] = x[pack_map[k]]
@@ -32,18 +36,14 @@ std::atomic<uint64_t> g_launches{0};
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kPerThread = kTile / kThreads;      // products per thread per block
-constexpr int kValCap = kTile + kPad;             // aligned over-read slack
-constexpr int kRpCap = kRowMax + kPad;
-constexpr int kStages = 2;
+constexpr int kThreads = 256;   // vector / pack kernels
 
-template <typename T>
+template <typename T, int TILE, int RMAX>
 struct __align__(16) Stage {
-    T val[kValCap];
-    int32_t col[kValCap];
-    int32_t rp[kRpCap];
-    int32_t hdr[4];  // r0, r1, a0 (aligned first nz), ra0 (aligned first row)
+    T val[TILE + kPad];
+    int32_t col[TILE + kPad];
+    int32_t rp[RMAX + kPad];
+    int32_t hdr[kDescInts];  // r0 r1 a0 ra0 flag wb[0..warps]
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -62,6 +62,9 @@ __device__ __forceinline__ void fence_proxy_async() {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
@@ -104,8 +107,7 @@ struct BlockArgs {
     const int32_t* rowptr;
     const int32_t* col;
     const void* val;
-    const int32_t* blk;
-    const uint8_t* flag;
+    const int32_t* desc;
     const int32_t* out;
     const int32_t* slot;
     int32_t nb;
@@ -132,78 +134,102 @@ __device__ __forceinline__ void combine(T acc, int32_t k, int32_t orow, const Sp
     }
 }
 
-// Thread 0: stage block b into `st`, arming `bar` with the byte count.
-template <typename T>
-__device__ __forceinline__ void issue_block(const BlockArgs& a, Stage<T>& st, uint64_t* bar, int b,
-                                            uint64_t pol) {
-    const int32_t r0 = a.blk[b], r1 = a.blk[b + 1];
-    const int32_t p0 = a.rowptr[r0], p1 = a.rowptr[r1];
-    const int32_t a0 = p0 & ~3, a1 = (p1 + 3) & ~3;
-    const int32_t ra0 = r0 & ~3, ra1 = (r1 + 1 + 3) & ~3;
-    st.hdr[0] = r0;
-    st.hdr[1] = r1;
-    st.hdr[2] = a0;
-    st.hdr[3] = ra0;
-    const uint32_t nz = uint32_t(a1 - a0);
-    const uint32_t bv = nz * sizeof(T), bc = nz * 4u, br = uint32_t(ra1 - ra0) * 4u;
-    fence_proxy_async();  // generic smem accesses of the last use -> async-proxy writes
-    mbar_arrive_expect_tx(bar, bv + bc + br);
-    if (nz) {
-        bulk_g2s(st.val, static_cast<const T*>(a.val) + a0, bv, bar, pol);
-        bulk_g2s(st.col, a.col + a0, bc, bar, pol);
+template <int CFG>
+struct Cfg {
+    static constexpr int kTile = kBlockCfgs[CFG].tile;
+    static constexpr int kRowMax = kBlockCfgs[CFG].rowmax;
+    static constexpr int kWarps = kBlockCfgs[CFG].warps;
+    static constexpr int kStages = kBlockCfgs[CFG].stages;
+    static constexpr int kThreadsPerCta = (kWarps + 1) * 32;
+    template <typename T>
+    static constexpr int smem_bytes() {
+        return kStages * int(sizeof(Stage<T, kTile, kRowMax>)) + 2 * kStages * 8;
     }
-    bulk_g2s(st.rp, a.rowptr + ra0, br, bar, pol);
-}
+};
 
-template <typename T, bool kCombine, bool kIdentity>
-__global__ void __launch_bounds__(kThreads) spmv_block_kernel(BlockArgs a, SpmvOperands o) {
+template <typename T, int CFG, bool kCombine, bool kIdentity>
+__global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_ctas)
+    spmv_block_kernel(BlockArgs a, SpmvOperands o) {
+    using C = Cfg<CFG>;
+    using St = Stage<T, C::kTile, C::kRowMax>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    Stage<T>* st = reinterpret_cast<Stage<T>*>(smem_raw);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + kStages * sizeof(Stage<T>));
-    const int tid = threadIdx.x;
-    const T* __restrict__ x = static_cast<const T*>(o.x);
-    T* __restrict__ y = static_cast<T*>(o.y);
+    St* st = reinterpret_cast<St*>(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::kStages * sizeof(St));
+    uint64_t* empty = full + C::kStages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    uint64_t pol = 0;
-    if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < C::kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], C::kWarps);
+        }
         fence_mbar_init();
-        pol = policy_evict_first();
-        if (int(blockIdx.x) < a.nb) issue_block<T>(a, st[0], &bar[0], blockIdx.x, pol);
     }
     __syncthreads();
 
+    if (warp == C::kWarps) {
+        // ------------------------------------------------ producer warp
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            int it = 0;
+            for (int b = blockIdx.x; b < a.nb; b += gridDim.x, ++it) {
+                const int s = it % C::kStages;
+                const int u = it / C::kStages;
+                if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+                const int4* d = reinterpret_cast<const int4*>(a.desc + size_t(b) * kDescInts);
+                const int4 d0 = __ldg(d), d1 = __ldg(d + 1), d2 = __ldg(d + 2), d3 = __ldg(d + 3);
+                const int32_t r0 = d0.x, r1 = d0.y, p0 = d0.z, p1 = d0.w;
+                const int32_t a0 = p0 & ~3, a1 = (p1 + 3) & ~3;
+                const int32_t ra0 = r0 & ~3, ra1 = (r1 + 1 + 3) & ~3;
+                St& S = st[s];
+                // hdr: r0 r1 a0 ra0 flag wb[0..warps] (wb = desc[5..])
+                reinterpret_cast<int4*>(S.hdr)[0] = make_int4(r0, r1, a0, ra0);
+                reinterpret_cast<int4*>(S.hdr)[1] = d1;
+                reinterpret_cast<int4*>(S.hdr)[2] = d2;
+                reinterpret_cast<int4*>(S.hdr)[3] = d3;
+                const uint32_t nz = uint32_t(a1 - a0);
+                const uint32_t bv = nz * sizeof(T), bc = nz * 4u, br = uint32_t(ra1 - ra0) * 4u;
+                fence_proxy_async();
+                mbar_arrive_expect_tx(&full[s], bv + bc + br);
+                if (nz) {
+                    bulk_g2s(S.val, static_cast<const T*>(a.val) + a0, bv, &full[s], pol);
+                    bulk_g2s(S.col, a.col + a0, bc, &full[s], pol);
+                }
+                bulk_g2s(S.rp, a.rowptr + ra0, br, &full[s], pol);
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------------ consumer warps
+    const T* __restrict__ x = static_cast<const T*>(o.x);
+    T* __restrict__ y = static_cast<T*>(o.y);
     int it = 0;
     for (int b = blockIdx.x; b < a.nb; b += gridDim.x, ++it) {
-        const int s = it & 1;
-        const uint32_t parity = (it >> 1) & 1;
-        const int bn = b + gridDim.x;
-        if (tid == 0 && bn < a.nb) issue_block<T>(a, st[s ^ 1], &bar[s ^ 1], bn, pol);
-        mbar_wait(&bar[s], parity);
-        Stage<T>& S = st[s];
-        const int32_t r0 = S.hdr[0], r1 = S.hdr[1], a0 = S.hdr[2], ra0 = S.hdr[3];
-        const int32_t q0 = S.rp[r0 - ra0] - a0, q1 = S.rp[r1 - ra0] - a0;
+        const int s = it % C::kStages;
+        const int u = it / C::kStages;
+        mbar_wait(&full[s], u & 1);
+        St& S = st[s];
+        const int32_t a0 = S.hdr[2], ra0 = S.hdr[3];
+        const bool blk_combine = kCombine && S.hdr[4] != 0;
+        const int32_t w0 = S.hdr[5 + warp], w1 = S.hdr[6 + warp];
 
-        // products in place: val[q] <- val[q] * x[col[q]]
-        T xv[kPerThread];
-#pragma unroll
-        for (int k = 0; k < kPerThread; ++k) {
-            const int q = q0 + tid + k * kThreads;
-            if (q < q1) xv[k] = __ldg(x + S.col[q]);
-        }
-#pragma unroll
-        for (int k = 0; k < kPerThread; ++k) {
-            const int q = q0 + tid + k * kThreads;
-            if (q < q1) S.val[q] = mul_rn(S.val[q], xv[k]);
-        }
-        __syncthreads();
-
-        // row sums in stored order, one thread per row
-        const bool blk_combine = kCombine && a.flag[b] != 0;
-        for (int r = r0 + tid; r < r1; r += kThreads) {
+        // one lane per row: sum_q val[q] * x[col[q]] in stored order, products
+        // and sums rounded separately (= O1).  Lanes walk consecutive rows, so
+        // for banded/stencil rows the x gathers of a warp are coalesced; up to
+        // 8 gathers per lane are in flight per chunk.
+        for (int r = w0 + lane; r < w1; r += 32) {
             const int32_t e0 = S.rp[r - ra0] - a0, e1 = S.rp[r + 1 - ra0] - a0;
             T acc = T(0);
-            for (int q = e0; q < e1; ++q) acc = add_rn(acc, S.val[q]);
+            for (int q = e0; q < e1; q += 8) {
+                T xv[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (q + k < e1) xv[k] = __ldg(x + S.col[q + k]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (q + k < e1) acc = add_rn(acc, mul_rn(S.val[q + k], xv[k]));
+            }
             const int32_t orow = kIdentity ? r : a.out[r];
             if (blk_combine) {
                 const int32_t k = a.slot[r];
@@ -214,7 +240,8 @@ __global__ void __launch_bounds__(kThreads) spmv_block_kernel(BlockArgs a, SpmvO
             }
             __stcs(y + orow, acc);
         }
-        __syncthreads();  // stage s is free for reuse
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
     }
 }
 
@@ -290,40 +317,60 @@ int num_sms() {
     return g_num_sms;
 }
 
-template <typename T, bool C, bool I>
+template <typename T, int CFG, bool C, bool I>
 cudaError_t prep_block_kernel() {
     static bool done[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && done[dev]) return cudaSuccess;
-    const int smem = kStages * sizeof(Stage<T>) + kStages * 8;
-    cudaError_t e = cudaFuncSetAttribute(spmv_block_kernel<T, C, I>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int smem = Cfg<CFG>::template smem_bytes<T>();
+    cudaError_t e = cudaFuncSetAttribute(spmv_block_kernel<T, CFG, C, I>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(spmv_block_kernel<T, C, I>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaFuncSetAttribute(spmv_block_kernel<T, CFG, C, I>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e == cudaSuccess && dev < 64) done[dev] = true;
     return e;
 }
 
-template <typename T, bool C, bool I>
+template <typename T, int CFG, bool C, bool I>
 cudaError_t launch_block(const DevLayout& L, const SpmvOperands& o, cudaStream_t s) {
-    cudaError_t e = prep_block_kernel<T, C, I>();
+    cudaError_t e = prep_block_kernel<T, CFG, C, I>();
     if (e != cudaSuccess) return e;
-    BlockArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_blk, L.s_flag, L.s_out, L.s_slot, L.nb};
-    const int smem = kStages * sizeof(Stage<T>) + kStages * 8;
-    spmv_block_kernel<T, C, I><<<L.grid_s, kThreads, smem, s>>>(a, o);
+    BlockArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_desc, L.s_out, L.s_slot, L.nb};
+    spmv_block_kernel<T, CFG, C, I>
+        <<<L.grid_s, Cfg<CFG>::kThreadsPerCta, Cfg<CFG>::template smem_bytes<T>(), s>>>(a, o);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
 }
+
+template <typename T, int CFG>
+cudaError_t launch_block_cfg(const DevLayout& L, const SpmvOperands& o, cudaStream_t s) {
+    const bool c = L.s_slot != nullptr, id = L.s_out == nullptr;
+    if (c && id) return launch_block<T, CFG, true, true>(L, o, s);
+    if (c) return launch_block<T, CFG, true, false>(L, o, s);
+    if (id) return launch_block<T, CFG, false, true>(L, o, s);
+    return launch_block<T, CFG, false, false>(L, o, s);
+}
+
+template <typename T>
+cudaError_t launch_block_any(const DevLayout& L, const SpmvOperands& o, cudaStream_t s) {
+    switch (L.cfg) {
+        case 0: return launch_block_cfg<T, 0>(L, o, s);
+        case 1: return launch_block_cfg<T, 1>(L, o, s);
+        case 2: return launch_block_cfg<T, 2>(L, o, s);
+        case 3: return launch_block_cfg<T, 3>(L, o, s);
+        case 4: return launch_block_cfg<T, 4>(L, o, s);
+        case 5: return launch_block_cfg<T, 5>(L, o, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+static_assert(kNumBlockCfgs == 6, "update launch_block_any / occupancy dispatch");
 
 template <typename T>
 cudaError_t launch_all(const DevLayout& L, const SpmvOperands& o, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
     if (L.nb > 0) {
-        const bool c = L.s_flag != nullptr, id = L.s_out == nullptr;
-        if (c && id) e = launch_block<T, true, true>(L, o, s);
-        else if (c) e = launch_block<T, true, false>(L, o, s);
-        else if (id) e = launch_block<T, false, true>(L, o, s);
-        else e = launch_block<T, false, false>(L, o, s);
+        e = launch_block_any<T>(L, o, s);
         if (e != cudaSuccess) return e;
     }
     if (L.nV > 0) {
@@ -336,25 +383,32 @@ cudaError_t launch_all(const DevLayout& L, const SpmvOperands& o, cudaStream_t s
     return e;
 }
 
-}  // namespace
-
-int stream_kernel_smem_bytes(int dtype) {
-    return dtype == DSPMV_F32 ? int(kStages * sizeof(Stage<float>) + kStages * 8)
-                              : int(kStages * sizeof(Stage<double>) + kStages * 8);
+template <typename T, int CFG>
+int occupancy() {
+    int n = 0;
+    if (prep_block_kernel<T, CFG, true, false>() != cudaSuccess) return 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_block_kernel<T, CFG, true, false>,
+                                                  Cfg<CFG>::kThreadsPerCta, Cfg<CFG>::template smem_bytes<T>());
+    return n > 0 ? n : 1;
 }
 
-int stream_kernel_ctas_per_sm(int dtype) {
-    int n = 0;
-    if (dtype == DSPMV_F32) {
-        if (prep_block_kernel<float, true, false>() != cudaSuccess) return 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_block_kernel<float, true, false>, kThreads,
-                                                      stream_kernel_smem_bytes(dtype));
-    } else {
-        if (prep_block_kernel<double, true, false>() != cudaSuccess) return 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_block_kernel<double, true, false>, kThreads,
-                                                      stream_kernel_smem_bytes(dtype));
+template <typename T>
+int occupancy_any(int cfg) {
+    switch (cfg) {
+        case 0: return occupancy<T, 0>();
+        case 1: return occupancy<T, 1>();
+        case 2: return occupancy<T, 2>();
+        case 3: return occupancy<T, 3>();
+        case 4: return occupancy<T, 4>();
+        case 5: return occupancy<T, 5>();
+        default: return 1;
     }
-    return n > 0 ? n : 1;
+}
+
+}  // namespace
+
+int block_kernel_ctas_per_sm(int dtype, int cfg) {
+    return dtype == DSPMV_F32 ? occupancy_any<float>(cfg) : occupancy_any<double>(cfg);
 }
 
 int device_sm_count() { return num_sms(); }

@@ -137,7 +137,8 @@ void plan_phase2_from_requests(RankPlan& p, const std::vector<std::vector<int32_
 
 // ---------------------------------------------------------------- layout
 void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, const uint8_t* val,
-                  int esize, const int32_t* out_row, const int32_t* slot, int vthr, Layout& L) {
+                  int esize, const int32_t* out_row, const int32_t* slot, int vthr,
+                  const BlockCfg& cfg, Layout& L) {
     L = Layout();
     L.nrows = nrows;
     std::vector<int32_t> srows, vrows;
@@ -178,23 +179,33 @@ void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, cons
     bool dummy = true;
     gather(srows, L.s_rowptr, L.s_col, L.s_val, L.s_out, L.s_slot, L.s_has_slot, L.s_identity);
     gather(vrows, L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, L.v_has_slot, dummy);
-    // row blocks of the S group: greedy, <= kTile nnz and <= kRowMax rows
-    L.s_blk.clear();
-    L.s_flag.clear();
+    // Row blocks of the S group: greedy, <= tile nnz and <= rowmax (= 32 x
+    // warps) rows.  Each block's descriptor: r0 r1 p0 p1 flag wb[0..warps],
+    // where the consumer-warp boundaries wb split the rows evenly.
+    L.s_desc.clear();
     int32_t r = 0;
+    const int W = cfg.warps;
     while (r < L.nS) {
         const int32_t r0 = r;
         const int32_t p0 = L.s_rowptr[r0];
         bool flag = false;
-        while (r < L.nS && r - r0 < kRowMax && L.s_rowptr[r + 1] - p0 <= kTile) {
+        while (r < L.nS && r - r0 < cfg.rowmax && L.s_rowptr[r + 1] - p0 <= cfg.tile) {
             flag |= L.s_slot[r] >= 0;
             ++r;
         }
-        L.s_blk.push_back(r0);
-        L.s_flag.push_back(flag ? 1 : 0);
+        const int32_t r1 = r, p1 = L.s_rowptr[r1];
+        int32_t d[kDescInts] = {};
+        d[0] = r0;
+        d[1] = r1;
+        d[2] = p0;
+        d[3] = p1;
+        d[4] = flag ? 1 : 0;
+        // consumer warps process one row per lane: split the rows evenly
+        const int32_t rpw = (r1 - r0 + W - 1) / W;
+        for (int w = 0; w <= W; ++w) d[5 + w] = std::min(r1, r0 + w * rpw);
+        L.s_desc.insert(L.s_desc.end(), d, d + kDescInts);
     }
-    L.s_blk.push_back(L.nS);
-    L.nb = int32_t(L.s_flag.size());
+    L.nb = int32_t(L.s_desc.size() / kDescInts);
 }
 
 }  // namespace dspmv

@@ -21,12 +21,12 @@ extern std::atomic<uint64_t> g_launches;
 struct DevLayout {
     int32_t nS = 0, nb = 0, nV = 0;
     int grid_s = 0, grid_v = 0;
+    int cfg = 0;                       // kBlockCfgs index of the row-block kernel
     bool combine = false;              // any row of this matrix needs the ticket combine
     int32_t* s_rowptr = nullptr;
     int32_t* s_col = nullptr;
     void* s_val = nullptr;
-    int32_t* s_blk = nullptr;
-    uint8_t* s_flag = nullptr;         // null when no block combines
+    int32_t* s_desc = nullptr;         // kDescInts per block
     int32_t* s_out = nullptr;          // null when identity
     int32_t* s_slot = nullptr;         // null when no combine
     int32_t* v_rowptr = nullptr;
@@ -46,8 +46,8 @@ struct SpmvOperands {
 };
 
 // kernels.cu
-int stream_kernel_smem_bytes(int dtype);
-int stream_kernel_ctas_per_sm(int dtype);
+int block_kernel_smem_bytes(int dtype, int cfg);
+int block_kernel_ctas_per_sm(int dtype, int cfg);
 cudaError_t launch_spmv(const DevLayout& L, int dtype, const SpmvOperands& o, cudaStream_t s);
 cudaError_t launch_pack(int dtype, const void* x, const int32_t* map, void* out, int64_t n,
                         cudaStream_t s);

@@ -47,7 +47,7 @@ def test_single_rank_stencil_bitwise_vs_o1(name):
 
 
 @pytest.mark.parametrize("name", ["pl20k", "rand300"])
-@pytest.mark.parametrize("vthr", [-1, 0, 2048])
+@pytest.mark.parametrize("vthr", [-1, 0, 1024])
 @pytest.mark.parametrize("P", [1, 2, 3, 8])
 def test_irregular_multi_rank_vs_oracle(name, vthr, P):
     for exact in (False, True):
@@ -85,7 +85,7 @@ def test_row_length_bins():
     x = gen.x_values((0, n))
     yref = O1.o1_spmv(rp, col, val, x)
     s = O1.o1_absdot(rp, col, val, x)
-    for vthr in (-1, 0, 1, 32, 2048):
+    for vthr in (-1, 0, 1, 32, 1024):
         for P in (1, 4):
             run = LocalRun(n, rp, col, val, P, vector_threshold=vthr)
             try:
@@ -268,3 +268,26 @@ def test_full_size_c2_bench_config():
         D.dspmv_schedule_destroy(s)
         D.dspmv_plan_destroy(plan)
         D.dspmv_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("cfg", list(range(6)))
+def test_every_block_cfg(cfg):
+    """Every row-block kernel configuration (tile / consumer warps / stages)
+    on an irregular multi-rank case and a stencil (bitwise vs O1)."""
+    n, (rp, col, val) = _mat("pl20k")
+    x = gen.x_values((0, n))
+    plans = O2.plan_all(rp, col, n, 3)
+    yref = O2.simulate(plans, val, x, [(v,) for v in S.topological_orders(S.EDGES)[0]])
+    run = LocalRun(n, rp, col, val, 3, block_cfg=cfg)
+    try:
+        y = run.apply(run.schedule(derive_ops()), x, reps=2)
+    finally:
+        run.close()
+    assert within_tol(y, yref, O1.o1_absdot(rp, col, val, x), 1e-12)
+    n, (rp, col, val) = _mat("27pt20")
+    run = LocalRun(n, rp, col, val, 1, block_cfg=cfg)
+    try:
+        y = run.apply(run.schedule(derive_ops()), x[:n])
+    finally:
+        run.close()
+    assert np.array_equal(y, O1.o1_spmv(rp, col, val, x[:n]))

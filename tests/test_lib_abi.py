@@ -44,3 +44,31 @@ def test_version_and_error_plumbing():
         assert "partition" in D.dspmv_last_error()
     else:
         raise AssertionError("expected DSPMV_ERR_ARG")
+
+
+def test_binding_marshalling_without_gpu():
+    """Every binding marshals its arguments and reaches the library, which
+    rejects the NULL handles (ERR_ARG) -- exercises the Python side on CPU."""
+    import numpy as np
+    import pytest
+    rp = np.array([0, 1], np.int64)
+    col = np.array([0], np.int32)
+    val = np.array([1.0])
+    calls = [
+        lambda: D.dspmv_plan_create(None, 1, rp, col, val),
+        lambda: D.dspmv_plan_create(None, 1, rp, col, val.astype(np.float32), dtype=D.DSPMV_F32),
+        lambda: D.dspmv_plan_info_get(None),
+        lambda: D.dspmv_plan_destroy(None),
+        lambda: D.dspmv_schedule_create(None, [(0, 0, 0, 0)], 1),
+        lambda: D.dspmv_schedule_destroy(None),
+        lambda: D.dspmv_schedule_set_timing(None, True),
+        lambda: D.dspmv_apply(None, 0, 0),
+        lambda: D.dspmv_apply_host(None, val, val),
+        lambda: D.dspmv_comm_destroy(None),
+        lambda: D.dspmv_comm_info(None),
+        lambda: D.dspmv_host_plan_destroy(None),
+    ]
+    for c in calls:
+        with pytest.raises(D.DspmvError) as e:
+            c()
+        assert e.value.status == D.DSPMV_ERR_ARG
