@@ -173,6 +173,25 @@ dspmv_status dspmv_host_plan_export(dspmv_host_plan_t hp, int rank, int what, vo
                                     size_t bytes, size_t* needed);
 dspmv_status dspmv_host_plan_destroy(dspmv_host_plan_t hp);
 
+/* Host-only, ONE rank: the distributed planning protocol that
+ * dspmv_plan_create runs over NCCL, with the transport left to the caller
+ * (used by the multi-process gloo tests).
+ *   1. dspmv_rank_plan_build_host: split + halo of this rank's rows (same
+ *      arguments as dspmv_plan_create); the handle holds one rank (index 0 in
+ *      dspmv_host_plan_info/export).
+ *   2. dspmv_host_plan_requests: the ascending global ids this rank needs from
+ *      `owner` (its halo segment); send them to `owner`.
+ *   3. dspmv_host_plan_set_requests: lists[r] (counts[r] entries) = what rank
+ *      r requested from this rank; builds send counts/displacements and the
+ *      pack map (R-Q7).  ERR_ARG if an id is not owned by this rank. */
+dspmv_status dspmv_rank_plan_build_host(int nranks, int rank, int64_t n_global, int64_t n_local,
+                                        const int64_t* rowptr, const int32_t* col_global,
+                                        const void* val, int dtype, dspmv_host_plan_t* out);
+dspmv_status dspmv_host_plan_requests(dspmv_host_plan_t hp, int owner, int32_t* dst, size_t cap,
+                                      size_t* count);
+dspmv_status dspmv_host_plan_set_requests(dspmv_host_plan_t hp, const int32_t* const* lists,
+                                          const int32_t* counts);
+
 /* ------------------------------------------------------------ schedules
  * A schedule is a traversal of the program DAG with every GPU
  * vertex bound to a stream (BoundGPU_s, tab:vertices P:250-264) and the
@@ -243,8 +262,10 @@ dspmv_status dspmv_schedule_format(const dspmv_op* ops, int n_ops, char* buf, si
 dspmv_status dspmv_schedule_create(dspmv_plan_t plan, const dspmv_op* ops, int n_ops,
                                    int n_streams, dspmv_schedule_t* out);
 dspmv_status dspmv_schedule_destroy(dspmv_schedule_t sched);
-/* Per-op CUDA-event timing on the op's stream (adds 2 event records per GPU
- * op).  After an apply, ms[i] = device time of ops[i] (0 for non-GPU ops). */
+/* Per-op CUDA-event timing on the op's stream (2 event records per timed
+ * op).  enable: 0 off, 1 every GPU vertex, else a bit mask (1 << op kind) of
+ * the GPU vertex kinds to time.  After an apply, ms[i] = device time of
+ * ops[i] (0 for untimed ops). */
 dspmv_status dspmv_schedule_set_timing(dspmv_schedule_t sched, int enable);
 dspmv_status dspmv_schedule_op_times(dspmv_schedule_t sched, float* ms, int n);
 

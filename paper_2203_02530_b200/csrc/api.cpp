@@ -284,7 +284,8 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
     const bool gpu = is_gpu_vertex(o.kind);
     const bool on_stream = gpu || o.kind == DSPMV_OP_EVENT_RECORD || o.kind == DSPMV_OP_STREAM_WAIT_EVENT;
     cudaStream_t st = on_stream ? p.streams[o.stream] : nullptr;
-    if (gpu && s.timing) CUDA_TRY(cudaEventRecord(s.t0[t], st));
+    const bool timed = gpu && s.timing && s.t0[t];
+    if (timed) CUDA_TRY(cudaEventRecord(s.t0[t], st));
     cudaError_t e = cudaSuccess;
     switch (o.kind) {
         case DSPMV_OP_START:
@@ -341,7 +342,7 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
         return fail(DSPMV_ERR_CUDA, std::string("op ") + std::to_string(t) + " (" + vertex_name(o.kind) +
                                         "): " + cudaGetErrorString(e));
     }
-    if (gpu && s.timing) CUDA_TRY(cudaEventRecord(s.t1[t], st));
+    if (timed) CUDA_TRY(cudaEventRecord(s.t1[t], st));
     return DSPMV_OK;
 }
 
@@ -721,6 +722,52 @@ dspmv_status dspmv_host_plan_export(dspmv_host_plan_t hp, int rank, int what, vo
     return export_array(hp->ranks[rank], what, dst, bytes, needed, true);
 }
 
+dspmv_status dspmv_rank_plan_build_host(int nranks, int rank, int64_t n_global, int64_t n_local,
+                                        const int64_t* rowptr, const int32_t* col_global, const void* val,
+                                        int dtype, dspmv_host_plan_t* out) {
+    if (!out) return fail(DSPMV_ERR_ARG, "null out");
+    if (dtype != DSPMV_F64 && dtype != DSPMV_F32) return fail(DSPMV_ERR_ARG, "bad dtype");
+    auto* hp = new dspmv_host_plan_s();
+    hp->esize = dtype == DSPMV_F32 ? 4 : 8;
+    hp->has_val = val != nullptr;
+    hp->ranks.resize(1);
+    dspmv_status st = plan_phase1(n_global, nranks, rank, n_local, rowptr, col_global, val, hp->esize, hp->ranks[0]);
+    if (st != DSPMV_OK) {
+        delete hp;
+        return st;
+    }
+    *out = hp;
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_host_plan_requests(dspmv_host_plan_t hp, int owner, int32_t* dst, size_t cap, size_t* count) {
+    if (!hp || hp->ranks.size() != 1) return fail(DSPMV_ERR_ARG, "need a one-rank host plan");
+    const RankPlan& h = hp->ranks[0];
+    if (owner < 0 || owner >= h.nranks) return fail(DSPMV_ERR_ARG, "bad owner");
+    const size_t n = size_t(h.recv_count[owner]);
+    if (count) *count = n;
+    if (!dst) return DSPMV_OK;
+    if (cap < n) return fail(DSPMV_ERR_ARG, "destination too small");
+    std::memcpy(dst, h.halo_gid.data() + h.recv_displ[owner], n * 4);
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_host_plan_set_requests(dspmv_host_plan_t hp, const int32_t* const* lists, const int32_t* counts) {
+    if (!hp || hp->ranks.size() != 1 || !counts) return fail(DSPMV_ERR_ARG, "need a one-rank host plan");
+    RankPlan& h = hp->ranks[0];
+    std::vector<std::vector<int32_t>> req(h.nranks);
+    for (int r = 0; r < h.nranks; ++r) {
+        if (counts[r] < 0 || (counts[r] > 0 && (!lists || !lists[r]))) return fail(DSPMV_ERR_ARG, "bad request list");
+        req[r].assign(lists ? lists[r] : nullptr, lists ? lists[r] + counts[r] : nullptr);
+        for (int32_t g : req[r])
+            if (g < h.row_begin || g >= h.row_end)
+                return fail(DSPMV_ERR_ARG, "rank " + std::to_string(r) + " requested id " + std::to_string(g) +
+                                               " not owned by this rank");
+    }
+    plan_phase2_from_requests(h, req);
+    return DSPMV_OK;
+}
+
 dspmv_status dspmv_host_plan_destroy(dspmv_host_plan_t hp) {
     if (!hp) return fail(DSPMV_ERR_ARG, "null host plan");
     delete hp;
@@ -782,8 +829,10 @@ dspmv_status dspmv_schedule_set_timing(dspmv_schedule_t s, int enable) {
     if (s->timing) {
         s->t0.assign(s->ops.size(), nullptr);
         s->t1.assign(s->ops.size(), nullptr);
+        // enable == 1: every GPU vertex; otherwise a bit mask (1 << kind)
+        const unsigned mask = enable == 1 ? ~0u : unsigned(enable);
         for (size_t t = 0; t < s->ops.size(); ++t) {
-            if (!is_gpu_vertex(s->ops[t].kind)) continue;
+            if (!is_gpu_vertex(s->ops[t].kind) || !(mask & (1u << s->ops[t].kind))) continue;
             CUDA_TRY(cudaEventCreate(&s->t0[t]));
             CUDA_TRY(cudaEventCreate(&s->t1[t]));
         }
@@ -879,6 +928,7 @@ dspmv_status dspmv_l2_flush(int dev, dspmv_stream_t stream) {
             g_flush_buf[dev] = nullptr;
             return fail(DSPMV_ERR_OOM, "flush buffer allocation failed");
         }
+        CUDA_TRY(cudaMemset(g_flush_buf[dev], 0, bytes));
         g_flush_bytes[dev] = bytes;
     }
     CUDA_TRY(launch_flush(g_flush_buf[dev], g_flush_bytes[dev], static_cast<cudaStream_t>(stream)));

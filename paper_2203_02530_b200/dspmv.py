@@ -100,6 +100,9 @@ _sig("dspmv_plan_build_host", [_I, _I64, _P, _P, _P, _I, _P])
 _sig("dspmv_host_plan_info", [_P, _I, _P])
 _sig("dspmv_host_plan_export", [_P, _I, _I, _P, ctypes.c_size_t, _P])
 _sig("dspmv_host_plan_destroy", [_P])
+_sig("dspmv_rank_plan_build_host", [_I, _I, _I64, _I64, _P, _P, _P, _I, _P])
+_sig("dspmv_host_plan_requests", [_P, _I, _P, ctypes.c_size_t, _P])
+_sig("dspmv_host_plan_set_requests", [_P, _P, _P])
 _sig("dspmv_schedule_validate", [_P, _I, _I])
 _sig("dspmv_schedule_derive", [_P, _P, _I, _P, _I, _P])
 _sig("dspmv_schedule_parse", [ctypes.c_char_p, _P, _I, _P, _P])
@@ -270,6 +273,37 @@ def dspmv_host_plan_destroy(hp):
     _check(lib.dspmv_host_plan_destroy(hp))
 
 
+def dspmv_rank_plan_build_host(nranks: int, rank: int, n_global: int, rowptr, col, val=None,
+                               dtype=DSPMV_F64):
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    col = np.ascontiguousarray(col, np.int32)
+    vp = None
+    if val is not None:
+        val = np.ascontiguousarray(val, np.float32 if dtype == DSPMV_F32 else np.float64)
+        vp = val.ctypes.data
+    h = _P()
+    _check(lib.dspmv_rank_plan_build_host(nranks, rank, n_global, len(rowptr) - 1, rowptr.ctypes.data,
+                                          col.ctypes.data, vp, dtype, ctypes.byref(h)))
+    h._dtype = dtype
+    return h
+
+
+def dspmv_host_plan_requests(hp, owner: int) -> np.ndarray:
+    n = ctypes.c_size_t()
+    _check(lib.dspmv_host_plan_requests(hp, owner, None, 0, ctypes.byref(n)))
+    out = np.zeros(n.value, np.int32)
+    _check(lib.dspmv_host_plan_requests(hp, owner, out.ctypes.data, n.value, None))
+    return out
+
+
+def dspmv_host_plan_set_requests(hp, lists):
+    lists = [np.ascontiguousarray(l, np.int32) for l in lists]
+    n = len(lists)
+    ptrs = (_P * n)(*[l.ctypes.data if len(l) else None for l in lists])
+    counts = np.array([len(l) for l in lists], np.int32)
+    _check(lib.dspmv_host_plan_set_requests(hp, ptrs, counts.ctypes.data))
+
+
 def dspmv_schedule_validate(ops, n_streams: int):
     a = _ops_array(ops)
     _check(lib.dspmv_schedule_validate(a.ctypes.data, len(a), n_streams))
@@ -312,7 +346,8 @@ def dspmv_schedule_destroy(sched):
     _check(lib.dspmv_schedule_destroy(sched))
 
 
-def dspmv_schedule_set_timing(sched, enable: bool):
+def dspmv_schedule_set_timing(sched, enable):
+    """enable: False/True (every GPU op) or a bit mask of (1 << op kind)."""
     _check(lib.dspmv_schedule_set_timing(sched, int(enable)))
 
 

@@ -1,6 +1,8 @@
 """The library's schedule layer (vector-clock validator, tab:sync derivation,
 S:197 text format) against the oracle's happens-before graph enumerator."""
 import itertools
+
+import numpy as np
 import random
 
 import pytest
@@ -162,3 +164,13 @@ def test_error_cases_of_the_boundary_table():
              "y_L", "y_R", "end"]
     dead = to_lib(S.derive(order, dict.fromkeys(GPUS, 0), S.EDGES_A))
     assert status(dead) == D.DSPMV_ERR_DEADLOCK                 # WaitRecv before PostSend
+
+
+def test_product_enumerator_equals_oracle_enumerator():
+    """The sweep's enumerator (package, library-derived syncs) yields exactly
+    the oracle's brute-force set of 768 canonical schedules."""
+    from paper_2203_02530_b200 import schedules as PS
+    mine = {PS.canonical_key(o) for o in PS.enumerate_derived(2)}
+    ref = {PS.canonical_key(np.array(to_lib(o), np.int32)) for o in S.enumerate_derived(2, S.EDGES)}
+    assert len(mine) == 768 and mine == ref
+    assert len(PS.topological_orders()) == 96
