@@ -271,6 +271,7 @@ dspmv_status begin_apply(Schedule& s, cudaStream_t caller) {
     if (p.poisoned) return fail(DSPMV_ERR_STATE, "plan is poisoned by an earlier error");
     if (!p.ready) return fail(DSPMV_ERR_STATE, "plan not ready (LOCAL group: not every rank has called plan_create)");
     CUDA_TRY(cudaSetDevice(p.device));
+    if (s.step0) CUDA_TRY(cudaEventRecord(s.step0, caller));
     CUDA_TRY(cudaEventRecord(p.ev_start, caller));
     for (int i = 0; i < s.n_streams; ++i) CUDA_TRY(cudaStreamWaitEvent(p.streams[i], p.ev_start, 0));
     p.posted_send = p.posted_recv = p.issued = false;
@@ -801,6 +802,8 @@ dspmv_status dspmv_schedule_create(dspmv_plan_t plan, const dspmv_op* ops, int n
 }
 
 static void destroy_timing(Schedule& s) {
+    if (s.step0) cudaEventDestroy(s.step0), s.step0 = nullptr;
+    if (s.step1) cudaEventDestroy(s.step1), s.step1 = nullptr;
     for (auto e : s.t0)
         if (e) cudaEventDestroy(e);
     for (auto e : s.t1)
@@ -831,6 +834,10 @@ dspmv_status dspmv_schedule_set_timing(dspmv_schedule_t s, int enable) {
         s->t1.assign(s->ops.size(), nullptr);
         // enable == 1: every GPU vertex; otherwise a bit mask (1 << kind)
         const unsigned mask = enable == 1 ? ~0u : unsigned(enable);
+        if (mask & 1u) {  // bit of START: whole apply, START..END on the caller stream
+            CUDA_TRY(cudaEventCreate(&s->step0));
+            CUDA_TRY(cudaEventCreate(&s->step1));
+        }
         for (size_t t = 0; t < s->ops.size(); ++t) {
             if (!is_gpu_vertex(s->ops[t].kind) || !(mask & (1u << s->ops[t].kind))) continue;
             CUDA_TRY(cudaEventCreate(&s->t0[t]));
@@ -847,6 +854,7 @@ dspmv_status dspmv_schedule_op_times(dspmv_schedule_t s, float* ms, int n) {
         ms[t] = 0.f;
         if (s->t0[t]) CUDA_TRY(cudaEventElapsedTime(&ms[t], s->t0[t], s->t1[t]));
     }
+    if (s->step0 && n > 0) CUDA_TRY(cudaEventElapsedTime(&ms[0], s->step0, s->step1));
     return DSPMV_OK;
 }
 
@@ -866,6 +874,7 @@ dspmv_status dspmv_apply(dspmv_schedule_t s, const void* x, void* y, dspmv_strea
             ST_TRY(issue_exchange_local(one));
         }
     }
+    if (s->step1) CUDA_TRY(cudaEventRecord(s->step1, static_cast<cudaStream_t>(stream)));
     s->timed_valid = s->timing;
     return DSPMV_OK;
 }
@@ -909,7 +918,10 @@ dspmv_status dspmv_apply_group(const dspmv_schedule_t* scheds, int nranks, const
         for (int r = 0; r < nranks; ++r) ST_TRY(exec_op(*scheds[r], t, x[r], y[r], true));
         if (plans[0]->posted_send && plans[0]->posted_recv && !plans[0]->issued) ST_TRY(issue_exchange_local(plans));
     }
-    for (int r = 0; r < nranks; ++r) scheds[r]->timed_valid = scheds[r]->timing;
+    for (int r = 0; r < nranks; ++r) {
+        if (scheds[r]->step1) CUDA_TRY(cudaEventRecord(scheds[r]->step1, static_cast<cudaStream_t>(stream)));
+        scheds[r]->timed_valid = scheds[r]->timing;
+    }
     return DSPMV_OK;
 }
 

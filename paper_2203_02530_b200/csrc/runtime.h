@@ -107,6 +107,7 @@ struct Schedule {
     cudaEvent_t ev[DSPMV_MAX_EVENTS] = {};
     bool timing = false;
     std::vector<cudaEvent_t> t0, t1;   // per op (GPU vertices only)
+    cudaEvent_t step0 = nullptr, step1 = nullptr;  // START / END on the caller stream
     bool timed_valid = false;
 };
 

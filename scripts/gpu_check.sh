@@ -7,9 +7,10 @@ mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $OUT/gpu_$TAG.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1; echo "smoke exit $?" >> $OUT/smoke_$TAG.log
 timeout 900 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest exit $?" >> $OUT/pytest_gpu_$TAG.log
-timeout 600 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench exit $?" >> $OUT/bench_$TAG.err
+timeout 900 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench exit $?" >> $OUT/bench_$TAG.err
+timeout 300 python bench.py --impl reference --steps 20 --warmup 2 > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
-    python bench.py --steps 3 --warmup 2 --no-cpu-baseline > $OUT/ncu_launch_$TAG.log 2>&1; echo "ncu1 exit $?" >> $OUT/ncu_launch_$TAG.log
+    python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-sweep > $OUT/ncu_launch_$TAG.log 2>&1; echo "ncu1 exit $?" >> $OUT/ncu_launch_$TAG.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmv_block -s 4 -c 1 \
-    -o $OUT/prof_block_$TAG -f python bench.py --steps 3 --warmup 2 --no-cpu-baseline > $OUT/ncu_full_$TAG.log 2>&1; echo "ncu2 exit $?" >> $OUT/ncu_full_$TAG.log
+    -o $OUT/prof_block_$TAG -f python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-sweep > $OUT/ncu_full_$TAG.log 2>&1; echo "ncu2 exit $?" >> $OUT/ncu_full_$TAG.log
 echo done
