@@ -13,7 +13,7 @@ CXXFLAGS  := -O2 -g -fPIC -std=c++17 -Wall -Wno-unused-function -I$(CUDA_HOME)/i
 
 OBJS := $(BUILD)/kernels.o $(BUILD)/api.o $(BUILD)/planner.o $(BUILD)/schedule.o
 
-all: $(OUT)/libdspmv.so oracle/libo1.so
+all: $(OUT)/libdspmv.so oracle/libo1.so gen/libgenc.so
 
 $(BUILD):
 	mkdir -p $(BUILD) $(OUT)
@@ -30,7 +30,10 @@ $(OUT)/libdspmv.so: $(OBJS)
 oracle/libo1.so: oracle/o1.c
 	gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -o $@ $< -lm
 
+gen/libgenc.so: gen/genc.c
+	gcc -O2 -ffp-contract=off -fPIC -shared -o $@ $< -lm
+
 clean:
-	rm -rf $(BUILD) $(OUT)/libdspmv.so oracle/libo1.so
+	rm -rf $(BUILD) $(OUT)/libdspmv.so oracle/libo1.so gen/libgenc.so
 
 .PHONY: all clean

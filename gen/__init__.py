@@ -147,8 +147,50 @@ def powerlaw_row_lengths(n: int, rows: np.ndarray, seed: int = SEED_MATRIX,
     return np.minimum(np.minimum(L, cap), n).astype(np.int64)
 
 
+_GENC = None
+
+
+def _genc():
+    """The C twin of powerlaw_numpy (gen/genc.c), or None if not built."""
+    global _GENC
+    if _GENC is None:
+        import ctypes
+        import os
+        so = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgenc.so")
+        if not os.path.exists(so):
+            return None
+        lib = ctypes.CDLL(so)
+        P, I64 = ctypes.c_void_p, ctypes.c_int64
+        lib.powerlaw_lengths.argtypes = [I64, I64, I64, ctypes.c_uint64, I64, P]
+        lib.powerlaw_lengths.restype = I64
+        lib.powerlaw_fill.argtypes = [I64, I64, I64, ctypes.c_uint64, ctypes.c_int, P, P, P]
+        lib.powerlaw_fill.restype = ctypes.c_int
+        _GENC = lib
+    return _GENC
+
+
 def powerlaw(n: int, row_range=None, seed: int = SEED_MATRIX, exact: bool = False,
-             dtype=np.float64, cap: int = POWERLAW_CAP, chunk: int = 1 << 18):
+             dtype=np.float64, cap: int = POWERLAW_CAP):
+    """Rows ``row_range`` of the G2 power-law matrix (module docstring); uses
+    the C twin when built (identical output, tests/test_gen.py)."""
+    lib = _genc()
+    if lib is None:
+        return powerlaw_numpy(n, row_range, seed, exact, dtype, cap)
+    lo, hi = (0, n) if row_range is None else row_range
+    lens = np.empty(hi - lo, np.int64)
+    tot = lib.powerlaw_lengths(n, lo, hi, seed, cap, lens.ctypes.data) if hi > lo else 0
+    rowptr = np.zeros(hi - lo + 1, np.int64)
+    np.cumsum(lens, out=rowptr[1:])
+    col = np.empty(tot, np.int32)
+    val = np.empty(tot, np.float64)
+    if hi > lo and lib.powerlaw_fill(n, lo, hi, seed, int(exact), rowptr.ctypes.data,
+                                     col.ctypes.data, val.ctypes.data) != 0:
+        raise MemoryError("powerlaw_fill")
+    return rowptr, col, val.astype(dtype, copy=False)
+
+
+def powerlaw_numpy(n: int, row_range=None, seed: int = SEED_MATRIX, exact: bool = False,
+                   dtype=np.float64, cap: int = POWERLAW_CAP, chunk: int = 1 << 18):
     """Rows ``row_range`` of the G2 power-law matrix (see module docstring).
 
     Candidate slots s = 0, 1, 2, ... of row i are drawn from the counter RNG

@@ -270,6 +270,10 @@ dspmv_status dspmv_schedule_destroy(dspmv_schedule_t sched);
  * START bit, ms[0] = END - START on the caller stream (the whole apply). */
 dspmv_status dspmv_schedule_set_timing(dspmv_schedule_t sched, int enable);
 dspmv_status dspmv_schedule_op_times(dspmv_schedule_t sched, float* ms, int n);
+/* Per-op timeline of the last apply (needs timing with the START bit):
+ * begin_ms[i] / end_ms[i] = start / end of timed op i relative to START on
+ * the caller stream (-1 for untimed ops); index 0 holds [0, END]. */
+dspmv_status dspmv_schedule_op_timeline(dspmv_schedule_t sched, float* begin_ms, float* end_ms, int n);
 
 /* ----------------------------------------------------------------- apply
  * COLLECTIVE for NCCL comms (every rank executes the same P).

@@ -118,6 +118,9 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
 
 // Phase 2 on the device side: pack map + send buffer.
 dspmv_status finalize_send(Plan& p) {
+    p.has_peers = false;
+    for (int q = 0; q < p.host.nranks; ++q)
+        p.has_peers |= (p.host.recv_count[q] > 0 || p.host.send_count[q] > 0);
     const size_t s = p.host.pack_map.size();
     ST_TRY(dev_upload(p, &p.d_pack_map, p.host.pack_map.data(), s));
     ST_TRY(dev_alloc(p, &p.d_sendbuf, s * p.esize, true));
@@ -198,6 +201,7 @@ dspmv_status exchange_requests_nccl(Plan& p) {
 
 // ------------------------------------------------------------- executor
 dspmv_status wait_exchange(Plan& p) {
+    if (!p.has_peers) return DSPMV_OK;  // nothing was sent or received
     if (p.comm->kind == DSPMV_COMM_LOCAL || p.host.nranks == 1) {
         CUDA_TRY(cudaEventSynchronize(p.ev_x));
         return DSPMV_OK;
@@ -226,9 +230,11 @@ dspmv_status wait_exchange(Plan& p) {
 dspmv_status issue_exchange_nccl(Plan& p) {
     const RankPlan& h = p.host;
     const int P = h.nranks;
-    bool any = false;
-    for (int q = 0; q < P; ++q) any |= (h.recv_count[q] > 0 || h.send_count[q] > 0);
-    if (any) {
+    if (!p.has_peers) {
+        p.issued = true;
+        return DSPMV_OK;
+    }
+    {
         const ncclDataType_t ty = nccl_type(p.dtype);
         char* rb = static_cast<char*>(p.d_recvbuf);
         char* sb = static_cast<char*>(p.d_sendbuf);
@@ -260,7 +266,7 @@ dspmv_status issue_exchange_local(const std::vector<Plan*>& ps) {
                                      static_cast<const char*>(src->d_sendbuf) + off_src, size_t(c) * pr->esize,
                                      cudaMemcpyDeviceToDevice, pr->comm_stream));
         }
-        CUDA_TRY(cudaEventRecord(pr->ev_x, pr->comm_stream));
+        if (pr->has_peers) CUDA_TRY(cudaEventRecord(pr->ev_x, pr->comm_stream));
         pr->issued = true;
     }
     return DSPMV_OK;
@@ -270,7 +276,8 @@ dspmv_status begin_apply(Schedule& s, cudaStream_t caller) {
     Plan& p = *s.plan;
     if (p.poisoned) return fail(DSPMV_ERR_STATE, "plan is poisoned by an earlier error");
     if (!p.ready) return fail(DSPMV_ERR_STATE, "plan not ready (LOCAL group: not every rank has called plan_create)");
-    CUDA_TRY(cudaSetDevice(p.device));
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != p.device) CUDA_TRY(cudaSetDevice(p.device));
     if (s.step0) CUDA_TRY(cudaEventRecord(s.step0, caller));
     CUDA_TRY(cudaEventRecord(p.ev_start, caller));
     for (int i = 0; i < s.n_streams; ++i) CUDA_TRY(cudaStreamWaitEvent(p.streams[i], p.ev_start, 0));
@@ -855,6 +862,24 @@ dspmv_status dspmv_schedule_op_times(dspmv_schedule_t s, float* ms, int n) {
         if (s->t0[t]) CUDA_TRY(cudaEventElapsedTime(&ms[t], s->t0[t], s->t1[t]));
     }
     if (s->step0 && n > 0) CUDA_TRY(cudaEventElapsedTime(&ms[0], s->step0, s->step1));
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_schedule_op_timeline(dspmv_schedule_t s, float* begin_ms, float* end_ms, int n) {
+    if (!s || !begin_ms || !end_ms) return fail(DSPMV_ERR_ARG, "null argument");
+    if (!s->timing || !s->timed_valid || !s->step0)
+        return fail(DSPMV_ERR_STATE, "timeline needs timing with the START bit and an apply");
+    for (int t = 0; t < n && t < int(s->ops.size()); ++t) {
+        begin_ms[t] = end_ms[t] = -1.f;
+        if (s->t0[t]) {
+            CUDA_TRY(cudaEventElapsedTime(&begin_ms[t], s->step0, s->t0[t]));
+            CUDA_TRY(cudaEventElapsedTime(&end_ms[t], s->step0, s->t1[t]));
+        }
+    }
+    if (n > 0) {
+        begin_ms[0] = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&end_ms[0], s->step0, s->step1));
+    }
     return DSPMV_OK;
 }
 

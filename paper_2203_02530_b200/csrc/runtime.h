@@ -94,6 +94,7 @@ struct Plan {
     std::vector<void*> allocs;
     int64_t device_bytes = 0;
     bool ready = false;                // phase 2 done (send lists, pack map)
+    bool has_peers = false;            // anything to send or receive
     bool poisoned = false;
     int live_scheds = 0;
     // per-apply exchange state

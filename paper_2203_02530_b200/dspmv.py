@@ -111,6 +111,7 @@ _sig("dspmv_schedule_create", [_P, _P, _I, _I, _P])
 _sig("dspmv_schedule_destroy", [_P])
 _sig("dspmv_schedule_set_timing", [_P, _I])
 _sig("dspmv_schedule_op_times", [_P, _P, _I])
+_sig("dspmv_schedule_op_timeline", [_P, _P, _P, _I])
 _sig("dspmv_apply", [_P, _P, _P, _P])
 _sig("dspmv_apply_host", [_P, _P, _P, _P])
 _sig("dspmv_apply_group", [_P, _I, _P, _P, _P])
@@ -356,6 +357,15 @@ def dspmv_schedule_op_times(sched, n: int | None = None) -> np.ndarray:
     out = np.zeros(n, np.float32)
     _check(lib.dspmv_schedule_op_times(sched, out.ctypes.data, n))
     return out
+
+
+def dspmv_schedule_op_timeline(sched, n: int | None = None):
+    """(begin_ms, end_ms) per op relative to START on the caller stream."""
+    n = getattr(sched, "_n_ops", 0) if n is None else n
+    b = np.zeros(n, np.float32)
+    e = np.zeros(n, np.float32)
+    _check(lib.dspmv_schedule_op_timeline(sched, b.ctypes.data, e.ctypes.data, n))
+    return b, e
 
 
 def dspmv_apply(sched, x, y, stream=None):
