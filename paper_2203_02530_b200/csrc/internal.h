@@ -36,7 +36,9 @@ constexpr int kDefaultBlockCfg = 3;
 constexpr int kTileMax = 2048;     // vector_threshold upper bound (a row fits a block)
 constexpr int kPad = 8;            // device arrays padded (aligned over-read)
 constexpr int kDescInts = 16;      // per-block descriptor: r0 r1 p0 p1 flag wb[0..warps]
-constexpr int kDefaultVectorThreshold = 32;
+constexpr int kDefaultVectorThreshold = 256;  // rows above: warp-per-row kernel
+constexpr int kMaxClass = 5;       // row classes: 2^c lanes per row, c = 0..5
+constexpr int kBinWindow = 4096;   // rows are binned by class within such windows
 
 // ----------------------------------------------------------- host planner
 // One rank's split of its rows (a1): A_L, A_R, halo, pack map.

@@ -147,6 +147,52 @@ struct Cfg {
     }
 };
 
+// One consumer warp's rows [w0, w1) of a staged block, L lanes per row
+// (L = 1: one lane per row, products and sums rounded separately in stored
+// order = the oracle's O1 loop, bitwise; L > 1: each lane sums every L-th
+// entry, then a shuffle tree over the L lanes -- tolerance, R-Q10).  Lanes
+// of consecutive rows read consecutive columns for banded rows, so the x
+// gathers coalesce; up to 8 gathers per lane are in flight per chunk.
+template <typename T, bool kIdentity, bool kOneLane, typename St>
+__device__ __forceinline__ void block_rows(const St& S, int lgL_rt, int w0, int w1, int a0, int ra0,
+                                           bool blk_combine, int lane, const T* __restrict__ x,
+                                           T* __restrict__ y, const int32_t* __restrict__ out,
+                                           const int32_t* __restrict__ slot, SpmvOperands o) {
+    const int lgL = kOneLane ? 0 : lgL_rt;
+    const int L = 1 << lgL;           // lanes per row (warp-uniform)
+    const int G = 32 >> lgL;          // rows per warp pass
+    const int sub = lane & (L - 1), grp = lane >> lgL;
+    for (int rb = w0; rb < w1; rb += G) {
+        const int r = rb + grp;
+        const bool valid = r < w1;
+        T acc = T(0);
+        if (valid) {
+            const int32_t e0 = S.rp[r - ra0] - a0, e1 = S.rp[r + 1 - ra0] - a0;
+            for (int q = e0 + sub; q < e1; q += 8 * L) {
+                T xv[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (q + k * L < e1) xv[k] = __ldg(x + S.col[q + k * L]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (q + k * L < e1) acc = add_rn(acc, mul_rn(S.val[q + k * L], xv[k]));
+            }
+        }
+        for (int off = L >> 1; off > 0; off >>= 1) acc = add_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+        if (valid && sub == 0) {
+            const int32_t orow = kIdentity ? r : out[r];
+            if (blk_combine) {
+                const int32_t k = slot[r];
+                if (k >= 0) {
+                    combine<T>(acc, k, orow, o);
+                    continue;
+                }
+            }
+            __stcs(y + orow, acc);
+        }
+    }
+}
+
 template <typename T, int CFG, bool kCombine, bool kIdentity>
 __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_ctas)
     spmv_block_kernel(BlockArgs a, SpmvOperands o) {
@@ -204,6 +250,8 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
     // ------------------------------------------------------ consumer warps
     const T* __restrict__ x = static_cast<const T*>(o.x);
     T* __restrict__ y = static_cast<T*>(o.y);
+    const int32_t* __restrict__ out = a.out;
+    const int32_t* __restrict__ slot = a.slot;
     int it = 0;
     for (int b = blockIdx.x; b < a.nb; b += gridDim.x, ++it) {
         const int s = it % C::kStages;
@@ -211,35 +259,12 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
         mbar_wait(&full[s], u & 1);
         St& S = st[s];
         const int32_t a0 = S.hdr[2], ra0 = S.hdr[3];
-        const bool blk_combine = kCombine && S.hdr[4] != 0;
+        const bool blk_combine = kCombine && (S.hdr[4] & 1) != 0;
         const int32_t w0 = S.hdr[5 + warp], w1 = S.hdr[6 + warp];
 
-        // one lane per row: sum_q val[q] * x[col[q]] in stored order, products
-        // and sums rounded separately (= O1).  Lanes walk consecutive rows, so
-        // for banded/stencil rows the x gathers of a warp are coalesced; up to
-        // 8 gathers per lane are in flight per chunk.
-        for (int r = w0 + lane; r < w1; r += 32) {
-            const int32_t e0 = S.rp[r - ra0] - a0, e1 = S.rp[r + 1 - ra0] - a0;
-            T acc = T(0);
-            for (int q = e0; q < e1; q += 8) {
-                T xv[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    if (q + k < e1) xv[k] = __ldg(x + S.col[q + k]);
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    if (q + k < e1) acc = add_rn(acc, mul_rn(S.val[q + k], xv[k]));
-            }
-            const int32_t orow = kIdentity ? r : a.out[r];
-            if (blk_combine) {
-                const int32_t k = a.slot[r];
-                if (k >= 0) {
-                    combine<T>(acc, k, orow, o);
-                    continue;
-                }
-            }
-            __stcs(y + orow, acc);
-        }
+        const int lgL = S.hdr[4] >> 8;
+        if (lgL == 0) block_rows<T, kIdentity, true>(S, 0, w0, w1, a0, ra0, blk_combine, lane, x, y, out, slot, o);
+        else block_rows<T, kIdentity, false>(S, lgL, w0, w1, a0, ra0, blk_combine, lane, x, y, out, slot, o);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     }

@@ -146,6 +146,29 @@ void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, cons
     for (int32_t i = 0; i < nrows; ++i) {
         if (rowptr[i + 1] - rowptr[i] > vthr) vrows.push_back(i); else srows.push_back(i);
     }
+    // Row-length binning (north_star: sub-warp-per-row chosen by row length):
+    // class c = log2(lanes per row), the smallest c with len <= 8 * 2^c.  Within
+    // windows of kBinWindow S rows the rows are stable-partitioned by class, so
+    // a block never mixes classes and y writes stay local to the window.
+    auto row_class = [&](int32_t i) {
+        const int32_t len = rowptr[i + 1] - rowptr[i];
+        int c = 0;
+        while (c < kMaxClass && len > (8 << c)) ++c;
+        return c;
+    };
+    {
+        std::vector<int32_t> sorted;
+        sorted.reserve(srows.size());
+        for (size_t w0 = 0; w0 < srows.size(); w0 += kBinWindow) {
+            const size_t w1 = std::min(srows.size(), w0 + kBinWindow);
+            for (int c = 0; c <= kMaxClass; ++c)
+                for (size_t k = w0; k < w1; ++k)
+                    if (row_class(srows[k]) == c) sorted.push_back(srows[k]);
+        }
+        srows.swap(sorted);
+    }
+    std::vector<uint8_t> scls(srows.size());
+    for (size_t k = 0; k < srows.size(); ++k) scls[k] = uint8_t(row_class(srows[k]));
     L.nS = int32_t(srows.size());
     L.nV = int32_t(vrows.size());
     auto gather = [&](const std::vector<int32_t>& rows, std::vector<int32_t>& rp,
@@ -179,17 +202,20 @@ void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, cons
     bool dummy = true;
     gather(srows, L.s_rowptr, L.s_col, L.s_val, L.s_out, L.s_slot, L.s_has_slot, L.s_identity);
     gather(vrows, L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, L.v_has_slot, dummy);
-    // Row blocks of the S group: greedy, <= tile nnz and <= rowmax (= 32 x
-    // warps) rows.  Each block's descriptor: r0 r1 p0 p1 flag wb[0..warps],
-    // where the consumer-warp boundaries wb split the rows evenly.
+    // Row blocks of the S group: greedy runs of one class c with <= tile nnz
+    // and <= rowmax >> c rows (each consumer warp then handles 32 >> c rows,
+    // 2^c lanes per row, in one pass).  Descriptor: r0 r1 p0 p1
+    // (flag | c << 8) wb[0..warps]; wb split the rows evenly over the warps.
     L.s_desc.clear();
     int32_t r = 0;
     const int W = cfg.warps;
     while (r < L.nS) {
         const int32_t r0 = r;
         const int32_t p0 = L.s_rowptr[r0];
+        const int c = scls[r0];
+        const int32_t rowmax = std::max(1, cfg.rowmax >> c);
         bool flag = false;
-        while (r < L.nS && r - r0 < cfg.rowmax && L.s_rowptr[r + 1] - p0 <= cfg.tile) {
+        while (r < L.nS && scls[r] == c && r - r0 < rowmax && L.s_rowptr[r + 1] - p0 <= cfg.tile) {
             flag |= L.s_slot[r] >= 0;
             ++r;
         }
@@ -199,7 +225,7 @@ void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, cons
         d[1] = r1;
         d[2] = p0;
         d[3] = p1;
-        d[4] = flag ? 1 : 0;
+        d[4] = (flag ? 1 : 0) | (c << 8);
         // consumer warps process one row per lane: split the rows evenly
         const int32_t rpw = (r1 - r0 + W - 1) / W;
         for (int w = 0; w <= W; ++w) d[5 + w] = std::min(r1, r0 + w * rpw);
