@@ -99,12 +99,14 @@ dspmv_status dspmv_partition(int64_t n_global, int nranks, int64_t* row_begin);
 typedef struct {
     int32_t dtype;             /* DSPMV_F64 (default) | DSPMV_F32                        */
     int32_t vector_threshold;  /* rows with more nnz than this use the warp-per-row
-                                  kernel; the rest the TMA-staged row-block kernel.
-                                  -1 = default (32); valid 0..tile of block_cfg        */
+                                  kernel; the rest the TMA-staged row-block kernel
+                                  (2^c lanes per row, c by row length).
+                                  -1 = default (256); valid 0..1024                     */
     int32_t keep_host;         /* 1: keep host copies of A_L/A_R for dspmv_plan_export  */
     int32_t comm_priority;     /* 1 (default): comm + stream 0 at the highest priority   */
     int32_t block_cfg;         /* row-block kernel configuration (tile nnz / consumer
-                                  warps / TMA stages), -1 = default; K1    */
+                                  warps / TMA stages), -1 = chosen per matrix from its
+                                  row lengths; K1                         */
     int32_t reserved[3];
 } dspmv_plan_opts;
 

@@ -481,12 +481,11 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
     if (opts_in) opts = *opts_in;
     if (opts.dtype != DSPMV_F64 && opts.dtype != DSPMV_F32) return fail(DSPMV_ERR_ARG, "bad dtype");
     int vthr = opts.vector_threshold < 0 ? kDefaultVectorThreshold : opts.vector_threshold;
-    int cfg = opts.block_cfg < 0 ? kDefaultBlockCfg : opts.block_cfg;
+    int cfg = opts.block_cfg;  // -1: chosen per layout (auto_block_cfg)
     if (const char* ev = std::getenv("DSPMV_BLOCK_CFG")) cfg = std::atoi(ev);  // tuning sweeps
-    if (cfg < 0 || cfg >= kNumBlockCfgs) return fail(DSPMV_ERR_ARG, "block_cfg out of range");
-    if (vthr > kBlockCfgs[cfg].tile)
-        return fail(DSPMV_ERR_ARG, "vector_threshold > tile of block_cfg (" +
-                                       std::to_string(kBlockCfgs[cfg].tile) + ")");
+    if (cfg < -1 || cfg >= kNumBlockCfgs) return fail(DSPMV_ERR_ARG, "block_cfg out of range");
+    if (vthr > (cfg < 0 ? kTileMin : kBlockCfgs[cfg].tile))
+        return fail(DSPMV_ERR_ARG, "vector_threshold > tile of block_cfg");
     if (n_local > 0 && !val) return fail(DSPMV_ERR_ARG, "null val");
     if (comm->kind == DSPMV_COMM_LOCAL && comm->group->plans[comm->rank])
         return fail(DSPMV_ERR_STATE, "this LOCAL rank already has a plan");
@@ -535,17 +534,19 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
     }
     {
         Layout L;
+        const int c = cfg >= 0 ? cfg : auto_block_cfg(h.al_rowptr.data(), int32_t(h.n_local()), vthr);
         build_layout(h.al_rowptr.data(), int32_t(h.n_local()), h.al_col.data(), h.al_val.data(), p->esize, nullptr,
-                     nR > 0 ? slotL.data() : nullptr, vthr, kBlockCfgs[cfg], L);
-        if ((st = upload_layout(*p, L, cfg, p->L)) != DSPMV_OK) return bail(st);
+                     nR > 0 ? slotL.data() : nullptr, vthr, kBlockCfgs[c], L);
+        if ((st = upload_layout(*p, L, c, p->L)) != DSPMV_OK) return bail(st);
     }
     {
         std::vector<int32_t> slotR(nR);
         for (int32_t k = 0; k < nR; ++k) slotR[k] = k;
         Layout R;
+        const int c = cfg >= 0 ? cfg : auto_block_cfg(h.ar_rowptr.data(), nR, vthr);
         build_layout(h.ar_rowptr.data(), nR, h.ar_col.data(), h.ar_val.data(), p->esize, h.ar_rows.data(),
-                     slotR.data(), vthr, kBlockCfgs[cfg], R);
-        if ((st = upload_layout(*p, R, cfg, p->R)) != DSPMV_OK) return bail(st);
+                     slotR.data(), vthr, kBlockCfgs[c], R);
+        if ((st = upload_layout(*p, R, c, p->R)) != DSPMV_OK) return bail(st);
     }
     const size_t hsz = h.halo_gid.size();
     if ((st = dev_alloc(*p, &p->d_recvbuf, hsz * p->esize, true)) != DSPMV_OK) return bail(st);

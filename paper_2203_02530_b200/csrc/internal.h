@@ -32,7 +32,9 @@ constexpr BlockCfg kBlockCfgs[] = {
     {512, 128, 4, 4, 6},    // 5
 };
 constexpr int kNumBlockCfgs = sizeof(kBlockCfgs) / sizeof(kBlockCfgs[0]);
-constexpr int kDefaultBlockCfg = 3;
+constexpr int kDefaultBlockCfg = 3;   // short rows (one lane per row)
+constexpr int kLongRowBlockCfg = 0;   // long, uniform rows (more consumer warps)
+constexpr int kTileMin = 1024;        // smallest tile among the auto-chosen configs
 constexpr int kTileMax = 2048;     // vector_threshold upper bound (a row fits a block)
 constexpr int kPad = 8;            // device arrays padded (aligned over-read)
 constexpr int kDescInts = 16;      // per-block descriptor: r0 r1 p0 p1 flag wb[0..warps]
@@ -83,6 +85,10 @@ struct Layout {
     bool v_has_slot = false;
 };
 // out_row / slot nullable: identity / no combine.
+// Plan-time choice of the row-block configuration for one matrix: measured
+// on B200 (K1 table), one-lane-per-row matrices (7-pt stencils,
+// power-law) run best with cfg 3, long uniform rows (27-pt) with cfg 0.
+int auto_block_cfg(const int32_t* rowptr, int32_t nrows, int vthr);
 void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, const uint8_t* val,
                   int esize, const int32_t* out_row, const int32_t* slot, int vthr,
                   const BlockCfg& cfg, Layout& L);

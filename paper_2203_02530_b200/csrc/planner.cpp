@@ -136,6 +136,20 @@ void plan_phase2_from_requests(RankPlan& p, const std::vector<std::vector<int32_
 }
 
 // ---------------------------------------------------------------- layout
+int auto_block_cfg(const int32_t* rowptr, int32_t nrows, int vthr) {
+    int64_t nnz = 0, nnz_short = 0, rows = 0;
+    for (int32_t i = 0; i < nrows; ++i) {
+        const int32_t len = rowptr[i + 1] - rowptr[i];
+        if (len > vthr) continue;
+        nnz += len;
+        ++rows;
+        if (len <= 8) nnz_short += len;
+    }
+    if (rows == 0) return kDefaultBlockCfg;
+    const double avg = double(nnz) / double(rows);
+    return (2 * nnz_short < nnz && avg >= 20.0) ? kLongRowBlockCfg : kDefaultBlockCfg;
+}
+
 void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, const uint8_t* val,
                   int esize, const int32_t* out_row, const int32_t* slot, int vthr,
                   const BlockCfg& cfg, Layout& L) {
