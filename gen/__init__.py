@@ -278,6 +278,48 @@ def powerlaw_numpy(n: int, row_range=None, seed: int = SEED_MATRIX, exact: bool 
     return rowptr, col, val
 
 
+# ------------------------------------------------------ paper replica (G3)
+def banded(n: int = 150000, nnz: int = 1500000, half_bw: int | None = None,
+           seed: int = SEED_MATRIX, exact: bool = False, dtype=np.float64):
+    """The paper's input: band-diagonal n x n, `nnz` distinct cells
+    uniform within the band |i - j| <= half_bw (reading R-Q20: "bandwidth
+    150000/4" = half-bandwidth n/4), values U[-1,1) (exact: [-8,8] minus 0).
+    Global generation (the whole matrix is small); slice rows per rank."""
+    b = n // 4 if half_bw is None else half_bw
+    cells = []
+    have = 0
+    draw = 0
+    seen = set()
+    while have < nnz:
+        m = int((nnz - have) * 1.2) + 1024
+        k = np.arange(draw, draw + m, dtype=np.uint64)
+        draw += m
+        i = (u01(counter_u64(seed, 8, k)) * n).astype(np.int64)
+        d = (u01(counter_u64(seed, 9, k)) * (2 * b + 1)).astype(np.int64) - b
+        j = i + d
+        ok = (j >= 0) & (j < n)
+        key = (i * n + j)[ok]
+        _, first = np.unique(key, return_index=True)
+        for kk in key[np.sort(first)]:
+            if kk not in seen:
+                seen.add(int(kk))
+                cells.append(int(kk))
+                have += 1
+                if have == nnz:
+                    break
+    cells = np.sort(np.array(cells, np.int64))
+    rows, cols = cells // n, cells % n
+    rowptr = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=rowptr[1:])
+    vb = counter_u64(seed, 10, cells.astype(np.uint64))
+    if exact:
+        t = (vb % np.uint64(16)).astype(np.int64)
+        vals = np.where(t < 8, t - 8, t - 7).astype(np.float64)
+    else:
+        vals = 2.0 * u01(vb) - 1.0
+    return rowptr, cols.astype(np.int32), vals.astype(dtype)
+
+
 # -------------------------------------------------------------- small randoms
 def random_csr(n: int, density: float, seed: int, exact: bool = True,
                ncols: int | None = None, dtype=np.float64, empty_rows=(), dense_rows=()):

@@ -1,0 +1,210 @@
+"""Design-rule generation from measured schedules (NEXT-2; §IV,
+P:475-628) -- CPU-side analysis of the sweep / MCTS dataset.
+
+* ``class_labels``  sort, convolve with a step kernel of radius r = 0.5 % of
+  the measurements (min 1), find peaks, keep peaks whose prominence is >= the
+  98th percentile (reading R-N2: percentile of the convolution signal, so
+  measurement-noise peaks are screened), use them as class boundaries
+  (P:483-512).  The paper's
+  kernel indices are inconsistent (k on -r..r-1, sum over -r+1..r); reading
+  R-N1: the balanced kernel k_m = -1 for m in [-r+1, 0], +1 for m in [1, r],
+  evaluated where it fully overlaps (r < i < len - r).  A peak at sorted
+  position i puts the boundary between positions i and i+1.
+* ``features``      ordering feature "u before v" for every pair of named
+  operations (inserted syncs included, named CER-after-u / CES-b4-v /
+  CSWE-b4-v as in P:607), stream feature "u same stream as v" for every pair
+  of GPU vertices; constant columns dropped.
+* ``train_tree``    scikit-learn CART, gini, class_weight=balanced,
+  max_depth = max_leaf_nodes - 1, hyper-parameters by Algorithm 1
+  (tab:tree-params P:542-555, alg:dt-params P:564-583).
+* ``rulesets``      every root-to-leaf path ending in a leaf of class c
+  (P:597-611), phrased like the paper's tables ("y_L before CES-b4-PostSend",
+  "y_L different stream than Pack"), sorted by training samples.
+* ``class_accuracy`` Table V protocol: classes from a subset,
+  tree from the subset, classify every implementation, report the share whose
+  time falls inside its predicted class's [fastest, slowest] range.
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+
+from . import dspmv as D
+from .schedules import EDGES, GPU
+
+NAMES = D.VERTEX_NAMES
+
+
+# ------------------------------------------------------------------ labels
+def default_radius(m: int) -> int:
+    """0.5 % (minimum 1) of the number of measurements."""
+    return max(1, int(round(0.005 * m)))
+
+
+def step_convolve(a, r: int) -> np.ndarray:
+    """c_i = sum_{m=1..r} a_{i+m} - sum_{m=-r+1..0} a_{i+m}, for r < i < len-r
+    (entries outside that range are nan)."""
+    a = np.asarray(a, np.float64)
+    n = len(a)
+    c = np.full(n, np.nan)
+    cs = np.concatenate([[0.0], np.cumsum(a)])
+    for i in range(r + 1, n - r):
+        c[i] = (cs[i + r + 1] - cs[i + 1]) - (cs[i + 1] - cs[i - r + 1])
+    return c
+
+
+def class_labels(times, radius: int | None = None, percentile: float = 98.0):
+    """Labels (1 = fastest) for `times` (any order) and the class ranges."""
+    from scipy.signal import find_peaks, peak_prominences
+    t = np.asarray(times, np.float64)
+    order = np.argsort(t, kind="stable")
+    a = t[order]
+    n = len(a)
+    r = default_radius(n) if radius is None else radius
+    bounds = []
+    if n > 2 * r + 2:
+        c = step_convolve(a, r)
+        valid = np.where(np.isnan(c), -np.inf, c)
+        peaks, _ = find_peaks(valid)
+        peaks = peaks[np.isfinite(valid[peaks])]
+        if len(peaks):
+            import warnings
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                prom = peak_prominences(np.where(np.isfinite(valid), valid, np.nanmin(c)), peaks)[0]
+            # R-N2: a peak is kept when its prominence is >= the 98th
+            # percentile of the convolution signal (noise peaks stay below it)
+            thr = np.percentile(c[~np.isnan(c)], percentile)
+            bounds = sorted(int(p) for p, q in zip(peaks, prom) if q >= thr and q > 0)
+    lab_sorted = np.ones(n, np.int64)
+    for b in bounds:
+        lab_sorted[b + 1:] += 1
+    labels = np.empty(n, np.int64)
+    labels[order] = lab_sorted
+    ranges = {int(k): (float(a[lab_sorted == k].min()), float(a[lab_sorted == k].max()))
+              for k in np.unique(lab_sorted)}
+    return labels, ranges, bounds
+
+
+# ---------------------------------------------------------------- features
+def op_names(ops) -> list:
+    """Names of every op: vertices by name, syncs as CER-after-u / CES-b4-v /
+    CSWE-b4-v (u = first DAG predecessor of the consumer v on the recorded
+    stream, edge order; a second wait before the same v gets ':u')."""
+    ops = np.asarray(ops).tolist()
+    names = [None] * len(ops)
+    where = {}
+    for t, (k, s, e, _) in enumerate(ops):
+        if k < 10:
+            names[t] = NAMES[k]
+            where[k] = (t, s)
+    for t, (k, s, e, _) in enumerate(ops):
+        if k != D.DSPMV_OP_EVENT_RECORD:
+            continue
+        v = next(kk for kk, *_ in ops[t + 1:] if kk < 10)
+        u = next((uu for (uu, vv) in EDGES if vv == v and uu in GPU and where[uu][1] == s
+                  and where[uu][0] < t), None)
+        uname = NAMES[u] if u is not None else "?"
+        names[t] = f"CER-after-{uname}"
+        w = next(tt for tt in range(t + 1, len(ops)) if ops[tt][0] in (11, 12) and ops[tt][2] == e)
+        base = ("CES-b4-" if ops[w][0] == D.DSPMV_OP_EVENT_SYNC else "CSWE-b4-") + NAMES[v]
+        names[w] = base if base not in names else f"{base}:{uname}"
+    return names
+
+
+def features(schedules):
+    """Binary feature matrix over a list of ops arrays; returns (X, columns)."""
+    rows = []
+    vocab = set()
+    for ops in schedules:
+        nm = op_names(ops)
+        pos = {n: i for i, n in enumerate(nm)}
+        stream = {NAMES[k]: s for k, s, e, _ in np.asarray(ops).tolist() if k in GPU}
+        rows.append((pos, stream))
+        vocab.update(nm)
+    names = sorted(vocab)
+    gpu_names = sorted(NAMES[k] for k in GPU)
+    cols = [("before", u, v) for u, v in itertools.combinations(names, 2)]
+    cols += [("same", u, v) for u, v in itertools.combinations(gpu_names, 2)]
+    X = np.zeros((len(rows), len(cols)), np.int8)
+    for i, (pos, stream) in enumerate(rows):
+        for j, (kind, u, v) in enumerate(cols):
+            if kind == "before":
+                X[i, j] = 1 if (u in pos and v in pos and pos[u] < pos[v]) else 0
+            else:
+                X[i, j] = 1 if stream[u] == stream[v] else 0
+    keep = [j for j in range(len(cols)) if X[:, j].min() != X[:, j].max()]
+    return X[:, keep], [cols[j] for j in keep]
+
+
+# -------------------------------------------------------------------- tree
+def _train(X, y, mln):
+    from sklearn.tree import DecisionTreeClassifier
+    clf = DecisionTreeClassifier(criterion="gini", max_leaf_nodes=mln, max_depth=max(1, mln - 1),
+                                 class_weight="balanced", random_state=0)
+    clf.fit(X, y)
+    err = 1.0 - float((clf.predict(X) == y).mean())
+    return err, clf
+
+
+def train_tree(X, y):
+    """Algorithm 1: grow max_leaf_nodes from 2, probing +1..+5,
+    while the training error shrinks.  Returns (clf, mln, history)."""
+    mln = 2
+    err = np.inf
+    cur, clf = _train(X, y, mln)
+    history = [(mln, cur, clf.get_depth())]
+    while cur < err:
+        err = cur
+        for i in range(1, 6):
+            c2, n2 = _train(X, y, mln + i)
+            history.append((mln + i, c2, n2.get_depth()))
+            if c2 < err:
+                clf, mln, cur = n2, mln + i, c2
+                break
+    return clf, mln, history
+
+
+def rule_text(col, value: int) -> str:
+    kind, u, v = col
+    if kind == "before":
+        return f"{u} before {v}" if value else f"{v} before {u}"
+    return f"{u} same stream as {v}" if value else f"{u} different stream than {v}"
+
+
+def rulesets(clf, cols):
+    """{class: [(n_samples, [rules])]} -- root-to-leaf paths per class."""
+    t = clf.tree_
+    out = {}
+
+    def walk(node, path):
+        if t.children_left[node] == -1:
+            cls = int(clf.classes_[int(np.argmax(t.value[node][0]))])
+            out.setdefault(cls, []).append((int(t.n_node_samples[node]), list(path)))
+            return
+        f = t.feature[node]
+        walk(t.children_left[node], path + [rule_text(cols[f], 0)])
+        walk(t.children_right[node], path + [rule_text(cols[f], 1)])
+
+    walk(0, [])
+    for k in out:
+        out[k].sort(key=lambda p: -p[0])
+    return out
+
+
+def class_accuracy(sub_ops, sub_times, all_ops, all_times):
+    """Table V protocol: fraction of all implementations whose time lies in
+    the [fastest, slowest] range of the class the subset's tree assigns."""
+    labels, ranges, _ = class_labels(sub_times)
+    X_all, cols = features(list(sub_ops) + list(all_ops))
+    Xs, Xa = X_all[:len(sub_ops)], X_all[len(sub_ops):]
+    if len(ranges) == 1:
+        lo, hi = ranges[1]
+        t = np.asarray(all_times)
+        return float(((t >= lo) & (t <= hi)).mean())
+    clf, _, _ = train_tree(Xs, labels)
+    pred = clf.predict(Xa)
+    t = np.asarray(all_times)
+    ok = [ranges[int(p)][0] <= ti <= ranges[int(p)][1] for p, ti in zip(pred, t)]
+    return float(np.mean(ok))

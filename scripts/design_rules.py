@@ -1,0 +1,140 @@
+#!/usr/bin/env python
+"""The paper's end-to-end experiment on B200 (NEXT-1 + NEXT-2; §III-C,
+§IV, §V): measure every schedule of the DAG with the paper's protocol, label
+performance classes, train the CART tree (Algorithm 1), print the rulesets,
+then run MCTS for 50/100/200/400 iterations and report the Table V class
+accuracy against the exhaustive space.
+
+    python scripts/design_rules.py --workload g3 --ranks 4 --out profiles/r1_rules_g3.json
+
+g3 = the paper's banded 150K matrix on `ranks` in-process LOCAL
+ranks of one B200 (only one GPU is reachable this round); c2 = 7-pt 128^3 on
+one rank (NCCL comm of size 1).
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+from paper_2203_02530_b200 import dspmv as D  # noqa: E402
+from paper_2203_02530_b200 import mcts as M  # noqa: E402
+from paper_2203_02530_b200 import rules as R  # noqa: E402
+from paper_2203_02530_b200 import schedules as PS  # noqa: E402
+
+
+def setup(workload, ranks):
+    if workload == "g3":
+        n = 150000
+        rp, col, val = gen.banded(n)
+    elif workload == "c5":
+        n, (rp, col, val) = gen.config_matrix("c5")
+    else:
+        n, (rp, col, val) = gen.config_matrix("c2")
+    x = gen.x_values((0, n))
+    rb = D.dspmv_partition(n, ranks)
+    if ranks == 1:
+        comms = [D.dspmv_comm_create(D.dspmv_comm_unique_id(), 1, 0, 0)]
+    else:
+        comms = D.dspmv_comm_create_local(ranks, 0)
+    plans, xs, ys = [], [], []
+    for r in range(ranks):
+        b, e = int(rb[r]), int(rb[r + 1])
+        lo, hi = int(rp[b]), int(rp[e])
+        plans.append(D.dspmv_plan_create(comms[r], n, rp[b:e + 1], col[lo:hi], val[lo:hi]))
+        xs.append(torch.from_numpy(x[b:e].copy()).cuda())
+        ys.append(torch.empty(e - b, dtype=torch.float64, device="cuda"))
+    return comms, plans, xs, ys
+
+
+def make_measure(plans, xs, ys, t_measure=0.01):
+    stream = torch.cuda.current_stream()
+    ranks = len(plans)
+
+    def apply(ss):
+        if ranks == 1:
+            D.dspmv_apply(ss[0], xs[0], ys[0], stream)
+        else:
+            D.dspmv_apply_group(ss, xs, ys, stream)
+
+    def measure(ops):
+        """repeat samples until t_measure has elapsed; time =
+        t_measure / n_samples (one process drives every rank here)."""
+        ss = [D.dspmv_schedule_create(p, ops, 2) for p in plans]
+        for _ in range(2):
+            apply(ss)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        apply(ss)
+        n = max(1, math.ceil(t_measure / max(time.perf_counter() - t0, 1e-7)))
+        t0 = time.perf_counter()
+        for _ in range(n):
+            apply(ss)
+        t = (time.perf_counter() - t0) / n
+        for s in ss:
+            D.dspmv_schedule_destroy(s)
+        return t
+    return measure
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="g3", choices=["g3", "c2", "c5"])
+    ap.add_argument("--ranks", type=int, default=4)
+    ap.add_argument("--out", default="gpurun_out/rules.json")
+    a = ap.parse_args()
+    comms, plans, xs, ys = setup(a.workload, a.ranks)
+    measure = make_measure(plans, xs, ys)
+    space = PS.enumerate_derived(2)
+    t0 = time.perf_counter()
+    times = np.array([measure(o) for o in space])
+    sweep_s = time.perf_counter() - t0
+    labels, ranges, bounds = R.class_labels(times)
+    X, cols = R.features(space)
+    clf, mln, hist = R.train_tree(X, labels)
+    rs = R.rulesets(clf, cols)
+    out = {
+        "workload": a.workload, "ranks": a.ranks, "n_schedules": len(space),
+        "sweep_wall_s": round(sweep_s, 2),
+        "fastest_us": float(times.min() * 1e6), "slowest_us": float(times.max() * 1e6),
+        "fast_slow_ratio": float(times.max() / times.min()),
+        "sorted_times_us": [round(float(t) * 1e6, 3) for t in np.sort(times)],
+        "classes": {str(k): {"range_us": [v[0] * 1e6, v[1] * 1e6], "count": int((labels == k).sum())}
+                    for k, v in ranges.items()},
+        "tree": {"max_leaf_nodes": int(mln), "depth": int(clf.get_depth()),
+                 "train_error": float(1 - (clf.predict(X) == labels).mean()),
+                 "alg1_history": [[int(m), float(e), int(d)] for m, e, d in hist]},
+        "rulesets": {str(k): [{"samples": n, "rules": r} for n, r in v[:3]] for k, v in rs.items()},
+        "fastest": PS.describe(space[int(times.argmin())]),
+        "slowest": PS.describe(space[int(times.argmax())]),
+    }
+    # Table V protocol: MCTS subsets vs the exhaustive space
+    acc = {}
+    for iters in (50, 100, 200, 400):
+        m = M.MCTS(measure, n_streams=2, seed=2203).run(iters)
+        recs = m.records()
+        sub_ops = [o for o, _ in recs]
+        sub_t = np.array([t for _, t in recs])
+        acc[str(iters)] = {"distinct": len(recs),
+                           "accuracy": R.class_accuracy(sub_ops, sub_t, space, times),
+                           "best_found_us": float(sub_t.min() * 1e6)}
+    out["mcts_table_v"] = acc
+    json.dump(out, open(a.out, "w"), indent=1)
+    print(json.dumps({k: v for k, v in out.items() if k != "sorted_times_us"}, indent=1))
+    for p in plans:
+        D.dspmv_plan_destroy(p)
+    for c in comms:
+        D.dspmv_comm_destroy(c)
+
+
+if __name__ == "__main__":
+    main()
