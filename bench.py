@@ -252,6 +252,7 @@ def run_ours(a):
     barrier()
     t_wall0 = time.perf_counter()
     step_ms_rank = 0.0
+    tl_begin, tl_end = [], []
     for k in range(a.steps):
         D.dspmv_l2_flush(local, stream)
         evs[k][0].record(stream)
@@ -260,6 +261,9 @@ def run_ours(a):
         t = D.dspmv_schedule_op_times(sched)
         yl_ms += float(t[iyl])
         step_ms_rank += float(t[0])   # START..END events recorded on `stream` by the library
+        b_, e_ = D.dspmv_schedule_op_timeline(sched)
+        tl_begin.append(float(b_[iyl]))
+        tl_end.append(float(e_[iyl]))
     barrier()
     t_wall = time.perf_counter() - t_wall0
     launches = D.dspmv_launch_count() - launches0
@@ -319,6 +323,8 @@ def run_ours(a):
                 "step_timing": ("CUDA events recorded by dspmv_apply on the caller stream at START "
                                 "and END (the whole schedule incl. host syncs); max over ranks"),
                 "ms_per_step_incl_python_call": round(py_step_ms, 6),
+                "yL_window_in_step_us_median": [round(float(np.median(tl_begin)) * 1e3, 2),
+                                                round(float(np.median(tl_end)) * 1e3, 2)],
                 "step_hbm_gbs_algorithmic": round(step_gbs, 1),
                 "wall_s_timed_region": round(t_wall, 3),
             },

@@ -107,7 +107,10 @@ typedef struct {
     int32_t block_cfg;         /* row-block kernel configuration (tile nnz / consumer
                                   warps / TMA stages), -1 = chosen per matrix from its
                                   row lengths; K1                         */
-    int32_t reserved[3];
+    int32_t caller_stream0;    /* 1: schedule stream 0 IS the stream passed to apply (its
+                                  ops need no cross-stream wait); 0 (default): a
+                                  library stream ordered after the caller's stream     */
+    int32_t reserved[2];
 } dspmv_plan_opts;
 
 void dspmv_plan_opts_default(dspmv_plan_opts* opts);

@@ -200,10 +200,24 @@ dspmv_status exchange_requests_nccl(Plan& p) {
 }
 
 // ------------------------------------------------------------- executor
+// CES: spin on cudaEventQuery (lower wake-up latency than the runtime's
+// cudaEventSynchronize); DSPMV_BLOCKING_SYNC=1 falls back to the latter.
+cudaError_t host_wait(cudaEvent_t ev) {
+    static const bool blocking = [] {
+        const char* v = std::getenv("DSPMV_BLOCKING_SYNC");
+        return v && std::atoi(v) != 0;
+    }();
+    if (blocking) return cudaEventSynchronize(ev);
+    for (;;) {
+        const cudaError_t q = cudaEventQuery(ev);
+        if (q != cudaErrorNotReady) return q;
+    }
+}
+
 dspmv_status wait_exchange(Plan& p) {
     if (!p.has_peers) return DSPMV_OK;  // nothing was sent or received
     if (p.comm->kind == DSPMV_COMM_LOCAL || p.host.nranks == 1) {
-        CUDA_TRY(cudaEventSynchronize(p.ev_x));
+        CUDA_TRY(host_wait(p.ev_x));
         return DSPMV_OK;
     }
     const auto t_start = std::chrono::steady_clock::now();
@@ -280,7 +294,11 @@ dspmv_status begin_apply(Schedule& s, cudaStream_t caller) {
     if (cudaGetDevice(&cur) != cudaSuccess || cur != p.device) CUDA_TRY(cudaSetDevice(p.device));
     if (s.step0) CUDA_TRY(cudaEventRecord(s.step0, caller));
     CUDA_TRY(cudaEventRecord(p.ev_start, caller));
-    for (int i = 0; i < s.n_streams; ++i) CUDA_TRY(cudaStreamWaitEvent(p.streams[i], p.ev_start, 0));
+    // schedule stream 0 may be the caller's stream itself (no cross-stream
+    // wait for its work); the others wait on the caller's START point
+    p.cur_stream0 = p.opts.caller_stream0 ? caller : p.streams[0];
+    for (int i = p.opts.caller_stream0 ? 1 : 0; i < s.n_streams; ++i)
+        CUDA_TRY(cudaStreamWaitEvent(p.streams[i], p.ev_start, 0));
     p.posted_send = p.posted_recv = p.issued = false;
     return DSPMV_OK;
 }
@@ -291,7 +309,7 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
     const dspmv_op& o = s.ops[t];
     const bool gpu = is_gpu_vertex(o.kind);
     const bool on_stream = gpu || o.kind == DSPMV_OP_EVENT_RECORD || o.kind == DSPMV_OP_STREAM_WAIT_EVENT;
-    cudaStream_t st = on_stream ? p.streams[o.stream] : nullptr;
+    cudaStream_t st = on_stream ? (o.stream == 0 ? p.cur_stream0 : p.streams[o.stream]) : nullptr;
     const bool timed = gpu && s.timing && s.t0[t];
     if (timed) CUDA_TRY(cudaEventRecord(s.t0[t], st));
     cudaError_t e = cudaSuccess;
@@ -337,7 +355,7 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
             e = cudaEventRecord(s.ev[o.event], st);
             break;
         case DSPMV_OP_EVENT_SYNC:
-            e = cudaEventSynchronize(s.ev[o.event]);
+            e = host_wait(s.ev[o.event]);
             break;
         case DSPMV_OP_STREAM_WAIT_EVENT:
             e = cudaStreamWaitEvent(st, s.ev[o.event], 0);
@@ -459,6 +477,9 @@ void dspmv_plan_opts_default(dspmv_plan_opts* o) {
     o->vector_threshold = -1;
     o->keep_host = 0;
     o->comm_priority = 1;
+    o->block_cfg = -1;
+    o->caller_stream0 = 0;
+    if (const char* ev = std::getenv("DSPMV_CALLER_STREAM0")) o->caller_stream0 = std::atoi(ev);
 }
 
 static void free_plan_device(Plan& p) {

@@ -96,6 +96,24 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// x gathers: read-only path with an L2 evict_last hint, so x stays resident
+// while the matrix streams (evict_first) pass through L2.
+__device__ __forceinline__ double ldg_x(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ldg_x(const float* p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 template <typename T> __device__ __forceinline__ T mul_rn(T a, T b);
 template <> __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 template <> __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
@@ -157,7 +175,7 @@ template <typename T, bool kIdentity, bool kOneLane, typename St>
 __device__ __forceinline__ void block_rows(const St& S, int lgL_rt, int w0, int w1, int a0, int ra0,
                                            bool blk_combine, int lane, const T* __restrict__ x,
                                            T* __restrict__ y, const int32_t* __restrict__ out,
-                                           const int32_t* __restrict__ slot, SpmvOperands o) {
+                                           const int32_t* __restrict__ slot, SpmvOperands o, uint64_t xpol) {
     const int lgL = kOneLane ? 0 : lgL_rt;
     const int L = 1 << lgL;           // lanes per row (warp-uniform)
     const int G = 32 >> lgL;          // rows per warp pass
@@ -172,7 +190,7 @@ __device__ __forceinline__ void block_rows(const St& S, int lgL_rt, int w0, int 
                 T xv[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
-                    if (q + k * L < e1) xv[k] = __ldg(x + S.col[q + k * L]);
+                    if (q + k * L < e1) xv[k] = ldg_x(x + S.col[q + k * L], xpol);
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
                     if (q + k * L < e1) acc = add_rn(acc, mul_rn(S.val[q + k * L], xv[k]));
@@ -252,6 +270,7 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
     T* __restrict__ y = static_cast<T*>(o.y);
     const int32_t* __restrict__ out = a.out;
     const int32_t* __restrict__ slot = a.slot;
+    const uint64_t xpol = policy_evict_last();
     int it = 0;
     for (int b = blockIdx.x; b < a.nb; b += gridDim.x, ++it) {
         const int s = it % C::kStages;
@@ -263,8 +282,8 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
         const int32_t w0 = S.hdr[5 + warp], w1 = S.hdr[6 + warp];
 
         const int lgL = S.hdr[4] >> 8;
-        if (lgL == 0) block_rows<T, kIdentity, true>(S, 0, w0, w1, a0, ra0, blk_combine, lane, x, y, out, slot, o);
-        else block_rows<T, kIdentity, false>(S, lgL, w0, w1, a0, ra0, blk_combine, lane, x, y, out, slot, o);
+        if (lgL == 0) block_rows<T, kIdentity, true>(S, 0, w0, w1, a0, ra0, blk_combine, lane, x, y, out, slot, o, xpol);
+        else block_rows<T, kIdentity, false>(S, lgL, w0, w1, a0, ra0, blk_combine, lane, x, y, out, slot, o, xpol);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     }
@@ -277,6 +296,7 @@ __global__ void __launch_bounds__(kThreads) spmv_vector_kernel(VecArgs a, SpmvOp
     const int nw = (gridDim.x * kThreads) >> 5;
     const T* __restrict__ val = static_cast<const T*>(a.val);
     const T* __restrict__ x = static_cast<const T*>(o.x);
+    const uint64_t xpol = policy_evict_last();
     for (int i = w; i < a.nV; i += nw) {
         const int32_t p0 = __ldg(a.rowptr + i), p1 = __ldg(a.rowptr + i + 1);
         T acc = T(0);
@@ -290,9 +310,9 @@ __global__ void __launch_bounds__(kThreads) spmv_vector_kernel(VecArgs a, SpmvOp
                 v[u] = __ldcs(val + p + 32 * u);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc += v[u] * __ldg(x + c[u]);
+            for (int u = 0; u < 4; ++u) acc += v[u] * ldg_x(x + c[u], xpol);
         }
-        for (; p < p1; p += 32) acc += __ldcs(val + p) * __ldg(x + __ldcs(a.col + p));
+        for (; p < p1; p += 32) acc += __ldcs(val + p) * ldg_x(x + __ldcs(a.col + p), xpol);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
         if (lane == 0) {

@@ -90,6 +90,7 @@ struct Plan {
     void* d_yout = nullptr;
     cudaStream_t streams[DSPMV_MAX_STREAMS] = {};
     cudaStream_t comm_stream = nullptr;
+    cudaStream_t cur_stream0 = nullptr;  // stream of schedule stream 0 in this apply
     cudaEvent_t ev_start = nullptr, ev_x = nullptr;
     std::vector<void*> allocs;
     int64_t device_bytes = 0;

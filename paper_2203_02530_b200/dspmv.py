@@ -48,7 +48,8 @@ class DspmvError(RuntimeError):
 class dspmv_plan_opts(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int32), ("vector_threshold", ctypes.c_int32),
                 ("keep_host", ctypes.c_int32), ("comm_priority", ctypes.c_int32),
-                ("block_cfg", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("block_cfg", ctypes.c_int32), ("caller_stream0", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 class dspmv_plan_info(ctypes.Structure):
@@ -197,7 +198,8 @@ def dspmv_comm_info(comm):
 
 def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_F64,
                       vector_threshold: int = -1, keep_host: bool = False,
-                      comm_priority: bool = True, block_cfg: int = -1):
+                      comm_priority: bool = True, block_cfg: int = -1,
+                      caller_stream0: bool | None = None):
     """rowptr int64[n_local+1], col int32[nnz] (global ids), val float64/32."""
     rowptr = np.ascontiguousarray(rowptr, np.int64)
     col = np.ascontiguousarray(col_global, np.int32)
@@ -209,6 +211,8 @@ def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_
     o.keep_host = int(keep_host)
     o.comm_priority = int(comm_priority)
     o.block_cfg = block_cfg
+    if caller_stream0 is not None:
+        o.caller_stream0 = int(caller_stream0)
     h = _P()
     _check(lib.dspmv_plan_create(comm, n_global, len(rowptr) - 1, rowptr.ctypes.data,
                                  col.ctypes.data, val.ctypes.data, ctypes.byref(o),

@@ -1,0 +1,25 @@
+"""Small runs of every kernel path for compute-sanitizer (memcheck /
+racecheck / synccheck): stencil (one lane per row), 27-pt (4 lanes/row),
+power-law (all classes + warp-per-row), 3 LOCAL ranks (pack, exchange,
+unpack, combine), fp32."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import gen
+from paper_2203_02530_b200 import dspmv as D
+from tests.gpu_helpers import LocalRun, derive_ops
+
+cases = [("7pt", 16 ** 3, gen.stencil("7pt", (16, 16, 16))),
+         ("27pt", 12 ** 3, gen.stencil("27pt", (12, 12, 12))),
+         ("pl", 6000, gen.powerlaw(6000))]
+for name, n, (rp, col, val) in cases:
+    for P in (1, 3):
+        for dt in (D.DSPMV_F64, D.DSPMV_F32):
+            v = val.astype(np.float32) if dt == D.DSPMV_F32 else val
+            run = LocalRun(n, rp, col, v, P, dtype=dt)
+            y = run.apply(run.schedule(derive_ops()), gen.x_values((0, n)), reps=2)
+            run.close()
+            assert np.isfinite(y).all()
+            print(name, P, dt, "ok", flush=True)
+D.dspmv_l2_flush(0)
+print("sanitize run complete")
