@@ -27,6 +27,17 @@ $(BUILD)/%.o: $(SRC)/%.cpp $(SRC)/runtime.h $(SRC)/internal.h include/dspmv.h | 
 $(OUT)/libdspmv.so: $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L$(NCCL_HOME)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_HOME)/lib
 
+# instrumented variant (per-phase clock64 counters), only with PROFILE=1
+$(BUILD)/kernels_prof.o: $(SRC)/kernels.cu $(SRC)/runtime.h $(SRC)/internal.h include/dspmv.h | $(BUILD)
+	$(NVCC) $(NVFLAGS) -DDSPMV_PROFILE -c $< -o $@ 2> $(BUILD)/ptxas_prof.txt || (cat $(BUILD)/ptxas_prof.txt; false)
+
+$(OUT)/libdspmv_prof.so: $(BUILD)/kernels_prof.o $(BUILD)/api.o $(BUILD)/planner.o $(BUILD)/schedule.o
+	$(NVCC) $(ARCH) -shared -o $@ $^ -L$(NCCL_HOME)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_HOME)/lib
+
+ifeq ($(PROFILE),1)
+all: $(OUT)/libdspmv_prof.so
+endif
+
 oracle/libo1.so: oracle/o1.c
 	gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -o $@ $< -lm
 

@@ -304,6 +304,12 @@ dspmv_status dspmv_apply_group(const dspmv_schedule_t* scheds, int nranks,
 dspmv_status dspmv_l2_flush(int cuda_device, dspmv_stream_t stream);
 /* Number of kernels this library has launched since it was loaded. */
 dspmv_status dspmv_launch_count(uint64_t* count);
+/* Instrumented builds only (make PROFILE=1 -> libdspmv_prof.so): per-phase
+ * clock64 totals of the row-block kernel ([0] producer waiting for an empty
+ * slot, [1] producer issuing, [2] consumers waiting for a full slot,
+ * [3] consumer row passes, [4] blocks, [5] consumer passes).  *n_out = 0 in
+ * normal builds. */
+dspmv_status dspmv_profile_counters(unsigned long long* out, int n, int reset, int* n_out);
 
 #ifdef __cplusplus
 }

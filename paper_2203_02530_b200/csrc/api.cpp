@@ -47,6 +47,7 @@ dspmv_status fail(dspmv_status st, const std::string& msg) {
     } while (0)
 
 int device_sm_count();
+int prof_read(unsigned long long* out, int n, bool reset);
 
 namespace {
 
@@ -991,6 +992,14 @@ dspmv_status dspmv_l2_flush(int dev, dspmv_stream_t stream) {
         g_flush_bytes[dev] = bytes;
     }
     CUDA_TRY(launch_flush(g_flush_buf[dev], g_flush_bytes[dev], static_cast<cudaStream_t>(stream)));
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_profile_counters(unsigned long long* out, int n, int reset, int* n_out) {
+    if (!out || !n_out) return fail(DSPMV_ERR_ARG, "null argument");
+    const int r = prof_read(out, n, reset != 0);
+    if (r < 0) return fail(DSPMV_ERR_CUDA, "reading profile counters failed");
+    *n_out = r;
     return DSPMV_OK;
 }
 

@@ -34,6 +34,21 @@ namespace dspmv {
 
 std::atomic<uint64_t> g_launches{0};
 
+#ifdef DSPMV_PROFILE
+// Instrumented build (make PROFILE=1): per-phase clock64 totals of the
+// row-block kernel, summed over warps -- [0] producer waiting for an empty
+// slot, [1] producer issuing, [2] consumer waiting for a full slot,
+// [3] consumer row passes, [4] blocks, [5] consumer passes.
+__device__ unsigned long long g_prof[8];
+#define PROF_T0() const long long _t0 = clock64()
+#define PROF_ADD(i, t0) atomicAdd(&g_prof[i], (unsigned long long)(clock64() - (t0)))
+#define PROF_INC(i, n) atomicAdd(&g_prof[i], (unsigned long long)(n))
+#else
+#define PROF_T0()
+#define PROF_ADD(i, t0)
+#define PROF_INC(i, n)
+#endif
+
 namespace {
 
 constexpr int kThreads = 256;   // vector / pack kernels
@@ -239,7 +254,14 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
             for (int b = blockIdx.x; b < a.nb; b += gridDim.x, ++it) {
                 const int s = it % C::kStages;
                 const int u = it / C::kStages;
+#ifdef DSPMV_PROFILE
+                const long long tw = clock64();
+#endif
                 if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+#ifdef DSPMV_PROFILE
+                PROF_ADD(0, tw);
+                const long long ti = clock64();
+#endif
                 const int4* d = reinterpret_cast<const int4*>(a.desc + size_t(b) * kDescInts);
                 const int4 d0 = __ldg(d), d1 = __ldg(d + 1), d2 = __ldg(d + 2), d3 = __ldg(d + 3);
                 const int32_t r0 = d0.x, r1 = d0.y, p0 = d0.z, p1 = d0.w;
@@ -260,6 +282,10 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
                     bulk_g2s(S.col, a.col + a0, bc, &full[s], pol);
                 }
                 bulk_g2s(S.rp, a.rowptr + ra0, br, &full[s], pol);
+#ifdef DSPMV_PROFILE
+                PROF_ADD(1, ti);
+                PROF_INC(4, 1);
+#endif
             }
         }
         return;
@@ -275,7 +301,14 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
     for (int b = blockIdx.x; b < a.nb; b += gridDim.x, ++it) {
         const int s = it % C::kStages;
         const int u = it / C::kStages;
+#ifdef DSPMV_PROFILE
+        const long long tf = clock64();
+#endif
         mbar_wait(&full[s], u & 1);
+#ifdef DSPMV_PROFILE
+        if (lane == 0) PROF_ADD(2, tf);
+        const long long tc = clock64();
+#endif
         St& S = st[s];
         const int32_t a0 = S.hdr[2], ra0 = S.hdr[3];
         const bool blk_combine = kCombine && (S.hdr[4] & 1) != 0;
@@ -285,6 +318,12 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
         if (lgL == 0) block_rows<T, kIdentity, true>(S, 0, w0, w1, a0, ra0, blk_combine, lane, x, y, out, slot, o, xpol);
         else block_rows<T, kIdentity, false>(S, lgL, w0, w1, a0, ra0, blk_combine, lane, x, y, out, slot, o, xpol);
         __syncwarp();
+#ifdef DSPMV_PROFILE
+        if (lane == 0) {
+            PROF_ADD(3, tc);
+            PROF_INC(5, 1);
+        }
+#endif
         if (lane == 0) mbar_arrive(&empty[s]);
     }
 }
@@ -457,6 +496,22 @@ int occupancy_any(int cfg) {
 }
 
 }  // namespace
+
+int prof_read(unsigned long long* out, int n, bool reset) {
+#ifdef DSPMV_PROFILE
+    unsigned long long h[8];
+    if (cudaMemcpyFromSymbol(h, g_prof, sizeof(h)) != cudaSuccess) return -1;
+    for (int i = 0; i < n && i < 8; ++i) out[i] = h[i];
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+    }
+    return 8;
+#else
+    (void)out; (void)n; (void)reset;
+    return 0;
+#endif
+}
 
 int block_kernel_ctas_per_sm(int dtype, int cfg) {
     return dtype == DSPMV_F32 ? occupancy_any<float>(cfg) : occupancy_any<double>(cfg);

@@ -14,7 +14,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libdspmv.so")
+# DSPMV_LIB=prof selects the instrumented build (make PROFILE=1)
+LIB_PATH = os.path.join(_HERE, "lib", "libdspmv_prof.so" if os.environ.get("DSPMV_LIB") == "prof"
+                        else "libdspmv.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libdspmv.so not built ({LIB_PATH}); run `make` or __graft_entry__.build()")
@@ -118,6 +120,7 @@ _sig("dspmv_apply_host", [_P, _P, _P, _P])
 _sig("dspmv_apply_group", [_P, _I, _P, _P, _P])
 _sig("dspmv_l2_flush", [_I, _P])
 _sig("dspmv_launch_count", [_P])
+_sig("dspmv_profile_counters", [_P, _I, _I, _P])
 
 
 def _check(st: int):
@@ -398,3 +401,10 @@ def dspmv_launch_count() -> int:
     c = ctypes.c_uint64()
     _check(lib.dspmv_launch_count(ctypes.byref(c)))
     return c.value
+
+
+def dspmv_profile_counters(reset: bool = True):
+    out = (ctypes.c_ulonglong * 8)()
+    n = _I()
+    _check(lib.dspmv_profile_counters(out, 8, int(reset), ctypes.byref(n)))
+    return list(out)[:n.value]

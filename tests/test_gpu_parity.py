@@ -305,3 +305,61 @@ def test_every_block_cfg(cfg):
             assert np.array_equal(y, y1)
         else:
             assert within_tol(y, y1, O1.o1_absdot(rp, col, val, xs), 1e-12)
+
+
+def _sampled_check(n, rp, col, val, P, n_sample=20000, seed=5):
+    """Full-size matrix over P ranks (LOCAL if P > 1, else the bench's NCCL
+    comm of one rank): y on sampled rows vs O1 computed row by row."""
+    x = gen.x_values((0, n))
+    if P == 1:
+        comm = D.dspmv_comm_create(D.dspmv_comm_unique_id(), 1, 0, 0)
+        plan = D.dspmv_plan_create(comm, n, rp, col, val)
+        s = D.dspmv_schedule_create(plan, derive_ops(), 2)
+        try:
+            xd = torch.from_numpy(x).cuda()
+            yd = torch.empty_like(xd)
+            D.dspmv_l2_flush(0)
+            D.dspmv_apply(s, xd, yd)
+            y = yd.cpu().numpy()
+        finally:
+            D.dspmv_schedule_destroy(s)
+            D.dspmv_plan_destroy(plan)
+            D.dspmv_comm_destroy(comm)
+    else:
+        run = LocalRun(n, rp, col, val, P)
+        try:
+            y = run.apply(run.schedule(derive_ops()), x)
+        finally:
+            run.close()
+    rng = np.random.default_rng(seed)
+    rows = np.unique(np.concatenate([rng.integers(0, n, n_sample), [0, n - 1],
+                                     D.dspmv_partition(n, P)[1:-1]]))
+    rows = rows[rows < n]
+    yref = O1.o1_spmv_rows(rows, rp, col, val, x)
+    rr = np.concatenate([[0], np.cumsum(np.diff(rp)[rows])])
+    sub_rp = rr.astype(np.int64)
+    sub_col = np.concatenate([col[rp[i]:rp[i + 1]] for i in rows])
+    sub_val = np.concatenate([val[rp[i]:rp[i + 1]] for i in rows])
+    scale = O1.o1_absdot(sub_rp, sub_col, sub_val, x)
+    assert within_tol(y[rows], yref, scale, 1e-12)
+    assert np.isfinite(y).all()
+
+
+def test_full_size_c3_27pt_256_sampled():
+    """BASELINE configs[2] at full size (449M nnz, 1 B200), sampled rows."""
+    n, (rp, col, val) = gen.config_matrix("c3")
+    _sampled_check(n, rp, col, val, 1)
+
+
+def test_full_size_c4_powerlaw_sampled():
+    """BASELINE configs[3] at full size (8M rows, 134M nnz) on 1 rank and on 8
+    in-process ranks (irregular halo, up to 7 peers), sampled rows."""
+    n, (rp, col, val) = gen.config_matrix("c4")
+    _sampled_check(n, rp, col, val, 1)
+    _sampled_check(n, rp, col, val, 8, n_sample=5000)
+
+
+def test_full_size_c5_7pt_192_four_ranks_sampled():
+    """BASELINE configs[4] matrix (7-pt 192^3) over 4 in-process ranks."""
+    n, (rp, col, val) = gen.config_matrix("c5")
+    _sampled_check(n, rp, col, val, 4)
