@@ -21,19 +21,22 @@ dspmv_status fail(dspmv_status st, const std::string& msg);
 // blocks into a ring of `stages` shared-memory slots with 1-D TMA copies.
 struct BlockCfg {
     int tile, rowmax, warps, stages, min_ctas;  // min_ctas: __launch_bounds__ occupancy
+    int chunk;                                  // x gathers in flight per lane (one lane per row)
 };
 constexpr BlockCfg kBlockCfgs[] = {
-    // tile  rowmax warps stages min_ctas   (rowmax = 32 x warps: one row per lane)
-    {2048, 256, 8, 2, 4},   // 0
-    {1024, 128, 4, 2, 8},   // 1
-    {2048, 256, 8, 3, 2},   // 2
-    {1024, 128, 4, 3, 5},   // 3
-    {1024, 256, 8, 2, 5},   // 4
-    {512, 128, 4, 4, 6},    // 5
+    // tile  rowmax warps stages min_ctas chunk  (rowmax = 32 x warps: one row per lane)
+    {2048, 256, 8, 2, 4, 8},    // 0
+    {1024, 128, 4, 2, 8, 8},    // 1
+    {2048, 256, 8, 3, 2, 8},    // 2
+    {1024, 128, 4, 3, 5, 8},    // 3
+    {1024, 256, 8, 2, 5, 8},    // 4
+    {512, 128, 4, 4, 6, 8},     // 5
+    {4096, 128, 4, 2, 2, 32},   // 6  long uniform rows, one lane per row
+    {4096, 128, 4, 2, 2, 16},   // 7
 };
 constexpr int kNumBlockCfgs = sizeof(kBlockCfgs) / sizeof(kBlockCfgs[0]);
 constexpr int kDefaultBlockCfg = 3;   // short rows (one lane per row)
-constexpr int kLongRowBlockCfg = 0;   // long, uniform rows (more consumer warps)
+constexpr int kLongRowBlockCfg = 6;   // long, uniform rows: one lane per row, 32 gathers in flight
 constexpr int kTileMin = 1024;        // smallest tile among the auto-chosen configs
 constexpr int kTileMax = 2048;     // vector_threshold upper bound (a row fits a block)
 constexpr int kPad = 8;            // device arrays padded (aligned over-read)

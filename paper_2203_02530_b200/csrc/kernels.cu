@@ -186,7 +186,7 @@ struct Cfg {
 // entry, then a shuffle tree over the L lanes -- tolerance, R-Q10).  Lanes
 // of consecutive rows read consecutive columns for banded rows, so the x
 // gathers coalesce; up to 8 gathers per lane are in flight per chunk.
-template <typename T, bool kIdentity, bool kOneLane, typename St>
+template <typename T, bool kIdentity, bool kOneLane, int CH, typename St>
 __device__ __forceinline__ void block_rows(const St& S, int lgL_rt, int w0, int w1, int a0, int ra0,
                                            bool blk_combine, int lane, const T* __restrict__ x,
                                            T* __restrict__ y, const int32_t* __restrict__ out,
@@ -201,13 +201,13 @@ __device__ __forceinline__ void block_rows(const St& S, int lgL_rt, int w0, int 
         T acc = T(0);
         if (valid) {
             const int32_t e0 = S.rp[r - ra0] - a0, e1 = S.rp[r + 1 - ra0] - a0;
-            for (int q = e0 + sub; q < e1; q += 8 * L) {
-                T xv[8];
+            for (int q = e0 + sub; q < e1; q += CH * L) {
+                T xv[CH];
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
+                for (int k = 0; k < CH; ++k)
                     if (q + k * L < e1) xv[k] = ldg_x(x + S.col[q + k * L], xpol);
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
+                for (int k = 0; k < CH; ++k)
                     if (q + k * L < e1) acc = add_rn(acc, mul_rn(S.val[q + k * L], xv[k]));
             }
         }
@@ -315,8 +315,12 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
         const int32_t w0 = S.hdr[5 + warp], w1 = S.hdr[6 + warp];
 
         const int lgL = S.hdr[4] >> 8;
-        if (lgL == 0) block_rows<T, kIdentity, true>(S, 0, w0, w1, a0, ra0, blk_combine, lane, x, y, out, slot, o, xpol);
-        else block_rows<T, kIdentity, false>(S, lgL, w0, w1, a0, ra0, blk_combine, lane, x, y, out, slot, o, xpol);
+        if (lgL == 0)
+            block_rows<T, kIdentity, true, kBlockCfgs[CFG].chunk>(S, 0, w0, w1, a0, ra0, blk_combine, lane, x, y,
+                                                                  out, slot, o, xpol);
+        else
+            block_rows<T, kIdentity, false, 8>(S, lgL, w0, w1, a0, ra0, blk_combine, lane, x, y, out, slot, o,
+                                               xpol);
         __syncwarp();
 #ifdef DSPMV_PROFILE
         if (lane == 0) {
@@ -451,10 +455,12 @@ cudaError_t launch_block_any(const DevLayout& L, const SpmvOperands& o, cudaStre
         case 3: return launch_block_cfg<T, 3>(L, o, s);
         case 4: return launch_block_cfg<T, 4>(L, o, s);
         case 5: return launch_block_cfg<T, 5>(L, o, s);
+        case 6: return launch_block_cfg<T, 6>(L, o, s);
+        case 7: return launch_block_cfg<T, 7>(L, o, s);
         default: return cudaErrorInvalidValue;
     }
 }
-static_assert(kNumBlockCfgs == 6, "update launch_block_any / occupancy dispatch");
+static_assert(kNumBlockCfgs == 8, "update launch_block_any / occupancy dispatch");
 
 template <typename T>
 cudaError_t launch_all(const DevLayout& L, const SpmvOperands& o, cudaStream_t s) {
@@ -491,6 +497,8 @@ int occupancy_any(int cfg) {
         case 3: return occupancy<T, 3>();
         case 4: return occupancy<T, 4>();
         case 5: return occupancy<T, 5>();
+        case 6: return occupancy<T, 6>();
+        case 7: return occupancy<T, 7>();
         default: return 1;
     }
 }

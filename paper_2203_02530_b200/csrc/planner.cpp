@@ -9,6 +9,7 @@
 // partition), R-Q4 (halo ascending by global id => grouped by owner), R-Q5
 // (stored order kept), R-Q6 (compressed A_R rows), R-Q7 (pack-map order).
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 
 #include "internal.h"
@@ -164,11 +165,18 @@ void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, cons
     // class c = log2(lanes per row), the smallest c with len <= 8 * 2^c.  Within
     // windows of kBinWindow S rows the rows are stable-partitioned by class, so
     // a block never mixes classes and y writes stay local to the window.
+    // one-lane configurations (chunk >= 16) keep rows up to `chunk` nnz in class 0
+    static const int max_class_env = [] {
+        const char* v = std::getenv("DSPMV_MAX_CLASS");
+        return v ? std::atoi(v) : kMaxClass;
+    }();
+    const int one_lane_len = std::max(8, cfg.chunk);
     auto row_class = [&](int32_t i) {
         const int32_t len = rowptr[i + 1] - rowptr[i];
+        if (len <= one_lane_len) return 0;
         int c = 0;
         while (c < kMaxClass && len > (8 << c)) ++c;
-        return c;
+        return std::min(c, max_class_env);
     };
     {
         std::vector<int32_t> sorted;

@@ -278,7 +278,7 @@ def test_full_size_c2_bench_config():
         D.dspmv_comm_destroy(comm)
 
 
-@pytest.mark.parametrize("cfg", list(range(6)))
+@pytest.mark.parametrize("cfg", list(range(8)))
 def test_every_block_cfg(cfg):
     """Every row-block kernel configuration (tile / consumer warps / stages)
     on an irregular multi-rank case and a stencil (bitwise vs O1)."""
