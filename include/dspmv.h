@@ -110,7 +110,10 @@ typedef struct {
     int32_t caller_stream0;    /* 1: schedule stream 0 IS the stream passed to apply (its
                                   ops need no cross-stream wait); 0 (default): a
                                   library stream ordered after the caller's stream     */
-    int32_t reserved[2];
+    int32_t reserve_sms;       /* SMs left free by the persistent SpMV grid so NCCL /
+                                  pack kernels can run concurrently; -1 (default) =
+                                  8 when the communicator has > 1 rank, else 0         */
+    int32_t reserved[1];
 } dspmv_plan_opts;
 
 void dspmv_plan_opts_default(dspmv_plan_opts* opts);

@@ -39,6 +39,12 @@ dspmv_status fail(dspmv_status st, const std::string& msg) {
         if (_e != cudaSuccess)                                                              \
             return fail(DSPMV_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
     } while (0)
+// inside ncclGroupStart/End: record the first error, keep going, end the group
+#define NCCL_GROUP_CALL(res, expr)                          \
+    do {                                                    \
+        ncclResult_t _r = (expr);                           \
+        if (_r != ncclSuccess && (res) == ncclSuccess) (res) = _r; \
+    } while (0)
 #define NCCL_TRY(expr)                                                                         \
     do {                                                                                       \
         ncclResult_t _r = (expr);                                                              \
@@ -103,7 +109,10 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
         if (!L.s_identity) ST_TRY(dev_upload(p, &D.s_out, L.s_out.data(), L.s_out.size()));
         D.cfg = cfg;
         const int per_sm = block_kernel_ctas_per_sm(p.dtype, cfg);
-        D.grid_s = std::max(1, std::min(L.nb, per_sm * sms));
+        // optionally leave SMs free for concurrent NCCL / pack kernels
+        const int reserve = p.opts.reserve_sms >= 0 ? p.opts.reserve_sms : (p.comm->nranks > 1 ? kAutoReserveSms : 0);
+        const int usable = std::max(1, sms - reserve);
+        D.grid_s = std::max(1, std::min(L.nb, per_sm * usable));
     }
     if (L.nV > 0) {
         ST_TRY(dev_upload(p, &D.v_rowptr, L.v_rowptr.data(), L.v_rowptr.size()));
@@ -158,13 +167,15 @@ dspmv_status exchange_requests_nccl(Plan& p) {
     CUDA_TRY(cudaMalloc(&d_scnt, sizeof(int32_t) * P));
     CUDA_TRY(cudaMemcpy(d_cnt, h.recv_count.data(), sizeof(int32_t) * P, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemset(d_scnt, 0, sizeof(int32_t) * P));
+    ncclResult_t gr = ncclSuccess;
     NCCL_TRY(ncclGroupStart());
     for (int q = 0; q < P; ++q) {
         if (q == me) continue;
-        NCCL_TRY(ncclSend(d_cnt + q, 1, ncclInt32, q, comm, s));
-        NCCL_TRY(ncclRecv(d_scnt + q, 1, ncclInt32, q, comm, s));
+        NCCL_GROUP_CALL(gr, ncclSend(d_cnt + q, 1, ncclInt32, q, comm, s));
+        NCCL_GROUP_CALL(gr, ncclRecv(d_scnt + q, 1, ncclInt32, q, comm, s));
     }
     NCCL_TRY(ncclGroupEnd());
+    NCCL_TRY(gr);
     CUDA_TRY(cudaStreamSynchronize(s));
     std::vector<int32_t> scnt(P);
     CUDA_TRY(cudaMemcpy(scnt.data(), d_scnt, sizeof(int32_t) * P, cudaMemcpyDeviceToHost));
@@ -183,10 +194,12 @@ dspmv_status exchange_requests_nccl(Plan& p) {
     NCCL_TRY(ncclGroupStart());
     for (int q = 0; q < P; ++q) {
         if (q == me) continue;
-        if (h.recv_count[q] > 0) NCCL_TRY(ncclSend(d_halo + h.recv_displ[q], h.recv_count[q], ncclInt32, q, comm, s));
-        if (scnt[q] > 0) NCCL_TRY(ncclRecv(d_req + sdis[q], scnt[q], ncclInt32, q, comm, s));
+        if (h.recv_count[q] > 0)
+            NCCL_GROUP_CALL(gr, ncclSend(d_halo + h.recv_displ[q], h.recv_count[q], ncclInt32, q, comm, s));
+        if (scnt[q] > 0) NCCL_GROUP_CALL(gr, ncclRecv(d_req + sdis[q], scnt[q], ncclInt32, q, comm, s));
     }
     NCCL_TRY(ncclGroupEnd());
+    NCCL_TRY(gr);
     CUDA_TRY(cudaStreamSynchronize(s));
     std::vector<int32_t> all(tot);
     if (tot) CUDA_TRY(cudaMemcpy(all.data(), d_req, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost));
@@ -253,16 +266,18 @@ dspmv_status issue_exchange_nccl(Plan& p) {
         const ncclDataType_t ty = nccl_type(p.dtype);
         char* rb = static_cast<char*>(p.d_recvbuf);
         char* sb = static_cast<char*>(p.d_sendbuf);
+        ncclResult_t gr = ncclSuccess;
         NCCL_TRY(ncclGroupStart());
         for (int q = 0; q < P; ++q)
             if (h.recv_count[q] > 0)
-                NCCL_TRY(ncclRecv(rb + size_t(h.recv_displ[q]) * p.esize, h.recv_count[q], ty, q, p.comm->nccl,
-                                  p.comm_stream));
+                NCCL_GROUP_CALL(gr, ncclRecv(rb + size_t(h.recv_displ[q]) * p.esize, h.recv_count[q], ty, q,
+                                             p.comm->nccl, p.comm_stream));
         for (int q = 0; q < P; ++q)
             if (h.send_count[q] > 0)
-                NCCL_TRY(ncclSend(sb + size_t(h.send_displ[q]) * p.esize, h.send_count[q], ty, q, p.comm->nccl,
-                                  p.comm_stream));
+                NCCL_GROUP_CALL(gr, ncclSend(sb + size_t(h.send_displ[q]) * p.esize, h.send_count[q], ty, q,
+                                             p.comm->nccl, p.comm_stream));
         NCCL_TRY(ncclGroupEnd());
+        NCCL_TRY(gr);
     }
     CUDA_TRY(cudaEventRecord(p.ev_x, p.comm_stream));
     p.issued = true;
@@ -480,7 +495,9 @@ void dspmv_plan_opts_default(dspmv_plan_opts* o) {
     o->comm_priority = 1;
     o->block_cfg = -1;
     o->caller_stream0 = 0;
+    o->reserve_sms = -1;
     if (const char* ev = std::getenv("DSPMV_CALLER_STREAM0")) o->caller_stream0 = std::atoi(ev);
+    if (const char* ev = std::getenv("DSPMV_RESERVE_SMS")) o->reserve_sms = std::atoi(ev);
 }
 
 static void free_plan_device(Plan& p) {

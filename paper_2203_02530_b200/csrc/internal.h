@@ -37,6 +37,8 @@ constexpr BlockCfg kBlockCfgs[] = {
 constexpr int kNumBlockCfgs = sizeof(kBlockCfgs) / sizeof(kBlockCfgs[0]);
 constexpr int kDefaultBlockCfg = 3;   // short rows (one lane per row)
 constexpr int kLongRowBlockCfg = 6;   // long, uniform rows: one lane per row, 32 gathers in flight
+constexpr int kAutoReserveSms = 8;    // SMs left to NCCL/pack when nranks > 1 (free on B200: y_L
+                                      // time unchanged with 148-16 SMs)
 constexpr int kTileMin = 1024;        // smallest tile among the auto-chosen configs
 constexpr int kTileMax = 2048;     // vector_threshold upper bound (a row fits a block)
 constexpr int kPad = 8;            // device arrays padded (aligned over-read)

@@ -51,7 +51,7 @@ class dspmv_plan_opts(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int32), ("vector_threshold", ctypes.c_int32),
                 ("keep_host", ctypes.c_int32), ("comm_priority", ctypes.c_int32),
                 ("block_cfg", ctypes.c_int32), ("caller_stream0", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("reserve_sms", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
 
 class dspmv_plan_info(ctypes.Structure):
@@ -202,7 +202,7 @@ def dspmv_comm_info(comm):
 def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_F64,
                       vector_threshold: int = -1, keep_host: bool = False,
                       comm_priority: bool = True, block_cfg: int = -1,
-                      caller_stream0: bool | None = None):
+                      caller_stream0: bool | None = None, reserve_sms: int | None = None):
     """rowptr int64[n_local+1], col int32[nnz] (global ids), val float64/32."""
     rowptr = np.ascontiguousarray(rowptr, np.int64)
     col = np.ascontiguousarray(col_global, np.int32)
@@ -216,6 +216,8 @@ def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_
     o.block_cfg = block_cfg
     if caller_stream0 is not None:
         o.caller_stream0 = int(caller_stream0)
+    if reserve_sms is not None:
+        o.reserve_sms = int(reserve_sms)
     h = _P()
     _check(lib.dspmv_plan_create(comm, n_global, len(rowptr) - 1, rowptr.ctypes.data,
                                  col.ctypes.data, val.ctypes.data, ctypes.byref(o),
