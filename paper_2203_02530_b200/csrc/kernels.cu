@@ -116,16 +116,26 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
-// x gathers: read-only path with an L2 evict_last hint, so x stays resident
-// while the matrix streams (evict_first) pass through L2.
+// x gathers: read-only path with an L2 evict_last hint (x stays resident
+// while the evict_first matrix streams pass through L2).  Irregular matrices
+// also skip L1 allocation (no reuse there; measured +10 % on C4), banded ones
+// keep it (neighbouring rows share x lines; C3).
+template <bool kNoL1>
 __device__ __forceinline__ double ldg_x(const double* p, uint64_t pol) {
     double v;
-    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    if constexpr (kNoL1)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    else
+        asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
     return v;
 }
+template <bool kNoL1>
 __device__ __forceinline__ float ldg_x(const float* p, uint64_t pol) {
     float v;
-    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    if constexpr (kNoL1)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    else
+        asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
     return v;
 }
 
@@ -174,6 +184,9 @@ struct Cfg {
     static constexpr int kWarps = kBlockCfgs[CFG].warps;
     static constexpr int kStages = kBlockCfgs[CFG].stages;
     static constexpr int kThreadsPerCta = (kWarps + 1) * 32;
+    // irregular / short-row configs skip L1 for x (no reuse); long uniform
+    // rows keep it (neighbouring rows share x lines)
+    static constexpr bool kNoL1 = kBlockCfgs[CFG].chunk < 16;
     template <typename T>
     static constexpr int smem_bytes() {
         return kStages * int(sizeof(Stage<T, kTile, kRowMax>)) + 2 * kStages * 8;
@@ -186,7 +199,7 @@ struct Cfg {
 // entry, then a shuffle tree over the L lanes -- tolerance, R-Q10).  Lanes
 // of consecutive rows read consecutive columns for banded rows, so the x
 // gathers coalesce; up to 8 gathers per lane are in flight per chunk.
-template <typename T, bool kIdentity, bool kOneLane, int CH, typename St>
+template <typename T, bool kIdentity, bool kOneLane, int CH, bool kNoL1, typename St>
 __device__ __forceinline__ void block_rows(const St& S, int lgL_rt, int w0, int w1, int a0, int ra0,
                                            bool blk_combine, int lane, const T* __restrict__ x,
                                            T* __restrict__ y, const int32_t* __restrict__ out,
@@ -205,7 +218,7 @@ __device__ __forceinline__ void block_rows(const St& S, int lgL_rt, int w0, int 
                 T xv[CH];
 #pragma unroll
                 for (int k = 0; k < CH; ++k)
-                    if (q + k * L < e1) xv[k] = ldg_x(x + S.col[q + k * L], xpol);
+                    if (q + k * L < e1) xv[k] = ldg_x<kNoL1>(x + S.col[q + k * L], xpol);
 #pragma unroll
                 for (int k = 0; k < CH; ++k)
                     if (q + k * L < e1) acc = add_rn(acc, mul_rn(S.val[q + k * L], xv[k]));
@@ -316,11 +329,11 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
 
         const int lgL = S.hdr[4] >> 8;
         if (lgL == 0)
-            block_rows<T, kIdentity, true, kBlockCfgs[CFG].chunk>(S, 0, w0, w1, a0, ra0, blk_combine, lane, x, y,
-                                                                  out, slot, o, xpol);
+            block_rows<T, kIdentity, true, kBlockCfgs[CFG].chunk, C::kNoL1>(S, 0, w0, w1, a0, ra0, blk_combine,
+                                                                            lane, x, y, out, slot, o, xpol);
         else
-            block_rows<T, kIdentity, false, 8>(S, lgL, w0, w1, a0, ra0, blk_combine, lane, x, y, out, slot, o,
-                                               xpol);
+            block_rows<T, kIdentity, false, 8, C::kNoL1>(S, lgL, w0, w1, a0, ra0, blk_combine, lane, x, y, out, slot,
+                                                         o, xpol);
         __syncwarp();
 #ifdef DSPMV_PROFILE
         if (lane == 0) {
@@ -353,9 +366,9 @@ __global__ void __launch_bounds__(kThreads) spmv_vector_kernel(VecArgs a, SpmvOp
                 v[u] = __ldcs(val + p + 32 * u);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc += v[u] * ldg_x(x + c[u], xpol);
+            for (int u = 0; u < 4; ++u) acc += v[u] * ldg_x<true>(x + c[u], xpol);
         }
-        for (; p < p1; p += 32) acc += __ldcs(val + p) * ldg_x(x + __ldcs(a.col + p), xpol);
+        for (; p < p1; p += 32) acc += __ldcs(val + p) * ldg_x<true>(x + __ldcs(a.col + p), xpol);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
         if (lane == 0) {

@@ -14,9 +14,10 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# DSPMV_LIB=prof selects the instrumented build (make PROFILE=1)
-LIB_PATH = os.path.join(_HERE, "lib", "libdspmv_prof.so" if os.environ.get("DSPMV_LIB") == "prof"
-                        else "libdspmv.so")
+# DSPMV_LIB=<variant> selects lib/libdspmv_<variant>.so (e.g. "prof": the
+# instrumented build of `make PROFILE=1`); default lib/libdspmv.so
+_VAR = os.environ.get("DSPMV_LIB", "")
+LIB_PATH = os.path.join(_HERE, "lib", f"libdspmv_{_VAR}.so" if _VAR else "libdspmv.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libdspmv.so not built ({LIB_PATH}); run `make` or __graft_entry__.build()")
