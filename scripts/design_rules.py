@@ -66,9 +66,10 @@ def make_measure(plans, xs, ys, t_measure=0.01):
         else:
             D.dspmv_apply_group(ss, xs, ys, stream)
 
-    def measure(ops):
-        """repeat samples until t_measure has elapsed; time =
-        t_measure / n_samples (one process drives every rank here)."""
+    def measure(ops, n_meas=3):
+        """a measurement repeats samples until t_measure has
+        elapsed, time = t_measure / n_samples (one process drives every rank
+        here); f = mean of n_meas measurements (R-Q19)."""
         ss = [D.dspmv_schedule_create(p, ops, 2) for p in plans]
         for _ in range(2):
             apply(ss)
@@ -76,13 +77,15 @@ def make_measure(plans, xs, ys, t_measure=0.01):
         t0 = time.perf_counter()
         apply(ss)
         n = max(1, math.ceil(t_measure / max(time.perf_counter() - t0, 1e-7)))
-        t0 = time.perf_counter()
-        for _ in range(n):
-            apply(ss)
-        t = (time.perf_counter() - t0) / n
+        ts = []
+        for _ in range(n_meas):
+            t0 = time.perf_counter()
+            for _ in range(n):
+                apply(ss)
+            ts.append((time.perf_counter() - t0) / n)
         for s in ss:
             D.dspmv_schedule_destroy(s)
-        return t
+        return float(np.mean(ts))
     return measure
 
 
