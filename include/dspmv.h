@@ -74,7 +74,7 @@ int dspmv_version(void);
  * The rank <-> GPU binding: one process per GPU (NCCL), or -- for tests on a
  * single device -- an in-process group of nranks simulated ranks sharing one
  * device whose exchange is a device-to-device copy (kind LOCAL).           */
-enum { DSPMV_COMM_NCCL = 0, DSPMV_COMM_LOCAL = 1 };
+enum { DSPMV_COMM_NCCL = 0, DSPMV_COMM_LOCAL = 1, DSPMV_COMM_HOST = 2 };
 
 /* Rank 0 obtains a 128-byte NCCL unique id; the caller broadcasts it (e.g.
  * torch.distributed.broadcast_object_list) to every rank. */
@@ -85,6 +85,16 @@ dspmv_status dspmv_comm_create(const unsigned char id[128], int nranks, int rank
                                int cuda_device, dspmv_comm_t* out);
 /* nranks in-process ranks on one device; out[r] is rank r's handle. */
 dspmv_status dspmv_comm_create_local(int nranks, int cuda_device, dspmv_comm_t* out);
+/* Host-transport communicator (kind HOST), one per process: plan-time
+ * collectives (request lists, IPC handles) go through the caller's
+ * `allgather(send, recv, bytes, ctx)` (every rank contributes `bytes`, recv
+ * receives nranks*bytes in rank order, returns 0 on success; e.g. backed by
+ * torch.distributed gloo or MPI); every apply-time byte moves device to device
+ * over peer memory, so plans on a HOST comm must use DSPMV_EXCHANGE_PUT.
+ * Ranks may share a device (separate processes). */
+typedef int (*dspmv_allgather_fn)(const void* send, void* recv, size_t bytes, void* ctx);
+dspmv_status dspmv_comm_create_host(int nranks, int rank, int cuda_device, dspmv_allgather_fn allgather,
+                                    void* ctx, dspmv_comm_t* out);
 /* ERR_STATE if plans created on it are still alive. */
 dspmv_status dspmv_comm_destroy(dspmv_comm_t comm);
 dspmv_status dspmv_comm_info(dspmv_comm_t comm, int* nranks, int* rank, int* kind);
@@ -113,8 +123,18 @@ typedef struct {
     int32_t reserve_sms;       /* SMs left free by the persistent SpMV grid so NCCL /
                                   pack kernels can run concurrently; -1 (default) =
                                   8 when the communicator has > 1 rank, else 0         */
-    int32_t reserved[1];
+    int32_t exchange;          /* DSPMV_EXCHANGE_COPY (default): PostSend/PostRecv issue
+                                  one NCCL group (LOCAL: device copies).
+                                  DSPMV_EXCHANGE_PUT: Pack is fused with the send -- it
+                                  stores each destination's segment straight into the
+                                  peer's receive buffer over peer memory (NVLink; CUDA
+                                  IPC handles exchanged at plan time for NCCL comms)
+                                  and publishes an epoch flag; the exchange waits on the
+                                  flags with stream memory operations               */
+    int32_t reserved[3];
 } dspmv_plan_opts;
+
+enum { DSPMV_EXCHANGE_COPY = 0, DSPMV_EXCHANGE_PUT = 1 };
 
 void dspmv_plan_opts_default(dspmv_plan_opts* opts);
 

@@ -12,7 +12,9 @@
 // WaitSend / WaitRecv synchronise on the group's completion event while
 // polling ncclCommGetAsyncError.  END returns (all GPU work was
 // already host-synchronised by the schedule's own CES ops, R-Q17).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -138,6 +140,133 @@ dspmv_status finalize_send(Plan& p) {
     return DSPMV_OK;
 }
 
+// ------------------------------------------------- DSPMV_EXCHANGE_PUT setup
+struct PutSeg {
+    int64_t begin;
+    char* dst0;        // peer receive buffer + its displacement for us (parity 0)
+    char* dst1;        // same, parity 1
+    unsigned* flag;    // peer flag slot for us
+};
+
+dspmv_status upload_put(Plan& p, const std::vector<PutSeg>& segs) {
+    const int n = int(segs.size());
+    p.put_nseg = n;
+    if (n == 0) return DSPMV_OK;
+    std::vector<int64_t> begin(n + 1);
+    std::vector<void*> dst(2 * n);
+    std::vector<unsigned*> flag(n);
+    for (int j = 0; j < n; ++j) {
+        begin[j] = segs[j].begin;
+        dst[j] = segs[j].dst0;
+        dst[n + j] = segs[j].dst1;
+        flag[j] = segs[j].flag;
+    }
+    begin[n] = int64_t(p.host.pack_map.size());
+    ST_TRY(dev_upload(p, &p.d_seg_begin, begin.data(), begin.size()));
+    ST_TRY(dev_upload(p, &p.d_seg_dst, dst.data(), dst.size()));
+    ST_TRY(dev_upload(p, &p.d_seg_flag, flag.data(), flag.size()));
+    return DSPMV_OK;
+}
+
+// In-process group: peers' buffers are plain device pointers.
+dspmv_status setup_put_local(LocalGroup& g) {
+    for (int r = 0; r < g.nranks; ++r) {
+        Plan& p = *g.plans[r];
+        std::vector<PutSeg> segs;
+        for (int d = 0; d < g.nranks; ++d) {
+            if (p.host.send_count[d] <= 0) continue;
+            Plan& q = *g.plans[d];
+            char* base = static_cast<char*>(q.d_recvbuf) + size_t(q.host.recv_displ[r]) * q.esize;
+            segs.push_back({p.host.send_displ[d], base, base + q.recv_stride * q.esize, q.d_flags + r});
+        }
+        ST_TRY(upload_put(p, segs));
+    }
+    return DSPMV_OK;
+}
+
+// Plan-time all-gather over the comm's transport (NCCL or the HOST callback).
+dspmv_status comm_allgather(Plan& p, const void* send, void* recv, size_t bytes) {
+    Comm& c = *p.comm;
+    if (c.kind == DSPMV_COMM_HOST) {
+        if (c.allgather(send, recv, bytes, c.allgather_ctx) != 0) return fail(DSPMV_ERR_ARG, "allgather callback failed");
+        return DSPMV_OK;
+    }
+    unsigned char *d_in = nullptr, *d_out = nullptr;
+    CUDA_TRY(cudaMalloc(&d_in, bytes));
+    CUDA_TRY(cudaMalloc(&d_out, bytes * c.nranks));
+    CUDA_TRY(cudaMemcpy(d_in, send, bytes, cudaMemcpyHostToDevice));
+    NCCL_TRY(ncclAllGather(d_in, d_out, bytes, ncclUint8, c.nccl, p.comm_stream));
+    CUDA_TRY(cudaStreamSynchronize(p.comm_stream));
+    CUDA_TRY(cudaMemcpy(recv, d_out, bytes * c.nranks, cudaMemcpyDeviceToHost));
+    cudaFree(d_in);
+    cudaFree(d_out);
+    return DSPMV_OK;
+}
+
+// The request-list protocol of plan_create over all-gathers (HOST comms):
+// counts matrix first, then every rank's halo (padded to the longest).
+dspmv_status exchange_requests_allgather(Plan& p) {
+    RankPlan& h = p.host;
+    const int P = h.nranks, me = h.rank;
+    std::vector<int32_t> counts(size_t(P) * P);
+    ST_TRY(comm_allgather(p, h.recv_count.data(), counts.data(), size_t(P) * 4));
+    int64_t hmax = 0;
+    for (int r = 0; r < P; ++r) {
+        int64_t t = 0;
+        for (int q = 0; q < P; ++q) t += counts[size_t(r) * P + q];
+        hmax = std::max(hmax, t);
+    }
+    std::vector<int32_t> mine(size_t(std::max<int64_t>(hmax, 1)), -1), all(size_t(std::max<int64_t>(hmax, 1)) * P);
+    std::copy(h.halo_gid.begin(), h.halo_gid.end(), mine.begin());
+    ST_TRY(comm_allgather(p, mine.data(), all.data(), mine.size() * 4));
+    std::vector<std::vector<int32_t>> req(P);
+    for (int r = 0; r < P; ++r) {
+        int64_t off = 0;
+        for (int q = 0; q < me; ++q) off += counts[size_t(r) * P + q];
+        const int32_t c = counts[size_t(r) * P + me];
+        const int32_t* src = all.data() + size_t(r) * mine.size() + off;
+        req[r].assign(src, src + c);
+    }
+    plan_phase2_from_requests(h, req);
+    return DSPMV_OK;
+}
+
+// Separate processes (NCCL or HOST comm): all-gather every rank's IPC handles
+// (receive buffer, flags), parity stride and receive displacements; map the
+// destinations' buffers (NVLink P2P between GPUs, or the same device).
+dspmv_status setup_put_nccl(Plan& p) {
+    const int P = p.host.nranks, me = p.host.rank;
+    struct Rec {
+        cudaIpcMemHandle_t recv, flags;
+        int64_t h;
+    };
+    const size_t rec_bytes = (sizeof(Rec) + size_t(P) * 4 + 15) & ~size_t(15);
+    std::vector<unsigned char> mine(rec_bytes, 0), all(rec_bytes * P, 0);
+    Rec r{};
+    if (p.d_recvbuf) CUDA_TRY(cudaIpcGetMemHandle(&r.recv, p.d_recvbuf));
+    CUDA_TRY(cudaIpcGetMemHandle(&r.flags, p.d_flags));
+    r.h = int64_t(p.recv_stride);  // parity stride of the receive buffer
+    std::memcpy(mine.data(), &r, sizeof(Rec));
+    std::memcpy(mine.data() + sizeof(Rec), p.host.recv_displ.data(), size_t(P) * 4);
+    ST_TRY(comm_allgather(p, mine.data(), all.data(), rec_bytes));
+    std::vector<PutSeg> segs;
+    for (int d = 0; d < P; ++d) {
+        if (p.host.send_count[d] <= 0) continue;
+        Rec rd;
+        std::memcpy(&rd, all.data() + rec_bytes * d, sizeof(Rec));
+        int32_t displ_me = 0;
+        std::memcpy(&displ_me, all.data() + rec_bytes * d + sizeof(Rec) + size_t(me) * 4, 4);
+        void *rb = nullptr, *fl = nullptr;
+        CUDA_TRY(cudaIpcOpenMemHandle(&rb, rd.recv, cudaIpcMemLazyEnablePeerAccess));
+        p.ipc_opened.push_back(rb);
+        CUDA_TRY(cudaIpcOpenMemHandle(&fl, rd.flags, cudaIpcMemLazyEnablePeerAccess));
+        p.ipc_opened.push_back(fl);
+        char* base = static_cast<char*>(rb) + size_t(displ_me) * p.esize;
+        segs.push_back({p.host.send_displ[d], base, base + size_t(rd.h) * p.esize, static_cast<unsigned*>(fl) + me});
+    }
+    return upload_put(p, segs);
+}
+
 dspmv_status finalize_local_group(LocalGroup& g) {
     const int P = g.nranks;
     for (int p = 0; p < P; ++p) {
@@ -149,6 +278,10 @@ dspmv_status finalize_local_group(LocalGroup& g) {
         CUDA_TRY(cudaSetDevice(g.plans[p]->device));
         ST_TRY(finalize_send(*g.plans[p]));
     }
+    for (int p = 1; p < P; ++p)
+        if (g.plans[p]->put_mode != g.plans[0]->put_mode)
+            return fail(DSPMV_ERR_ARG, "every rank of a group must use the same exchange mode");
+    if (g.plans[0]->put_mode) ST_TRY(setup_put_local(g));
     return DSPMV_OK;
 }
 
@@ -230,9 +363,22 @@ cudaError_t host_wait(cudaEvent_t ev) {
 
 dspmv_status wait_exchange(Plan& p) {
     if (!p.has_peers) return DSPMV_OK;  // nothing was sent or received
-    if (p.comm->kind == DSPMV_COMM_LOCAL || p.host.nranks == 1) {
-        CUDA_TRY(host_wait(p.ev_x));
-        return DSPMV_OK;
+    if (p.comm->kind != DSPMV_COMM_NCCL || p.host.nranks == 1) {
+        if (!p.put_mode || p.comm->kind == DSPMV_COMM_LOCAL) {
+            CUDA_TRY(host_wait(p.ev_x));
+            return DSPMV_OK;
+        }
+        // PUT across processes: a peer that never publishes must not hang us
+        const auto t0 = std::chrono::steady_clock::now();
+        for (;;) {
+            const cudaError_t q = cudaEventQuery(p.ev_x);
+            if (q == cudaSuccess) return DSPMV_OK;
+            if (q != cudaErrorNotReady) return fail(DSPMV_ERR_CUDA, std::string("exchange: ") + cudaGetErrorString(q));
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60)) {
+                p.poisoned = true;
+                return fail(DSPMV_ERR_STATE, "PUT exchange: peer flags not published within 60 s");
+            }
+        }
     }
     const auto t_start = std::chrono::steady_clock::now();
     for (;;) {
@@ -284,7 +430,40 @@ dspmv_status issue_exchange_nccl(Plan& p) {
     return DSPMV_OK;
 }
 
+PFN_cuStreamWaitValue32_v11070 wait_value32() {
+    static PFN_cuStreamWaitValue32_v11070 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(f);
+    }();
+    return fn;
+}
+
+// PUT mode: the data moves inside the fused Pack kernels; the exchange is the
+// comm stream waiting until every source rank has published this epoch.
+dspmv_status issue_exchange_put(Plan& p) {
+    p.issued = true;
+    if (!p.has_peers) return DSPMV_OK;
+    auto wv = wait_value32();
+    if (!wv) return fail(DSPMV_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+    for (int q = 0; q < p.host.nranks; ++q) {
+        if (p.host.recv_count[q] <= 0) continue;
+        const CUresult r = wv(reinterpret_cast<CUstream>(p.comm_stream), reinterpret_cast<CUdeviceptr>(p.d_flags + q),
+                              p.epoch, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS) return fail(DSPMV_ERR_CUDA, "cuStreamWaitValue32 failed (" + std::to_string(int(r)) + ")");
+    }
+    CUDA_TRY(cudaEventRecord(p.ev_x, p.comm_stream));
+    return DSPMV_OK;
+}
+
 dspmv_status issue_exchange_local(const std::vector<Plan*>& ps) {
+    if (!ps.empty() && ps[0]->put_mode) {
+        for (Plan* pr : ps) ST_TRY(issue_exchange_put(*pr));
+        return DSPMV_OK;
+    }
     for (Plan* pr : ps) {
         const RankPlan& h = pr->host;
         for (int q = 0; q < h.nranks; ++q) {
@@ -309,6 +488,7 @@ dspmv_status begin_apply(Schedule& s, cudaStream_t caller) {
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess || cur != p.device) CUDA_TRY(cudaSetDevice(p.device));
     if (s.step0) CUDA_TRY(cudaEventRecord(s.step0, caller));
+    ++p.epoch;
     CUDA_TRY(cudaEventRecord(p.ev_start, caller));
     // schedule stream 0 may be the caller's stream itself (no cross-stream
     // wait for its work); the others wait on the caller's START point
@@ -334,16 +514,27 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
         case DSPMV_OP_END:
             break;
         case DSPMV_OP_PACK:
-            e = launch_pack(p.dtype, x, p.d_pack_map, p.d_sendbuf, int64_t(p.host.pack_map.size()), st);
+            if (p.put_mode) {
+                PutArgs a{x, p.d_pack_map, int64_t(p.host.pack_map.size()), p.d_seg_begin,
+                          p.d_seg_dst + (p.epoch & 1u) * p.put_nseg, p.d_seg_flag, p.put_nseg, p.epoch,
+                          p.d_put_counter};
+                e = launch_pack_put(p.dtype, a, st);
+            } else {
+                e = launch_pack(p.dtype, x, p.d_pack_map, p.d_sendbuf, int64_t(p.host.pack_map.size()), st);
+            }
             break;
         case DSPMV_OP_SPMV_LOCAL: {
             SpmvOperands op{x, y, p.d_partL, p.d_partR, p.d_ticket};
             e = launch_spmv(p.L, p.dtype, op, st);
             break;
         }
-        case DSPMV_OP_UNPACK:
-            e = launch_copy(p.dtype, p.d_recvbuf, p.d_xhalo, int64_t(p.host.halo_gid.size()), st);
+        case DSPMV_OP_UNPACK: {
+            const size_t h = p.host.halo_gid.size();
+            const char* src = static_cast<const char*>(p.d_recvbuf) +
+                              (p.put_mode && (p.epoch & 1u) ? p.recv_stride * size_t(p.esize) : 0);
+            e = launch_copy(p.dtype, src, p.d_xhalo, int64_t(h), st);
             break;
+        }
         case DSPMV_OP_SPMV_REMOTE: {
             SpmvOperands op{p.d_xhalo, y, p.d_partR, p.d_partL, p.d_ticket};
             e = launch_spmv(p.R, p.dtype, op, st);
@@ -353,7 +544,7 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
         case DSPMV_OP_POST_RECV:
             if (o.kind == DSPMV_OP_POST_SEND) p.posted_send = true; else p.posted_recv = true;
             if (!defer && p.posted_send && p.posted_recv && !p.issued) {
-                dspmv_status r = issue_exchange_nccl(p);
+                dspmv_status r = p.put_mode ? issue_exchange_put(p) : issue_exchange_nccl(p);
                 if (r != DSPMV_OK) {
                     p.poisoned = true;
                     return r;
@@ -469,6 +660,21 @@ dspmv_status dspmv_comm_create_local(int nranks, int cuda_device, dspmv_comm_t* 
     return DSPMV_OK;
 }
 
+dspmv_status dspmv_comm_create_host(int nranks, int rank, int cuda_device, dspmv_allgather_fn allgather, void* ctx,
+                                    dspmv_comm_t* out) {
+    if (!out || !allgather || nranks < 1 || rank < 0 || rank >= nranks) return fail(DSPMV_ERR_ARG, "bad host comm arguments");
+    CUDA_TRY(cudaSetDevice(cuda_device));
+    auto* c = new dspmv_comm_s();
+    c->kind = DSPMV_COMM_HOST;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = cuda_device;
+    c->allgather = allgather;
+    c->allgather_ctx = ctx;
+    *out = c;
+    return DSPMV_OK;
+}
+
 dspmv_status dspmv_comm_destroy(dspmv_comm_t comm) {
     if (!comm) return fail(DSPMV_ERR_ARG, "null comm");
     if (comm->live_plans > 0) return fail(DSPMV_ERR_STATE, "comm still has live plans");
@@ -496,11 +702,14 @@ void dspmv_plan_opts_default(dspmv_plan_opts* o) {
     o->block_cfg = -1;
     o->caller_stream0 = 0;
     o->reserve_sms = -1;
+    o->exchange = DSPMV_EXCHANGE_COPY;
     if (const char* ev = std::getenv("DSPMV_CALLER_STREAM0")) o->caller_stream0 = std::atoi(ev);
     if (const char* ev = std::getenv("DSPMV_RESERVE_SMS")) o->reserve_sms = std::atoi(ev);
 }
 
 static void free_plan_device(Plan& p) {
+    for (void* a : p.ipc_opened) cudaIpcCloseMemHandle(a);
+    p.ipc_opened.clear();
     for (void* a : p.allocs) cudaFree(a);
     p.allocs.clear();
     for (auto& s : p.streams)
@@ -588,7 +797,22 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
         if ((st = upload_layout(*p, R, c, p->R)) != DSPMV_OK) return bail(st);
     }
     const size_t hsz = h.halo_gid.size();
-    if ((st = dev_alloc(*p, &p->d_recvbuf, hsz * p->esize, true)) != DSPMV_OK) return bail(st);
+    p->put_mode = opts.exchange == DSPMV_EXCHANGE_PUT;
+    if (opts.exchange != DSPMV_EXCHANGE_COPY && opts.exchange != DSPMV_EXCHANGE_PUT)
+        return bail(fail(DSPMV_ERR_ARG, "bad exchange mode"));
+    // PUT: two receive buffers (apply parity) -- a rank may run one apply ahead
+    // parity stride padded to 256 B so both halves stay 16-B aligned for Unpack
+    p->recv_stride = ((hsz * p->esize + 255) / 256 * 256) / p->esize;
+    if ((st = dev_alloc(*p, &p->d_recvbuf,
+                        p->put_mode ? std::max<size_t>(2 * p->recv_stride * p->esize, 256) : hsz * p->esize, true)) !=
+        DSPMV_OK)
+        return bail(st);
+    if (p->put_mode) {
+        // own allocation (IPC-exportable); at least one word so every rank has a handle
+        if ((st = dev_alloc(*p, reinterpret_cast<void**>(&p->d_flags), size_t(comm->nranks) * 4, true)) != DSPMV_OK)
+            return bail(st);
+        if ((st = dev_alloc(*p, reinterpret_cast<void**>(&p->d_put_counter), 4, true)) != DSPMV_OK) return bail(st);
+    }
     if ((st = dev_alloc(*p, &p->d_xhalo, hsz * p->esize, true)) != DSPMV_OK) return bail(st);
     if ((st = dev_alloc(*p, &p->d_partL, size_t(nR) * p->esize, true)) != DSPMV_OK) return bail(st);
     if ((st = dev_alloc(*p, &p->d_partR, size_t(nR) * p->esize, true)) != DSPMV_OK) return bail(st);
@@ -604,9 +828,13 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
     }
 
     // phase 2: request lists -> send counts + pack maps
-    if (comm->kind == DSPMV_COMM_NCCL) {
-        if ((st = exchange_requests_nccl(*p)) != DSPMV_OK) return bail(st);
+    if (comm->kind == DSPMV_COMM_NCCL || comm->kind == DSPMV_COMM_HOST) {
+        if (comm->kind == DSPMV_COMM_HOST && !p->put_mode)
+            return bail(fail(DSPMV_ERR_ARG, "plans on a HOST comm need exchange = DSPMV_EXCHANGE_PUT"));
+        st = comm->kind == DSPMV_COMM_NCCL ? exchange_requests_nccl(*p) : exchange_requests_allgather(*p);
+        if (st != DSPMV_OK) return bail(st);
         if ((st = finalize_send(*p)) != DSPMV_OK) return bail(st);
+        if (p->put_mode && comm->nranks > 1 && (st = setup_put_nccl(*p)) != DSPMV_OK) return bail(st);
     } else {
         LocalGroup& g = *comm->group;
         g.plans[comm->rank] = p;

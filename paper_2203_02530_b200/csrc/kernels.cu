@@ -392,6 +392,33 @@ __global__ void pack_kernel(const T* __restrict__ x, const int32_t* __restrict__
         out[i] = __ldg(x + __ldg(map + i));
 }
 
+// Fused Pack + put over peer memory (NEXT-3 (ii)): each entry of
+// the send list is gathered from x and stored straight into the destination
+// rank's receive buffer; after a system-scope fence the last CTA to finish
+// publishes the epoch flag of this rank on every destination.
+template <typename T>
+__global__ void pack_put_kernel(PutArgs a) {
+    const T* __restrict__ x = static_cast<const T*>(a.x);
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < a.n; k += int64_t(gridDim.x) * blockDim.x) {
+        int j = 0;
+        while (j + 1 < a.nseg && a.seg_begin[j + 1] <= k) ++j;   // nseg = destinations (<= P)
+        static_cast<T*>(a.seg_dst[j])[k - a.seg_begin[j]] = __ldg(x + __ldg(a.pack_map + k));
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        cuda::atomic_ref<unsigned, cuda::thread_scope_device> c(*a.counter);
+        if (c.fetch_add(1u, cuda::memory_order_acq_rel) == gridDim.x - 1) {
+            c.store(0u, cuda::memory_order_relaxed);          // ready for the next apply
+            __threadfence_system();
+            for (int j = 0; j < a.nseg; ++j) {
+                cuda::atomic_ref<unsigned, cuda::thread_scope_system> f(*a.seg_flag[j]);
+                f.store(a.epoch, cuda::memory_order_release);
+            }
+        }
+    }
+}
+
 __global__ void copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int64_t n16,
                             const unsigned char* __restrict__ s8, unsigned char* __restrict__ d8,
                             int64_t tail_from, int64_t tail_to) {
@@ -551,6 +578,15 @@ cudaError_t launch_pack(int dtype, const void* x, const int32_t* map, void* out,
         pack_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), map, static_cast<float*>(out), n);
     else
         pack_kernel<double><<<grid, 256, 0, s>>>(static_cast<const double*>(x), map, static_cast<double*>(out), n);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_put(int dtype, const PutArgs& a, cudaStream_t s) {
+    if (a.nseg <= 0) return cudaSuccess;
+    const int grid = int(std::max<int64_t>(1, std::min<int64_t>((a.n + 255) / 256, int64_t(num_sms()) * 4)));
+    if (dtype == DSPMV_F32) pack_put_kernel<float><<<grid, 256, 0, s>>>(a);
+    else pack_put_kernel<double><<<grid, 256, 0, s>>>(a);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
 }

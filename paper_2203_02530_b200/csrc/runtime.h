@@ -53,6 +53,21 @@ cudaError_t launch_pack(int dtype, const void* x, const int32_t* map, void* out,
                         cudaStream_t s);
 cudaError_t launch_copy(int dtype, const void* src, void* dst, int64_t n, cudaStream_t s);
 cudaError_t launch_flush(void* buf, size_t bytes, cudaStream_t s);
+// fused Pack + put (DSPMV_EXCHANGE_PUT): entries [seg_begin[j], seg_begin[j+1])
+// go to seg_dst[j] (peer receive buffer, this apply's parity); the last CTA
+// publishes `epoch` to every seg_flag[j] with a system-scope release.
+struct PutArgs {
+    const void* x;
+    const int32_t* pack_map;
+    int64_t n;
+    const int64_t* seg_begin;   // [nseg + 1]
+    void* const* seg_dst;       // [nseg]
+    unsigned* const* seg_flag;  // [nseg]
+    int nseg;
+    unsigned epoch;
+    unsigned* counter;          // last-CTA detection, self-resetting
+};
+cudaError_t launch_pack_put(int dtype, const PutArgs& a, cudaStream_t s);
 
 struct Plan;
 
@@ -68,6 +83,8 @@ struct Comm {
     int nranks = 1, rank = 0, device = 0;
     ncclComm_t nccl = nullptr;
     std::shared_ptr<LocalGroup> group;
+    dspmv_allgather_fn allgather = nullptr;  // HOST comms
+    void* allgather_ctx = nullptr;
     int live_plans = 0;
     bool poisoned = false;
 };
@@ -96,6 +113,17 @@ struct Plan {
     int64_t device_bytes = 0;
     bool ready = false;                // phase 2 done (send lists, pack map)
     bool has_peers = false;            // anything to send or receive
+    // DSPMV_EXCHANGE_PUT state
+    bool put_mode = false;
+    size_t recv_stride = 0;            // elements between the two receive buffers
+    unsigned epoch = 0;                // applies so far (parity selects the receive buffer)
+    unsigned* d_flags = nullptr;       // [P] epoch written by each source rank
+    unsigned* d_put_counter = nullptr;
+    int put_nseg = 0;
+    int64_t* d_seg_begin = nullptr;    // [nseg + 1]
+    void** d_seg_dst = nullptr;        // [2][nseg] (parity 0 / 1)
+    unsigned** d_seg_flag = nullptr;   // [nseg]
+    std::vector<void*> ipc_opened;     // peer mappings to close
     bool poisoned = false;
     int live_scheds = 0;
     // per-apply exchange state

@@ -29,7 +29,8 @@ DSPMV_OK, DSPMV_ERR_ARG, DSPMV_ERR_RANGE, DSPMV_ERR_SCHEDULE, DSPMV_ERR_DEADLOCK
 STATUS_NAMES = ["OK", "ERR_ARG", "ERR_RANGE", "ERR_SCHEDULE", "ERR_DEADLOCK", "ERR_STATE",
                 "ERR_CUDA", "ERR_NCCL", "ERR_OOM"]
 DSPMV_F64, DSPMV_F32 = 0, 1
-DSPMV_COMM_NCCL, DSPMV_COMM_LOCAL = 0, 1
+DSPMV_COMM_NCCL, DSPMV_COMM_LOCAL, DSPMV_COMM_HOST = 0, 1, 2
+DSPMV_EXCHANGE_COPY, DSPMV_EXCHANGE_PUT = 0, 1
 (DSPMV_OP_START, DSPMV_OP_PACK, DSPMV_OP_SPMV_LOCAL, DSPMV_OP_POST_SEND, DSPMV_OP_POST_RECV,
  DSPMV_OP_WAIT_SEND, DSPMV_OP_WAIT_RECV, DSPMV_OP_UNPACK, DSPMV_OP_SPMV_REMOTE, DSPMV_OP_END,
  DSPMV_OP_EVENT_RECORD, DSPMV_OP_EVENT_SYNC, DSPMV_OP_STREAM_WAIT_EVENT) = range(13)
@@ -52,7 +53,8 @@ class dspmv_plan_opts(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int32), ("vector_threshold", ctypes.c_int32),
                 ("keep_host", ctypes.c_int32), ("comm_priority", ctypes.c_int32),
                 ("block_cfg", ctypes.c_int32), ("caller_stream0", ctypes.c_int32),
-                ("reserve_sms", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
+                ("reserve_sms", ctypes.c_int32), ("exchange", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 3)]
 
 
 class dspmv_plan_info(ctypes.Structure):
@@ -93,6 +95,8 @@ _sig("dspmv_comm_unique_id", [_P])
 _sig("dspmv_comm_create", [_P, _I, _I, _I, _P])
 _sig("dspmv_comm_create_local", [_I, _I, _P])
 _sig("dspmv_comm_destroy", [_P])
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+_sig("dspmv_comm_create_host", [_I, _I, _I, ALLGATHER_FN, _P, _P])
 _sig("dspmv_comm_info", [_P, _P, _P, _P])
 _sig("dspmv_partition", [_I64, _I, _P])
 _sig("dspmv_plan_opts_default", [_P], None)
@@ -190,6 +194,25 @@ def dspmv_comm_create_local(nranks: int, device: int):
     return [_P(h) for h in hs]
 
 
+def dspmv_comm_create_host(nranks: int, rank: int, device: int, allgather):
+    """allgather(send: bytes) -> bytes (nranks*len(send), rank order); e.g.
+    backed by torch.distributed (gloo).  The callback object is kept alive
+    on the returned handle."""
+    def _cb(send, recv, nbytes, ctx):
+        try:
+            out = allgather(ctypes.string_at(send, nbytes))
+            assert len(out) == nranks * nbytes
+            ctypes.memmove(recv, out, len(out))
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to C as a failure status
+            return 1
+    cb = ALLGATHER_FN(_cb)
+    h = _P()
+    _check(lib.dspmv_comm_create_host(nranks, rank, device, cb, None, ctypes.byref(h)))
+    h._cb = cb
+    return h
+
+
 def dspmv_comm_destroy(comm):
     _check(lib.dspmv_comm_destroy(comm))
 
@@ -203,7 +226,8 @@ def dspmv_comm_info(comm):
 def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_F64,
                       vector_threshold: int = -1, keep_host: bool = False,
                       comm_priority: bool = True, block_cfg: int = -1,
-                      caller_stream0: bool | None = None, reserve_sms: int | None = None):
+                      caller_stream0: bool | None = None, reserve_sms: int | None = None,
+                      exchange: int = DSPMV_EXCHANGE_COPY):
     """rowptr int64[n_local+1], col int32[nnz] (global ids), val float64/32."""
     rowptr = np.ascontiguousarray(rowptr, np.int64)
     col = np.ascontiguousarray(col_global, np.int32)
@@ -219,6 +243,7 @@ def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_
         o.caller_stream0 = int(caller_stream0)
     if reserve_sms is not None:
         o.reserve_sms = int(reserve_sms)
+    o.exchange = int(exchange)
     h = _P()
     _check(lib.dspmv_plan_create(comm, n_global, len(rowptr) - 1, rowptr.ctypes.data,
                                  col.ctypes.data, val.ctypes.data, ctypes.byref(o),

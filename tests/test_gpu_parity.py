@@ -363,3 +363,48 @@ def test_full_size_c5_7pt_192_four_ranks_sampled():
     """BASELINE configs[4] matrix (7-pt 192^3) over 4 in-process ranks."""
     n, (rp, col, val) = gen.config_matrix("c5")
     _sampled_check(n, rp, col, val, 4)
+
+
+@pytest.mark.parametrize("name,P", [("pl20k", 2), ("pl20k", 8), ("27pt20", 4), ("rand300", 3), ("5pt64", 2)])
+def test_fused_pack_put_exchange(name, P):
+    """DSPMV_EXCHANGE_PUT: Pack stores straight into the peers' receive
+    buffers (parity double-buffered, epoch flags, stream wait-value) -- same
+    bits as the copy exchange, over several applies (both parities)."""
+    for exact in (True, False):
+        n, (rp, col, val) = _mat(name, exact)
+        x = gen.x_values((0, n), exact=exact)
+        out = {}
+        for mode in (D.DSPMV_EXCHANGE_COPY, D.DSPMV_EXCHANGE_PUT):
+            run = LocalRun(n, rp, col, val, P, exchange=mode)
+            try:
+                out[mode] = run.apply(run.schedule(derive_ops()), x, reps=3)
+            finally:
+                run.close()
+        assert np.array_equal(out[0].view(np.uint64), out[1].view(np.uint64))
+        plans = O2.plan_all(rp, col, n, P)
+        yref = O2.simulate(plans, val, x, [(v,) for v in S.topological_orders(S.EDGES)[0]])
+        if exact:
+            assert np.array_equal(out[1], yref)
+        else:
+            assert within_tol(out[1], yref, O1.o1_absdot(rp, col, val, x), 1e-12)
+
+
+def test_fused_pack_put_every_schedule_c1():
+    """All 768 schedules with the fused exchange: identical bits (C1)."""
+    n, (rp, col, val) = gen.config_matrix("c1")
+    x = gen.x_values((0, n))
+    run = LocalRun(n, rp, col, val, 2, exchange=D.DSPMV_EXCHANGE_PUT)
+    try:
+        first = None
+        for ops in S.enumerate_derived(2, S.EDGES):
+            ss = run.schedule(oracle_ops_to_lib(ops))
+            y = run.apply(ss, x)
+            for s_ in ss:
+                D.dspmv_schedule_destroy(s_)
+            run.scheds.pop()
+            if first is None:
+                first = y
+            assert np.array_equal(y.view(np.uint64), first.view(np.uint64))
+    finally:
+        run.close()
+    assert within_tol(first, O1.o1_spmv(rp, col, val, x), O1.o1_absdot(rp, col, val, x), 1e-12)
