@@ -57,6 +57,9 @@ def parse():
                     help="schedule stream 0 is the caller's stream (plan option)")
     ap.add_argument("--rerank", type=int, default=16,
                     help="re-time the k fastest sweep schedules with the step method")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "copy", "put"],
+                    help="halo exchange: NCCL group (copy), fused Pack+put over peer memory "
+                         "(put), or auto = time both at N>1 and keep the faster")
     return ap.parse_args()
 
 
@@ -225,10 +228,18 @@ def run_ours(a):
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     comm = D.dspmv_comm_create(uid, world, rank, local)
-    plan = D.dspmv_plan_create(comm, n, rp, col, val.astype(npdt), dtype=dt,
-                               caller_stream0=bool(a.caller_stream0))
+    valn = val.astype(npdt)
+    mk = lambda ex: D.dspmv_plan_create(comm, n, rp, col, valn, dtype=dt,  # noqa: E731
+                                        caller_stream0=bool(a.caller_stream0), exchange=ex)
+    exchange_note = None
+    if world == 1 or a.exchange == "copy":
+        plan, exchange = mk(D.DSPMV_EXCHANGE_COPY), "copy (NCCL group)"
+    elif a.exchange == "put":
+        plan, exchange = mk(D.DSPMV_EXCHANGE_PUT), "put (fused Pack+put over peer memory)"
+    else:
+        plan, exchange, exchange_note = choose_exchange(D, mk, n, lo, hi, npdt, world, dist)
     info = D.dspmv_plan_info_get(plan)
-    del col, val
+    del col, val, valn
     import gen
     x = torch.from_numpy(gen.x_values((lo, hi)).astype(npdt)).cuda()
     y = torch.empty_like(x)
@@ -379,7 +390,8 @@ def run_ours(a):
             "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
             "config": {
                 "workload": desc, "n_global": n, "nnz_global": int(nnz_total),
-                "ranks": world, "parallelism": f"row-partition x{world} (NCCL halo exchange)",
+                "ranks": world, "parallelism": f"row-partition x{world}, halo exchange: {exchange}",
+                "exchange_selection": exchange_note,
                 "schedule": sched_desc,
                 "l2": "flushed between timed steps (flush kernel reads 2x L2, outside per-step CUDA events)",
                 "step_timing": ("CUDA events recorded by dspmv_apply on the caller stream at START "
@@ -414,6 +426,48 @@ def run_ours(a):
     D.dspmv_comm_destroy(comm)
     if world > 1:
         dist.destroy_process_group()
+
+
+def choose_exchange(D, mk, n, lo, hi, npdt, world, dist):
+    """N > 1: build both exchange variants, time each with the class-1
+    schedule (same inputs, max over ranks) and keep the faster.  A PUT setup
+    or run failure falls back to the NCCL copy exchange."""
+    import torch
+    import gen
+    order = [VERTS.index(v) for v in BEST_ORDER]
+    ops = D.dspmv_schedule_derive(order, [BEST_STREAMS.get(v, 0) for v in BEST_ORDER], 2)
+    x = torch.from_numpy(gen.x_values((lo, hi)).astype(npdt)).cuda()
+    y = torch.empty_like(x)
+    times, plans = {}, {}
+    for name, ex in (("copy", D.DSPMV_EXCHANGE_COPY), ("put", D.DSPMV_EXCHANGE_PUT)):
+        ok = 1.0
+        try:
+            p = mk(ex)
+            s = D.dspmv_schedule_create(p, ops, 2)
+            for _ in range(10):
+                D.dspmv_apply(s, x, y)
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(50):
+                D.dspmv_apply(s, x, y)
+            torch.cuda.synchronize()
+            t = (time.perf_counter() - t0) / 50
+            D.dspmv_schedule_destroy(s)
+            plans[name] = p
+        except Exception:  # noqa: BLE001 -- the alternative is reported, not fatal
+            ok, t = 0.0, float("inf")
+        tt = torch.tensor([t if ok else 1e9, ok], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt[1:], op=dist.ReduceOp.MIN)
+        times[name] = float(tt[0].item()) if tt[1].item() > 0 else None
+    best = "put" if times.get("put") is not None and times["put"] < times["copy"] else "copy"
+    for name, p in plans.items():
+        if name != best:
+            D.dspmv_plan_destroy(p)
+    label = {"copy": "copy (NCCL group)", "put": "put (fused Pack+put over peer memory)"}[best]
+    note = {k: (round(v * 1e6, 2) if v is not None else "failed") for k, v in times.items()}
+    return plans[best], label, {"us_per_apply_class1_schedule": note, "chosen": best}
 
 
 def schedule_sweep(D, plan, x, y, stream, world, rank, dist, barrier, t_measure=0.01):
