@@ -461,7 +461,10 @@ def choose_exchange(D, mk, n, lo, hi, npdt, world, dist):
         dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
         dist.all_reduce(tt[1:], op=dist.ReduceOp.MIN)
         times[name] = float(tt[0].item()) if tt[1].item() > 0 else None
-    best = "put" if times.get("put") is not None and times["put"] < times["copy"] else "copy"
+    if times.get("copy") is None and times.get("put") is None:
+        raise RuntimeError("neither halo exchange variant could be set up")
+    best = "put" if times.get("put") is not None and (times.get("copy") is None or times["put"] < times["copy"]) \
+        else "copy"
     for name, p in plans.items():
         if name != best:
             D.dspmv_plan_destroy(p)
