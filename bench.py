@@ -31,6 +31,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+_RED_DEV = "cuda"   # device of the small reduction tensors ("cpu" with gloo)
 METRIC = "SpMV GFLOP/s, HBM GB/s vs peak at 1/2/4/8 B200; schedule fast/slow ratio"
 BEST_ORDER = ["start", "PostRecv", "Pack", "y_L", "PostSend", "WaitRecv", "Unpack", "y_R",
               "WaitSend", "end"]
@@ -57,6 +58,9 @@ def parse():
                     help="schedule stream 0 is the caller's stream (plan option)")
     ap.add_argument("--rerank", type=int, default=16,
                     help="re-time the k fastest sweep schedules with the step method")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "host"],
+                    help="host: gloo process group + HOST-transport communicator with the fused "
+                         "put exchange (lets N ranks share one GPU, for testing the N>1 path)")
     ap.add_argument("--exchange", default="auto", choices=["auto", "copy", "put"],
                     help="halo exchange: NCCL group (copy), fused Pack+put over peer memory "
                          "(put), or auto = time both at N>1 and keep the faster")
@@ -211,9 +215,15 @@ def run_ours(a):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != a.gpus:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
+    device = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(device)
+    global _RED_DEV
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if a.comm == "host":
+            dist.init_process_group("gloo")
+            _RED_DEV = "cpu"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
     dt = D.DSPMV_F32 if a.dtype == "f32" else D.DSPMV_F64
     v = 4 if dt == D.DSPMV_F32 else 8
     npdt = np.float32 if dt == D.DSPMV_F32 else np.float64
@@ -222,17 +232,25 @@ def run_ours(a):
     desc, n, (lo, hi), rp, col, val = workload(a.workload, world, rank)
     nnz_rank = int(rp[-1] - rp[0])
     # library NCCL communicator (bootstrapped through torch.distributed)
-    uid = D.dspmv_comm_unique_id() if rank == 0 else None
-    if world > 1:
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
-    comm = D.dspmv_comm_create(uid, world, rank, local)
+    if a.comm == "host":
+        def allgather(b: bytes) -> bytes:
+            out = [None] * world
+            dist.all_gather_object(out, b) if world > 1 else out.__setitem__(0, b)
+            return b"".join(out)
+        comm = D.dspmv_comm_create_host(world, rank, device, allgather)
+        a.exchange = "put"
+    else:
+        uid = D.dspmv_comm_unique_id() if rank == 0 else None
+        if world > 1:
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        comm = D.dspmv_comm_create(uid, world, rank, device)
     valn = val.astype(npdt)
     mk = lambda ex: D.dspmv_plan_create(comm, n, rp, col, valn, dtype=dt,  # noqa: E731
                                         caller_stream0=bool(a.caller_stream0), exchange=ex)
     exchange_note = None
-    if world == 1 or a.exchange == "copy":
+    if (world == 1 and a.comm == "nccl") or a.exchange == "copy":
         plan, exchange = mk(D.DSPMV_EXCHANGE_COPY), "copy (NCCL group)"
     elif a.exchange == "put":
         plan, exchange = mk(D.DSPMV_EXCHANGE_PUT), "put (fused Pack+put over peer memory)"
@@ -252,14 +270,14 @@ def run_ours(a):
 
     def allmax(t):
         if world > 1:
-            tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+            tt = torch.tensor([t], dtype=torch.float64, device=_RED_DEV)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             return float(tt.item())
         return t
 
     def allsum(t):
         if world > 1:
-            tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+            tt = torch.tensor([t], dtype=torch.float64, device=_RED_DEV)
             dist.all_reduce(tt, op=dist.ReduceOp.SUM)
             return float(tt.item())
         return t
@@ -285,7 +303,7 @@ def run_ours(a):
                     D.dspmv_apply(sc, x, y, stream)
                 barrier()
                 for _ in range(30):
-                    D.dspmv_l2_flush(local, stream)
+                    D.dspmv_l2_flush(device, stream)
                     D.dspmv_apply(sc, x, y, stream)
                     tot += float(D.dspmv_schedule_op_times(sc)[0])
                 tot = allmax(tot)
@@ -306,10 +324,10 @@ def run_ours(a):
     D.dspmv_schedule_set_timing(sched, (1 << D.DSPMV_OP_SPMV_LOCAL) | (1 << D.DSPMV_OP_START))
     iyl = [i for i, o in enumerate(ops) if o[0] == D.DSPMV_OP_SPMV_LOCAL][0]
 
-    clocks = Clocks(list(range(world))) if rank == 0 else None
+    clocks = Clocks(list(range(min(world, torch.cuda.device_count())))) if rank == 0 else None
     # ---- warmup
     for _ in range(a.warmup):
-        D.dspmv_l2_flush(local, stream)
+        D.dspmv_l2_flush(device, stream)
         D.dspmv_apply(sched, x, y, stream)
     barrier()
 
@@ -325,7 +343,7 @@ def run_ours(a):
     step_ms_rank = 0.0
     tl_begin, tl_end = [], []
     for k in range(a.steps):
-        D.dspmv_l2_flush(local, stream)
+        D.dspmv_l2_flush(device, stream)
         evs[k][0].record(stream)
         D.dspmv_apply(sched, x, y, stream)
         evs[k][1].record(stream)
@@ -368,7 +386,7 @@ def run_ours(a):
                for _ in range(e2e_steps)]
     barrier()
     for k in range(e2e_steps):
-        D.dspmv_l2_flush(local, stream)
+        D.dspmv_l2_flush(device, stream)
         e2e_evs[k][0].record(stream)
         D.dspmv_apply_host(sched, xh, yh, stream)
         e2e_evs[k][1].record(stream)
@@ -457,7 +475,7 @@ def choose_exchange(D, mk, n, lo, hi, npdt, world, dist):
             plans[name] = p
         except Exception:  # noqa: BLE001 -- the alternative is reported, not fatal
             ok, t = 0.0, float("inf")
-        tt = torch.tensor([t if ok else 1e9, ok], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([t if ok else 1e9, ok], dtype=torch.float64, device=_RED_DEV)
         dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
         dist.all_reduce(tt[1:], op=dist.ReduceOp.MIN)
         times[name] = float(tt[0].item()) if tt[1].item() > 0 else None
@@ -495,7 +513,7 @@ def schedule_sweep(D, plan, x, y, stream, world, rank, dist, barrier, t_measure=
         D.dspmv_apply(s, x, y, stream)
         n = max(1, math.ceil(t_measure / max(time.perf_counter() - t0, 1e-7)))
         if dist is not None:
-            nt = torch.tensor([n], dtype=torch.int64, device="cuda")
+            nt = torch.tensor([n], dtype=torch.int64, device=_RED_DEV)
             dist.broadcast(nt, src=0)
             n = int(nt.item())
         barrier()
@@ -504,7 +522,7 @@ def schedule_sweep(D, plan, x, y, stream, world, rank, dist, barrier, t_measure=
             D.dspmv_apply(s, x, y, stream)
         t = (time.perf_counter() - t0) / n
         if dist is not None:
-            tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+            tt = torch.tensor([t], dtype=torch.float64, device=_RED_DEV)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t = float(tt.item())
         times.append(t)

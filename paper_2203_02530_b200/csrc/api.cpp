@@ -1125,6 +1125,7 @@ dspmv_status dspmv_schedule_set_timing(dspmv_schedule_t s, int enable) {
 dspmv_status dspmv_schedule_op_times(dspmv_schedule_t s, float* ms, int n) {
     if (!s || !ms) return fail(DSPMV_ERR_ARG, "null argument");
     if (!s->timing || !s->timed_valid) return fail(DSPMV_ERR_STATE, "timing not enabled or no apply yet");
+    if (s->step1) CUDA_TRY(cudaEventSynchronize(s->step1));  // recorded at END, may still be queued
     for (int t = 0; t < n && t < int(s->ops.size()); ++t) {
         ms[t] = 0.f;
         if (s->t0[t]) CUDA_TRY(cudaEventElapsedTime(&ms[t], s->t0[t], s->t1[t]));
@@ -1137,6 +1138,7 @@ dspmv_status dspmv_schedule_op_timeline(dspmv_schedule_t s, float* begin_ms, flo
     if (!s || !begin_ms || !end_ms) return fail(DSPMV_ERR_ARG, "null argument");
     if (!s->timing || !s->timed_valid || !s->step0)
         return fail(DSPMV_ERR_STATE, "timeline needs timing with the START bit and an apply");
+    CUDA_TRY(cudaEventSynchronize(s->step1));
     for (int t = 0; t < n && t < int(s->ops.size()); ++t) {
         begin_ms[t] = end_ms[t] = -1.f;
         if (s->t0[t]) {

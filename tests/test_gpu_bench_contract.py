@@ -44,3 +44,25 @@ def test_bench_line_reference():
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_bench_multirank_path_on_one_gpu():
+    """torchrun with 2 ranks sharing cuda:0 (--comm host: gloo + HOST
+    communicator + fused put exchange): the N>1 code path of bench.py --
+    schedule sweep across ranks, max-over-ranks timing, JSON line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--comm", "host", "--steps", "10", "--warmup", "3", "--rerank", "2"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-4000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert "put" in d["config"]["parallelism"] and d["schedule_sweep"]["n_schedules"] == 768
+    assert d["config"]["nnz_global"] > 2 * 14_000_000
