@@ -15,11 +15,12 @@ cases = [("7pt", 16 ** 3, gen.stencil("7pt", (16, 16, 16))),
 for name, n, (rp, col, val) in cases:
     for P in (1, 3):
         for dt in (D.DSPMV_F64, D.DSPMV_F32):
-            v = val.astype(np.float32) if dt == D.DSPMV_F32 else val
-            run = LocalRun(n, rp, col, v, P, dtype=dt)
-            y = run.apply(run.schedule(derive_ops()), gen.x_values((0, n)), reps=2)
-            run.close()
-            assert np.isfinite(y).all()
-            print(name, P, dt, "ok", flush=True)
+            for ex in (D.DSPMV_EXCHANGE_COPY, D.DSPMV_EXCHANGE_PUT):
+                v = val.astype(np.float32) if dt == D.DSPMV_F32 else val
+                run = LocalRun(n, rp, col, v, P, dtype=dt, exchange=ex)
+                y = run.apply(run.schedule(derive_ops()), gen.x_values((0, n)), reps=2)
+                run.close()
+                assert np.isfinite(y).all()
+                print(name, P, dt, ex, "ok", flush=True)
 D.dspmv_l2_flush(0)
 print("sanitize run complete")
