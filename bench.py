@@ -58,6 +58,10 @@ def parse():
                     help="schedule stream 0 is the caller's stream (plan option)")
     ap.add_argument("--rerank", type=int, default=16,
                     help="re-time the k fastest sweep schedules with the step method")
+    ap.add_argument("--execution", default="auto", choices=["auto", "host", "graph"],
+                    help="host: dspmv_apply (host-synchronised schedule, the paper's model); "
+                         "graph: dspmv_apply_graph (GPU-resident CUDA graph of the same schedule); "
+                         "auto: time both and report the faster as the headline")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "host"],
                     help="host: gloo process group + HOST-transport communicator with the fused "
                          "put exchange (lets N ranks share one GPU, for testing the N>1 path)")
@@ -261,7 +265,8 @@ def run_ours(a):
     import gen
     x = torch.from_numpy(gen.x_values((lo, hi)).astype(npdt)).cuda()
     y = torch.empty_like(x)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()   # a non-default stream (the graph mode captures on it)
+    torch.cuda.synchronize()
 
     def barrier():
         if world > 1:
@@ -325,10 +330,35 @@ def run_ours(a):
     iyl = [i for i, o in enumerate(ops) if o[0] == D.DSPMV_OP_SPMV_LOCAL][0]
 
     clocks = Clocks(list(range(min(world, torch.cuda.device_count())))) if rank == 0 else None
+    # ---- execution mode: host-synchronised apply vs GPU-resident graph
+    exec_note = None
+    apply_fn, execution = D.dspmv_apply, "host-synchronised (dspmv_apply)"
+    graph_ok = a.execution != "host" and not (world > 1 and "put" in exchange)
+    if graph_ok:
+        try:
+            for _ in range(3):
+                D.dspmv_apply_graph(sched, x, y, stream)
+            torch.cuda.synchronize()
+        except Exception as e:  # noqa: BLE001 -- falls back to the host mode, reported
+            graph_ok, exec_note = False, f"graph capture failed: {e}"
+    if graph_ok and a.execution == "graph":
+        apply_fn, execution = D.dspmv_apply_graph, "GPU-resident CUDA graph (dspmv_apply_graph)"
+    elif graph_ok:
+        tms = {}
+        for name, fn in (("host", D.dspmv_apply), ("graph", D.dspmv_apply_graph)):
+            tot = 0.0
+            for _ in range(30):
+                D.dspmv_l2_flush(device, stream)
+                fn(sched, x, y, stream)
+                tot += float(D.dspmv_schedule_op_times(sched)[0])
+            tms[name] = allmax(tot / 30)
+        if tms["graph"] < tms["host"]:
+            apply_fn, execution = D.dspmv_apply_graph, "GPU-resident CUDA graph (dspmv_apply_graph)"
+        exec_note = {"ms_per_step_30": {k: round(v, 5) for k, v in tms.items()}}
     # ---- warmup
     for _ in range(a.warmup):
         D.dspmv_l2_flush(device, stream)
-        D.dspmv_apply(sched, x, y, stream)
+        apply_fn(sched, x, y, stream)
     barrier()
 
     # ---- timed region: K steps, flush between steps outside the per-step events
@@ -345,7 +375,7 @@ def run_ours(a):
     for k in range(a.steps):
         D.dspmv_l2_flush(device, stream)
         evs[k][0].record(stream)
-        D.dspmv_apply(sched, x, y, stream)
+        apply_fn(sched, x, y, stream)
         evs[k][1].record(stream)
         t = D.dspmv_schedule_op_times(sched)
         yl_ms += float(t[iyl])
@@ -410,6 +440,7 @@ def run_ours(a):
                 "workload": desc, "n_global": n, "nnz_global": int(nnz_total),
                 "ranks": world, "parallelism": f"row-partition x{world}, halo exchange: {exchange}",
                 "exchange_selection": exchange_note,
+                "execution": execution, "execution_selection": exec_note,
                 "schedule": sched_desc,
                 "l2": "flushed between timed steps (flush kernel reads 2x L2, outside per-step CUDA events)",
                 "step_timing": ("CUDA events recorded by dspmv_apply on the caller stream at START "

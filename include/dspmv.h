@@ -315,6 +315,16 @@ dspmv_status dspmv_apply(dspmv_schedule_t sched, const void* x_local, void* y_lo
  * y, all inside the call (the end-to-end path). */
 dspmv_status dspmv_apply_host(dspmv_schedule_t sched, const void* x_host, void* y_host,
                               dspmv_stream_t stream);
+/* GPU-resident execution of the same schedule (NEXT-3 (iii)): on first use
+ * (and whenever x / y change) the schedule is captured into a CUDA graph in
+ * which every host synchronisation point (CES, WaitSend, WaitRecv) becomes a
+ * device-side join of all streams on that event, the NCCL exchange is captured
+ * on the comm stream, and START/END fork from / join into `stream`; each call
+ * then launches the graph.  Stream-ordered: returns immediately, y is complete
+ * when `stream` reaches this point.  Same results as dspmv_apply.  Not for
+ * LOCAL groups with > 1 rank or the PUT exchange; `stream` must not be NULL. */
+dspmv_status dspmv_apply_graph(dspmv_schedule_t sched, const void* x_local, void* y_local,
+                               dspmv_stream_t stream);
 /* LOCAL comms: all nranks ranks of one in-process group in lock-step (op k on
  * every rank before op k+1).  scheds[r], x[r], y[r] belong to rank r. */
 dspmv_status dspmv_apply_group(const dspmv_schedule_t* scheds, int nranks,

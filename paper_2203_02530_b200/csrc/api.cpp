@@ -579,6 +579,129 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
     return DSPMV_OK;
 }
 
+// ------------------------------------------------ GPU-resident schedules
+// Capture the schedule into a CUDA graph (NEXT-3 (iii)): GPU vertices,
+// CER and CSWE are captured as they are; a host synchronisation point (CES,
+// WaitSend, WaitRecv) -- after which the host would enqueue every later op --
+// becomes "every stream waits on that event", which orders all later work
+// after it exactly as the host sync did; the exchange (NCCL group) is
+// captured on the comm stream; START/END are the fork from / join into the
+// caller's stream.  Timed ops record external events, so op times and the
+// timeline work unchanged.
+dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t origin) {
+    Plan& p = *s.plan;
+    if (p.put_mode && p.has_peers)
+        return fail(DSPMV_ERR_ARG, "apply_graph: the PUT exchange carries a per-apply epoch; use dspmv_apply");
+    if (p.comm->kind == DSPMV_COMM_LOCAL && p.host.nranks > 1)
+        return fail(DSPMV_ERR_ARG, "apply_graph: LOCAL groups with > 1 rank run with dspmv_apply_group");
+    for (auto& e : s.gev)
+        if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const int ns = s.n_streams;
+    std::vector<cudaStream_t> st(ns);
+    for (int i = 0; i < ns; ++i) st[i] = (i == 0 && p.opts.caller_stream0) ? origin : p.streams[i];
+    std::vector<cudaStream_t> all(st);
+    if (p.has_peers) all.push_back(p.comm_stream);
+    auto is_origin = [&](cudaStream_t q) { return q == origin; };
+    CUDA_TRY(cudaStreamBeginCapture(origin, cudaStreamCaptureModeThreadLocal));
+    auto abort_capture = [&](dspmv_status stt) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(origin, &g);
+        if (g) cudaGraphDestroy(g);
+        return stt;
+    };
+#define CAP_TRY(expr)                                                                          \
+    do {                                                                                       \
+        cudaError_t _e = (expr);                                                               \
+        if (_e != cudaSuccess)                                                                 \
+            return abort_capture(fail(DSPMV_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e))); \
+    } while (0)
+    if (s.step0) CAP_TRY(cudaEventRecordWithFlags(s.step0, origin, cudaEventRecordExternal));
+    CAP_TRY(cudaEventRecord(s.gev[0], origin));
+    for (cudaStream_t q : all)
+        if (!is_origin(q)) CAP_TRY(cudaStreamWaitEvent(q, s.gev[0], 0));
+    auto all_wait = [&](cudaEvent_t ev) -> cudaError_t {
+        for (cudaStream_t q : all) {
+            cudaError_t e = cudaStreamWaitEvent(q, ev, 0);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    };
+    bool ps = false, pr = false, issued = false;
+    for (int t = 0; t < int(s.ops.size()); ++t) {
+        const dspmv_op& o = s.ops[t];
+        const bool gpu = is_gpu_vertex(o.kind);
+        cudaStream_t q = (gpu || o.kind == DSPMV_OP_EVENT_RECORD || o.kind == DSPMV_OP_STREAM_WAIT_EVENT)
+                             ? st[o.stream] : nullptr;
+        const bool timed = gpu && s.timing && s.t0[t];
+        if (timed) CAP_TRY(cudaEventRecordWithFlags(s.t0[t], q, cudaEventRecordExternal));
+        switch (o.kind) {
+            case DSPMV_OP_PACK:
+                CAP_TRY(launch_pack(p.dtype, x, p.d_pack_map, p.d_sendbuf, int64_t(p.host.pack_map.size()), q));
+                break;
+            case DSPMV_OP_SPMV_LOCAL: {
+                SpmvOperands op{x, y, p.d_partL, p.d_partR, p.d_ticket};
+                CAP_TRY(launch_spmv(p.L, p.dtype, op, q));
+                break;
+            }
+            case DSPMV_OP_UNPACK:
+                CAP_TRY(launch_copy(p.dtype, p.d_recvbuf, p.d_xhalo, int64_t(p.host.halo_gid.size()), q));
+                break;
+            case DSPMV_OP_SPMV_REMOTE: {
+                SpmvOperands op{p.d_xhalo, y, p.d_partR, p.d_partL, p.d_ticket};
+                CAP_TRY(launch_spmv(p.R, p.dtype, op, q));
+                break;
+            }
+            case DSPMV_OP_POST_SEND:
+            case DSPMV_OP_POST_RECV:
+                (o.kind == DSPMV_OP_POST_SEND ? ps : pr) = true;
+                if (ps && pr && !issued) {
+                    issued = true;
+                    if (p.has_peers) {
+                        dspmv_status r = issue_exchange_nccl(p);  // captured on the comm stream
+                        if (r != DSPMV_OK) return abort_capture(r);
+                    }
+                }
+                break;
+            case DSPMV_OP_WAIT_SEND:
+            case DSPMV_OP_WAIT_RECV:
+                if (p.has_peers) CAP_TRY(all_wait(p.ev_x));
+                break;
+            case DSPMV_OP_EVENT_RECORD:
+                CAP_TRY(cudaEventRecord(s.ev[o.event], q));
+                break;
+            case DSPMV_OP_EVENT_SYNC:
+                CAP_TRY(all_wait(s.ev[o.event]));
+                break;
+            case DSPMV_OP_STREAM_WAIT_EVENT:
+                CAP_TRY(cudaStreamWaitEvent(q, s.ev[o.event], 0));
+                break;
+            default:
+                break;
+        }
+        if (timed) CAP_TRY(cudaEventRecordWithFlags(s.t1[t], q, cudaEventRecordExternal));
+    }
+    // join every stream back into the origin
+    int k = 1;
+    for (cudaStream_t q : all) {
+        if (is_origin(q)) continue;
+        CAP_TRY(cudaEventRecord(s.gev[k], q));
+        CAP_TRY(cudaStreamWaitEvent(origin, s.gev[k], 0));
+        ++k;
+    }
+    if (s.step1) CAP_TRY(cudaEventRecordWithFlags(s.step1, origin, cudaEventRecordExternal));
+#undef CAP_TRY
+    cudaGraph_t g = nullptr;
+    CUDA_TRY(cudaStreamEndCapture(origin, &g));
+    if (s.gexec) cudaGraphExecDestroy(s.gexec), s.gexec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&s.gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) return fail(DSPMV_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie));
+    s.gx = x;
+    s.gy = y;
+    s.g_timing = s.timing;
+    return DSPMV_OK;
+}
+
 std::mutex g_flush_mu;
 void* g_flush_buf[64] = {};
 size_t g_flush_bytes[64] = {};
@@ -1090,6 +1213,9 @@ static void destroy_timing(Schedule& s) {
 dspmv_status dspmv_schedule_destroy(dspmv_schedule_t s) {
     if (!s) return fail(DSPMV_ERR_ARG, "null schedule");
     cudaSetDevice(s->plan->device);
+    if (s->gexec) cudaGraphExecDestroy(s->gexec);
+    for (auto& e : s->gev)
+        if (e) cudaEventDestroy(e);
     for (auto& e : s->ev)
         if (e) cudaEventDestroy(e);
     destroy_timing(*s);
@@ -1102,6 +1228,7 @@ dspmv_status dspmv_schedule_set_timing(dspmv_schedule_t s, int enable) {
     if (!s) return fail(DSPMV_ERR_ARG, "null schedule");
     CUDA_TRY(cudaSetDevice(s->plan->device));
     destroy_timing(*s);
+    if (s->gexec) cudaGraphExecDestroy(s->gexec), s->gexec = nullptr;  // captured the old events
     s->timing = enable != 0;
     s->timed_valid = false;
     if (s->timing) {
@@ -1170,6 +1297,26 @@ dspmv_status dspmv_apply(dspmv_schedule_t s, const void* x, void* y, dspmv_strea
         }
     }
     if (s->step1) CUDA_TRY(cudaEventRecord(s->step1, static_cast<cudaStream_t>(stream)));
+    s->timed_valid = s->timing;
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_apply_graph(dspmv_schedule_t s, const void* x, void* y, dspmv_stream_t stream) {
+    if (!s) return fail(DSPMV_ERR_ARG, "null schedule");
+    Plan& p = *s->plan;
+    if (p.poisoned) return fail(DSPMV_ERR_STATE, "plan is poisoned by an earlier error");
+    if (!p.ready) return fail(DSPMV_ERR_STATE, "plan not ready");
+    if (p.host.n_local() > 0 && (!x || !y)) return fail(DSPMV_ERR_ARG, "null x/y");
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != p.device) CUDA_TRY(cudaSetDevice(p.device));
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    if (!cs) return fail(DSPMV_ERR_ARG, "apply_graph needs a non-default stream");
+    if (!s->gexec || s->gx != x || s->gy != y || s->g_timing != s->timing) ST_TRY(capture_graph(*s, x, y, cs));
+    const cudaError_t e = cudaGraphLaunch(s->gexec, cs);
+    if (e != cudaSuccess) {
+        p.poisoned = true;
+        return fail(DSPMV_ERR_CUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
+    }
     s->timed_valid = s->timing;
     return DSPMV_OK;
 }

@@ -138,6 +138,14 @@ struct Schedule {
     bool timing = false;
     std::vector<cudaEvent_t> t0, t1;   // per op (GPU vertices only)
     cudaEvent_t step0 = nullptr, step1 = nullptr;  // START / END on the caller stream
+    // GPU-resident execution (dspmv_apply_graph): the schedule captured once
+    // per (x, y) into a CUDA graph with host synchronisation turned into
+    // device-side joins
+    cudaGraphExec_t gexec = nullptr;
+    const void* gx = nullptr;
+    void* gy = nullptr;
+    bool g_timing = false;
+    cudaEvent_t gev[DSPMV_MAX_STREAMS + 2] = {};  // fork / join helpers
     bool timed_valid = false;
 };
 

@@ -122,6 +122,7 @@ _sig("dspmv_schedule_op_times", [_P, _P, _I])
 _sig("dspmv_schedule_op_timeline", [_P, _P, _P, _I])
 _sig("dspmv_apply", [_P, _P, _P, _P])
 _sig("dspmv_apply_host", [_P, _P, _P, _P])
+_sig("dspmv_apply_graph", [_P, _P, _P, _P])
 _sig("dspmv_apply_group", [_P, _I, _P, _P, _P])
 _sig("dspmv_l2_flush", [_I, _P])
 _sig("dspmv_launch_count", [_P])
@@ -406,6 +407,11 @@ def dspmv_schedule_op_timeline(sched, n: int | None = None):
 def dspmv_apply(sched, x, y, stream=None):
     """x, y: device buffers (torch tensors or raw pointers)."""
     _check(lib.dspmv_apply(sched, _ptr(x), _ptr(y), _stream(stream)))
+
+
+def dspmv_apply_graph(sched, x, y, stream):
+    """GPU-resident (CUDA-graph) execution; stream-ordered, non-blocking."""
+    _check(lib.dspmv_apply_graph(sched, _ptr(x), _ptr(y), _stream(stream)))
 
 
 def dspmv_apply_host(sched, x_host, y_host, stream=None):
