@@ -905,7 +905,7 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
     }
     {
         Layout L;
-        const int c = cfg >= 0 ? cfg : auto_block_cfg(h.al_rowptr.data(), int32_t(h.n_local()), vthr);
+        const int c = cfg >= 0 ? cfg : auto_block_cfg(h.al_rowptr.data(), int32_t(h.n_local()), vthr, p->esize);
         build_layout(h.al_rowptr.data(), int32_t(h.n_local()), h.al_col.data(), h.al_val.data(), p->esize, nullptr,
                      nR > 0 ? slotL.data() : nullptr, vthr, kBlockCfgs[c], L);
         if ((st = upload_layout(*p, L, c, p->L)) != DSPMV_OK) return bail(st);
@@ -914,7 +914,7 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
         std::vector<int32_t> slotR(nR);
         for (int32_t k = 0; k < nR; ++k) slotR[k] = k;
         Layout R;
-        const int c = cfg >= 0 ? cfg : auto_block_cfg(h.ar_rowptr.data(), nR, vthr);
+        const int c = cfg >= 0 ? cfg : auto_block_cfg(h.ar_rowptr.data(), nR, vthr, p->esize);
         build_layout(h.ar_rowptr.data(), nR, h.ar_col.data(), h.ar_val.data(), p->esize, h.ar_rows.data(),
                      slotR.data(), vthr, kBlockCfgs[c], R);
         if ((st = upload_layout(*p, R, c, p->R)) != DSPMV_OK) return bail(st);

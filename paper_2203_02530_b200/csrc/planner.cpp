@@ -137,7 +137,7 @@ void plan_phase2_from_requests(RankPlan& p, const std::vector<std::vector<int32_
 }
 
 // ---------------------------------------------------------------- layout
-int auto_block_cfg(const int32_t* rowptr, int32_t nrows, int vthr) {
+int auto_block_cfg(const int32_t* rowptr, int32_t nrows, int vthr, int esize) {
     int64_t nnz = 0, nnz_short = 0, rows = 0;
     for (int32_t i = 0; i < nrows; ++i) {
         const int32_t len = rowptr[i + 1] - rowptr[i];
@@ -148,7 +148,8 @@ int auto_block_cfg(const int32_t* rowptr, int32_t nrows, int vthr) {
     }
     if (rows == 0) return kDefaultBlockCfg;
     const double avg = double(nnz) / double(rows);
-    return (2 * nnz_short < nnz && avg >= 20.0) ? kLongRowBlockCfg : kDefaultBlockCfg;
+    if (2 * nnz_short < nnz && avg >= 20.0) return kLongRowBlockCfg;
+    return esize == 4 ? kShortRowBlockCfgF32 : kDefaultBlockCfg;
 }
 
 void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, const uint8_t* val,

@@ -67,14 +67,23 @@ def canonical_key(ops) -> tuple:
     return tuple(key)
 
 
+def canonical_ops(ops) -> np.ndarray:
+    """The representative of a schedule's bijection class: streams relabelled
+    by first use (the first GPU op runs on stream 0, which can be the caller's
+    stream) and events numbered in record order."""
+    return np.array([(k, s, e, 0) for k, s, e in canonical_key(ops)], np.int32)
+
+
 def enumerate_derived(n_streams: int = 2):
-    """Every distinct (canonical) schedule with derived syncs: list of ops arrays."""
+    """Every distinct schedule with derived syncs, as canonical ops arrays."""
     seen = {}
     for order in topological_orders():
         for assign in itertools.product(range(n_streams), repeat=len(GPU)):
             st = dict(zip(GPU, assign))
             ops = D.dspmv_schedule_derive(order, [st.get(v, 0) for v in order], n_streams)
-            seen.setdefault(canonical_key(ops), ops)
+            key = canonical_key(ops)
+            if key not in seen:
+                seen[key] = canonical_ops(ops)
     return list(seen.values())
 
 
