@@ -89,12 +89,89 @@ def make_measure(plans, xs, ys, t_measure=0.01):
     return measure
 
 
+def setup_distributed(workload, comm_kind):
+    """One process per rank (torchrun): this rank's rows, NCCL comm (or the
+    HOST-transport comm with the fused put exchange for ranks sharing a GPU)."""
+    import torch.distributed as dist
+    world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
+    dev = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    if comm_kind == "host":
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    if workload == "g3":
+        n = 150000
+        rp, col, val = gen.banded(n)
+    elif workload == "c5":
+        n, (rp, col, val) = gen.config_matrix("c5")
+    else:
+        n, (rp, col, val) = gen.config_matrix("c2")
+    rb = D.dspmv_partition(n, world)
+    b, e = int(rb[rank]), int(rb[rank + 1])
+    lo, hi = int(rp[b]), int(rp[e])
+    if comm_kind == "host":
+        def allgather(bb):
+            out = [None] * world
+            dist.all_gather_object(out, bb)
+            return b"".join(out)
+        comm = D.dspmv_comm_create_host(world, rank, dev, allgather)
+        ex = D.DSPMV_EXCHANGE_PUT
+    else:
+        uid = [D.dspmv_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = D.dspmv_comm_create(uid[0], world, rank, dev)
+        ex = D.DSPMV_EXCHANGE_COPY
+    plan = D.dspmv_plan_create(comm, n, rp[b:e + 1], col[lo:hi], val[lo:hi], exchange=ex)
+    x = torch.from_numpy(gen.x_values((b, e))).cuda()
+    y = torch.empty_like(x)
+    return dist, world, rank, comm, plan, x, y
+
+
+def make_measure_distributed(dist, rank, plan, x, y, t_measure=0.01, n_meas=3):
+    """P:460-464 across processes: rank 0 proposes ops, every rank builds the
+    schedule, rank 0 calibrates n_samples (broadcast, R-Q19), every rank times
+    the same number of samples, time = max over ranks, f = mean of n_meas."""
+    red = "cpu" if dist.get_backend() == "gloo" else "cuda"
+
+    def measure(ops):
+        box = [ops]
+        dist.broadcast_object_list(box, src=0)         # P:460 "broadcast to all ranks"
+        ops = box[0]
+        if ops is None:
+            return None
+        s = D.dspmv_schedule_create(plan, ops, 2)
+        for _ in range(2):
+            D.dspmv_apply(s, x, y)
+        dist.barrier()
+        t0 = time.perf_counter()
+        D.dspmv_apply(s, x, y)
+        n = torch.tensor([max(1, math.ceil(t_measure / max(time.perf_counter() - t0, 1e-7)))], device=red)
+        dist.broadcast(n, src=0)
+        ts = []
+        for _ in range(n_meas):
+            dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(int(n.item())):
+                D.dspmv_apply(s, x, y)
+            tt = torch.tensor([(time.perf_counter() - t0) / int(n.item())], dtype=torch.float64, device=red)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ts.append(float(tt.item()))
+        D.dspmv_schedule_destroy(s)
+        return float(np.mean(ts))
+    return measure
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="g3", choices=["g3", "c2", "c5"])
-    ap.add_argument("--ranks", type=int, default=4)
+    ap.add_argument("--ranks", type=int, default=4, help="in-process ranks (single process mode)")
+    ap.add_argument("--comm", default=None, choices=[None, "nccl", "host"],
+                    help="torchrun mode: one process per rank over NCCL (or host + fused put)")
     ap.add_argument("--out", default="gpurun_out/rules.json")
     a = ap.parse_args()
+    if a.comm is not None:
+        return main_distributed(a)
     comms, plans, xs, ys = setup(a.workload, a.ranks)
     measure = make_measure(plans, xs, ys)
     space = PS.enumerate_derived(2)
@@ -137,6 +214,55 @@ def main():
         D.dspmv_plan_destroy(p)
     for c in comms:
         D.dspmv_comm_destroy(c)
+
+
+def analyse(space, times, measure_sub, workload, ranks, sweep_s):
+    labels, ranges, bounds = R.class_labels(times)
+    X, cols = R.features(space)
+    clf, mln, hist = R.train_tree(X, labels)
+    rs = R.rulesets(clf, cols)
+    out = {
+        "workload": workload, "ranks": ranks, "n_schedules": len(space), "sweep_wall_s": round(sweep_s, 2),
+        "fastest_us": float(times.min() * 1e6), "slowest_us": float(times.max() * 1e6),
+        "fast_slow_ratio": float(times.max() / times.min()),
+        "sorted_times_us": [round(float(t) * 1e6, 3) for t in np.sort(times)],
+        "classes": {str(k): {"range_us": [v[0] * 1e6, v[1] * 1e6], "count": int((labels == k).sum())}
+                    for k, v in ranges.items()},
+        "tree": {"max_leaf_nodes": int(mln), "depth": int(clf.get_depth()),
+                 "train_error": float(1 - (clf.predict(X) == labels).mean())},
+        "rulesets": {str(k): [{"samples": n, "rules": r} for n, r in v[:3]] for k, v in rs.items()},
+        "fastest": PS.describe(space[int(times.argmin())]),
+        "slowest": PS.describe(space[int(times.argmax())]),
+    }
+    acc = {}
+    for iters in (50, 100, 200, 400):
+        m = M.MCTS(measure_sub, n_streams=2, seed=2203).run(iters)
+        recs = m.records()
+        sub_t = np.array([t for _, t in recs])
+        acc[str(iters)] = {"distinct": len(recs),
+                           "accuracy": R.class_accuracy([o for o, _ in recs], sub_t, space, times),
+                           "best_found_us": float(sub_t.min() * 1e6)}
+    out["mcts_table_v"] = acc
+    return out
+
+
+def main_distributed(a):
+    dist, world, rank, comm, plan, x, y = setup_distributed(a.workload, a.comm)
+    measure = make_measure_distributed(dist, rank, plan, x, y)
+    if rank == 0:
+        space = PS.enumerate_derived(2)
+        t0 = time.perf_counter()
+        times = np.array([measure(o) for o in space])
+        out = analyse(space, times, measure, a.workload, world, time.perf_counter() - t0)
+        measure(None)                                     # release the other ranks
+        json.dump(out, open(a.out, "w"), indent=1)
+        print(json.dumps({k: v for k, v in out.items() if k != "sorted_times_us"}, indent=1))
+    else:
+        while measure(None) is not None:                  # follow rank 0's proposals
+            pass
+    D.dspmv_plan_destroy(plan)
+    D.dspmv_comm_destroy(comm)
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":
