@@ -220,6 +220,15 @@ dspmv_status dspmv_host_plan_requests(dspmv_host_plan_t hp, int owner, int32_t* 
 dspmv_status dspmv_host_plan_set_requests(dspmv_host_plan_t hp, const int32_t* const* lists,
                                           const int32_t* counts);
 
+/* Host-only, test hook: the device row layout the planner builds for one
+ * matrix (rowptr int64[nrows+1], relative) -- S-group row order (int32[nS]),
+ * block descriptors (int32[nb*16]: r0 r1 p0 p1 flag|class<<8 warp bounds),
+ * V-group rows (int32[nV]) -- with block configuration `cfg` (-1 = auto) and
+ * vector threshold `vthr` (-1 = default).  Pass NULL outputs to get sizes. */
+dspmv_status dspmv_layout_host(const int64_t* rowptr, int32_t nrows, int dtype, int cfg, int vthr,
+                               int32_t* s_rows, int32_t* n_s, int32_t* desc, int32_t* n_blocks,
+                               int32_t* v_rows, int32_t* n_v, int32_t* cfg_used);
+
 /* ------------------------------------------------------------ schedules
  * A schedule is a traversal of the program DAG with every GPU
  * vertex bound to a stream (BoundGPU_s, tab:vertices P:250-264) and the

@@ -1167,6 +1167,37 @@ dspmv_status dspmv_host_plan_set_requests(dspmv_host_plan_t hp, const int32_t* c
     return DSPMV_OK;
 }
 
+dspmv_status dspmv_layout_host(const int64_t* rowptr, int32_t nrows, int dtype, int cfg, int vthr, int32_t* s_rows,
+                               int32_t* n_s, int32_t* desc, int32_t* n_blocks, int32_t* v_rows, int32_t* n_v,
+                               int32_t* cfg_used) {
+    if (!rowptr || nrows < 0 || !n_s || !n_blocks || !n_v) return fail(DSPMV_ERR_ARG, "null argument");
+    const int esize = dtype == DSPMV_F32 ? 4 : 8;
+    if (vthr < 0) vthr = kDefaultVectorThreshold;
+    std::vector<int32_t> rp(static_cast<size_t>(nrows) + 1);
+    for (int32_t i = 0; i <= nrows; ++i) {
+        const int64_t v = rowptr[i] - rowptr[0];
+        if (v >= (int64_t(1) << 31)) return fail(DSPMV_ERR_RANGE, "nnz >= 2^31");
+        rp[i] = int32_t(v);
+    }
+    const int c = cfg >= 0 ? cfg : auto_block_cfg(rp.data(), nrows, vthr, esize);
+    if (c < 0 || c >= kNumBlockCfgs || vthr > kBlockCfgs[c].tile) return fail(DSPMV_ERR_ARG, "bad cfg / vthr");
+    std::vector<int32_t> col(size_t(rp[nrows]), 0);
+    std::vector<int32_t> ident(static_cast<size_t>(nrows));
+    for (int32_t i = 0; i < nrows; ++i) ident[i] = i;
+    Layout L;
+    build_layout(rp.data(), nrows, col.data(), nullptr, esize, ident.data(), nullptr, vthr, kBlockCfgs[c], L);
+    const bool fit = (!s_rows || *n_s >= L.nS) && (!desc || *n_blocks >= L.nb) && (!v_rows || *n_v >= L.nV);
+    if (s_rows && fit) std::copy(L.s_out.begin(), L.s_out.end(), s_rows);
+    if (desc && fit) std::copy(L.s_desc.begin(), L.s_desc.end(), desc);
+    if (v_rows && fit) std::copy(L.v_out.begin(), L.v_out.end(), v_rows);
+    *n_s = L.nS;
+    *n_blocks = L.nb;
+    *n_v = L.nV;
+    if (cfg_used) *cfg_used = c;
+    if (!fit) return fail(DSPMV_ERR_ARG, "output arrays too small");
+    return DSPMV_OK;
+}
+
 dspmv_status dspmv_host_plan_destroy(dspmv_host_plan_t hp) {
     if (!hp) return fail(DSPMV_ERR_ARG, "null host plan");
     delete hp;

@@ -111,6 +111,7 @@ _sig("dspmv_host_plan_destroy", [_P])
 _sig("dspmv_rank_plan_build_host", [_I, _I, _I64, _I64, _P, _P, _P, _I, _P])
 _sig("dspmv_host_plan_requests", [_P, _I, _P, ctypes.c_size_t, _P])
 _sig("dspmv_host_plan_set_requests", [_P, _P, _P])
+_sig("dspmv_layout_host", [_P, ctypes.c_int32, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P])
 _sig("dspmv_schedule_validate", [_P, _I, _I])
 _sig("dspmv_schedule_derive", [_P, _P, _I, _P, _I, _P])
 _sig("dspmv_schedule_parse", [ctypes.c_char_p, _P, _I, _P, _P])
@@ -339,6 +340,22 @@ def dspmv_host_plan_set_requests(hp, lists):
     ptrs = (_P * n)(*[l.ctypes.data if len(l) else None for l in lists])
     counts = np.array([len(l) for l in lists], np.int32)
     _check(lib.dspmv_host_plan_set_requests(hp, ptrs, counts.ctypes.data))
+
+
+def dspmv_layout_host(rowptr, dtype=DSPMV_F64, cfg: int = -1, vthr: int = -1):
+    """(s_rows, desc[nb,16], v_rows, cfg_used) of the planner's row layout."""
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    nr = len(rowptr) - 1
+    ns, nb, nv, cu = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_int32(0)
+    _check(lib.dspmv_layout_host(rowptr.ctypes.data, nr, dtype, cfg, vthr, None, ctypes.byref(ns), None,
+                                 ctypes.byref(nb), None, ctypes.byref(nv), ctypes.byref(cu)))
+    s_rows = np.zeros(max(ns.value, 1), np.int32)
+    desc = np.zeros(max(nb.value, 1) * 16, np.int32)
+    v_rows = np.zeros(max(nv.value, 1), np.int32)
+    _check(lib.dspmv_layout_host(rowptr.ctypes.data, nr, dtype, cfg, vthr, s_rows.ctypes.data, ctypes.byref(ns),
+                                 desc.ctypes.data, ctypes.byref(nb), v_rows.ctypes.data, ctypes.byref(nv),
+                                 ctypes.byref(cu)))
+    return s_rows[:ns.value], desc[:nb.value * 16].reshape(-1, 16), v_rows[:nv.value], cu.value
 
 
 def dspmv_schedule_validate(ops, n_streams: int):

@@ -1,0 +1,80 @@
+"""The planner's device row layout (host-only hook): S/V split, row classes
+(2^c lanes per row), windowed stable class partition, block limits, warp
+bounds -- the invariants the row-block kernel relies on (K1)."""
+import numpy as np
+import pytest
+
+import gen
+from paper_2203_02530_b200 import dspmv as D
+
+TILE = {0: 2048, 1: 1024, 2: 2048, 3: 1024, 4: 1024, 5: 512, 6: 4096, 7: 4096}
+ROWMAX = {0: 256, 1: 128, 2: 256, 3: 128, 4: 256, 5: 128, 6: 128, 7: 128}
+WARPS = {0: 8, 1: 4, 2: 8, 3: 4, 4: 8, 5: 4, 6: 4, 7: 4}
+CHUNK = {0: 8, 1: 8, 2: 8, 3: 8, 4: 8, 5: 8, 6: 32, 7: 16}
+
+
+def _cls(length, cfg):
+    if length <= max(8, CHUNK[cfg]):
+        return 0
+    c = 0
+    while c < 5 and length > (8 << c):
+        c += 1
+    return c
+
+
+MATS = {
+    "pl": lambda: gen.powerlaw(20000)[0],
+    "7pt": lambda: gen.stencil("7pt", (20, 20, 20))[0],
+    "27pt": lambda: gen.stencil("27pt", (14, 14, 14))[0],
+    "rand": lambda: gen.random_csr(600, 0.05, seed=2, empty_rows=(0, 5, 599), dense_rows=(7,))[0],
+    "empty": lambda: np.zeros(100, np.int64),
+}
+
+
+@pytest.mark.parametrize("mat", list(MATS))
+@pytest.mark.parametrize("cfg", [-1, 0, 3, 5, 6])
+@pytest.mark.parametrize("vthr", [-1, 0, 64])
+def test_layout_invariants(mat, cfg, vthr):
+    rp = MATS[mat]()
+    n = len(rp) - 1
+    L = np.diff(rp)
+    s_rows, desc, v_rows, cu = D.dspmv_layout_host(rp, cfg=cfg, vthr=vthr)
+    thr = 256 if vthr < 0 else vthr
+    # S / V split and coverage (every row exactly once)
+    assert sorted(np.concatenate([s_rows, v_rows]).tolist()) == list(range(n))
+    assert np.all(L[s_rows] <= thr) and np.all(L[v_rows] > thr)
+    assert np.all(np.diff(v_rows) > 0)
+    cls = np.array([_cls(l, cu) for l in L[s_rows]])
+    # windowed stable partition: inside each 4096-row window, classes ascend and
+    # rows of one class keep ascending order; windows cover S rows in order
+    for w0 in range(0, len(s_rows), 4096):
+        w = s_rows[w0:w0 + 4096]
+        c = cls[w0:w0 + 4096]
+        assert np.all(np.diff(c) >= 0)
+        for k in np.unique(c):
+            assert np.all(np.diff(w[c == k]) > 0)
+        if w0:
+            assert w.min() > s_rows[:w0].max()
+    # blocks: contiguous, one class, nnz <= tile, rows <= rowmax >> c, warp bounds
+    prefix = np.concatenate([[0], np.cumsum(L[s_rows])])
+    r_next = 0
+    for d in desc:
+        r0, r1, p0, p1, fl = d[:5]
+        c = fl >> 8
+        assert r0 == r_next and r1 > r0
+        r_next = r1
+        assert p0 == prefix[r0] and p1 == prefix[r1]
+        assert np.all(cls[r0:r1] == c)
+        assert p1 - p0 <= TILE[cu] and r1 - r0 <= max(1, ROWMAX[cu] >> c)
+        W = WARPS[cu]
+        wb = d[5:6 + W]
+        assert wb[0] == r0 and wb[-1] == r1 and np.all(np.diff(wb) >= 0)
+        assert np.all(np.diff(wb) <= max(1, 32 >> c) + (32 >> c))
+    assert r_next == len(s_rows)
+
+
+def test_auto_config_choice():
+    assert D.dspmv_layout_host(gen.stencil("7pt", (16, 16, 16))[0])[3] == 3
+    assert D.dspmv_layout_host(gen.stencil("27pt", (16, 16, 16))[0])[3] == 6
+    assert D.dspmv_layout_host(gen.powerlaw(20000)[0])[3] == 3
+    assert D.dspmv_layout_host(gen.stencil("7pt", (16, 16, 16))[0], dtype=D.DSPMV_F32)[3] == 0
