@@ -90,6 +90,18 @@ dspmv_status dev_alloc(Plan& p, void** dst, size_t bytes, bool zero) {
     return DSPMV_OK;
 }
 
+// Scratch device buffer freed on every exit path.
+struct DevScratch {
+    void* p = nullptr;
+    ~DevScratch() {
+        if (p) cudaFree(p);
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
 #define ST_TRY(expr)                       \
     do {                                   \
         dspmv_status _s = (expr);          \
@@ -191,15 +203,13 @@ dspmv_status comm_allgather(Plan& p, const void* send, void* recv, size_t bytes)
         if (c.allgather(send, recv, bytes, c.allgather_ctx) != 0) return fail(DSPMV_ERR_ARG, "allgather callback failed");
         return DSPMV_OK;
     }
-    unsigned char *d_in = nullptr, *d_out = nullptr;
-    CUDA_TRY(cudaMalloc(&d_in, bytes));
-    CUDA_TRY(cudaMalloc(&d_out, bytes * c.nranks));
-    CUDA_TRY(cudaMemcpy(d_in, send, bytes, cudaMemcpyHostToDevice));
-    NCCL_TRY(ncclAllGather(d_in, d_out, bytes, ncclUint8, c.nccl, p.comm_stream));
+    DevScratch d_in, d_out;
+    CUDA_TRY(cudaMalloc(&d_in.p, bytes));
+    CUDA_TRY(cudaMalloc(&d_out.p, bytes * c.nranks));
+    CUDA_TRY(cudaMemcpy(d_in.p, send, bytes, cudaMemcpyHostToDevice));
+    NCCL_TRY(ncclAllGather(d_in.p, d_out.p, bytes, ncclUint8, c.nccl, p.comm_stream));
     CUDA_TRY(cudaStreamSynchronize(p.comm_stream));
-    CUDA_TRY(cudaMemcpy(recv, d_out, bytes * c.nranks, cudaMemcpyDeviceToHost));
-    cudaFree(d_in);
-    cudaFree(d_out);
+    CUDA_TRY(cudaMemcpy(recv, d_out.p, bytes * c.nranks, cudaMemcpyDeviceToHost));
     return DSPMV_OK;
 }
 
@@ -295,9 +305,11 @@ dspmv_status exchange_requests_nccl(Plan& p) {
     }
     ncclComm_t comm = p.comm->nccl;
     cudaStream_t s = p.comm_stream;
-    int32_t *d_cnt = nullptr, *d_scnt = nullptr;
-    CUDA_TRY(cudaMalloc(&d_cnt, sizeof(int32_t) * P));
-    CUDA_TRY(cudaMalloc(&d_scnt, sizeof(int32_t) * P));
+    DevScratch s_cnt, s_scnt, s_halo, s_req;
+    CUDA_TRY(cudaMalloc(&s_cnt.p, sizeof(int32_t) * P));
+    CUDA_TRY(cudaMalloc(&s_scnt.p, sizeof(int32_t) * P));
+    int32_t* d_cnt = s_cnt.as<int32_t>();
+    int32_t* d_scnt = s_scnt.as<int32_t>();
     CUDA_TRY(cudaMemcpy(d_cnt, h.recv_count.data(), sizeof(int32_t) * P, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemset(d_scnt, 0, sizeof(int32_t) * P));
     ncclResult_t gr = ncclSuccess;
@@ -318,12 +330,13 @@ dspmv_status exchange_requests_nccl(Plan& p) {
         sdis[q] = tot;
         tot += scnt[q];
     }
-    int32_t *d_halo = nullptr, *d_req = nullptr;
     if (!h.halo_gid.empty()) {
-        CUDA_TRY(cudaMalloc(&d_halo, sizeof(int32_t) * h.halo_gid.size()));
-        CUDA_TRY(cudaMemcpy(d_halo, h.halo_gid.data(), sizeof(int32_t) * h.halo_gid.size(), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMalloc(&s_halo.p, sizeof(int32_t) * h.halo_gid.size()));
+        CUDA_TRY(cudaMemcpy(s_halo.p, h.halo_gid.data(), sizeof(int32_t) * h.halo_gid.size(), cudaMemcpyHostToDevice));
     }
-    if (tot) CUDA_TRY(cudaMalloc(&d_req, sizeof(int32_t) * tot));
+    if (tot) CUDA_TRY(cudaMalloc(&s_req.p, sizeof(int32_t) * tot));
+    int32_t* d_halo = s_halo.as<int32_t>();
+    int32_t* d_req = s_req.as<int32_t>();
     NCCL_TRY(ncclGroupStart());
     for (int q = 0; q < P; ++q) {
         if (q == me) continue;
@@ -338,10 +351,6 @@ dspmv_status exchange_requests_nccl(Plan& p) {
     if (tot) CUDA_TRY(cudaMemcpy(all.data(), d_req, sizeof(int32_t) * tot, cudaMemcpyDeviceToHost));
     std::vector<std::vector<int32_t>> req(P);
     for (int q = 0; q < P; ++q) req[q].assign(all.begin() + sdis[q], all.begin() + sdis[q] + scnt[q]);
-    cudaFree(d_cnt);
-    cudaFree(d_scnt);
-    if (d_halo) cudaFree(d_halo);
-    if (d_req) cudaFree(d_req);
     plan_phase2_from_requests(h, req);
     return DSPMV_OK;
 }
