@@ -348,8 +348,14 @@ def run_ours(a):
         sched_desc = a.schedule + ": " + " ".join(order) + f" streams={streams}"
     sched = D.dspmv_schedule_create(plan, ops, 2)
     # y_L op on its own stream + START..END of every apply on the caller stream
-    D.dspmv_schedule_set_timing(sched, (1 << D.DSPMV_OP_SPMV_LOCAL) | (1 << D.DSPMV_OP_START))
+    # (+ the halo exchange on the comm stream at N > 1)
+    tmask = (1 << D.DSPMV_OP_SPMV_LOCAL) | (1 << D.DSPMV_OP_START)
+    if world > 1:
+        tmask |= (1 << D.DSPMV_OP_POST_SEND) | (1 << D.DSPMV_OP_POST_RECV)
+    D.dspmv_schedule_set_timing(sched, tmask)
     iyl = [i for i, o in enumerate(ops) if o[0] == D.DSPMV_OP_SPMV_LOCAL][0]
+    iposts = [i for i, o in enumerate(ops) if o[0] in (D.DSPMV_OP_POST_SEND, D.DSPMV_OP_POST_RECV)]
+    x_us = []
 
     clocks = Clocks(list(range(min(world, torch.cuda.device_count())))) if rank == 0 else None
     # ---- execution mode: host-synchronised apply vs GPU-resident graph
@@ -403,6 +409,8 @@ def run_ours(a):
         t = D.dspmv_schedule_op_times(sched)
         yl_ms += float(t[iyl])
         step_ms_rank += float(t[0])   # START..END events recorded on `stream` by the library
+        if world > 1:
+            x_us.append(max(float(t[i]) for i in iposts) * 1e3)
         b_, e_ = D.dspmv_schedule_op_timeline(sched)
         tl_begin.append(float(b_[iyl]))
         tl_end.append(float(e_[iyl]))
@@ -429,6 +437,20 @@ def run_ours(a):
     step_bytes = allsum(float(alg_bytes_rank(info, v)))
     step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
 
+    # ---- halo exchange vs NVLink (N > 1): bytes received per rank / exchange time
+    xinfo = None
+    if world > 1:
+        xmed = float(np.median(x_us)) if x_us else 0.0
+        bytes_in = float(info["n_halo"] * v)
+        xmax = allmax(xmed)
+        bmax = allmax(bytes_in)
+        xinfo = {"bytes_in_per_rank_max": int(bmax), "bytes_out_rank0": int(info["n_send"] * v),
+                 "exchange_us_median_max_rank": round(xmax, 2),
+                 "GB_s": round(bmax / (xmax * 1e-6) / 1e9, 1) if xmax > 0 else None,
+                 "nvlink_ref_GB_s": 770.0,
+                 "note": "comm-stream time of the exchange issued at the later Post (NCCL group, or the "
+                         "wait on peers' put flags); 770 GB/s = measured peer copy per direction "
+                         "(B200_PROFILING.md)"}
     # ---- e2e: the same apply through the C ABI with HOST buffers (pinned)
     xh = torch.from_numpy(gen.x_values((lo, hi)).astype(npdt)).pin_memory()
     yh = torch.empty_like(xh).pin_memory()
@@ -489,6 +511,8 @@ def run_ours(a):
         }
         if sweep is not None:
             out["schedule_sweep"] = sweep
+        if xinfo is not None:
+            out["exchange"] = xinfo
         if cpu is not None:
             out["cpu_baseline"] = cpu
         print(json.dumps(out), flush=True)

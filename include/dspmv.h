@@ -301,7 +301,9 @@ dspmv_status dspmv_schedule_create(dspmv_plan_t plan, const dspmv_op* ops, int n
 dspmv_status dspmv_schedule_destroy(dspmv_schedule_t sched);
 /* Per-op CUDA-event timing on the op's stream (2 event records per timed
  * op).  enable: 0 off, 1 every GPU vertex, else a bit mask (1 << op kind) of
- * the GPU vertex kinds to time; bit (1 << DSPMV_OP_START) additionally
+ * the GPU vertex kinds to time (bits of POST_SEND / POST_RECV time the
+ * halo exchange on the comm stream, reported at the Post that issues it);
+ * bit (1 << DSPMV_OP_START) additionally
  * records an event on the caller stream at START and at END.  After an
  * apply, ms[i] = device time of ops[i] (0 for untimed ops) and, with the
  * START bit, ms[0] = END - START on the caller stream (the whole apply). */

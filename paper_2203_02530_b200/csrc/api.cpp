@@ -517,6 +517,7 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
     cudaStream_t st = on_stream ? (o.stream == 0 ? p.cur_stream0 : p.streams[o.stream]) : nullptr;
     const bool timed = gpu && s.timing && s.t0[t];
     if (timed) CUDA_TRY(cudaEventRecord(s.t0[t], st));
+    const bool timed_x = !gpu && s.timing && s.t0[t];  // a Post: time the exchange it issues
     cudaError_t e = cudaSuccess;
     switch (o.kind) {
         case DSPMV_OP_START:
@@ -553,11 +554,17 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
         case DSPMV_OP_POST_RECV:
             if (o.kind == DSPMV_OP_POST_SEND) p.posted_send = true; else p.posted_recv = true;
             if (!defer && p.posted_send && p.posted_recv && !p.issued) {
+                // exchange time on the comm stream (0 in op_times unless this op issued it)
+                if (timed_x) CUDA_TRY(cudaEventRecord(s.t0[t], p.comm_stream));
                 dspmv_status r = p.put_mode ? issue_exchange_put(p) : issue_exchange_nccl(p);
                 if (r != DSPMV_OK) {
                     p.poisoned = true;
                     return r;
                 }
+                if (timed_x) CUDA_TRY(cudaEventRecord(s.t1[t], p.comm_stream));
+            } else if (timed_x) {
+                CUDA_TRY(cudaEventRecord(s.t0[t], p.comm_stream));
+                CUDA_TRY(cudaEventRecord(s.t1[t], p.comm_stream));
             }
             break;
         case DSPMV_OP_WAIT_SEND:
@@ -663,12 +670,18 @@ dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t ori
             case DSPMV_OP_POST_SEND:
             case DSPMV_OP_POST_RECV:
                 (o.kind == DSPMV_OP_POST_SEND ? ps : pr) = true;
-                if (ps && pr && !issued) {
-                    issued = true;
-                    if (p.has_peers) {
-                        dspmv_status r = issue_exchange_nccl(p);  // captured on the comm stream
-                        if (r != DSPMV_OK) return abort_capture(r);
+                {
+                    const bool tx = s.timing && s.t0[t];
+                    cudaStream_t xs = p.has_peers ? p.comm_stream : origin;  // comm joins the capture only with peers
+                    if (tx) CAP_TRY(cudaEventRecordWithFlags(s.t0[t], xs, cudaEventRecordExternal));
+                    if (ps && pr && !issued) {
+                        issued = true;
+                        if (p.has_peers) {
+                            dspmv_status r = issue_exchange_nccl(p);  // captured on the comm stream
+                            if (r != DSPMV_OK) return abort_capture(r);
+                        }
                     }
+                    if (tx) CAP_TRY(cudaEventRecordWithFlags(s.t1[t], xs, cudaEventRecordExternal));
                 }
                 break;
             case DSPMV_OP_WAIT_SEND:
@@ -1281,7 +1294,9 @@ dspmv_status dspmv_schedule_set_timing(dspmv_schedule_t s, int enable) {
             CUDA_TRY(cudaEventCreate(&s->step1));
         }
         for (size_t t = 0; t < s->ops.size(); ++t) {
-            if (!is_gpu_vertex(s->ops[t].kind) || !(mask & (1u << s->ops[t].kind))) continue;
+            const int k = s->ops[t].kind;
+            const bool post = k == DSPMV_OP_POST_SEND || k == DSPMV_OP_POST_RECV;
+            if (!(is_gpu_vertex(k) || post) || !(mask & (1u << k))) continue;
             CUDA_TRY(cudaEventCreate(&s->t0[t]));
             CUDA_TRY(cudaEventCreate(&s->t1[t]));
         }
