@@ -25,14 +25,14 @@ struct BlockCfg {
 };
 constexpr BlockCfg kBlockCfgs[] = {
     // tile  rowmax warps stages min_ctas chunk  (rowmax = 32 x warps: one row per lane)
-    {2048, 256, 8, 2, 4, 8},    // 0
-    {1024, 128, 4, 2, 8, 8},    // 1
+    {2048, 256, 8, 2, 4, 8},    // 0  fp32 short rows
+    {1024, 128, 4, 2, 6, 8},    // 1
     {2048, 256, 8, 3, 2, 8},    // 2
-    {1024, 128, 4, 3, 5, 8},    // 3
-    {1024, 256, 8, 2, 5, 8},    // 4
-    {512, 128, 4, 4, 6, 8},     // 5
+    {1024, 128, 4, 3, 5, 8},    // 3  fp64 short / irregular rows (default)
+    {768, 96, 3, 3, 7, 8},      // 4
+    {2048, 64, 2, 3, 3, 32},    // 5  long rows: 2 warps, 3 stages, 3 CTAs/SM
     {4096, 128, 4, 2, 2, 32},   // 6  long uniform rows, one lane per row
-    {4096, 128, 4, 2, 2, 16},   // 7
+    {3072, 96, 3, 2, 3, 32},    // 7  long rows: 3 warps, 3 CTAs/SM
 };
 constexpr int kNumBlockCfgs = sizeof(kBlockCfgs) / sizeof(kBlockCfgs[0]);
 constexpr int kDefaultBlockCfg = 3;   // short rows (one lane per row)

@@ -7,10 +7,10 @@ import pytest
 import gen
 from paper_2203_02530_b200 import dspmv as D
 
-TILE = {0: 2048, 1: 1024, 2: 2048, 3: 1024, 4: 1024, 5: 512, 6: 4096, 7: 4096}
-ROWMAX = {0: 256, 1: 128, 2: 256, 3: 128, 4: 256, 5: 128, 6: 128, 7: 128}
-WARPS = {0: 8, 1: 4, 2: 8, 3: 4, 4: 8, 5: 4, 6: 4, 7: 4}
-CHUNK = {0: 8, 1: 8, 2: 8, 3: 8, 4: 8, 5: 8, 6: 32, 7: 16}
+TILE = {0: 2048, 1: 1024, 2: 2048, 3: 1024, 4: 768, 5: 2048, 6: 4096, 7: 3072}
+ROWMAX = {0: 256, 1: 128, 2: 256, 3: 128, 4: 96, 5: 64, 6: 128, 7: 96}
+WARPS = {0: 8, 1: 4, 2: 8, 3: 4, 4: 3, 5: 2, 6: 4, 7: 3}
+CHUNK = {0: 8, 1: 8, 2: 8, 3: 8, 4: 8, 5: 32, 6: 32, 7: 32}
 
 
 def _cls(length, cfg):
