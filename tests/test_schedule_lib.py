@@ -174,3 +174,79 @@ def test_product_enumerator_equals_oracle_enumerator():
     ref = {PS.canonical_key(np.array(to_lib(o), np.int32)) for o in S.enumerate_derived(2, S.EDGES)}
     assert len(mine) == 768 and mine == ref
     assert len(PS.topological_orders()) == 96
+
+
+def _random_schedule(rng):
+    """A random op list: a random order of the 10 vertices (not necessarily
+    topological), random streams, and random CER / CES / CSWE insertions."""
+    verts = S.VERTICES[1:-1]
+    rng.shuffle(verts)
+    ops = [("start",)]
+    ev = 0
+    recorded = []
+    for v in verts:
+        for _ in range(rng.choice([0, 0, 1, 2])):
+            kind = rng.choice(["CER", "CES", "CSWE"])
+            if kind == "CER" or not recorded:
+                ops.append(("CER", rng.randrange(2), ev))
+                recorded.append(ev)
+                ev += 1
+            elif kind == "CES":
+                ops.append(("CES", rng.choice(recorded)))
+            else:
+                ops.append(("CSWE", rng.randrange(2), rng.choice(recorded)))
+        ops.append((v, rng.randrange(2)) if v in S.GPU_VERTICES else (v,))
+    for _ in range(rng.choice([1, 2, 3])):
+        s_ = rng.randrange(2)
+        ops.append(("CER", s_, ev))
+        ops.append(("CES", ev))
+        ev += 1
+    ops.append(("end",))
+    return ops
+
+
+def test_validator_fuzz_random_schedules_vs_oracle():
+    """Library validator (vector clocks) == oracle validator (explicit
+    happens-before reachability) on 20000 random op lists."""
+    rng = random.Random(2530)
+    orders = S.topological_orders()
+    n_ok = 0
+    for i in range(20000):
+        if i % 2:
+            ops = _random_schedule(rng)
+        else:
+            # a derived schedule with one sync dropped and/or a random extra sync
+            order = rng.choice(orders)
+            streams = [rng.randrange(2) if v in S.GPU_VERTICES else 0 for v in order]
+            ops = S.derive(order, dict(zip(order, streams)))
+            if rng.random() < 0.5:
+                syncs = [t for t, o in enumerate(ops) if o[0] in ("CER", "CES", "CSWE")]
+                if syncs:
+                    del ops[rng.choice(syncs)]
+            if rng.random() < 0.5:
+                recs = [o[-1] for o in ops if o[0] == "CER"]
+                if recs:
+                    t = rng.randrange(1, len(ops) - 1)
+                    ops.insert(t, ("CES", rng.choice(recs)) if rng.random() < 0.5
+                               else ("CSWE", rng.randrange(2), rng.choice(recs)))
+        a, b = lib_status(ops), oracle_status(ops)
+        assert a == b, ops
+        n_ok += a == "ok"
+    assert n_ok > 2000    # both valid and invalid schedules are exercised
+
+
+def test_parse_rejects_garbage_without_crashing():
+    rng = random.Random(7)
+    words = ["start", "Pack", "y_L", "Cpu", "BoundGpu", "EventRecord", "EventSync", "StreamWaitEvent",
+             "stream=1", "event=3", "stream=-1", "event=x", "#", "end", "PostSend"]
+    for _ in range(3000):
+        text = "\n".join(" ".join(rng.choice(words) for _ in range(rng.randrange(0, 5)))
+                         for _ in range(rng.randrange(0, 20)))
+        try:
+            ops, ns = D.dspmv_schedule_parse(text)
+            try:
+                D.dspmv_schedule_validate(ops, ns)
+            except D.DspmvError:
+                pass
+        except D.DspmvError:
+            pass
