@@ -13,7 +13,8 @@ Follows the paper's problem statement step by step, in its order and notation:
    buffer for each other rank (the Pack vertex)".  Readings R-Q4
    (halo ascending by global id), R-Q6 (compressed A_R rows), R-Q7 (pack map:
    destinations ascending, then ascending local index).
-3. ``simulate`` -- executes one schedule's DAG vertices in lock-step over all
+3. ``simulate`` -- executes one schedule's DAG vertices (coarse or
+   per-destination) in lock-step over all
    ranks (op k on every rank before op k+1: a legal serialisation of the SPMD
    run), with MPI_Isend/Irecv/Wait semantics; sync ops
    are no-ops in this sequential semantics.  y_L and y_R are O1 loops; the
@@ -118,16 +119,24 @@ class Deadlock(Exception):
 def simulate(plans, val_g, x_g, ops):
     """Run one schedule (oracle.schedules tuple format) on every rank in
     lock-step and return the global y (fp64).  Raises Deadlock when a Wait
-    finds its matching communication not posted by the peer."""
+    finds its matching communication not posted by the peer.
+
+    Exchange vertices are coarse (every peer) or per-destination (P:281-284,
+    reading R-N4): ``Pack[+1]`` packs only the segment for rank r+1,
+    ``PostRecv[-1]`` posts only the receive from rank r-1, and so on; a
+    per-destination vertex whose peer r+d does not exist does nothing.  Halo
+    entries no Unpack vertex wrote stay NaN."""
+    from .schedules import split_name
     P = len(plans)
     val_g = np.asarray(val_g, np.float64)
     x_g = np.asarray(x_g, np.float64)
     st = []
     for pl in plans:
         b, e = pl["row_begin"], pl["row_end"]
-        st.append(dict(x=x_g[b:e].copy(), sendbuf=None,
-                       recvbuf=np.zeros(len(pl["halo_gid"])), x_halo=None,
-                       posted_send=False, posted_recv=False,
+        st.append(dict(x=x_g[b:e].copy(), sendbuf=np.full(len(pl["pack_map"]), np.nan),
+                       recvbuf=np.full(len(pl["halo_gid"]), np.nan),
+                       x_halo=np.full(len(pl["halo_gid"]), np.nan),
+                       posted_send=[False] * P, posted_recv=[False] * P,
                        arrived=[False] * P, yL=None, yR=None, y=None))
 
     def deliver(p, r):
@@ -138,32 +147,42 @@ def simulate(plans, val_g, x_g, ops):
         st[r]["recvbuf"][ro:ro + cnt] = st[p]["sendbuf"][so:so + cnt]
         st[r]["arrived"][p] = True
 
+    def peers(r, d):
+        """Ranks a vertex with offset d addresses on rank r (d = 0: all)."""
+        if d == 0:
+            return [q for q in range(P) if q != r]
+        return [r + d] if 0 <= r + d < P else []
+
     for op in ops:
-        name = op[0]
+        name, d = split_name(op[0])
         for r in range(P):
             pl, s = plans[r], st[r]
             if name == "Pack":
-                s["sendbuf"] = s["x"][pl["pack_map"]]
+                for q in peers(r, d):
+                    a, c = int(pl["send_displ"][q]), int(pl["send_count"][q])
+                    s["sendbuf"][a:a + c] = s["x"][pl["pack_map"][a:a + c]]
             elif name == "PostSend":
-                s["posted_send"] = True
-                for d in range(P):
-                    if pl["send_count"][d] > 0 and st[d]["posted_recv"]:
-                        deliver(r, d)
+                for q in peers(r, d):
+                    s["posted_send"][q] = True
+                    if pl["send_count"][q] > 0 and st[q]["posted_recv"][r]:
+                        deliver(r, q)
             elif name == "PostRecv":
-                s["posted_recv"] = True
-                for p in range(P):
-                    if pl["recv_count"][p] > 0 and st[p]["posted_send"]:
+                for p in peers(r, d):
+                    s["posted_recv"][p] = True
+                    if pl["recv_count"][p] > 0 and st[p]["posted_send"][r]:
                         deliver(p, r)
             elif name == "WaitRecv":
-                for p in range(P):
+                for p in peers(r, d):
                     if pl["recv_count"][p] > 0 and not s["arrived"][p]:
                         raise Deadlock(f"rank {r} WaitRecv: nothing from {p}")
             elif name == "WaitSend":
-                for d in range(P):
-                    if pl["send_count"][d] > 0 and not st[d]["arrived"][r]:
-                        raise Deadlock(f"rank {r} WaitSend: {d} never received")
+                for q in peers(r, d):
+                    if pl["send_count"][q] > 0 and not st[q]["arrived"][r]:
+                        raise Deadlock(f"rank {r} WaitSend: {q} never received")
             elif name == "Unpack":
-                s["x_halo"] = s["recvbuf"].copy()
+                for p in peers(r, d):
+                    a, c = int(pl["recv_displ"][p]), int(pl["recv_count"][p])
+                    s["x_halo"][a:a + c] = s["recvbuf"][a:a + c]
             elif name == "y_L":
                 s["yL"] = O1.o1_spmv(pl["al_rowptr"].astype(np.int64), pl["al_col"],
                                      val_g[pl["al_src"]], s["x"])

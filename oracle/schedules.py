@@ -16,10 +16,20 @@ Sources
   GPU_i->GPU_i: none; GPU_i->GPU_j: cudaEventRecord -> cudaStreamWaitEvent.
 * Stream-bijection pruning: P:426-428 ("children that represent equivalent P_k
   under a stream bijection are pruned") -- first-use relabelling.
+* Per-destination granularity (NEXT-3 (i)): P:281-284 -- "SpMV could have been
+  implemented with a set of parallel independent vertices for each separate
+  pack and MPI_Isend instead of collecting them into single Pack and PostSends
+  vertices".  DESIGN.md reading R-N4: an SPMD schedule names a peer by its rank
+  offset d (the exchange with rank r+d), written ``Pack[+1]``; the send side
+  (Pack, PostSend, WaitSend) has one vertex per offset d in S, the receive
+  side (PostRecv, WaitRecv, Unpack) one per offset in -S (rank r's send to
+  r+d is received by rank r+d from offset -d).  The R-Q13 edges become
+  PostSend[-e] -> WaitRecv[e] and PostRecv[-d] -> WaitSend[d].
 
 A schedule here is a list of tuples:
   (name,)                    CPU vertex  (start, PostSend, PostRecv, WaitSend, WaitRecv, end)
   (name, stream)             GPU vertex  (Pack, y_L, Unpack, y_R) bound to a stream
+                             (fine granularity: name = "Pack[+1]", "WaitRecv[-1]", ...)
   ("CER", stream, event)     cudaEventRecord on ``stream``
   ("CES", event)             cudaEventSynchronize (host blocks)
   ("CSWE", stream, event)    cudaStreamWaitEvent(stream, event)
@@ -41,6 +51,69 @@ EDGES_A = [("start", "Pack"), ("start", "y_L"), ("start", "PostRecv"),
 # DESIGN.md reading R-Q13: SPMD deadlock-freedom edges
 DEADLOCK_EDGES = [("PostSend", "WaitRecv"), ("PostRecv", "WaitSend")]
 EDGES = EDGES_A + DEADLOCK_EDGES
+
+
+SEND_SIDE = ("Pack", "PostSend", "WaitSend")
+RECV_SIDE = ("PostRecv", "WaitRecv", "Unpack")
+
+
+def vname(base: str, d: int) -> str:
+    """Per-destination vertex name, e.g. vname("Pack", 1) == "Pack[+1]"."""
+    return f"{base}[{d:+d}]"
+
+
+def split_name(name: str):
+    """("Pack[+1]" -> ("Pack", 1); "Pack" -> ("Pack", 0))."""
+    if name.endswith("]") and "[" in name:
+        b, d = name[:-1].split("[")
+        return b, int(d)
+    return name, 0
+
+
+def base(name: str) -> str:
+    return split_name(name)[0]
+
+
+def fine_dag(S):
+    """(vertices, edges, deadlock_edges) of the per-destination DAG for the
+    send-offset set S (reading R-N4).  With S = {d} the DAG is the
+    coarse one with every exchange vertex renamed."""
+    S = sorted(set(int(d) for d in S))
+    if not S or 0 in S:
+        raise ValueError("offsets must be non-empty and non-zero")
+    R = sorted(-d for d in S)
+    V = (["start"] + [vname(b, d) for d in S for b in SEND_SIDE] + ["y_L"]
+         + [vname(b, e) for e in R for b in RECV_SIDE] + ["y_R", "end"])
+    E = [("start", "y_L"), ("y_L", "end"), ("y_R", "end")]
+    for d in S:
+        E += [("start", vname("Pack", d)), (vname("Pack", d), vname("PostSend", d)),
+              (vname("PostSend", d), vname("WaitSend", d)), (vname("WaitSend", d), "end")]
+    for e in R:
+        E += [("start", vname("PostRecv", e)), (vname("PostRecv", e), vname("WaitRecv", e)),
+              (vname("WaitRecv", e), vname("Unpack", e)), (vname("Unpack", e), "y_R")]
+    # a Wait needs the peer's matching Post, and every rank runs the same P
+    Dl = ([(vname("PostSend", -e), vname("WaitRecv", e)) for e in R]
+          + [(vname("PostRecv", -d), vname("WaitSend", d)) for d in S])
+    return V, E + Dl, Dl
+
+
+def dag_of(ops):
+    """The DAG a schedule is checked against: the coarse one unless its
+    exchange vertices carry offsets; then fine_dag(S) with S = the send-side
+    offsets and the negated receive-side offsets (a vertex missing from
+    either side is reported by validate).  Raises ValueError on mixed
+    granularity."""
+    names = [op[0] for op in ops if base(op[0]) in VERTICES]
+    fine = {n for n in names if split_name(n)[1] != 0}
+    if not fine:
+        return VERTICES, EDGES, DEADLOCK_EDGES
+    if any(base(n) in SEND_SIDE + RECV_SIDE and split_name(n)[1] == 0 for n in names):
+        raise ValueError("mixed coarse and per-destination exchange vertices")
+    S = set()
+    for n in fine:
+        b, d = split_name(n)
+        S.add(d if b in SEND_SIDE else -d)
+    return fine_dag(S)
 
 
 def preds(v, edges=EDGES):
@@ -88,7 +161,7 @@ def _hb_graph(ops):
     for t, op in enumerate(ops):
         h = ("H", t)
         edge(hprev, h)
-        name = op[0]
+        name = base(op[0])
         if name in CPU_VERTICES:
             c = ("C", t)
             edge(hprev, c)
@@ -153,17 +226,26 @@ def edge_satisfied(ops, iu, iv):
     return _reaches(succ, node_of[iu], node_of[iv])
 
 
-def validate(ops, n_streams, edges=EDGES):
-    """Return (True, '') or (False, 'schedule'|'deadlock', reason)."""
+def validate(ops, n_streams, edges=None):
+    """Return (True, '') or (False, 'schedule'|'deadlock', reason).  The DAG is
+    ``dag_of(ops)`` (coarse or per-destination) unless ``edges`` is given."""
+    try:
+        vertices, dag_edges, dead = dag_of(ops)
+    except ValueError as e:
+        return (False, "schedule", str(e))
+    if edges is None:
+        edges = dag_edges
     pos = {}
     recorded = set()
     for t, op in enumerate(ops):
         name = op[0]
-        if name in VERTICES:
+        if base(name) in VERTICES:
+            if name not in vertices:
+                return (False, "schedule", f"unknown vertex {name}")
             if name in pos:
                 return (False, "schedule", f"duplicate vertex {name}")
             pos[name] = t
-            if name in GPU_VERTICES and not (0 <= op[1] < n_streams):
+            if base(name) in GPU_VERTICES and not (0 <= op[1] < n_streams):
                 return (False, "schedule", f"{name}: stream {op[1]} out of range")
         elif name == "CER":
             if not (0 <= op[1] < n_streams):
@@ -179,7 +261,7 @@ def validate(ops, n_streams, edges=EDGES):
                 return (False, "schedule", "CSWE stream out of range")
         else:
             return (False, "schedule", f"unknown op {name}")
-    for v in VERTICES:
+    for v in vertices:
         if v not in pos:
             return (False, "schedule", f"missing vertex {v}")
     if pos["start"] != 0:
@@ -188,7 +270,7 @@ def validate(ops, n_streams, edges=EDGES):
         return (False, "schedule", "end is not last")
     for (u, v) in edges:
         if pos[u] > pos[v]:
-            kind = "deadlock" if (u, v) in DEADLOCK_EDGES else "schedule"
+            kind = "deadlock" if (u, v) in dead else "schedule"
             return (False, kind, f"{v} before {u}")
     succ, node_of = _hb_graph(ops)
     for (u, v) in edges:
@@ -198,15 +280,18 @@ def validate(ops, n_streams, edges=EDGES):
 
 
 # ------------------------------------------------------------ sync insertion
-def derive(order, streams, edges=EDGES):
+def derive(order, streams, edges=None):
     """Schedule from a vertex order and a {GPU vertex: stream} map, inserting
     syncs per tab:sync immediately before the vertex that needs them
     (already-satisfied edges insert nothing).  Events get
-    sequential ids in emission order."""
+    sequential ids in emission order.  ``edges`` defaults to the DAG of the
+    order's vertices (coarse or per-destination)."""
+    if edges is None:
+        edges = dag_of([(v,) for v in order])[1]
     ops = []
     ev = 0
     for v in order:
-        vop = (v, streams[v]) if v in GPU_VERTICES else (v,)
+        vop = (v, streams[v]) if base(v) in GPU_VERTICES else (v,)
         for u in preds(v, edges):
             iu = next(t for t, op in enumerate(ops) if op[0] == u)
             trial = ops + [vop]
@@ -214,7 +299,7 @@ def derive(order, streams, edges=EDGES):
                 continue
             su = ops[iu][1]
             ops.append(("CER", su, ev))
-            if v in GPU_VERTICES:
+            if base(v) in GPU_VERTICES:
                 ops.append(("CSWE", streams[v], ev))
             else:
                 ops.append(("CES", ev))
@@ -229,7 +314,7 @@ def canonical(ops):
     out = []
     for op in ops:
         name = op[0]
-        if name in GPU_VERTICES:
+        if base(name) in GPU_VERTICES:
             s = smap.setdefault(op[1], len(smap))
             out.append((name, s))
         elif name == "CER":
