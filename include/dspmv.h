@@ -239,7 +239,19 @@ dspmv_status dspmv_layout_host(const int64_t* rowptr, int32_t nrows, int dtype, 
  * WaitRecv->Unpack, Unpack->y_R, y_L->end, y_R->end, WaitSend->end,
  * PostSend->WaitRecv, PostRecv->WaitSend.
  * GPU vertices: PACK, SPMV_LOCAL (y_L), UNPACK, SPMV_REMOTE (y_R); all others
- * are synchronous CPU operations. */
+ * are synchronous CPU operations.
+ *
+ * Per-destination granularity ("a set of parallel independent
+ * vertices for each separate pack and MPI_Isend"; DESIGN.md R-N4): the six
+ * exchange vertices may instead carry a peer offset d != 0 (dspmv_op.peer),
+ * meaning "the exchange with rank r+d" on every rank r (SPMD).  With the
+ * send-offset set S, the DAG has Pack[d], PostSend[d], WaitSend[d] and
+ * PostRecv[-d], WaitRecv[-d], Unpack[-d] for each d in S, the coarse edges
+ * per offset (Unpack[e]->y_R for every e, WaitSend[d]->end for every d) and
+ * the deadlock edges PostSend[d]->WaitRecv[-d], PostRecv[-d]->WaitSend[d].
+ * A schedule is all coarse (peer 0) or all per destination.  A vertex whose
+ * rank r+d does not exist or exchanges nothing with r does nothing; at
+ * schedule_create every peer the plan exchanges with must be named. */
 typedef enum {
     DSPMV_OP_START = 0,
     DSPMV_OP_PACK = 1,         /* GPU: sendbuf[k] = x[pack_map[k]]                   */
@@ -260,7 +272,9 @@ typedef struct {
     int32_t kind;      /* dspmv_op_kind                                        */
     int32_t stream;    /* GPU vertices, CER, CSWE: 0..n_streams-1; else ignored */
     int32_t event;     /* CER, CES, CSWE: 0..DSPMV_MAX_EVENTS-1; else ignored   */
-    int32_t reserved;
+    int32_t peer;      /* exchange vertices: 0 = every peer (coarse), d != 0 =
+                          the peer at rank offset d (per destination); must be
+                          0 for start, y_L, y_R, end; ignored for sync ops     */
 } dspmv_op;
 
 #define DSPMV_MAX_STREAMS 4
@@ -282,12 +296,17 @@ dspmv_status dspmv_schedule_validate(const dspmv_op* ops, int n_ops, int n_strea
  * Writes up to cap ops to out; *n_out = count. */
 dspmv_status dspmv_schedule_derive(const int32_t* order, const int32_t* streams, int n_streams,
                                    dspmv_op* out, int cap, int* n_out);
+/* Same for any granularity: order[i] / peers[i] (NULL = all 0) name the
+ * n_vertices DAG vertices in traversal order (per destination: 4 + 6|S|). */
+dspmv_status dspmv_schedule_derive_peers(const int32_t* order, const int32_t* streams, const int32_t* peers,
+                                         int n_vertices, int n_streams, dspmv_op* out, int cap, int* n_out);
 
 /* Host-only.  External schedule text format: one op per line
- * "<name> <kind> [stream=<i>] [event=<id>]", kind in {Cpu, BoundGpu,
+ * "<name> <kind> [stream=<i>] [event=<id>] [peer=<d>]", kind in {Cpu, BoundGpu,
  * EventRecord, EventSync, StreamWaitEvent}; names start, Pack, y_L,
- * PostSend, PostRecv, WaitSend, WaitRecv, Unpack, y_R, end (sync op names are
- * free text, e.g. CER-after-Pack).  Blank lines and '#' comments ignored.
+ * PostSend, PostRecv, WaitSend, WaitRecv, Unpack, y_R, end, per-destination
+ * vertices as e.g. Pack[+1] (sync op names are free text, e.g.
+ * CER-after-Pack).  Blank lines and '#' comments ignored.
  * *n_streams = 1 + highest stream used. */
 dspmv_status dspmv_schedule_parse(const char* text, dspmv_op* out, int cap, int* n_out,
                                   int* n_streams);
@@ -295,7 +314,9 @@ dspmv_status dspmv_schedule_parse(const char* text, dspmv_op* out, int cap, int*
 dspmv_status dspmv_schedule_format(const dspmv_op* ops, int n_ops, char* buf, size_t cap);
 
 /* Validate and compile a schedule for a plan (pre-creates its events).
- * Not collective, but every rank must use identical ops in apply. */
+ * Not collective, but every rank must use identical ops in apply.
+ * ERR_SCHEDULE if a per-destination schedule names no vertices for a peer
+ * offset this rank exchanges data with. */
 dspmv_status dspmv_schedule_create(dspmv_plan_t plan, const dspmv_op* ops, int n_ops,
                                    int n_streams, dspmv_schedule_t* out);
 dspmv_status dspmv_schedule_destroy(dspmv_schedule_t sched);

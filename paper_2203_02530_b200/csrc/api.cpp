@@ -180,13 +180,21 @@ dspmv_status upload_put(Plan& p, const std::vector<PutSeg>& segs) {
     return DSPMV_OK;
 }
 
+// PUT: a rank publishes its epoch to, and waits for the epoch of, every rank
+// it exchanges anything with in either direction (empty segments carry only
+// the flag).  Otherwise a rank that only sends could run two applies ahead
+// and overwrite the receive buffer its peer is still unpacking.
+bool flag_peer(const RankPlan& h, int q) {
+    return q != h.rank && (h.send_count[q] > 0 || h.recv_count[q] > 0);
+}
+
 // In-process group: peers' buffers are plain device pointers.
 dspmv_status setup_put_local(LocalGroup& g) {
     for (int r = 0; r < g.nranks; ++r) {
         Plan& p = *g.plans[r];
         std::vector<PutSeg> segs;
         for (int d = 0; d < g.nranks; ++d) {
-            if (p.host.send_count[d] <= 0) continue;
+            if (!flag_peer(p.host, d)) continue;
             Plan& q = *g.plans[d];
             char* base = static_cast<char*>(q.d_recvbuf) + size_t(q.host.recv_displ[r]) * q.esize;
             segs.push_back({p.host.send_displ[d], base, base + q.recv_stride * q.esize, q.d_flags + r});
@@ -261,7 +269,7 @@ dspmv_status setup_put_nccl(Plan& p) {
     ST_TRY(comm_allgather(p, mine.data(), all.data(), rec_bytes));
     std::vector<PutSeg> segs;
     for (int d = 0; d < P; ++d) {
-        if (p.host.send_count[d] <= 0) continue;
+        if (!flag_peer(p.host, d)) continue;
         Rec rd;
         std::memcpy(&rd, all.data() + rec_bytes * d, sizeof(Rec));
         int32_t displ_me = 0;
@@ -370,17 +378,17 @@ cudaError_t host_wait(cudaEvent_t ev) {
     }
 }
 
-dspmv_status wait_exchange(Plan& p) {
-    if (!p.has_peers) return DSPMV_OK;  // nothing was sent or received
+dspmv_status wait_group(Plan& p, const ExGroup& g) {
+    if (g.empty()) return DSPMV_OK;  // nothing sent or received in this group
     if (p.comm->kind != DSPMV_COMM_NCCL || p.host.nranks == 1) {
         if (!p.put_mode || p.comm->kind == DSPMV_COMM_LOCAL) {
-            CUDA_TRY(host_wait(p.ev_x));
+            CUDA_TRY(host_wait(g.ev));
             return DSPMV_OK;
         }
         // PUT across processes: a peer that never publishes must not hang us
         const auto t0 = std::chrono::steady_clock::now();
         for (;;) {
-            const cudaError_t q = cudaEventQuery(p.ev_x);
+            const cudaError_t q = cudaEventQuery(g.ev);
             if (q == cudaSuccess) return DSPMV_OK;
             if (q != cudaErrorNotReady) return fail(DSPMV_ERR_CUDA, std::string("exchange: ") + cudaGetErrorString(q));
             if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60)) {
@@ -391,7 +399,7 @@ dspmv_status wait_exchange(Plan& p) {
     }
     const auto t_start = std::chrono::steady_clock::now();
     for (;;) {
-        cudaError_t q = cudaEventQuery(p.ev_x);
+        cudaError_t q = cudaEventQuery(g.ev);
         if (q == cudaSuccess) return DSPMV_OK;
         if (q != cudaErrorNotReady) return fail(DSPMV_ERR_CUDA, std::string("exchange: ") + cudaGetErrorString(q));
         ncclResult_t ar = ncclSuccess;
@@ -410,32 +418,25 @@ dspmv_status wait_exchange(Plan& p) {
     }
 }
 
-dspmv_status issue_exchange_nccl(Plan& p) {
+// COPY over NCCL: the group's receives and sends as one NCCL group.
+dspmv_status issue_group_nccl(Plan& p, ExGroup& g) {
+    g.issued = true;
+    if (g.empty()) return DSPMV_OK;
     const RankPlan& h = p.host;
-    const int P = h.nranks;
-    if (!p.has_peers) {
-        p.issued = true;
-        return DSPMV_OK;
-    }
-    {
-        const ncclDataType_t ty = nccl_type(p.dtype);
-        char* rb = static_cast<char*>(p.d_recvbuf);
-        char* sb = static_cast<char*>(p.d_sendbuf);
-        ncclResult_t gr = ncclSuccess;
-        NCCL_TRY(ncclGroupStart());
-        for (int q = 0; q < P; ++q)
-            if (h.recv_count[q] > 0)
-                NCCL_GROUP_CALL(gr, ncclRecv(rb + size_t(h.recv_displ[q]) * p.esize, h.recv_count[q], ty, q,
-                                             p.comm->nccl, p.comm_stream));
-        for (int q = 0; q < P; ++q)
-            if (h.send_count[q] > 0)
-                NCCL_GROUP_CALL(gr, ncclSend(sb + size_t(h.send_displ[q]) * p.esize, h.send_count[q], ty, q,
-                                             p.comm->nccl, p.comm_stream));
-        NCCL_TRY(ncclGroupEnd());
-        NCCL_TRY(gr);
-    }
-    CUDA_TRY(cudaEventRecord(p.ev_x, p.comm_stream));
-    p.issued = true;
+    const ncclDataType_t ty = nccl_type(p.dtype);
+    char* rb = static_cast<char*>(p.d_recvbuf);
+    char* sb = static_cast<char*>(p.d_sendbuf);
+    ncclResult_t gr = ncclSuccess;
+    NCCL_TRY(ncclGroupStart());
+    for (int q : g.recv_from)
+        NCCL_GROUP_CALL(gr, ncclRecv(rb + size_t(h.recv_displ[q]) * p.esize, h.recv_count[q], ty, q, p.comm->nccl,
+                                     p.comm_stream));
+    for (int q : g.send_to)
+        NCCL_GROUP_CALL(gr, ncclSend(sb + size_t(h.send_displ[q]) * p.esize, h.send_count[q], ty, q, p.comm->nccl,
+                                     p.comm_stream));
+    NCCL_TRY(ncclGroupEnd());
+    NCCL_TRY(gr);
+    CUDA_TRY(cudaEventRecord(g.ev, p.comm_stream));
     return DSPMV_OK;
 }
 
@@ -452,41 +453,120 @@ PFN_cuStreamWaitValue32_v11070 wait_value32() {
 }
 
 // PUT mode: the data moves inside the fused Pack kernels; the exchange is the
-// comm stream waiting until every source rank has published this epoch.
-dspmv_status issue_exchange_put(Plan& p) {
-    p.issued = true;
-    if (!p.has_peers) return DSPMV_OK;
+// comm stream waiting until every source of the group has published this epoch.
+dspmv_status issue_group_put(Plan& p, ExGroup& g) {
+    g.issued = true;
+    if (g.empty()) return DSPMV_OK;
     auto wv = wait_value32();
     if (!wv) return fail(DSPMV_ERR_CUDA, "cuStreamWaitValue32 unavailable");
-    for (int q = 0; q < p.host.nranks; ++q) {
-        if (p.host.recv_count[q] <= 0) continue;
+    for (int q : g.recv_from) {
         const CUresult r = wv(reinterpret_cast<CUstream>(p.comm_stream), reinterpret_cast<CUdeviceptr>(p.d_flags + q),
                               p.epoch, CU_STREAM_WAIT_VALUE_GEQ);
         if (r != CUDA_SUCCESS) return fail(DSPMV_ERR_CUDA, "cuStreamWaitValue32 failed (" + std::to_string(int(r)) + ")");
     }
-    CUDA_TRY(cudaEventRecord(p.ev_x, p.comm_stream));
+    CUDA_TRY(cudaEventRecord(g.ev, p.comm_stream));
     return DSPMV_OK;
 }
 
-dspmv_status issue_exchange_local(const std::vector<Plan*>& ps) {
-    if (!ps.empty() && ps[0]->put_mode) {
-        for (Plan* pr : ps) ST_TRY(issue_exchange_put(*pr));
+// LOCAL group: group gi of every rank (lock-step, so all ranks have posted it).
+dspmv_status issue_group_local(const std::vector<Schedule*>& ss, int gi) {
+    if (!ss.empty() && ss[0]->plan->put_mode) {
+        for (Schedule* s : ss) ST_TRY(issue_group_put(*s->plan, s->groups[gi]));
         return DSPMV_OK;
     }
-    for (Plan* pr : ps) {
-        const RankPlan& h = pr->host;
-        for (int q = 0; q < h.nranks; ++q) {
-            const int32_t c = h.recv_count[q];
-            if (c <= 0) continue;
-            Plan* src = ps[q];
-            const size_t off_src = size_t(src->host.send_displ[h.rank]) * pr->esize;
-            CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(pr->d_recvbuf) + size_t(h.recv_displ[q]) * pr->esize,
-                                     static_cast<const char*>(src->d_sendbuf) + off_src, size_t(c) * pr->esize,
-                                     cudaMemcpyDeviceToDevice, pr->comm_stream));
+    for (Schedule* s : ss) {
+        Plan& pr = *s->plan;
+        ExGroup& g = s->groups[gi];
+        g.issued = true;
+        const RankPlan& h = pr.host;
+        for (int q : g.recv_from) {
+            const Plan* src = ss[q]->plan;
+            const size_t off_src = size_t(src->host.send_displ[h.rank]) * pr.esize;
+            CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(pr.d_recvbuf) + size_t(h.recv_displ[q]) * pr.esize,
+                                     static_cast<const char*>(src->d_sendbuf) + off_src,
+                                     size_t(h.recv_count[q]) * pr.esize, cudaMemcpyDeviceToDevice, pr.comm_stream));
         }
-        if (pr->has_peers) CUDA_TRY(cudaEventRecord(pr->ev_x, pr->comm_stream));
-        pr->issued = true;
+        if (!g.empty()) CUDA_TRY(cudaEventRecord(g.ev, pr.comm_stream));
     }
+    return DSPMV_OK;
+}
+
+// Resolve a schedule's exchange vertices against its plan (once the plan is
+// ready): groups, peers, PUT segments, and the per-destination coverage check.
+dspmv_status compile_exchange(Schedule& s) {
+    Plan& p = *s.plan;
+    const RankPlan& h = p.host;
+    const int P = h.nranks, me = h.rank;
+    auto data_send = [&](int q) { return q != me && h.send_count[q] > 0; };
+    auto data_recv = [&](int q) { return q != me && h.recv_count[q] > 0; };
+    auto sends = [&](int q) { return p.put_mode ? flag_peer(h, q) : data_send(q); };
+    auto recvs = [&](int q) { return p.put_mode ? flag_peer(h, q) : data_recv(q); };
+    std::vector<int> seg_of(P, -1);  // PUT segment index per destination
+    for (int q = 0, j = 0; q < P; ++q)
+        if (p.put_mode && flag_peer(h, q)) seg_of[q] = j++;
+    const std::vector<int>& S = s.dag.offsets;
+    auto has = [&](int d) { return std::binary_search(S.begin(), S.end(), d); };
+    std::vector<ExGroup> groups;
+    if (!s.dag.fine) {
+        ExGroup g;
+        for (int q = 0; q < P; ++q) {
+            if (sends(q)) g.send_to.push_back(q);
+            if (recvs(q)) g.recv_from.push_back(q);
+        }
+        groups.push_back(g);
+    } else {
+        for (int q = 0; q < P; ++q) {
+            if ((sends(q) && !has(q - me)) || (recvs(q) && !has(me - q)))
+                return fail(DSPMV_ERR_SCHEDULE, "per-destination schedule names no exchange with rank offset " +
+                                                    std::to_string(q - me) + " (rank " + std::to_string(me) +
+                                                    " exchanges with rank " + std::to_string(q) + ")");
+        }
+        for (int d : S) {
+            ExGroup g;
+            g.d = d;
+            const int to = me + d, from = me - d;
+            if (to >= 0 && to < P && sends(to)) g.send_to.push_back(to);
+            if (from >= 0 && from < P && recvs(from)) g.recv_from.push_back(from);
+            groups.push_back(g);
+        }
+    }
+    auto group_of = [&](int d) {
+        for (size_t i = 0; i < groups.size(); ++i)
+            if (groups[i].d == d) return int(i);
+        return -1;
+    };
+    const int n = int(s.ops.size());
+    s.op_group.assign(n, -1);
+    s.op_peer.assign(n, -2);
+    s.op_seg.assign(n, -1);
+    for (int t = 0; t < n; ++t) {
+        const dspmv_op& o = s.ops[t];
+        switch (o.kind) {
+            case DSPMV_OP_POST_SEND:
+            case DSPMV_OP_WAIT_SEND: s.op_group[t] = group_of(o.peer); break;
+            case DSPMV_OP_POST_RECV:
+            case DSPMV_OP_WAIT_RECV: s.op_group[t] = group_of(-o.peer); break;
+            case DSPMV_OP_PACK:
+                if (o.peer) {
+                    const int q = me + o.peer;
+                    const bool ok = q >= 0 && q < P && (p.put_mode ? flag_peer(h, q) : data_send(q));
+                    s.op_peer[t] = ok ? q : -1;
+                    s.op_seg[t] = ok && p.put_mode ? seg_of[q] : -1;
+                }
+                break;
+            case DSPMV_OP_UNPACK:
+                if (o.peer) {
+                    const int q = me + o.peer;
+                    s.op_peer[t] = (q >= 0 && q < P && data_recv(q)) ? q : -1;
+                }
+                break;
+            default: break;
+        }
+    }
+    for (ExGroup& g : groups)
+        if (!g.ev) CUDA_TRY(cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming));
+    s.groups.swap(groups);
+    s.compiled = true;
     return DSPMV_OK;
 }
 
@@ -496,6 +576,7 @@ dspmv_status begin_apply(Schedule& s, cudaStream_t caller) {
     if (!p.ready) return fail(DSPMV_ERR_STATE, "plan not ready (LOCAL group: not every rank has called plan_create)");
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess || cur != p.device) CUDA_TRY(cudaSetDevice(p.device));
+    if (!s.compiled) ST_TRY(compile_exchange(s));
     if (s.step0) CUDA_TRY(cudaEventRecord(s.step0, caller));
     ++p.epoch;
     CUDA_TRY(cudaEventRecord(p.ev_start, caller));
@@ -504,8 +585,68 @@ dspmv_status begin_apply(Schedule& s, cudaStream_t caller) {
     p.cur_stream0 = p.opts.caller_stream0 ? caller : p.streams[0];
     for (int i = p.opts.caller_stream0 ? 1 : 0; i < s.n_streams; ++i)
         CUDA_TRY(cudaStreamWaitEvent(p.streams[i], p.ev_start, 0));
-    p.posted_send = p.posted_recv = p.issued = false;
+    for (ExGroup& g : s.groups) g.ps = g.pr = g.issued = false;
     return DSPMV_OK;
+}
+
+// The kernel(s) of GPU vertex op t on stream st (shared by the host-driven
+// executor and graph capture).
+cudaError_t launch_gpu_vertex(Schedule& s, int t, const void* x, void* y, cudaStream_t st) {
+    Plan& p = *s.plan;
+    cudaError_t e = cudaSuccess;
+    switch (s.ops[t].kind) {
+        case DSPMV_OP_PACK: {
+            const int q = s.op_peer[t];  // -2: every destination; -1: nothing to send
+            if (q == -1) break;
+            if (p.put_mode) {
+                void* const* dst = p.d_seg_dst + (p.epoch & 1u) * p.put_nseg;
+                if (q == -2) {
+                    PutArgs a{x, p.d_pack_map, 0, int64_t(p.host.pack_map.size()), p.d_seg_begin, dst, p.d_seg_flag,
+                              p.put_nseg, p.epoch, p.d_put_counter + p.put_nseg};
+                    e = launch_pack_put(p.dtype, a, st);
+                } else {
+                    const int j = s.op_seg[t];
+                    const int64_t k0 = p.host.send_displ[q];
+                    PutArgs a{x, p.d_pack_map, k0, k0 + p.host.send_count[q], p.d_seg_begin + j, dst + j,
+                              p.d_seg_flag + j, 1, p.epoch, p.d_put_counter + j};
+                    e = launch_pack_put(p.dtype, a, st);
+                }
+            } else if (q == -2) {
+                e = launch_pack(p.dtype, x, p.d_pack_map, p.d_sendbuf, int64_t(p.host.pack_map.size()), st);
+            } else {
+                const int64_t k0 = p.host.send_displ[q];
+                e = launch_pack(p.dtype, x, p.d_pack_map + k0, static_cast<char*>(p.d_sendbuf) + k0 * p.esize,
+                                p.host.send_count[q], st);
+            }
+            break;
+        }
+        case DSPMV_OP_SPMV_LOCAL: {
+            SpmvOperands op{x, y, p.d_partL, p.d_partR, p.d_ticket};
+            e = launch_spmv(p.L, p.dtype, op, st);
+            break;
+        }
+        case DSPMV_OP_UNPACK: {
+            const int q = s.op_peer[t];
+            if (q == -1) break;
+            const char* src = static_cast<const char*>(p.d_recvbuf) +
+                              (p.put_mode && (p.epoch & 1u) ? p.recv_stride * size_t(p.esize) : 0);
+            if (q == -2) {
+                e = launch_copy(p.dtype, src, p.d_xhalo, int64_t(p.host.halo_gid.size()), st);
+            } else {
+                const size_t off = size_t(p.host.recv_displ[q]) * p.esize;
+                e = launch_copy(p.dtype, src + off, static_cast<char*>(p.d_xhalo) + off, p.host.recv_count[q], st);
+            }
+            break;
+        }
+        case DSPMV_OP_SPMV_REMOTE: {
+            SpmvOperands op{p.d_xhalo, y, p.d_partR, p.d_partL, p.d_ticket};
+            e = launch_spmv(p.R, p.dtype, op, st);
+            break;
+        }
+        default:
+            break;
+    }
+    return e;
 }
 
 // Execute op t of schedule s. `defer` = LOCAL group (exchange issued by caller).
@@ -524,39 +665,19 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
         case DSPMV_OP_END:
             break;
         case DSPMV_OP_PACK:
-            if (p.put_mode) {
-                PutArgs a{x, p.d_pack_map, int64_t(p.host.pack_map.size()), p.d_seg_begin,
-                          p.d_seg_dst + (p.epoch & 1u) * p.put_nseg, p.d_seg_flag, p.put_nseg, p.epoch,
-                          p.d_put_counter};
-                e = launch_pack_put(p.dtype, a, st);
-            } else {
-                e = launch_pack(p.dtype, x, p.d_pack_map, p.d_sendbuf, int64_t(p.host.pack_map.size()), st);
-            }
+        case DSPMV_OP_SPMV_LOCAL:
+        case DSPMV_OP_UNPACK:
+        case DSPMV_OP_SPMV_REMOTE:
+            e = launch_gpu_vertex(s, t, x, y, st);
             break;
-        case DSPMV_OP_SPMV_LOCAL: {
-            SpmvOperands op{x, y, p.d_partL, p.d_partR, p.d_ticket};
-            e = launch_spmv(p.L, p.dtype, op, st);
-            break;
-        }
-        case DSPMV_OP_UNPACK: {
-            const size_t h = p.host.halo_gid.size();
-            const char* src = static_cast<const char*>(p.d_recvbuf) +
-                              (p.put_mode && (p.epoch & 1u) ? p.recv_stride * size_t(p.esize) : 0);
-            e = launch_copy(p.dtype, src, p.d_xhalo, int64_t(h), st);
-            break;
-        }
-        case DSPMV_OP_SPMV_REMOTE: {
-            SpmvOperands op{p.d_xhalo, y, p.d_partR, p.d_partL, p.d_ticket};
-            e = launch_spmv(p.R, p.dtype, op, st);
-            break;
-        }
         case DSPMV_OP_POST_SEND:
-        case DSPMV_OP_POST_RECV:
-            if (o.kind == DSPMV_OP_POST_SEND) p.posted_send = true; else p.posted_recv = true;
-            if (!defer && p.posted_send && p.posted_recv && !p.issued) {
+        case DSPMV_OP_POST_RECV: {
+            ExGroup& g = s.groups[s.op_group[t]];
+            if (o.kind == DSPMV_OP_POST_SEND) g.ps = true; else g.pr = true;
+            if (!defer && g.ps && g.pr && !g.issued) {
                 // exchange time on the comm stream (0 in op_times unless this op issued it)
                 if (timed_x) CUDA_TRY(cudaEventRecord(s.t0[t], p.comm_stream));
-                dspmv_status r = p.put_mode ? issue_exchange_put(p) : issue_exchange_nccl(p);
+                dspmv_status r = p.put_mode ? issue_group_put(p, g) : issue_group_nccl(p, g);
                 if (r != DSPMV_OK) {
                     p.poisoned = true;
                     return r;
@@ -567,10 +688,12 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
                 CUDA_TRY(cudaEventRecord(s.t1[t], p.comm_stream));
             }
             break;
+        }
         case DSPMV_OP_WAIT_SEND:
         case DSPMV_OP_WAIT_RECV: {
-            if (!p.issued) return fail(DSPMV_ERR_STATE, "Wait before the exchange was issued");
-            dspmv_status r = wait_exchange(p);
+            const ExGroup& g = s.groups[s.op_group[t]];
+            if (!g.issued) return fail(DSPMV_ERR_STATE, "Wait before the exchange was issued");
+            dspmv_status r = wait_group(p, g);
             if (r != DSPMV_OK) return r;
             break;
         }
@@ -588,8 +711,10 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
     }
     if (e != cudaSuccess) {
         p.poisoned = true;
-        return fail(DSPMV_ERR_CUDA, std::string("op ") + std::to_string(t) + " (" + vertex_name(o.kind) +
-                                        "): " + cudaGetErrorString(e));
+        const char* sync_names[] = {"CER", "CES", "CSWE"};
+        const std::string nm = is_dag_vertex(o.kind) ? vertex_label(o.kind, o.peer)
+                                                     : std::string(sync_names[(o.kind - DSPMV_OP_EVENT_RECORD) % 3]);
+        return fail(DSPMV_ERR_CUDA, "op " + std::to_string(t) + " (" + nm + "): " + cudaGetErrorString(e));
     }
     if (timed) CUDA_TRY(cudaEventRecord(s.t1[t], st));
     return DSPMV_OK;
@@ -610,6 +735,7 @@ dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t ori
         return fail(DSPMV_ERR_ARG, "apply_graph: the PUT exchange carries a per-apply epoch; use dspmv_apply");
     if (p.comm->kind == DSPMV_COMM_LOCAL && p.host.nranks > 1)
         return fail(DSPMV_ERR_ARG, "apply_graph: LOCAL groups with > 1 rank run with dspmv_apply_group");
+    if (!s.compiled) ST_TRY(compile_exchange(s));
     for (auto& e : s.gev)
         if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     const int ns = s.n_streams;
@@ -642,7 +768,7 @@ dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t ori
         }
         return cudaSuccess;
     };
-    bool ps = false, pr = false, issued = false;
+    for (ExGroup& g : s.groups) g.ps = g.pr = g.issued = false;
     for (int t = 0; t < int(s.ops.size()); ++t) {
         const dspmv_op& o = s.ops[t];
         const bool gpu = is_gpu_vertex(o.kind);
@@ -652,42 +778,31 @@ dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t ori
         if (timed) CAP_TRY(cudaEventRecordWithFlags(s.t0[t], q, cudaEventRecordExternal));
         switch (o.kind) {
             case DSPMV_OP_PACK:
-                CAP_TRY(launch_pack(p.dtype, x, p.d_pack_map, p.d_sendbuf, int64_t(p.host.pack_map.size()), q));
-                break;
-            case DSPMV_OP_SPMV_LOCAL: {
-                SpmvOperands op{x, y, p.d_partL, p.d_partR, p.d_ticket};
-                CAP_TRY(launch_spmv(p.L, p.dtype, op, q));
-                break;
-            }
+            case DSPMV_OP_SPMV_LOCAL:
             case DSPMV_OP_UNPACK:
-                CAP_TRY(launch_copy(p.dtype, p.d_recvbuf, p.d_xhalo, int64_t(p.host.halo_gid.size()), q));
+            case DSPMV_OP_SPMV_REMOTE:
+                CAP_TRY(launch_gpu_vertex(s, t, x, y, q));
                 break;
-            case DSPMV_OP_SPMV_REMOTE: {
-                SpmvOperands op{p.d_xhalo, y, p.d_partR, p.d_partL, p.d_ticket};
-                CAP_TRY(launch_spmv(p.R, p.dtype, op, q));
+            case DSPMV_OP_POST_SEND:
+            case DSPMV_OP_POST_RECV: {
+                ExGroup& g = s.groups[s.op_group[t]];
+                (o.kind == DSPMV_OP_POST_SEND ? g.ps : g.pr) = true;
+                const bool tx = s.timing && s.t0[t];
+                cudaStream_t xs = p.has_peers ? p.comm_stream : origin;  // comm joins the capture only with peers
+                if (tx) CAP_TRY(cudaEventRecordWithFlags(s.t0[t], xs, cudaEventRecordExternal));
+                if (g.ps && g.pr && !g.issued) {
+                    dspmv_status r = issue_group_nccl(p, g);  // captured on the comm stream
+                    if (r != DSPMV_OK) return abort_capture(r);
+                }
+                if (tx) CAP_TRY(cudaEventRecordWithFlags(s.t1[t], xs, cudaEventRecordExternal));
                 break;
             }
-            case DSPMV_OP_POST_SEND:
-            case DSPMV_OP_POST_RECV:
-                (o.kind == DSPMV_OP_POST_SEND ? ps : pr) = true;
-                {
-                    const bool tx = s.timing && s.t0[t];
-                    cudaStream_t xs = p.has_peers ? p.comm_stream : origin;  // comm joins the capture only with peers
-                    if (tx) CAP_TRY(cudaEventRecordWithFlags(s.t0[t], xs, cudaEventRecordExternal));
-                    if (ps && pr && !issued) {
-                        issued = true;
-                        if (p.has_peers) {
-                            dspmv_status r = issue_exchange_nccl(p);  // captured on the comm stream
-                            if (r != DSPMV_OK) return abort_capture(r);
-                        }
-                    }
-                    if (tx) CAP_TRY(cudaEventRecordWithFlags(s.t1[t], xs, cudaEventRecordExternal));
-                }
-                break;
             case DSPMV_OP_WAIT_SEND:
-            case DSPMV_OP_WAIT_RECV:
-                if (p.has_peers) CAP_TRY(all_wait(p.ev_x));
+            case DSPMV_OP_WAIT_RECV: {
+                const ExGroup& g = s.groups[s.op_group[t]];
+                if (!g.empty()) CAP_TRY(all_wait(g.ev));
                 break;
+            }
             case DSPMV_OP_EVENT_RECORD:
                 CAP_TRY(cudaEventRecord(s.ev[o.event], q));
                 break;
@@ -861,7 +976,6 @@ static void free_plan_device(Plan& p) {
         if (s) cudaStreamDestroy(s), s = nullptr;
     if (p.comm_stream) cudaStreamDestroy(p.comm_stream), p.comm_stream = nullptr;
     if (p.ev_start) cudaEventDestroy(p.ev_start), p.ev_start = nullptr;
-    if (p.ev_x) cudaEventDestroy(p.ev_x), p.ev_x = nullptr;
 }
 
 dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_local, const int64_t* rowptr,
@@ -914,8 +1028,7 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
     }
     if (cudaStreamCreateWithPriority(&p->comm_stream, cudaStreamNonBlocking, opts.comm_priority ? hi : lo) !=
             cudaSuccess ||
-        cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->ev_x, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(DSPMV_ERR_CUDA, "stream/event creation failed"));
 
     // device layouts of A_L (slots = position of the row in ar_rows) and A_R
@@ -956,7 +1069,10 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
         // own allocation (IPC-exportable); at least one word so every rank has a handle
         if ((st = dev_alloc(*p, reinterpret_cast<void**>(&p->d_flags), size_t(comm->nranks) * 4, true)) != DSPMV_OK)
             return bail(st);
-        if ((st = dev_alloc(*p, reinterpret_cast<void**>(&p->d_put_counter), 4, true)) != DSPMV_OK) return bail(st);
+        // last-CTA counters: one per destination segment (per-destination Pack) + one
+        if ((st = dev_alloc(*p, reinterpret_cast<void**>(&p->d_put_counter), size_t(comm->nranks + 1) * 4, true)) !=
+            DSPMV_OK)
+            return bail(st);
     }
     if ((st = dev_alloc(*p, &p->d_xhalo, hsz * p->esize, true)) != DSPMV_OK) return bail(st);
     if ((st = dev_alloc(*p, &p->d_partL, size_t(nR) * p->esize, true)) != DSPMV_OK) return bail(st);
@@ -1237,6 +1353,7 @@ dspmv_status dspmv_schedule_create(dspmv_plan_t plan, const dspmv_op* ops, int n
     s->plan = plan;
     s->ops.assign(ops, ops + n_ops);
     s->n_streams = n_streams;
+    s->dag = std::move(c.dag);
     for (const dspmv_op& o : s->ops) {
         if (o.kind == DSPMV_OP_EVENT_RECORD && !s->ev[o.event]) {
             if (cudaEventCreateWithFlags(&s->ev[o.event], cudaEventDisableTiming) != cudaSuccess) {
@@ -1245,6 +1362,22 @@ dspmv_status dspmv_schedule_create(dspmv_plan_t plan, const dspmv_op* ops, int n
                 delete s;
                 return fail(DSPMV_ERR_CUDA, "cudaEventCreate failed");
             }
+        }
+    }
+    // per-destination coverage is checked here when the plan is ready (a LOCAL
+    // rank's plan becomes ready when the whole group has planned: then at the
+    // first apply)
+    if (plan->ready) {
+        const dspmv_status cs = compile_exchange(*s);
+        if (cs != DSPMV_OK) {
+            std::string keep = t_err;
+            for (auto& e : s->ev)
+                if (e) cudaEventDestroy(e);
+            for (auto& g : s->groups)
+                if (g.ev) cudaEventDestroy(g.ev);
+            delete s;
+            t_err = keep;
+            return cs;
         }
     }
     plan->live_scheds++;
@@ -1271,6 +1404,8 @@ dspmv_status dspmv_schedule_destroy(dspmv_schedule_t s) {
         if (e) cudaEventDestroy(e);
     for (auto& e : s->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& g : s->groups)
+        if (g.ev) cudaEventDestroy(g.ev);
     destroy_timing(*s);
     s->plan->live_scheds--;
     delete s;
@@ -1346,10 +1481,9 @@ dspmv_status dspmv_apply(dspmv_schedule_t s, const void* x, void* y, dspmv_strea
     const bool local = p.comm->kind == DSPMV_COMM_LOCAL;
     for (int t = 0; t < int(s->ops.size()); ++t) {
         ST_TRY(exec_op(*s, t, x, y, local));
-        if (local && p.posted_send && p.posted_recv && !p.issued) {
-            std::vector<Plan*> one{&p};
-            ST_TRY(issue_exchange_local(one));
-        }
+        const int gi = s->op_group[t];
+        if (local && gi >= 0 && s->groups[gi].ps && s->groups[gi].pr && !s->groups[gi].issued)
+            ST_TRY(issue_group_local({s}, gi));
     }
     if (s->step1) CUDA_TRY(cudaEventRecord(s->step1, static_cast<cudaStream_t>(stream)));
     s->timed_valid = s->timing;
@@ -1410,10 +1544,14 @@ dspmv_status dspmv_apply_group(const dspmv_schedule_t* scheds, int nranks, const
         plans[r] = p;
     }
     for (int r = 0; r < nranks; ++r) ST_TRY(begin_apply(*scheds[r], static_cast<cudaStream_t>(stream)));
+    std::vector<Schedule*> ss(scheds, scheds + nranks);
     const int n_ops = int(scheds[0]->ops.size());
     for (int t = 0; t < n_ops; ++t) {
         for (int r = 0; r < nranks; ++r) ST_TRY(exec_op(*scheds[r], t, x[r], y[r], true));
-        if (plans[0]->posted_send && plans[0]->posted_recv && !plans[0]->issued) ST_TRY(issue_exchange_local(plans));
+        // lock-step and SPMD: a group is posted on every rank at the same op
+        const int gi = scheds[0]->op_group[t];
+        if (gi >= 0 && scheds[0]->groups[gi].ps && scheds[0]->groups[gi].pr && !scheds[0]->groups[gi].issued)
+            ST_TRY(issue_group_local(ss, gi));
     }
     for (int r = 0; r < nranks; ++r) {
         if (scheds[r]->step1) CUDA_TRY(cudaEventRecord(scheds[r]->step1, static_cast<cudaStream_t>(stream)));

@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <array>
 #include <string>
 #include <vector>
 
@@ -100,13 +101,31 @@ void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, cons
                   const BlockCfg& cfg, Layout& L);
 
 // -------------------------------------------------------------- schedules
+// A DAG vertex instance: kind + peer offset (0 = coarse / not an exchange vertex)
+struct DagVertex {
+    int kind;
+    int peer;
+};
+// The program DAG of one granularity (schedule.cpp build_dag).
+struct Dag {
+    std::vector<DagVertex> v;
+    std::vector<std::array<int, 3>> edges;  // u, v, deadlock edge
+    bool fine = false;
+    std::vector<int> offsets;                // S (sorted); {0} when coarse
+    int find(int kind, int peer) const;
+};
+bool build_dag(const std::vector<DagVertex>& present, Dag& g, std::string& why);
 struct SchedCheck {
     dspmv_status st = DSPMV_OK;
     std::string why;
+    Dag dag;
+    std::vector<int> inst;                   // op -> DAG vertex id (-1 for syncs)
 };
 bool is_gpu_vertex(int kind);
 bool is_dag_vertex(int kind);
+bool is_exchange_vertex(int kind);
 SchedCheck validate_schedule(const dspmv_op* ops, int n_ops, int n_streams);
 const char* vertex_name(int kind);
+std::string vertex_label(int kind, int peer);
 
 }  // namespace dspmv

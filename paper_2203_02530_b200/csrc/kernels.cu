@@ -17,7 +17,8 @@
 //   spmv_vector_kernel rows with > vector_threshold nnz: one warp per row,
 //                      unrolled coalesced loads, warp-shuffle reduction.
 //   pack_kernel        sendbuf[k] = x[pack_map[k]]
-//   copy_kernel        x_halo = recvbuf (Unpack, DESIGN.md R-Q8)
+//   copy_kernel        x_halo = recvbuf (Unpack, DESIGN.md R-Q8); element-wise
+//                      for unaligned per-destination segments
 //   flush_kernel       L2 eviction between timed iterations (reads 2x L2)
 //
 // y = y_L + y_R on rows with remote entries is combined without an extra DAG
@@ -399,9 +400,10 @@ __global__ void pack_kernel(const T* __restrict__ x, const int32_t* __restrict__
 template <typename T>
 __global__ void pack_put_kernel(PutArgs a) {
     const T* __restrict__ x = static_cast<const T*>(a.x);
-    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < a.n; k += int64_t(gridDim.x) * blockDim.x) {
-        int j = 0;
-        while (j + 1 < a.nseg && a.seg_begin[j + 1] <= k) ++j;   // nseg = destinations (<= P)
+    for (int64_t k = a.k0 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < a.n;
+         k += int64_t(gridDim.x) * blockDim.x) {
+        int j = 0;  // nseg = destinations (<= P); empty segments only carry a flag
+        while (j + 1 < a.nseg && a.seg_begin[j + 1] <= k) ++j;
         static_cast<T*>(a.seg_dst[j])[k - a.seg_begin[j]] = __ldg(x + __ldg(a.pack_map + k));
     }
     __threadfence_system();
@@ -426,6 +428,13 @@ __global__ void copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ d
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t i = tid; i < n16; i += stride) dst[i] = __ldcs(src + i);
     for (int64_t i = tail_from + tid; i < tail_to; i += stride) d8[i] = s8[i];
+}
+
+// Element-wise copy for segments not 16-B aligned (per-destination Unpack).
+template <typename T>
+__global__ void copy_elems_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        dst[i] = __ldcs(src + i);
 }
 
 // Read 2x L2 of scratch (leaves L2 clean and holding none of the SpMV data);
@@ -584,7 +593,8 @@ cudaError_t launch_pack(int dtype, const void* x, const int32_t* map, void* out,
 
 cudaError_t launch_pack_put(int dtype, const PutArgs& a, cudaStream_t s) {
     if (a.nseg <= 0) return cudaSuccess;
-    const int grid = int(std::max<int64_t>(1, std::min<int64_t>((a.n + 255) / 256, int64_t(num_sms()) * 4)));
+    const int grid =
+        int(std::max<int64_t>(1, std::min<int64_t>((a.n - a.k0 + 255) / 256, int64_t(num_sms()) * 4)));
     if (dtype == DSPMV_F32) pack_put_kernel<float><<<grid, 256, 0, s>>>(a);
     else pack_put_kernel<double><<<grid, 256, 0, s>>>(a);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -593,6 +603,15 @@ cudaError_t launch_pack_put(int dtype, const PutArgs& a, cudaStream_t s) {
 
 cudaError_t launch_copy(int dtype, const void* src, void* dst, int64_t n, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
+    if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) {
+        const int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(num_sms()) * 8));
+        if (dtype == DSPMV_F32)
+            copy_elems_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(src), static_cast<float*>(dst), n);
+        else
+            copy_elems_kernel<double><<<grid, 256, 0, s>>>(static_cast<const double*>(src), static_cast<double*>(dst), n);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return cudaGetLastError();
+    }
     const int64_t bytes = n * (dtype == DSPMV_F32 ? 4 : 8);
     const int64_t n16 = bytes / 16;
     const int grid = int(std::min<int64_t>((n16 + 255) / 256 + 1, int64_t(num_sms()) * 8));

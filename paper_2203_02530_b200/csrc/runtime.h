@@ -59,7 +59,7 @@ cudaError_t launch_flush(void* buf, size_t bytes, cudaStream_t s);
 struct PutArgs {
     const void* x;
     const int32_t* pack_map;
-    int64_t n;
+    int64_t k0, n;              // send-list entries [k0, n)
     const int64_t* seg_begin;   // [nseg + 1]
     void* const* seg_dst;       // [nseg]
     unsigned* const* seg_flag;  // [nseg]
@@ -108,7 +108,7 @@ struct Plan {
     cudaStream_t streams[DSPMV_MAX_STREAMS] = {};
     cudaStream_t comm_stream = nullptr;
     cudaStream_t cur_stream0 = nullptr;  // stream of schedule stream 0 in this apply
-    cudaEvent_t ev_start = nullptr, ev_x = nullptr;
+    cudaEvent_t ev_start = nullptr;
     std::vector<void*> allocs;
     int64_t device_bytes = 0;
     bool ready = false;                // phase 2 done (send lists, pack map)
@@ -126,14 +126,34 @@ struct Plan {
     std::vector<void*> ipc_opened;     // peer mappings to close
     bool poisoned = false;
     int live_scheds = 0;
-    // per-apply exchange state
-    bool posted_send = false, posted_recv = false, issued = false;
+};
+
+// One halo-exchange group of a schedule, issued once both its PostSend and
+// its PostRecv have executed (R-Q16).  Coarse: every peer.  Per destination
+// (R-N4): the shift by d -- send to rank r+d, receive from rank r-d -- made
+// of PostSend[d] and PostRecv[-d].  COPY: the ranks data moves to / from;
+// PUT: the ranks epoch flags go to / come from (both directions of every
+// pair that exchanges anything, so a sender never runs two applies ahead of
+// a receiver that still reads the other receive buffer).
+struct ExGroup {
+    int d = 0;
+    std::vector<int> send_to, recv_from;
+    cudaEvent_t ev = nullptr;          // recorded on the comm stream at issue
+    bool ps = false, pr = false, issued = false;
+    bool empty() const { return send_to.empty() && recv_from.empty(); }
 };
 
 struct Schedule {
     Plan* plan = nullptr;
     std::vector<dspmv_op> ops;
     int n_streams = 1;
+    Dag dag;                           // granularity (coarse / per destination)
+    // resolved against the plan (compile_exchange): exchange groups, the group
+    // of every Post/Wait op, the peer rank of every per-destination Pack /
+    // Unpack (-2 = all peers, -1 = nothing to do) and its PUT segment
+    bool compiled = false;
+    std::vector<ExGroup> groups;
+    std::vector<int> op_group, op_peer, op_seg;
     cudaEvent_t ev[DSPMV_MAX_EVENTS] = {};
     bool timing = false;
     std::vector<cudaEvent_t> t0, t1;   // per op (GPU vertices only)

@@ -14,6 +14,9 @@
 // Every enqueue on a stream inherits the host's knowledge (it is issued after
 // everything the host has synchronised).  Edge u->v is enforced iff the
 // consumer's clock covers u's position.
+// Exchange vertices may be per destination (dspmv_op.peer = rank offset,
+// P:281-284, DESIGN.md R-N4); build_dag derives the DAG of the granularity a
+// schedule uses.
 #include <algorithm>
 #include <array>
 #include <cstdio>
@@ -24,21 +27,13 @@
 namespace dspmv {
 
 namespace {
-constexpr int NV = 10;  // DAG vertices = op kinds 0..9
-// SPEC.md S:125 edge list + DESIGN.md R-Q13 (deadlock-freedom edges last)
-const int kEdges[][2] = {
-    {DSPMV_OP_START, DSPMV_OP_PACK},          {DSPMV_OP_START, DSPMV_OP_SPMV_LOCAL},
-    {DSPMV_OP_START, DSPMV_OP_POST_RECV},     {DSPMV_OP_PACK, DSPMV_OP_POST_SEND},
-    {DSPMV_OP_POST_SEND, DSPMV_OP_WAIT_SEND}, {DSPMV_OP_POST_RECV, DSPMV_OP_WAIT_RECV},
-    {DSPMV_OP_WAIT_RECV, DSPMV_OP_UNPACK},    {DSPMV_OP_UNPACK, DSPMV_OP_SPMV_REMOTE},
-    {DSPMV_OP_SPMV_LOCAL, DSPMV_OP_END},      {DSPMV_OP_SPMV_REMOTE, DSPMV_OP_END},
-    {DSPMV_OP_WAIT_SEND, DSPMV_OP_END},
-    {DSPMV_OP_POST_SEND, DSPMV_OP_WAIT_RECV}, {DSPMV_OP_POST_RECV, DSPMV_OP_WAIT_SEND}};
-constexpr int kNumEdges = sizeof(kEdges) / sizeof(kEdges[0]);
-constexpr int kFirstDeadlockEdge = 11;
+constexpr int NV = 10;  // op kinds 0..9 are DAG vertex kinds
 
 const char* kNames[NV] = {"start", "Pack", "y_L", "PostSend", "PostRecv",
                           "WaitSend", "WaitRecv", "Unpack", "y_R", "end"};
+
+bool send_side(int k) { return k == DSPMV_OP_PACK || k == DSPMV_OP_POST_SEND || k == DSPMV_OP_WAIT_SEND; }
+bool recv_side(int k) { return k == DSPMV_OP_POST_RECV || k == DSPMV_OP_WAIT_RECV || k == DSPMV_OP_UNPACK; }
 
 using Clock = std::array<int32_t, DSPMV_MAX_STREAMS>;
 
@@ -46,21 +41,23 @@ inline void merge(Clock& a, const Clock& b) {
     for (int i = 0; i < DSPMV_MAX_STREAMS; ++i) a[i] = std::max(a[i], b[i]);
 }
 
-// Incremental happens-before state over a prefix of a schedule.
+// Incremental happens-before state over a prefix of a schedule; DAG vertex
+// instances are indexed by Dag ids.
 struct HB {
     Clock host{};
     std::array<Clock, DSPMV_MAX_STREAMS> vc{};
     std::array<int32_t, DSPMV_MAX_STREAMS> len{};
     std::array<Clock, DSPMV_MAX_EVENTS> ev{};
-    std::array<bool, DSPMV_MAX_EVENTS> recorded{};
-    std::array<int, NV> stream_of{};  // GPU vertex -> stream
-    std::array<int32_t, NV> pos{};    // GPU vertex -> position in its stream
-    std::array<bool, NV> done{};
+    std::vector<int> stream_of;   // instance -> stream (GPU vertices)
+    std::vector<int32_t> pos;     // instance -> position in its stream
+    std::vector<bool> done;
+    const Dag* dag;
 
+    explicit HB(const Dag& d) : stream_of(d.v.size(), 0), pos(d.v.size(), 0), done(d.v.size(), false), dag(&d) {}
     void enqueue(int s) { merge(vc[s], host); }
     // would a DAG edge u->v be enforced if v (on stream sv, or CPU if sv<0) ran now?
     bool enforced(int u, int sv) const {
-        if (!is_gpu_vertex(u)) return true;
+        if (!is_gpu_vertex(dag->v[u].kind)) return true;
         const int su = stream_of[u];
         if (sv < 0) return host[su] >= pos[u];
         if (sv == su) return true;
@@ -68,21 +65,21 @@ struct HB {
         merge(c, host);
         return c[su] >= pos[u];
     }
-    void apply(const dspmv_op& op) {
+    void vertex(int id, int stream) {
+        if (is_gpu_vertex(dag->v[id].kind)) {
+            enqueue(stream);
+            pos[id] = ++len[stream];
+            stream_of[id] = stream;
+        }
+        done[id] = true;
+    }
+    void sync(const dspmv_op& op) {
         const int k = op.kind;
-        if (k >= 0 && k < NV) {
-            if (is_gpu_vertex(k)) {
-                enqueue(op.stream);
-                pos[k] = ++len[op.stream];
-                stream_of[k] = op.stream;
-            }
-            done[k] = true;
-        } else if (k == DSPMV_OP_EVENT_RECORD) {
+        if (k == DSPMV_OP_EVENT_RECORD) {
             enqueue(op.stream);
             Clock c = vc[op.stream];
             c[op.stream] = len[op.stream];
             ev[op.event] = c;
-            recorded[op.event] = true;
         } else if (k == DSPMV_OP_EVENT_SYNC) {
             merge(host, ev[op.event]);
         } else if (k == DSPMV_OP_STREAM_WAIT_EVENT) {
@@ -98,7 +95,115 @@ bool is_gpu_vertex(int kind) {
     return kind == DSPMV_OP_PACK || kind == DSPMV_OP_SPMV_LOCAL || kind == DSPMV_OP_UNPACK ||
            kind == DSPMV_OP_SPMV_REMOTE;
 }
+bool is_exchange_vertex(int kind) { return send_side(kind) || recv_side(kind); }
 const char* vertex_name(int kind) { return is_dag_vertex(kind) ? kNames[kind] : "?"; }
+std::string vertex_label(int kind, int peer) {
+    std::string s = vertex_name(kind);
+    if (peer) s += std::string("[") + (peer > 0 ? "+" : "") + std::to_string(peer) + "]";
+    return s;
+}
+
+int Dag::find(int kind, int peer) const {
+    for (size_t i = 0; i < v.size(); ++i)
+        if (v[i].kind == kind && v[i].peer == peer) return int(i);
+    return -1;
+}
+
+// The program DAG for the granularity of `present` (the DAG vertices a
+// schedule names).  Coarse (every exchange vertex peer 0): SPEC S:125 +
+// R-Q13.  Per destination (reading R-N4): the send-offset set S is
+// the offsets of the send-side vertices and the negated offsets of the
+// receive-side ones; each d in S contributes Pack/PostSend/WaitSend[d] and
+// PostRecv/WaitRecv/Unpack[-d], with PostSend[d] -> WaitRecv[-d] and
+// PostRecv[-d] -> WaitSend[d] as the deadlock edges.  Edges are emitted so
+// that every vertex sees its predecessors in the oracle's order.
+bool build_dag(const std::vector<DagVertex>& present, Dag& g, std::string& why) {
+    g = Dag{};
+    bool any_fine = false, any_coarse = false;
+    std::vector<int> S;
+    for (const DagVertex& x : present) {
+        if (!is_dag_vertex(x.kind)) {
+            why = "not a DAG vertex";
+            return false;
+        }
+        if (!is_exchange_vertex(x.kind)) {
+            if (x.peer != 0) {
+                why = std::string(kNames[x.kind]) + " takes no peer offset";
+                return false;
+            }
+            continue;
+        }
+        if (x.peer == 0) {
+            any_coarse = true;
+        } else {
+            if (x.peer < -(1 << 20) || x.peer > (1 << 20)) {
+                why = "peer offset out of range";
+                return false;
+            }
+            any_fine = true;
+            S.push_back(send_side(x.kind) ? x.peer : -x.peer);
+        }
+    }
+    if (any_fine && any_coarse) {
+        why = "mixed coarse and per-destination exchange vertices";
+        return false;
+    }
+    g.fine = any_fine;
+    if (!g.fine) S = {0};
+    std::sort(S.begin(), S.end());
+    S.erase(std::unique(S.begin(), S.end()), S.end());
+    g.offsets = S;
+    std::vector<int> R;
+    for (int d : S) R.push_back(-d);
+    std::sort(R.begin(), R.end());
+    auto add = [&](int k, int d) {
+        g.v.push_back({k, d});
+        return int(g.v.size()) - 1;
+    };
+    const int vs = add(DSPMV_OP_START, 0);
+    for (int d : S)
+        for (int k : {DSPMV_OP_PACK, DSPMV_OP_POST_SEND, DSPMV_OP_WAIT_SEND}) add(k, d);
+    const int vl = add(DSPMV_OP_SPMV_LOCAL, 0);
+    for (int e : R)
+        for (int k : {DSPMV_OP_POST_RECV, DSPMV_OP_WAIT_RECV, DSPMV_OP_UNPACK}) add(k, e);
+    const int vr = add(DSPMV_OP_SPMV_REMOTE, 0), ve = add(DSPMV_OP_END, 0);
+    auto E = [&](int u, int v, bool dead = false) { g.edges.push_back({u, v, dead ? 1 : 0}); };
+    auto I = [&](int k, int d) { return g.find(k, d); };
+    if (!g.fine) {
+        // SPEC S:125 order (kept for the derived-sync order of the coarse space)
+        E(vs, I(DSPMV_OP_PACK, 0));
+        E(vs, vl);
+        E(vs, I(DSPMV_OP_POST_RECV, 0));
+        E(I(DSPMV_OP_PACK, 0), I(DSPMV_OP_POST_SEND, 0));
+        E(I(DSPMV_OP_POST_SEND, 0), I(DSPMV_OP_WAIT_SEND, 0));
+        E(I(DSPMV_OP_POST_RECV, 0), I(DSPMV_OP_WAIT_RECV, 0));
+        E(I(DSPMV_OP_WAIT_RECV, 0), I(DSPMV_OP_UNPACK, 0));
+        E(I(DSPMV_OP_UNPACK, 0), vr);
+        E(vl, ve);
+        E(vr, ve);
+        E(I(DSPMV_OP_WAIT_SEND, 0), ve);
+    } else {
+        E(vs, vl);
+        E(vl, ve);
+        E(vr, ve);
+        for (int d : S) {
+            E(vs, I(DSPMV_OP_PACK, d));
+            E(I(DSPMV_OP_PACK, d), I(DSPMV_OP_POST_SEND, d));
+            E(I(DSPMV_OP_POST_SEND, d), I(DSPMV_OP_WAIT_SEND, d));
+            E(I(DSPMV_OP_WAIT_SEND, d), ve);
+        }
+        for (int e : R) {
+            E(vs, I(DSPMV_OP_POST_RECV, e));
+            E(I(DSPMV_OP_POST_RECV, e), I(DSPMV_OP_WAIT_RECV, e));
+            E(I(DSPMV_OP_WAIT_RECV, e), I(DSPMV_OP_UNPACK, e));
+            E(I(DSPMV_OP_UNPACK, e), vr);
+        }
+    }
+    // R-Q13 / R-N4: a Wait needs the peer's matching Post (SPMD)
+    for (int e : R) E(I(DSPMV_OP_POST_SEND, -e), I(DSPMV_OP_WAIT_RECV, e), true);
+    for (int d : S) E(I(DSPMV_OP_POST_RECV, -d), I(DSPMV_OP_WAIT_SEND, d), true);
+    return true;
+}
 
 SchedCheck validate_schedule(const dspmv_op* ops, int n_ops, int n_streams) {
     SchedCheck r;
@@ -110,17 +215,18 @@ SchedCheck validate_schedule(const dspmv_op* ops, int n_ops, int n_streams) {
     if (!ops || n_ops <= 0) return bad(DSPMV_ERR_ARG, "empty schedule");
     if (n_ops > DSPMV_MAX_OPS) return bad(DSPMV_ERR_SCHEDULE, "too many ops");
     if (n_streams < 1 || n_streams > DSPMV_MAX_STREAMS) return bad(DSPMV_ERR_ARG, "n_streams out of range");
-    std::array<int, NV> where;
-    where.fill(-1);
     std::array<bool, DSPMV_MAX_EVENTS> rec{};
+    std::vector<DagVertex> present;
     for (int t = 0; t < n_ops; ++t) {
         const dspmv_op& o = ops[t];
         const std::string at = "op " + std::to_string(t) + ": ";
         if (is_dag_vertex(o.kind)) {
-            if (where[o.kind] >= 0) return bad(DSPMV_ERR_SCHEDULE, at + "duplicate " + kNames[o.kind]);
-            where[o.kind] = t;
             if (is_gpu_vertex(o.kind) && (o.stream < 0 || o.stream >= n_streams))
                 return bad(DSPMV_ERR_SCHEDULE, at + "stream out of range");
+            for (const DagVertex& x : present)
+                if (x.kind == o.kind && x.peer == o.peer)
+                    return bad(DSPMV_ERR_SCHEDULE, at + "duplicate " + vertex_label(o.kind, o.peer));
+            present.push_back({o.kind, o.peer});
         } else if (o.kind == DSPMV_OP_EVENT_RECORD || o.kind == DSPMV_OP_EVENT_SYNC ||
                    o.kind == DSPMV_OP_STREAM_WAIT_EVENT) {
             if (o.event < 0 || o.event >= DSPMV_MAX_EVENTS) return bad(DSPMV_ERR_SCHEDULE, at + "event id out of range");
@@ -136,29 +242,43 @@ SchedCheck validate_schedule(const dspmv_op* ops, int n_ops, int n_streams) {
             return bad(DSPMV_ERR_SCHEDULE, at + "unknown op kind " + std::to_string(o.kind));
         }
     }
-    for (int v = 0; v < NV; ++v)
-        if (where[v] < 0) return bad(DSPMV_ERR_SCHEDULE, std::string("missing vertex ") + kNames[v]);
-    if (where[DSPMV_OP_START] != 0) return bad(DSPMV_ERR_SCHEDULE, "start is not the first op");
-    if (where[DSPMV_OP_END] != n_ops - 1) return bad(DSPMV_ERR_SCHEDULE, "end is not the last op");
-    for (int e = 0; e < kNumEdges; ++e) {
-        const int u = kEdges[e][0], v = kEdges[e][1];
-        if (where[u] > where[v])
-            return bad(e >= kFirstDeadlockEdge ? DSPMV_ERR_DEADLOCK : DSPMV_ERR_SCHEDULE,
-                       std::string(kNames[v]) + " before " + kNames[u]);
+    std::string why;
+    if (!build_dag(present, r.dag, why)) return bad(DSPMV_ERR_SCHEDULE, why);
+    const Dag& g = r.dag;
+    std::vector<int> where(g.v.size(), -1);
+    r.inst.assign(n_ops, -1);
+    for (int t = 0; t < n_ops; ++t) {
+        if (!is_dag_vertex(ops[t].kind)) continue;
+        const int id = g.find(ops[t].kind, ops[t].peer);
+        where[id] = t;
+        r.inst[t] = id;
     }
-    HB hb;
+    for (size_t i = 0; i < g.v.size(); ++i)
+        if (where[i] < 0) return bad(DSPMV_ERR_SCHEDULE, "missing vertex " + vertex_label(g.v[i].kind, g.v[i].peer));
+    if (where[g.find(DSPMV_OP_START, 0)] != 0) return bad(DSPMV_ERR_SCHEDULE, "start is not the first op");
+    if (where[g.find(DSPMV_OP_END, 0)] != n_ops - 1) return bad(DSPMV_ERR_SCHEDULE, "end is not the last op");
+    for (const auto& e : g.edges) {
+        if (where[e[0]] > where[e[1]])
+            return bad(e[2] ? DSPMV_ERR_DEADLOCK : DSPMV_ERR_SCHEDULE,
+                       vertex_label(g.v[e[1]].kind, g.v[e[1]].peer) + " before " +
+                           vertex_label(g.v[e[0]].kind, g.v[e[0]].peer));
+    }
+    HB hb(g);
     for (int t = 0; t < n_ops; ++t) {
         const dspmv_op& o = ops[t];
         if (is_dag_vertex(o.kind)) {
+            const int id = r.inst[t];
             const int sv = is_gpu_vertex(o.kind) ? o.stream : -1;
-            for (int e = 0; e < kNumEdges; ++e) {
-                if (kEdges[e][1] != o.kind) continue;
-                if (!hb.enforced(kEdges[e][0], sv))
-                    return bad(DSPMV_ERR_SCHEDULE, std::string("edge ") + kNames[kEdges[e][0]] + "->" +
-                                                       kNames[o.kind] + " not synchronised (tab:sync)");
+            for (const auto& e : g.edges) {
+                if (e[1] != id) continue;
+                if (!hb.enforced(e[0], sv))
+                    return bad(DSPMV_ERR_SCHEDULE, "edge " + vertex_label(g.v[e[0]].kind, g.v[e[0]].peer) + "->" +
+                                                       vertex_label(o.kind, o.peer) + " not synchronised (tab:sync)");
             }
+            hb.vertex(id, o.stream);
+        } else {
+            hb.sync(o);
         }
-        hb.apply(o);
     }
     return r;
 }
@@ -173,43 +293,63 @@ extern "C" dspmv_status dspmv_schedule_validate(const dspmv_op* ops, int n_ops, 
     return DSPMV_OK;
 }
 
-extern "C" dspmv_status dspmv_schedule_derive(const int32_t* order, const int32_t* streams,
-                                              int n_streams, dspmv_op* out, int cap, int* n_out) {
+extern "C" dspmv_status dspmv_schedule_derive_peers(const int32_t* order, const int32_t* streams,
+                                                    const int32_t* peers, int n_vertices, int n_streams,
+                                                    dspmv_op* out, int cap, int* n_out) {
     if (!order || !out || !n_out) return fail(DSPMV_ERR_ARG, "null argument");
     if (n_streams < 1 || n_streams > DSPMV_MAX_STREAMS) return fail(DSPMV_ERR_ARG, "n_streams out of range");
+    if (n_vertices < NV || n_vertices > DSPMV_MAX_OPS) return fail(DSPMV_ERR_ARG, "n_vertices out of range");
+    std::vector<DagVertex> present(n_vertices);
+    for (int i = 0; i < n_vertices; ++i) {
+        present[i] = {order[i], peers ? peers[i] : 0};
+        if (!is_dag_vertex(order[i])) return fail(DSPMV_ERR_ARG, "order holds a non-vertex kind");
+    }
+    Dag g;
+    std::string why;
+    if (!build_dag(present, g, why)) return fail(DSPMV_ERR_ARG, why);
+    if (int(g.v.size()) != n_vertices) return fail(DSPMV_ERR_ARG, "order is not a permutation of the DAG vertices");
+    std::vector<bool> seen(g.v.size(), false);
     std::vector<dspmv_op> ops;
-    HB hb;
+    HB hb(g);
     int ev = 0;
-    bool seen[NV] = {};
-    for (int i = 0; i < NV; ++i) {
-        const int v = order[i];
-        if (!is_dag_vertex(v) || seen[v]) return fail(DSPMV_ERR_ARG, "order is not a permutation of the 10 vertices");
-        seen[v] = true;
+    for (int i = 0; i < n_vertices; ++i) {
+        const int id = g.find(present[i].kind, present[i].peer);
+        if (id < 0 || seen[id]) return fail(DSPMV_ERR_ARG, "order is not a permutation of the DAG vertices");
+        seen[id] = true;
+        const int v = present[i].kind;
         const int sv = is_gpu_vertex(v) ? (streams ? streams[i] : 0) : -1;
         if (is_gpu_vertex(v) && (sv < 0 || sv >= n_streams)) return fail(DSPMV_ERR_ARG, "stream out of range");
-        for (int e = 0; e < kNumEdges; ++e) {
-            if (kEdges[e][1] != v) continue;
-            const int u = kEdges[e][0];
-            if (!hb.done[u]) return fail(DSPMV_ERR_ARG, std::string("order not topological at ") + kNames[v]);
+        for (const auto& e : g.edges) {
+            if (e[1] != id) continue;
+            const int u = e[0];
+            if (!hb.done[u])
+                return fail(DSPMV_ERR_ARG, "order not topological at " + vertex_label(v, present[i].peer));
             if (hb.enforced(u, sv)) continue;
             if (ev >= DSPMV_MAX_EVENTS) return fail(DSPMV_ERR_SCHEDULE, "too many events");
             dspmv_op rec{DSPMV_OP_EVENT_RECORD, hb.stream_of[u], ev, 0};
             dspmv_op wait = sv < 0 ? dspmv_op{DSPMV_OP_EVENT_SYNC, 0, ev, 0}
                                    : dspmv_op{DSPMV_OP_STREAM_WAIT_EVENT, sv, ev, 0};
             ops.push_back(rec);
-            hb.apply(rec);
+            hb.sync(rec);
             ops.push_back(wait);
-            hb.apply(wait);
+            hb.sync(wait);
             ++ev;
         }
-        dspmv_op vop{v, sv < 0 ? 0 : sv, 0, 0};
-        ops.push_back(vop);
-        hb.apply(vop);
+        ops.push_back(dspmv_op{v, sv < 0 ? 0 : sv, 0, present[i].peer});
+        hb.vertex(id, sv < 0 ? 0 : sv);
     }
     *n_out = int(ops.size());
     if (int(ops.size()) > cap) return fail(DSPMV_ERR_ARG, "output capacity too small");
     std::copy(ops.begin(), ops.end(), out);
     return DSPMV_OK;
+}
+
+extern "C" dspmv_status dspmv_schedule_derive(const int32_t* order, const int32_t* streams,
+                                              int n_streams, dspmv_op* out, int cap, int* n_out) {
+    if (order)
+        for (int i = 0; i < NV; ++i)
+            if (!is_dag_vertex(order[i])) return fail(DSPMV_ERR_ARG, "order is not a permutation of the 10 vertices");
+    return dspmv_schedule_derive_peers(order, streams, nullptr, NV, n_streams, out, cap, n_out);
 }
 
 extern "C" dspmv_status dspmv_schedule_parse(const char* text, dspmv_op* out, int cap, int* n_out,
@@ -226,10 +366,11 @@ extern "C" dspmv_status dspmv_schedule_parse(const char* text, dspmv_op* out, in
         std::string name, kind, tok;
         if (!(ls >> name)) continue;
         if (!(ls >> kind)) return fail(DSPMV_ERR_ARG, "line " + std::to_string(lineno) + ": missing kind");
-        int stream = -1, event = -1;
+        int stream = -1, event = -1, peer = 0;
         while (ls >> tok) {
             if (tok.rfind("stream=", 0) == 0) stream = std::atoi(tok.c_str() + 7);
             else if (tok.rfind("event=", 0) == 0) event = std::atoi(tok.c_str() + 6);
+            else if (tok.rfind("peer=", 0) == 0) peer = std::atoi(tok.c_str() + 5);
             else return fail(DSPMV_ERR_ARG, "line " + std::to_string(lineno) + ": bad token " + tok);
         }
         dspmv_op op{-1, 0, 0, 0};
@@ -238,9 +379,16 @@ extern "C" dspmv_status dspmv_schedule_parse(const char* text, dspmv_op* out, in
         else if (kind == "StreamWaitEvent") op = {DSPMV_OP_STREAM_WAIT_EVENT, stream, event, 0};
         else if (kind == "Cpu" || kind == "BoundGpu" || kind == "PostSend" || kind == "PostRecv" ||
                  kind == "WaitSend" || kind == "WaitRecv") {
+            std::string vname = name;
+            const size_t br = vname.find('[');  // "Pack[+1]" = Pack with peer=+1
+            if (br != std::string::npos && vname.back() == ']') {
+                peer = std::atoi(vname.substr(br + 1, vname.size() - br - 2).c_str());
+                vname = vname.substr(0, br);
+            }
             for (int v = 0; v < NV; ++v)
-                if (name == kNames[v]) op.kind = v;
+                if (vname == kNames[v]) op.kind = v;
             if (op.kind < 0) return fail(DSPMV_ERR_ARG, "line " + std::to_string(lineno) + ": unknown vertex " + name);
+            op.peer = peer;
             if ((kind == "BoundGpu") != is_gpu_vertex(op.kind))
                 return fail(DSPMV_ERR_ARG, "line " + std::to_string(lineno) + ": kind does not match vertex");
             op.stream = is_gpu_vertex(op.kind) ? stream : 0;
@@ -269,19 +417,22 @@ extern "C" dspmv_status dspmv_schedule_format(const dspmv_op* ops, int n_ops, ch
     for (int t = 0; t < n_ops; ++t) {
         const dspmv_op& o = ops[t];
         if (is_dag_vertex(o.kind)) {
-            if (is_gpu_vertex(o.kind)) os << kNames[o.kind] << " BoundGpu stream=" << o.stream << "\n";
-            else os << kNames[o.kind] << " Cpu\n";
+            const std::string nm = vertex_label(o.kind, o.peer);
+            if (is_gpu_vertex(o.kind)) os << nm << " BoundGpu stream=" << o.stream << "\n";
+            else os << nm << " Cpu\n";
         } else if (o.kind == DSPMV_OP_EVENT_RECORD) {
             const char* prev = "start";
+            std::string prev_l = prev;
             for (int q = t - 1; q >= 0; --q)
-                if (is_dag_vertex(ops[q].kind)) { prev = kNames[ops[q].kind]; break; }
-            os << "CER-after-" << prev << " EventRecord stream=" << o.stream << " event=" << o.event << "\n";
+                if (is_dag_vertex(ops[q].kind)) { prev_l = vertex_label(ops[q].kind, ops[q].peer); break; }
+            os << "CER-after-" << prev_l << " EventRecord stream=" << o.stream << " event=" << o.event << "\n";
         } else {
             const char* next = "end";
+            std::string next_l = next;
             for (int q = t + 1; q < n_ops; ++q)
-                if (is_dag_vertex(ops[q].kind)) { next = kNames[ops[q].kind]; break; }
-            if (o.kind == DSPMV_OP_EVENT_SYNC) os << "CES-b4-" << next << " EventSync event=" << o.event << "\n";
-            else os << "CSWE-b4-" << next << " StreamWaitEvent stream=" << o.stream << " event=" << o.event << "\n";
+                if (is_dag_vertex(ops[q].kind)) { next_l = vertex_label(ops[q].kind, ops[q].peer); break; }
+            if (o.kind == DSPMV_OP_EVENT_SYNC) os << "CES-b4-" << next_l << " EventSync event=" << o.event << "\n";
+            else os << "CSWE-b4-" << next_l << " StreamWaitEvent stream=" << o.stream << " event=" << o.event << "\n";
         }
     }
     const std::string s = os.str();

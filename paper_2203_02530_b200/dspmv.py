@@ -73,7 +73,7 @@ class dspmv_plan_info(ctypes.Structure):
 
 class dspmv_op(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("stream", ctypes.c_int32),
-                ("event", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("event", ctypes.c_int32), ("peer", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p
@@ -114,6 +114,7 @@ _sig("dspmv_host_plan_set_requests", [_P, _P, _P])
 _sig("dspmv_layout_host", [_P, ctypes.c_int32, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P])
 _sig("dspmv_schedule_validate", [_P, _I, _I])
 _sig("dspmv_schedule_derive", [_P, _P, _I, _P, _I, _P])
+_sig("dspmv_schedule_derive_peers", [_P, _P, _P, _I, _I, _P, _I, _P])
 _sig("dspmv_schedule_parse", [ctypes.c_char_p, _P, _I, _P, _P])
 _sig("dspmv_schedule_format", [_P, _I, _P, ctypes.c_size_t])
 _sig("dspmv_schedule_create", [_P, _P, _I, _I, _P])
@@ -370,6 +371,19 @@ def dspmv_schedule_derive(order, streams, n_streams: int) -> np.ndarray:
     n = _I()
     _check(lib.dspmv_schedule_derive(order.ctypes.data, streams.ctypes.data, n_streams,
                                      out.ctypes.data, DSPMV_MAX_OPS, ctypes.byref(n)))
+    return out[:n.value].copy()
+
+
+def dspmv_schedule_derive_peers(order, streams, peers, n_streams: int) -> np.ndarray:
+    """Any granularity: order / streams / peers name the DAG vertices (kinds,
+    streams of GPU vertices, peer offsets; per destination P:281-284)."""
+    order = np.ascontiguousarray(order, np.int32)
+    streams = np.ascontiguousarray(streams, np.int32)
+    peers = np.ascontiguousarray(peers, np.int32)
+    out = np.zeros((DSPMV_MAX_OPS, 4), np.int32)
+    n = _I()
+    _check(lib.dspmv_schedule_derive_peers(order.ctypes.data, streams.ctypes.data, peers.ctypes.data, len(order),
+                                           n_streams, out.ctypes.data, DSPMV_MAX_OPS, ctypes.byref(n)))
     return out[:n.value].copy()
 
 

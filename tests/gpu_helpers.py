@@ -27,8 +27,9 @@ def oracle_ops_to_lib(ops):
     out = []
     for op in ops:
         n = op[0]
-        if n in KIND:
-            out.append((KIND[n], op[1] if n in S.GPU_VERTICES else 0, 0, 0))
+        b, d = S.split_name(n)
+        if b in KIND:
+            out.append((KIND[b], op[1] if b in S.GPU_VERTICES else 0, 0, d))
         elif n == "CER":
             out.append((D.DSPMV_OP_EVENT_RECORD, op[1], op[2], 0))
         elif n == "CES":

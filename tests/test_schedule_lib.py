@@ -18,8 +18,9 @@ def to_lib(ops):
     out = []
     for op in ops:
         n = op[0]
-        if n in KIND:
-            out.append((KIND[n], op[1] if n in S.GPU_VERTICES else 0, 0, 0))
+        b, d = S.split_name(n)
+        if b in KIND:
+            out.append((KIND[b], op[1] if b in S.GPU_VERTICES else 0, 0, d))
         elif n == "CER":
             out.append((D.DSPMV_OP_EVENT_RECORD, op[1], op[2], 0))
         elif n == "CES":
@@ -250,3 +251,94 @@ def test_parse_rejects_garbage_without_crashing():
                 pass
         except D.DspmvError:
             pass
+
+
+# ------------------------------------------------ per-destination schedules
+def _rand_topo(V, E, rng):
+    pred = {v: {u for u, w in E if w == v} for v in V}
+    done, out = set(), []
+    while len(out) < len(V):
+        v = rng.choice([v for v in V if v not in done and pred[v] <= done])
+        out.append(v)
+        done.add(v)
+    return out
+
+
+@pytest.mark.parametrize("offsets", [[1], [-1, 1], [-2, -1, 1, 2], [-3, 1]])
+def test_fine_derive_matches_oracle(offsets):
+    """dspmv_schedule_derive_peers == oracle derive on random traversals of the
+    per-destination DAG (R-N4), every stream assignment sampled."""
+    V, E, _ = S.fine_dag(offsets)
+    rng = random.Random(len(offsets))
+    for _ in range(300):
+        order = _rand_topo(V, E, rng)
+        streams = {v: rng.randrange(2) for v in order if S.base(v) in S.GPU_VERTICES}
+        want = to_lib(S.derive(order, streams))
+        kinds = [KIND[S.base(v)] for v in order]
+        peers = [S.split_name(v)[1] for v in order]
+        got = D.dspmv_schedule_derive_peers(kinds, [streams.get(v, 0) for v in order], peers, 2)
+        assert [tuple(r) for r in got] == want, order
+        assert lib_status(S.derive(order, streams)) == "ok"
+
+
+def test_fine_validator_fuzz_vs_oracle():
+    """Vector-clock validator == happens-before oracle on per-destination
+    schedules: derived ones, derived with a sync dropped / a vertex moved /
+    a vertex restreamed, and traversals that ignore the deadlock edges."""
+    rng = random.Random(99)
+    n_ok = n_dead = 0
+    for i in range(3000):
+        offsets = rng.choice([[-1, 1], [-2, -1, 1, 2], [2], [-3, 1]])
+        V, E, Dl = S.fine_dag(offsets)
+        edges = E if i % 3 else [e for e in E if e not in Dl]
+        order = _rand_topo(V, edges, rng)
+        streams = {v: rng.randrange(2) for v in order if S.base(v) in S.GPU_VERTICES}
+        ops = S.derive(order, streams, edges)
+        r = rng.random()
+        if r < 0.25:
+            syncs = [t for t, o in enumerate(ops) if o[0] in ("CER", "CES", "CSWE")]
+            if syncs:
+                del ops[rng.choice(syncs)]
+        elif r < 0.5:
+            t = rng.randrange(1, len(ops) - 1)
+            op = ops.pop(t)
+            ops.insert(rng.randrange(1, len(ops)), op)
+        elif r < 0.6:
+            t = rng.randrange(len(ops))
+            if S.base(ops[t][0]) in S.GPU_VERTICES:
+                ops[t] = (ops[t][0], 1 - ops[t][1])
+        a, b = lib_status(ops), oracle_status(ops)
+        assert a == b, ops
+        n_ok += a == "ok"
+        n_dead += a == "deadlock"
+    assert n_ok > 500 and n_dead > 100
+
+
+def test_fine_schedule_errors():
+    V, E, _ = S.fine_dag([-1, 1])
+    ops = S.derive(S.topological_orders(E, V)[0], {v: 0 for v in V})
+    lib = to_lib(ops)
+    D.dspmv_schedule_validate(lib, 1)
+    mixed = [(k, s_, e, 0) if k == D.DSPMV_OP_PACK and p == 1 else (k, s_, e, p) for k, s_, e, p in lib]
+    with pytest.raises(D.DspmvError, match="mixed"):
+        D.dspmv_schedule_validate(mixed, 1)
+    bad_peer = [(k, s_, e, 3) if k == D.DSPMV_OP_SPMV_LOCAL else (k, s_, e, p) for k, s_, e, p in lib]
+    with pytest.raises(D.DspmvError, match="no peer offset"):
+        D.dspmv_schedule_validate(bad_peer, 1)
+    dup = lib[:2] + [lib[1]] + lib[2:]
+    with pytest.raises(D.DspmvError):
+        D.dspmv_schedule_validate(dup, 1)
+
+
+def test_fine_parse_format_roundtrip():
+    V, E, _ = S.fine_dag([-2, 1])
+    rng = random.Random(3)
+    for _ in range(50):
+        order = _rand_topo(V, E, rng)
+        ops = np.array(to_lib(S.derive(order, {v: rng.randrange(2) for v in V})), np.int32)
+        text = D.dspmv_schedule_format(ops)
+        assert "Pack[+1]" in text and "Unpack[+2]" in text
+        back, ns = D.dspmv_schedule_parse(text)
+        assert np.array_equal(back, ops)
+    back, _ = D.dspmv_schedule_parse("start Cpu\nPack BoundGpu stream=0 peer=-1\n")
+    assert back[1].tolist() == [D.DSPMV_OP_PACK, 0, 0, -1]
