@@ -301,6 +301,15 @@ dspmv_status dspmv_schedule_derive(const int32_t* order, const int32_t* streams,
 dspmv_status dspmv_schedule_derive_peers(const int32_t* order, const int32_t* streams, const int32_t* peers,
                                          int n_vertices, int n_streams, dspmv_op* out, int cap, int* n_out);
 
+/* Host-only.  The program DAG of a granularity: n_offsets = 0 -> coarse,
+ * else the per-destination DAG of the send-offset set `offsets`.  Writes
+ * the vertices (kinds[i], peers[i], i < *n_v; in the order start, send side
+ * per offset, y_L, receive side per offset, y_R, end) and the edges
+ * (edges[3*j..3*j+2] = u, v, 1 if a deadlock edge (R-Q13 / R-N4), j < *n_e).
+ * Pass NULL arrays to get the counts. */
+dspmv_status dspmv_schedule_dag(const int32_t* offsets, int n_offsets, int32_t* kinds, int32_t* peers, int cap_v,
+                                int* n_v, int32_t* edges, int cap_e, int* n_e);
+
 /* Host-only.  External schedule text format: one op per line
  * "<name> <kind> [stream=<i>] [event=<id>] [peer=<d>]", kind in {Cpu, BoundGpu,
  * EventRecord, EventSync, StreamWaitEvent}; names start, Pack, y_L,

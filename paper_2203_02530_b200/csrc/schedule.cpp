@@ -293,6 +293,31 @@ extern "C" dspmv_status dspmv_schedule_validate(const dspmv_op* ops, int n_ops, 
     return DSPMV_OK;
 }
 
+extern "C" dspmv_status dspmv_schedule_dag(const int32_t* offsets, int n_offsets, int32_t* kinds, int32_t* peers,
+                                          int cap_v, int* n_v, int32_t* edges, int cap_e, int* n_e) {
+    if (!n_v || !n_e || n_offsets < 0 || (n_offsets > 0 && !offsets)) return fail(DSPMV_ERR_ARG, "bad argument");
+    std::vector<DagVertex> present;
+    for (int i = 0; i < n_offsets; ++i) {
+        if (offsets[i] == 0) return fail(DSPMV_ERR_ARG, "offsets must be non-zero");
+        present.push_back({DSPMV_OP_PACK, offsets[i]});
+    }
+    Dag g;
+    std::string why;
+    if (!build_dag(present, g, why)) return fail(DSPMV_ERR_ARG, why);
+    *n_v = int(g.v.size());
+    *n_e = int(g.edges.size());
+    if ((kinds || peers) && cap_v < *n_v) return fail(DSPMV_ERR_ARG, "vertex capacity too small");
+    if (edges && cap_e < *n_e) return fail(DSPMV_ERR_ARG, "edge capacity too small");
+    for (int i = 0; i < *n_v; ++i) {
+        if (kinds) kinds[i] = g.v[i].kind;
+        if (peers) peers[i] = g.v[i].peer;
+    }
+    if (edges)
+        for (int i = 0; i < *n_e; ++i)
+            for (int j = 0; j < 3; ++j) edges[3 * i + j] = g.edges[i][j];
+    return DSPMV_OK;
+}
+
 extern "C" dspmv_status dspmv_schedule_derive_peers(const int32_t* order, const int32_t* streams,
                                                     const int32_t* peers, int n_vertices, int n_streams,
                                                     dspmv_op* out, int cap, int* n_out) {

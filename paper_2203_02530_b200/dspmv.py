@@ -115,6 +115,7 @@ _sig("dspmv_layout_host", [_P, ctypes.c_int32, _I, _I, _I, _P, _P, _P, _P, _P, _
 _sig("dspmv_schedule_validate", [_P, _I, _I])
 _sig("dspmv_schedule_derive", [_P, _P, _I, _P, _I, _P])
 _sig("dspmv_schedule_derive_peers", [_P, _P, _P, _I, _I, _P, _I, _P])
+_sig("dspmv_schedule_dag", [_P, _I, _P, _P, _I, _P, _P, _I, _P])
 _sig("dspmv_schedule_parse", [ctypes.c_char_p, _P, _I, _P, _P])
 _sig("dspmv_schedule_format", [_P, _I, _P, ctypes.c_size_t])
 _sig("dspmv_schedule_create", [_P, _P, _I, _I, _P])
@@ -385,6 +386,27 @@ def dspmv_schedule_derive_peers(order, streams, peers, n_streams: int) -> np.nda
     _check(lib.dspmv_schedule_derive_peers(order.ctypes.data, streams.ctypes.data, peers.ctypes.data, len(order),
                                            n_streams, out.ctypes.data, DSPMV_MAX_OPS, ctypes.byref(n)))
     return out[:n.value].copy()
+
+
+def dspmv_schedule_dag(offsets=()):
+    """(vertices [(kind, peer)], edges [(u, v, is_deadlock_edge)]) of the coarse
+    DAG (no offsets) or the per-destination DAG of send offsets `offsets`."""
+    offs = np.ascontiguousarray(list(offsets), np.int32)
+    nv, ne = _I(), _I()
+    _check(lib.dspmv_schedule_dag(offs.ctypes.data if len(offs) else None, len(offs), None, None, 0,
+                                  ctypes.byref(nv), None, 0, ctypes.byref(ne)))
+    kinds = np.zeros(nv.value, np.int32)
+    peers = np.zeros(nv.value, np.int32)
+    edges = np.zeros((ne.value, 3), np.int32)
+    _check(lib.dspmv_schedule_dag(offs.ctypes.data if len(offs) else None, len(offs), kinds.ctypes.data,
+                                  peers.ctypes.data, nv.value, ctypes.byref(nv), edges.ctypes.data, ne.value,
+                                  ctypes.byref(ne)))
+    return list(zip(kinds.tolist(), peers.tolist())), [tuple(e) for e in edges.tolist()]
+
+
+def vertex_label(kind: int, peer: int = 0) -> str:
+    """"Pack", "Pack[+1]" (per destination)."""
+    return VERTEX_NAMES[kind] + (f"[{peer:+d}]" if peer else "")
 
 
 def dspmv_schedule_parse(text: str):

@@ -24,6 +24,10 @@ Phases (SPEC.md S:204-304 semantics):
   backprop    t_min <- min(t, t_min), t_max <- max(t, t_max) on the path
               (P:469-472); a node is fully explored when its terminal is
               benchmarked / all its children are fully explored.
+
+The tree walks any ``schedules.Space``: the coarse DAG (default) or the
+per-destination DAG of a set of peer offsets, whose traversal
+space is too large to enumerate.
 """
 from __future__ import annotations
 
@@ -33,10 +37,9 @@ import random
 import numpy as np
 
 from . import dspmv as D
-from .schedules import EDGES, GPU, canonical_key
+from .schedules import COARSE, Space, canonical_key
 
 C_EXPLORE = math.sqrt(2.0)
-_PRED = {v: {u for (u, w) in EDGES if w == v} for v in range(10)}
 
 
 def explore_value(parent_n: int, child_n: int, child_fully_explored: bool) -> float:
@@ -79,15 +82,16 @@ class Node:
         return out[::-1]
 
 
-def legal_moves(prefix, n_streams: int):
-    """Frontier vertices x stream choices under bijection pruning."""
+def legal_moves(prefix, n_streams: int, space: Space = COARSE):
+    """Frontier vertices x stream choices under bijection pruning (vertices
+    are indices into ``space.vertices``)."""
     done = {v for v, _ in prefix}
-    used = len({s for v, s in prefix if v in GPU})
+    used = len({s for v, s in prefix if v in space.gpu})
     moves = []
-    for v in range(10):
-        if v in done or not _PRED[v] <= done:
+    for v in range(len(space.vertices)):
+        if v in done or not space.pred[v] <= done:
             continue
-        if v in GPU:
+        if v in space.gpu:
             for s in range(min(used + 1, n_streams)):
                 moves.append((v, s))
         else:
@@ -95,18 +99,19 @@ def legal_moves(prefix, n_streams: int):
     return moves
 
 
-def ops_of(prefix, n_streams: int) -> np.ndarray:
+def ops_of(prefix, n_streams: int, space: Space = COARSE) -> np.ndarray:
     order = [v for v, _ in prefix]
     streams = [s if s is not None else 0 for _, s in prefix]
-    return D.dspmv_schedule_derive(order, streams, n_streams)
+    return space.derive(order, streams, n_streams)
 
 
 class MCTS:
     """measure(ops) -> seconds benchmarks one complete schedule."""
 
-    def __init__(self, measure, n_streams: int = 2, seed: int = 2203):
+    def __init__(self, measure, n_streams: int = 2, seed: int = 2203, space: Space = COARSE):
         self.measure = measure
         self.n_streams = n_streams
+        self.space = space
         self.rng = random.Random(seed)
         self.root = Node(None, None, None)
         self.dataset = {}               # canonical key -> {"ops", "times"}
@@ -115,7 +120,7 @@ class MCTS:
     # -- tree helpers
     def _materialise(self, node):
         if node.children is None:
-            node.children = [Node(v, s, node) for v, s in legal_moves(node.prefix(), self.n_streams)]
+            node.children = [Node(v, s, node) for v, s in legal_moves(node.prefix(), self.n_streams, self.space)]
         return node.children
 
     def select(self):
@@ -150,7 +155,7 @@ class MCTS:
                 break
             path_end = self.rng.choice(kids)
         prefix = path_end.prefix()
-        ops = ops_of(prefix, self.n_streams)
+        ops = ops_of(prefix, self.n_streams, self.space)
         t = float(self.measure(ops))
         rec = self.dataset.setdefault(canonical_key(ops), {"ops": ops, "times": []})
         rec["times"].append(t)

@@ -31,7 +31,7 @@ import itertools
 import numpy as np
 
 from . import dspmv as D
-from .schedules import EDGES, GPU
+from .schedules import GPU, Space
 
 NAMES = D.VERTEX_NAMES
 
@@ -88,27 +88,38 @@ def class_labels(times, radius: int | None = None, percentile: float = 98.0):
 
 
 # ---------------------------------------------------------------- features
+_SPACES = {}
+
+
+def _space(ops) -> Space:
+    sp = Space.of_ops(ops)
+    return _SPACES.setdefault(tuple(sp.offsets), sp)
+
+
 def op_names(ops) -> list:
-    """Names of every op: vertices by name, syncs as CER-after-u / CES-b4-v /
-    CSWE-b4-v (u = first DAG predecessor of the consumer v on the recorded
-    stream, edge order; a second wait before the same v gets ':u')."""
+    """Names of every op: vertices by name (per-destination ones as
+    "Pack[+1]"), syncs as CER-after-u / CES-b4-v / CSWE-b4-v (u = first DAG
+    predecessor of the consumer v on the recorded stream, edge order; a second
+    wait before the same v gets ':u')."""
     ops = np.asarray(ops).tolist()
+    sp = _space(ops)
     names = [None] * len(ops)
     where = {}
-    for t, (k, s, e, _) in enumerate(ops):
+    for t, (k, s, e, p) in enumerate(ops):
         if k < 10:
-            names[t] = NAMES[k]
-            where[k] = (t, s)
+            names[t] = sp.names[sp.index[(k, p)]]
+            where[sp.index[(k, p)]] = (t, s)
     for t, (k, s, e, _) in enumerate(ops):
         if k != D.DSPMV_OP_EVENT_RECORD:
             continue
-        v = next(kk for kk, *_ in ops[t + 1:] if kk < 10)
-        u = next((uu for (uu, vv) in EDGES if vv == v and uu in GPU and where[uu][1] == s
+        kv, pv = next((kk, pp) for kk, _, _, pp in ops[t + 1:] if kk < 10)
+        v = sp.index[(kv, pv)]
+        u = next((uu for (uu, vv) in sp.edges if vv == v and uu in sp.gpu and where[uu][1] == s
                   and where[uu][0] < t), None)
-        uname = NAMES[u] if u is not None else "?"
+        uname = sp.names[u] if u is not None else "?"
         names[t] = f"CER-after-{uname}"
         w = next(tt for tt in range(t + 1, len(ops)) if ops[tt][0] in (11, 12) and ops[tt][2] == e)
-        base = ("CES-b4-" if ops[w][0] == D.DSPMV_OP_EVENT_SYNC else "CSWE-b4-") + NAMES[v]
+        base = ("CES-b4-" if ops[w][0] == D.DSPMV_OP_EVENT_SYNC else "CSWE-b4-") + sp.names[v]
         names[w] = base if base not in names else f"{base}:{uname}"
     return names
 
@@ -116,15 +127,16 @@ def op_names(ops) -> list:
 def features(schedules):
     """Binary feature matrix over a list of ops arrays; returns (X, columns)."""
     rows = []
-    vocab = set()
+    vocab, gpu_vocab = set(), set()
     for ops in schedules:
         nm = op_names(ops)
         pos = {n: i for i, n in enumerate(nm)}
-        stream = {NAMES[k]: s for k, s, e, _ in np.asarray(ops).tolist() if k in GPU}
+        stream = {D.vertex_label(k, p): s for k, s, e, p in np.asarray(ops).tolist() if k in GPU}
         rows.append((pos, stream))
         vocab.update(nm)
+        gpu_vocab.update(stream)
     names = sorted(vocab)
-    gpu_names = sorted(NAMES[k] for k in GPU)
+    gpu_names = sorted(gpu_vocab)
     cols = [("before", u, v) for u, v in itertools.combinations(names, 2)]
     cols += [("same", u, v) for u, v in itertools.combinations(gpu_names, 2)]
     X = np.zeros((len(rows), len(cols)), np.int8)
@@ -133,7 +145,7 @@ def features(schedules):
             if kind == "before":
                 X[i, j] = 1 if (u in pos and v in pos and pos[u] < pos[v]) else 0
             else:
-                X[i, j] = 1 if stream[u] == stream[v] else 0
+                X[i, j] = 1 if (u in stream and v in stream and stream[u] == stream[v]) else 0
     keep = [j for j in range(len(cols)) if X[:, j].min() != X[:, j].max()]
     return X[:, keep], [cols[j] for j in keep]
 

@@ -36,11 +36,13 @@ def test_explore_exploit_closed_forms():
 
 
 def test_bijection_pruning_first_gpu_vertex():
-    mv = M.legal_moves([(D.DSPMV_OP_START, None)], 2)
-    gpu = [m for m in mv if m[0] in PS.GPU]
-    assert all(s == 0 for _, s in gpu)
-    mv2 = M.legal_moves([(D.DSPMV_OP_START, None), (D.DSPMV_OP_PACK, 0)], 2)
-    assert sorted(s for v, s in mv2 if v == D.DSPMV_OP_SPMV_LOCAL) == [0, 1]
+    I = PS.COARSE.index
+    start, pack, yl = I[(D.DSPMV_OP_START, 0)], I[(D.DSPMV_OP_PACK, 0)], I[(D.DSPMV_OP_SPMV_LOCAL, 0)]
+    mv = M.legal_moves([(start, None)], 2)
+    gpu = [m for m in mv if m[0] in PS.COARSE.gpu]
+    assert gpu and all(s == 0 for _, s in gpu)
+    mv2 = M.legal_moves([(start, None), (pack, 0)], 2)
+    assert sorted(s for v, s in mv2 if v == yl) == [0, 1]
 
 
 def test_full_search_covers_design_space():
@@ -74,3 +76,24 @@ def test_seed_determinism_and_containment():
 def test_iterations_bound_dataset(iters):
     m = M.MCTS(cost, seed=3).run(iters)
     assert m.iterations == iters and len(m.dataset) <= iters
+
+
+def test_mcts_on_the_per_destination_space():
+    """The same search over the per-destination DAG of offsets {-1, +1}
+    (P:281-284): every benchmarked schedule is valid for that DAG, distinct,
+    and the search is seed-deterministic."""
+    sp = PS.Space([-1, 1])
+    assert len(sp.vertices) == 16
+
+    def cost_f(ops):
+        ops = np.asarray(ops)
+        k = list(ops[:, 0])
+        return 1.0 + 0.01 * k.index(D.DSPMV_OP_SPMV_LOCAL) + 0.001 * len(k)
+
+    a = M.MCTS(cost_f, seed=5, space=sp).run(300)
+    b = M.MCTS(cost_f, seed=5, space=sp).run(300)
+    assert list(a.dataset) == list(b.dataset)
+    assert len(a.dataset) == 300                 # nothing repeats in a space this large
+    for ops, _ in a.records():
+        D.dspmv_schedule_validate(ops, 2)
+        assert PS.Space.of_ops(ops).offsets == [-1, 1]

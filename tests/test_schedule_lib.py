@@ -342,3 +342,22 @@ def test_fine_parse_format_roundtrip():
         assert np.array_equal(back, ops)
     back, _ = D.dspmv_schedule_parse("start Cpu\nPack BoundGpu stream=0 peer=-1\n")
     assert back[1].tolist() == [D.DSPMV_OP_PACK, 0, 0, -1]
+
+
+@pytest.mark.parametrize("offsets", [[], [1], [-1, 1], [-3, -1, 2]])
+def test_library_dag_equals_oracle_dag(offsets):
+    """dspmv_schedule_dag (used by the sweep / MCTS / rules) has exactly the
+    oracle's vertices, edges and deadlock edges, with each vertex's
+    predecessors in the oracle's order (it fixes the derived-sync order)."""
+    verts, edges = D.dspmv_schedule_dag(offsets)
+    names = [D.vertex_label(k, p) for k, p in verts]
+    if offsets:
+        V, E, Dl = S.fine_dag(offsets)
+    else:
+        V, E, Dl = S.VERTICES, S.EDGES, S.DEADLOCK_EDGES
+    assert sorted(names) == sorted(V)
+    got = [(names[u], names[v]) for u, v, _ in edges]
+    assert set(got) == set(E) and len(got) == len(E)
+    assert {(names[u], names[v]) for u, v, dead in edges if dead} == set(Dl)
+    for v in V:
+        assert [a for a, b in got if b == v] == S.preds(v, E)
