@@ -135,6 +135,63 @@ def stencil(kind: str, dims, row_range=None, dtype=np.float64, chunk: int = 1 <<
     return rowptr, col, val
 
 
+def blocked_index(dims, pgrid):
+    """3D domain decomposition numbering (NEXT-4): the grid is cut into
+    px x py x pz equal blocks, rank R = bx + px*(by + py*bz) owns block
+    (bx, by, bz), and its points are numbered contiguously (x fastest) from
+    R * block volume.  Returns new_index(natural linear index array)."""
+    mx, my, mz = dims
+    px, py, pz = pgrid
+    if mx % px or my % py or mz % pz:
+        raise ValueError("grid dims must be divisible by the process grid")
+    bx, by, bz = mx // px, my // py, mz // pz
+    vol = bx * by * bz
+
+    def new_index(nat):
+        nat = np.asarray(nat, np.int64)
+        i, j, k = nat % mx, (nat // mx) % my, nat // (mx * my)
+        R = i // bx + px * (j // by + py * (k // bz))
+        return R * vol + (i % bx) + bx * ((j % by) + by * (k % bz))
+
+    return new_index
+
+
+def stencil_blocked(kind: str, dims, pgrid, row_range=None, dtype=np.float64):
+    """Rows ``row_range`` of the stencil matrix on ``dims`` renumbered by
+    ``blocked_index`` (P A P^T): with the library's even row partition over
+    px*py*pz ranks every rank owns one block, and its peers sit at rank
+    offsets +-1 (x), +-px (y), +-px*py (z) for a 7-pt stencil -- one
+    per-destination exchange vertex set per face of the block ("3D halo
+    exchange ... per dimension").  Columns ascending per row."""
+    mx, my, mz = dims
+    px, py, pz = pgrid
+    n = mx * my * mz
+    bx, by, bz = mx // px, my // py, mz // pz
+    vol = bx * by * bz
+    new_index = blocked_index(dims, pgrid)
+    lo, hi = (0, n) if row_range is None else row_range
+    r = np.arange(lo, hi, dtype=np.int64)                 # new row ids
+    R, loc = r // vol, r % vol
+    i = (R % px) * bx + loc % bx
+    j = ((R // px) % py) * by + (loc // bx) % by
+    k = (R // (px * py)) * bz + loc // (bx * by)
+    offs = stencil_offsets(kind)
+    diag = _STENCIL_DIAG[kind]
+    cols = np.full((len(r), len(offs)), -1, np.int64)
+    vals = np.zeros((len(r), len(offs)), np.float64)
+    for t, (dk, dj, di) in enumerate(offs):
+        ok = ((i + di >= 0) & (i + di < mx) & (j + dj >= 0) & (j + dj < my) & (k + dk >= 0) & (k + dk < mz))
+        nat = (i + di) + mx * ((j + dj) + my * (k + dk))
+        cols[ok, t] = new_index(nat[ok])
+        vals[ok, t] = diag if (dk, dj, di) == (0, 0, 0) else -1.0
+    order = np.argsort(np.where(cols < 0, np.iinfo(np.int64).max, cols), axis=1, kind="stable")
+    cols = np.take_along_axis(cols, order, 1)
+    vals = np.take_along_axis(vals, order, 1)
+    valid = cols >= 0
+    rowptr = np.concatenate([[0], np.cumsum(valid.sum(1))]).astype(np.int64)
+    return rowptr, cols[valid].astype(np.int32), vals[valid].astype(dtype)
+
+
 # ------------------------------------------------------------------ power-law
 POWERLAW_C = 8.25
 POWERLAW_CAP = 4096
@@ -357,6 +414,8 @@ CONFIGS = {
     "c3": dict(kind="27pt", m=256, ranks=8),
     "c4": dict(kind="powerlaw", n=1 << 23, ranks=8),
     "c5": dict(kind="7pt", m=192, ranks=4),
+    # NEXT-4: C5's grid in a 2 x 2 x 1 block decomposition
+    "c5b": dict(kind="7pt", m=192, ranks=4, pgrid=(2, 2, 1)),
 }
 
 
@@ -366,4 +425,6 @@ def config_matrix(name: str, row_range=None, exact: bool = False, dtype=np.float
         return c["n"], powerlaw(c["n"], row_range, exact=exact, dtype=dtype)
     dims = stencil_dims(c["kind"], c["m"], mz)
     n = dims[0] * dims[1] * dims[2]
+    if "pgrid" in c:
+        return n, stencil_blocked(c["kind"], dims, c["pgrid"], row_range, dtype=dtype)
     return n, stencil(c["kind"], dims, row_range, dtype=dtype)

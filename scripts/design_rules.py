@@ -10,6 +10,12 @@ accuracy against the exhaustive space.
 g3 = the paper's banded 150K matrix on `ranks` in-process LOCAL
 ranks of one B200 (only one GPU is reachable this round); c2 = 7-pt 128^3 on
 one rank (NCCL comm of size 1).
+
+--granularity fine: the per-destination DAG (DESIGN.md R-N4) of the
+peer offsets the partition uses.  Its space cannot be enumerated, so MCTS and
+the random-rollout baseline sample it with equal budgets; rules
+are learned from the MCTS samples and checked on the random samples, and the
+best schedules are compared with the coarse sweep's.
 """
 import argparse
 import json
@@ -30,6 +36,24 @@ from paper_2203_02530_b200 import dspmv as D  # noqa: E402
 from paper_2203_02530_b200 import mcts as M  # noqa: E402
 from paper_2203_02530_b200 import rules as R  # noqa: E402
 from paper_2203_02530_b200 import schedules as PS  # noqa: E402
+
+
+def peer_offsets(workload, ranks):
+    """Rank offsets d with some rank r sending to r+d (plus their negatives)."""
+    if workload == "g3":
+        n = 150000
+        rp, col, _ = gen.banded(n)
+    elif workload == "c5":
+        n, (rp, col, _) = gen.config_matrix("c5")
+    else:
+        n, (rp, col, _) = gen.config_matrix("c2")
+    rb = np.asarray(D.dspmv_partition(n, ranks))
+    row_owner = np.repeat(np.arange(ranks), np.diff(rb))
+    nnz_owner = np.repeat(row_owner, np.diff(rp))
+    col_owner = np.searchsorted(rb, col, side="right") - 1
+    d = np.unique(col_owner - nnz_owner)
+    d = set(int(v) for v in d if v != 0)
+    return sorted(d | {-v for v in d})
 
 
 def setup(workload, ranks):
@@ -169,9 +193,13 @@ def main():
     ap.add_argument("--comm", default=None, choices=[None, "nccl", "host"],
                     help="torchrun mode: one process per rank over NCCL (or host + fused put)")
     ap.add_argument("--out", default="gpurun_out/rules.json")
+    ap.add_argument("--granularity", default="coarse", choices=["coarse", "fine"])
+    ap.add_argument("--budget", type=int, default=800, help="fine: MCTS / random-rollout samples")
     a = ap.parse_args()
     if a.comm is not None:
         return main_distributed(a)
+    if a.granularity == "fine":
+        return main_fine(a)
     comms, plans, xs, ys = setup(a.workload, a.ranks)
     measure = make_measure(plans, xs, ys)
     space = PS.enumerate_derived(2)
@@ -210,6 +238,80 @@ def main():
     out["mcts_table_v"] = acc
     json.dump(out, open(a.out, "w"), indent=1)
     print(json.dumps({k: v for k, v in out.items() if k != "sorted_times_us"}, indent=1))
+    for p in plans:
+        D.dspmv_plan_destroy(p)
+    for c in comms:
+        D.dspmv_comm_destroy(c)
+
+
+def main_fine(a):
+    import random
+    offs = peer_offsets(a.workload, a.ranks)
+    sp = PS.Space(offs)
+    comms, plans, xs, ys = setup(a.workload, a.ranks)
+    measure = make_measure(plans, xs, ys)
+    t0 = time.perf_counter()
+    coarse = PS.enumerate_derived(2)
+    ct = np.array([measure(o) for o in coarse])
+    coarse_s = time.perf_counter() - t0
+    # MCTS over the per-destination space
+    t0 = time.perf_counter()
+    m = M.MCTS(measure, n_streams=2, seed=2203, space=sp).run(a.budget)
+    mcts_s = time.perf_counter() - t0
+    recs = m.records()
+    mo = [o for o, _ in recs]
+    mt = np.array([t for _, t in recs])
+    # random-rollout baseline with the same budget
+    rng = random.Random(2530)
+    ro, rt = [], []
+    seen = set()
+    while len(ro) < a.budget:
+        prefix = []
+        while True:
+            mv = M.legal_moves(prefix, 2, sp)
+            if not mv:
+                break
+            prefix.append(rng.choice(mv))
+        ops = M.ops_of(prefix, 2, sp)
+        k = PS.canonical_key(ops)
+        if k in seen:
+            continue
+        seen.add(k)
+        ro.append(ops)
+        rt.append(measure(ops))
+    rt = np.array(rt)
+    labels, ranges, _ = R.class_labels(mt)
+    X, cols = R.features(mo)
+    clf, mln, hist = R.train_tree(X, labels)
+    rs = R.rulesets(clf, cols)
+    out = {
+        "workload": a.workload, "ranks": a.ranks, "granularity": "per-destination (P:281-284)",
+        "offsets": offs, "n_vertices": len(sp.vertices), "budget": a.budget,
+        "coarse": {"n_schedules": len(coarse), "fastest_us": float(ct.min() * 1e6),
+                   "slowest_us": float(ct.max() * 1e6), "fast_slow_ratio": float(ct.max() / ct.min()),
+                   "fastest": PS.describe(coarse[int(ct.argmin())]), "sweep_wall_s": round(coarse_s, 1)},
+        "mcts": {"distinct": len(recs), "fastest_us": float(mt.min() * 1e6), "slowest_us": float(mt.max() * 1e6),
+                 "fast_slow_ratio": float(mt.max() / mt.min()), "median_us": float(np.median(mt) * 1e6),
+                 "fastest": PS.describe(mo[int(mt.argmin())]), "wall_s": round(mcts_s, 1),
+                 "best_after": {str(k): float(min(mt[:k]) * 1e6) for k in (50, 100, 200, 400, a.budget)
+                                if k <= len(mt)}},
+        "random": {"distinct": len(ro), "fastest_us": float(rt.min() * 1e6), "slowest_us": float(rt.max() * 1e6),
+                   "median_us": float(np.median(rt) * 1e6),
+                   "best_after": {str(k): float(min(rt[:k]) * 1e6) for k in (50, 100, 200, 400, a.budget)
+                                  if k <= len(rt)}},
+        "fine_vs_coarse_best": float(ct.min() / mt.min()),
+        "classes": {str(k): {"range_us": [v[0] * 1e6, v[1] * 1e6], "count": int((labels == k).sum())}
+                    for k, v in ranges.items()},
+        "tree": {"max_leaf_nodes": int(mln), "depth": int(clf.get_depth()),
+                 "train_error": float(1 - (clf.predict(X) == labels).mean())},
+        "rulesets": {str(k): [{"samples": n, "rules": r} for n, r in v[:3]] for k, v in rs.items()},
+        # Table V protocol with the random samples standing in for the
+        # (unenumerable) full space
+        "accuracy_on_random_samples": {str(k): R.class_accuracy(mo[:k], mt[:k], ro, rt)
+                                       for k in (100, 200, 400, a.budget) if k <= len(mo)},
+    }
+    json.dump(out, open(a.out, "w"), indent=1)
+    print(json.dumps(out, indent=1))
     for p in plans:
         D.dspmv_plan_destroy(p)
     for c in comms:

@@ -35,21 +35,29 @@ def _offsets(plans):
                   | {r - q for r in range(P) for q in range(P) if plans[r]["send_count"][q] > 0})
 
 
-def _workloads():
-    n1, (rp1, c1, v1) = gen.config_matrix("c1")
-    rp2, c2, v2 = gen.banded(3000, 30000, 750)
-    return [("c1-P3", n1, rp1, c1, v1, 3), ("banded-P6", 3000, rp2, c2, v2, 6)]
+def _build(name, exact):
+    if name == "c1-P3":
+        n, (rp, col, val) = gen.config_matrix("c1", exact=exact)
+        return n, rp, col, val, 3
+    if name == "banded-P6":
+        rp, col, val = gen.banded(3000, 30000, 750, exact=exact)
+        return 3000, rp, col, val, 6
+    # NEXT-4: 7-pt on a 2x2x2 block decomposition, per-dimension vertices
+    rp, col, val = gen.stencil_blocked("7pt", (16, 16, 16), (2, 2, 2))
+    return 16 ** 3, rp, col, val, 8
 
 
 @pytest.mark.parametrize("exchange", [D.DSPMV_EXCHANGE_COPY, D.DSPMV_EXCHANGE_PUT], ids=["copy", "put"])
-@pytest.mark.parametrize("wl", _workloads(), ids=lambda w: w[0])
-def test_fine_schedules_vs_oracle(wl, exchange):
+@pytest.mark.parametrize("name", ["c1-P3", "banded-P6", "blocked3d-P8"])
+def test_fine_schedules_vs_oracle(name, exchange):
     """Random per-destination traversals on 2 streams: y bitwise identical
     across schedules (ticket combine) and equal to the oracle's simulation of
     the same per-destination schedule (exact mode bitwise, else tolerance)."""
-    _, n, rp, col, val, P = wl
+    n, rp, col, val, P = _build(name, False)
     plans = O2.plan_all(rp, col, n, P)
     offs = _offsets(plans)
+    if name.startswith("blocked"):
+        assert offs == [-4, -2, -1, 1, 2, 4]
     V, E, _ = S.fine_dag(offs)
     rng = random.Random(P)
     x = gen.x_values((0, n))
@@ -71,19 +79,15 @@ def test_fine_schedules_vs_oracle(wl, exchange):
     finally:
         run.close()
     # exact mode: bitwise against the simulation
-    n_, (rpe, cole, vale) = n, (rp, col, val)
-    if wl[0].startswith("c1"):
-        n_, (rpe, cole, vale) = gen.config_matrix("c1", exact=True)
-    else:
-        rpe, cole, vale = gen.banded(3000, 30000, 750, exact=True)
-    xe = gen.x_values((0, n_), exact=True)
+    n, rp, col, val, P = _build(name, True)
+    xe = gen.x_values((0, n), exact=True)
     ops = S.derive(_rand_topo(V, E, rng), {v: 1 for v in V})
-    run = LocalRun(n_, rpe, cole, vale, P, exchange=exchange)
+    run = LocalRun(n, rp, col, val, P, exchange=exchange)
     try:
         y = run.apply(run.schedule(oracle_ops_to_lib(ops)), xe, reps=2)
     finally:
         run.close()
-    assert np.array_equal(y, O2.simulate(O2.plan_all(rpe, cole, n_, P), vale, xe, ops))
+    assert np.array_equal(y, O2.simulate(O2.plan_all(rp, col, n, P), val, xe, ops))
 
 
 def test_fine_schedule_must_cover_every_peer():
@@ -116,7 +120,7 @@ def test_put_one_directional_pattern(fine):
     plans = O2.plan_all(rp, col, n, P)
     assert all(plans[r]["send_count"][q] == 0 for r in range(P) for q in range(r + 1))
     if fine:
-        V, E, _ = S.fine_dag([-1, 1] if P < 3 else _offsets(plans))
+        V, E, _ = S.fine_dag(_offsets(plans))
         ops = oracle_ops_to_lib(S.derive(S.topological_orders(E, V)[-1], {v: 0 for v in V}))
     else:
         ops = oracle_ops_to_lib(S.derive(S.topological_orders(S.EDGES)[0], dict.fromkeys(S.GPU_VERTICES, 0)))
