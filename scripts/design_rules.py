@@ -43,8 +43,8 @@ def peer_offsets(workload, ranks):
     if workload == "g3":
         n = 150000
         rp, col, _ = gen.banded(n)
-    elif workload == "c5":
-        n, (rp, col, _) = gen.config_matrix("c5")
+    elif workload in ("c5", "c5b"):
+        n, (rp, col, _) = gen.config_matrix(workload)
     else:
         n, (rp, col, _) = gen.config_matrix("c2")
     rb = np.asarray(D.dspmv_partition(n, ranks))
@@ -60,8 +60,8 @@ def setup(workload, ranks):
     if workload == "g3":
         n = 150000
         rp, col, val = gen.banded(n)
-    elif workload == "c5":
-        n, (rp, col, val) = gen.config_matrix("c5")
+    elif workload in ("c5", "c5b"):
+        n, (rp, col, val) = gen.config_matrix(workload)
     else:
         n, (rp, col, val) = gen.config_matrix("c2")
     x = gen.x_values((0, n))
@@ -127,8 +127,8 @@ def setup_distributed(workload, comm_kind):
     if workload == "g3":
         n = 150000
         rp, col, val = gen.banded(n)
-    elif workload == "c5":
-        n, (rp, col, val) = gen.config_matrix("c5")
+    elif workload in ("c5", "c5b"):
+        n, (rp, col, val) = gen.config_matrix(workload)
     else:
         n, (rp, col, val) = gen.config_matrix("c2")
     rb = D.dspmv_partition(n, world)
@@ -188,7 +188,7 @@ def make_measure_distributed(dist, rank, plan, x, y, t_measure=0.01, n_meas=3):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--workload", default="g3", choices=["g3", "c2", "c5"])
+    ap.add_argument("--workload", default="g3", choices=["g3", "c2", "c5", "c5b"])
     ap.add_argument("--ranks", type=int, default=4, help="in-process ranks (single process mode)")
     ap.add_argument("--comm", default=None, choices=[None, "nccl", "host"],
                     help="torchrun mode: one process per rank over NCCL (or host + fused put)")
