@@ -373,10 +373,11 @@ dspmv_status dspmv_apply_group(const dspmv_schedule_t* scheds, int nranks,
                                dspmv_stream_t stream);
 
 /* ------------------------------------------------------------- utilities */
-/* Write a device scratch buffer of 2x the L2 size (allocated on first use)
+/* Read a device scratch buffer of 2x the L2 size (allocated on first use)
  * on `stream`, evicting the working set from L2 between timed iterations. */
 dspmv_status dspmv_l2_flush(int cuda_device, dspmv_stream_t stream);
-/* Number of kernels this library has launched since it was loaded. */
+/* Number of kernels this library has launched since it was loaded (kernel
+ * nodes of a captured graph count at every dspmv_apply_graph). */
 dspmv_status dspmv_launch_count(uint64_t* count);
 /* Instrumented builds only (make PROFILE=1 -> libdspmv_prof.so): per-phase
  * clock64 totals of the row-block kernel ([0] producer waiting for an empty

@@ -744,6 +744,7 @@ dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t ori
     std::vector<cudaStream_t> all(st);
     if (p.has_peers) all.push_back(p.comm_stream);
     auto is_origin = [&](cudaStream_t q) { return q == origin; };
+    const uint64_t launches0 = g_launches.load();
     CUDA_TRY(cudaStreamBeginCapture(origin, cudaStreamCaptureModeThreadLocal));
     auto abort_capture = [&](dspmv_status stt) {
         cudaGraph_t g = nullptr;
@@ -829,6 +830,9 @@ dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t ori
 #undef CAP_TRY
     cudaGraph_t g = nullptr;
     CUDA_TRY(cudaStreamEndCapture(origin, &g));
+    // captured launches run with each graph launch, not now
+    s.graph_kernels = g_launches.load() - launches0;
+    g_launches.fetch_sub(s.graph_kernels);
     if (s.gexec) cudaGraphExecDestroy(s.gexec), s.gexec = nullptr;
     const cudaError_t ie = cudaGraphInstantiate(&s.gexec, g, 0);
     cudaGraphDestroy(g);
@@ -1506,6 +1510,7 @@ dspmv_status dspmv_apply_graph(dspmv_schedule_t s, const void* x, void* y, dspmv
         p.poisoned = true;
         return fail(DSPMV_ERR_CUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
     }
+    g_launches.fetch_add(s->graph_kernels, std::memory_order_relaxed);
     s->timed_valid = s->timing;
     return DSPMV_OK;
 }

@@ -165,6 +165,7 @@ struct Schedule {
     const void* gx = nullptr;
     void* gy = nullptr;
     bool g_timing = false;
+    uint64_t graph_kernels = 0;        // kernel nodes per graph launch (launch counter)
     cudaEvent_t gev[DSPMV_MAX_STREAMS + 2] = {};  // fork / join helpers
     bool timed_valid = false;
 };
