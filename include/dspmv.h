@@ -352,8 +352,11 @@ dspmv_status dspmv_schedule_op_timeline(dspmv_schedule_t sched, float* begin_ms,
  * host synchronisation point).  Not re-entrant per plan. */
 dspmv_status dspmv_apply(dspmv_schedule_t sched, const void* x_local, void* y_local,
                          dspmv_stream_t stream);
-/* Same with HOST x/y (pageable or pinned): H2D copy of x, apply, D2H copy of
- * y, all inside the call (the end-to-end path). */
+/* Same with HOST x/y, all transfers inside the call (the end-to-end path).
+ * Pageable memory: H2D copy of x, apply, D2H copy of y.  Pinned (page-locked,
+ * device-mapped) x and y: x is copied in up to 8 chunks and y_L runs, row-block
+ * group by group, behind the chunk each group reads; the SpMV kernels store y
+ * directly into the mapped host buffer.  Same bits either way. */
 dspmv_status dspmv_apply_host(dspmv_schedule_t sched, const void* x_host, void* y_host,
                               dspmv_stream_t stream);
 /* GPU-resident execution of the same schedule (NEXT-3 (iii)): on first use

@@ -140,6 +140,41 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
     return DSPMV_OK;
 }
 
+// Streamed host input of dspmv_apply_host (plan time, host only).  x is cut
+// into K chunks; y_L's row blocks are grouped so that group k reads x chunks
+// <= k only (prefix max of each block's highest column chunk).
+void build_host_pipe(Plan& p, Layout& L) {
+    auto& H = p.pipe;
+    H.K = 0;
+    const int64_t n = p.host.n_local();
+    const int64_t bytes = n * p.esize;
+    if (L.nb < 2 || bytes < (int64_t(2) << 20)) return;   // small: one transfer is as good
+    // 4 chunks measured best on C2 (scripts/diag_pcie5.py: K = 1 / 2 / 4 / 8 / 12 ->
+    // 0.647 / 0.527 / 0.487 / 0.510 / 0.560 ms per apply_host): each chunk
+    // boundary costs a copy-engine drain, the last chunk's rows trail the copy
+    int kmax = 4;
+    if (const char* ev = std::getenv("DSPMV_HOST_CHUNKS")) kmax = std::max(1, std::min(64, std::atoi(ev)));  // tuning
+    const int K = int(std::min<int64_t>(kmax, bytes / (int64_t(1) << 20)));
+    H.x_chunk.assign(K + 1, 0);
+    for (int k = 1; k < K; ++k) H.x_chunk[k] = std::min<int64_t>(n, (int64_t(k) * n / K + 255) / 256 * 256);
+    H.x_chunk[K] = n;
+    auto chunk_of = [&](int64_t c) {
+        return int(std::upper_bound(H.x_chunk.begin(), H.x_chunk.end(), c) - H.x_chunk.begin()) - 1;
+    };
+    H.grp.assign(K + 1, L.nb);
+    H.grp[0] = 0;
+    int pm = 0;
+    for (int32_t b = 0; b < L.nb; ++b) {
+        const int32_t* d = L.s_desc.data() + size_t(b) * kDescInts;
+        int32_t cmax = 0;
+        for (int32_t q = d[2]; q < d[3]; ++q) cmax = std::max(cmax, L.s_col[q]);
+        pm = std::max(pm, d[3] > d[2] ? chunk_of(cmax) : 0);
+        for (int k = 0; k < pm; ++k) H.grp[k + 1] = std::min(H.grp[k + 1], b);
+        L.s_desc[size_t(b) * kDescInts + 15] = pm;
+    }
+    H.K = K;
+}
+
 // Phase 2 on the device side: pack map + send buffer.
 dspmv_status finalize_send(Plan& p) {
     p.has_peers = false;
@@ -452,6 +487,18 @@ PFN_cuStreamWaitValue32_v11070 wait_value32() {
     return fn;
 }
 
+PFN_cuStreamWriteValue32_v11070 write_value32() {
+    static PFN_cuStreamWriteValue32_v11070 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(f);
+    }();
+    return fn;
+}
+
 // PUT mode: the data moves inside the fused Pack kernels; the exchange is the
 // comm stream waiting until every source of the group has published this epoch.
 dspmv_status issue_group_put(Plan& p, ExGroup& g) {
@@ -598,6 +645,10 @@ cudaError_t launch_gpu_vertex(Schedule& s, int t, const void* x, void* y, cudaSt
         case DSPMV_OP_PACK: {
             const int q = s.op_peer[t];  // -2: every destination; -1: nothing to send
             if (q == -1) break;
+            if (p.streaming && p.pipe.pack_chunk >= 0) {  // x still arriving (apply_host)
+                e = cudaStreamWaitEvent(st, p.pipe.ev_x[p.pipe.pack_chunk], 0);
+                if (e != cudaSuccess) break;
+            }
             if (p.put_mode) {
                 void* const* dst = p.d_seg_dst + (p.epoch & 1u) * p.put_nseg;
                 if (q == -2) {
@@ -622,7 +673,21 @@ cudaError_t launch_gpu_vertex(Schedule& s, int t, const void* x, void* y, cudaSt
         }
         case DSPMV_OP_SPMV_LOCAL: {
             SpmvOperands op{x, y, p.d_partL, p.d_partR, p.d_ticket};
-            e = launch_spmv(p.L, p.dtype, op, st);
+            if (!p.streaming) {
+                e = launch_spmv(p.L, p.dtype, op, st);
+                break;
+            }
+            // apply_host pipeline: one launch; the producer warp of each CTA
+            // waits for the x chunk flag of a block before staging it
+            auto& H = p.pipe;
+            op.xflag = H.d_xflag;
+            op.epoch = p.epoch;
+            e = launch_spmv_part(p.L, p.dtype, op, st, 0, p.L.nb, false);
+            op.xflag = nullptr;
+            if (e == cudaSuccess && p.L.nV > 0) {
+                e = cudaStreamWaitEvent(st, H.ev_x[H.K - 1], 0);
+                if (e == cudaSuccess) e = launch_spmv_part(p.L, p.dtype, op, st, p.L.nb, p.L.nb, true);
+            }
             break;
         }
         case DSPMV_OP_UNPACK: {
@@ -979,6 +1044,10 @@ static void free_plan_device(Plan& p) {
     for (auto& s : p.streams)
         if (s) cudaStreamDestroy(s), s = nullptr;
     if (p.comm_stream) cudaStreamDestroy(p.comm_stream), p.comm_stream = nullptr;
+    if (p.pipe.h2d) cudaStreamDestroy(p.pipe.h2d), p.pipe.h2d = nullptr;
+    for (auto& e : p.pipe.ev_x)
+        if (e) cudaEventDestroy(e), e = nullptr;
+    if (p.pipe.ev_in) cudaEventDestroy(p.pipe.ev_in), p.pipe.ev_in = nullptr;
     if (p.ev_start) cudaEventDestroy(p.ev_start), p.ev_start = nullptr;
 }
 
@@ -1047,6 +1116,7 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
         const int c = cfg >= 0 ? cfg : auto_block_cfg(h.al_rowptr.data(), int32_t(h.n_local()), vthr, p->esize);
         build_layout(h.al_rowptr.data(), int32_t(h.n_local()), h.al_col.data(), h.al_val.data(), p->esize, nullptr,
                      nR > 0 ? slotL.data() : nullptr, vthr, kBlockCfgs[c], L);
+        build_host_pipe(*p, L);   // also stores each block's x chunk in desc[15]
         if ((st = upload_layout(*p, L, c, p->L)) != DSPMV_OK) return bail(st);
     }
     {
@@ -1515,6 +1585,15 @@ dspmv_status dspmv_apply_graph(dspmv_schedule_t s, const void* x, void* y, dspmv
     return DSPMV_OK;
 }
 
+static bool pinned_host(const void* ptr) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 dspmv_status dspmv_apply_host(dspmv_schedule_t s, const void* x_host, void* y_host, dspmv_stream_t stream) {
     if (!s) return fail(DSPMV_ERR_ARG, "null schedule");
     Plan& p = *s->plan;
@@ -1526,9 +1605,65 @@ dspmv_status dspmv_apply_host(dspmv_schedule_t s, const void* x_host, void* y_ho
         ST_TRY(dev_alloc(p, &p.d_yout, bytes, false));
     }
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
-    if (bytes) CUDA_TRY(cudaMemcpyAsync(p.d_xin, x_host, bytes, cudaMemcpyHostToDevice, cs));
-    ST_TRY(dspmv_apply(s, p.d_xin, p.d_yout, stream));
-    if (bytes) CUDA_TRY(cudaMemcpyAsync(y_host, p.d_yout, bytes, cudaMemcpyDeviceToHost, cs));
+    auto& H = p.pipe;
+    if (!bytes || H.K == 0 || !pinned_host(x_host) || !pinned_host(y_host)) {
+        // one transfer each way around the apply
+        if (bytes) CUDA_TRY(cudaMemcpyAsync(p.d_xin, x_host, bytes, cudaMemcpyHostToDevice, cs));
+        ST_TRY(dspmv_apply(s, p.d_xin, p.d_yout, stream));
+        if (bytes) CUDA_TRY(cudaMemcpyAsync(y_host, p.d_yout, bytes, cudaMemcpyDeviceToHost, cs));
+        CUDA_TRY(cudaStreamSynchronize(cs));
+        return DSPMV_OK;
+    }
+    // pinned x/y: x goes over in K chunks on a copy stream and y_L runs group
+    // by group right behind it; the kernels store y straight into the mapped
+    // host buffer (zero-copy), so no device-to-host copy follows and the one
+    // copy engine in use never shares PCIe with a second transfer direction
+    void* y_map = nullptr;
+    if (cudaHostGetDevicePointer(&y_map, y_host, 0) != cudaSuccess || !y_map) {
+        cudaGetLastError();
+        if (bytes) CUDA_TRY(cudaMemcpyAsync(p.d_xin, x_host, bytes, cudaMemcpyHostToDevice, cs));
+        ST_TRY(dspmv_apply(s, p.d_xin, p.d_yout, stream));
+        if (bytes) CUDA_TRY(cudaMemcpyAsync(y_host, p.d_yout, bytes, cudaMemcpyDeviceToHost, cs));
+        CUDA_TRY(cudaStreamSynchronize(cs));
+        return DSPMV_OK;
+    }
+    auto wv = write_value32();
+    if (!wv) return fail(DSPMV_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+    if (!H.h2d) {
+        ST_TRY(dev_alloc(p, reinterpret_cast<void**>(&H.d_xflag), size_t(H.K) * 4, true));
+        CUDA_TRY(cudaStreamCreateWithFlags(&H.h2d, cudaStreamNonBlocking));
+        H.ev_x.assign(H.K, nullptr);
+        for (auto& e : H.ev_x) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&H.ev_in, cudaEventDisableTiming));
+    }
+    if (H.pack_chunk == -1) {
+        H.pack_chunk = -2;                               // no Pack reads of x
+        if (!p.host.pack_map.empty()) {
+            const int32_t mx = *std::max_element(p.host.pack_map.begin(), p.host.pack_map.end());
+            H.pack_chunk = int(std::upper_bound(H.x_chunk.begin(), H.x_chunk.end(), int64_t(mx)) - H.x_chunk.begin()) - 1;
+        }
+    }
+    CUDA_TRY(cudaEventRecord(H.ev_in, cs));              // after prior work on the caller stream
+    CUDA_TRY(cudaStreamWaitEvent(H.h2d, H.ev_in, 0));
+    const unsigned epoch = p.epoch + 1;                  // begin_apply's epoch of this apply
+    for (int k = 0; k < H.K; ++k) {
+        const size_t off = size_t(H.x_chunk[k]) * p.esize, len = size_t(H.x_chunk[k + 1] - H.x_chunk[k]) * p.esize;
+        cudaStream_t q = H.h2d;
+        CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(p.d_xin) + off, static_cast<const char*>(x_host) + off, len,
+                                 cudaMemcpyHostToDevice, q));
+        const CUresult r =
+            wv(reinterpret_cast<CUstream>(q), reinterpret_cast<CUdeviceptr>(H.d_xflag + k), epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
+        if (r != CUDA_SUCCESS) return fail(DSPMV_ERR_CUDA, "cuStreamWriteValue32 failed (" + std::to_string(int(r)) + ")");
+        CUDA_TRY(cudaEventRecord(H.ev_x[k], q));
+    }
+    p.streaming = true;
+    const dspmv_status st = dspmv_apply(s, p.d_xin, y_map, stream);
+    p.streaming = false;
+    if (st != DSPMV_OK) {
+        cudaStreamSynchronize(H.h2d);
+        return st;
+    }
+    CUDA_TRY(cudaStreamWaitEvent(cs, H.ev_x[H.K - 1], 0));   // every H2D done before d_xin is reused
     CUDA_TRY(cudaStreamSynchronize(cs));
     return DSPMV_OK;
 }

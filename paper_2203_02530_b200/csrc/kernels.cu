@@ -112,6 +112,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -154,7 +160,7 @@ struct BlockArgs {
     const int32_t* desc;
     const int32_t* out;
     const int32_t* slot;
-    int32_t nb;
+    int32_t b0, nb;     // row blocks [b0, nb)
 };
 
 struct VecArgs {
@@ -265,7 +271,7 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             int it = 0;
-            for (int b = blockIdx.x; b < a.nb; b += gridDim.x, ++it) {
+            for (int b = a.b0 + blockIdx.x; b < a.nb; b += gridDim.x, ++it) {
                 const int s = it % C::kStages;
                 const int u = it / C::kStages;
 #ifdef DSPMV_PROFILE
@@ -278,6 +284,9 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
 #endif
                 const int4* d = reinterpret_cast<const int4*>(a.desc + size_t(b) * kDescInts);
                 const int4 d0 = __ldg(d), d1 = __ldg(d + 1), d2 = __ldg(d + 2), d3 = __ldg(d + 3);
+                if (o.xflag) {  // streamed x: wait until x chunks <= desc[15] have landed
+                    while (ld_acquire_gpu(o.xflag + d3.w) < o.epoch) __nanosleep(256);
+                }
                 const int32_t r0 = d0.x, r1 = d0.y, p0 = d0.z, p1 = d0.w;
                 const int32_t a0 = p0 & ~3, a1 = (p1 + 3) & ~3;
                 const int32_t ra0 = r0 & ~3, ra1 = (r1 + 1 + 3) & ~3;
@@ -312,7 +321,7 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
     const int32_t* __restrict__ slot = a.slot;
     const uint64_t xpol = policy_evict_last();
     int it = 0;
-    for (int b = blockIdx.x; b < a.nb; b += gridDim.x, ++it) {
+    for (int b = a.b0 + blockIdx.x; b < a.nb; b += gridDim.x, ++it) {
         const int s = it % C::kStages;
         const int u = it / C::kStages;
 #ifdef DSPMV_PROFILE
@@ -476,49 +485,50 @@ cudaError_t prep_block_kernel() {
 }
 
 template <typename T, int CFG, bool C, bool I>
-cudaError_t launch_block(const DevLayout& L, const SpmvOperands& o, cudaStream_t s) {
+cudaError_t launch_block(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, int32_t b0, int32_t b1) {
     cudaError_t e = prep_block_kernel<T, CFG, C, I>();
     if (e != cudaSuccess) return e;
-    BlockArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_desc, L.s_out, L.s_slot, L.nb};
+    BlockArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_desc, L.s_out, L.s_slot, b0, b1};
+    const int grid = std::min(L.grid_s, b1 - b0);
     spmv_block_kernel<T, CFG, C, I>
-        <<<L.grid_s, Cfg<CFG>::kThreadsPerCta, Cfg<CFG>::template smem_bytes<T>(), s>>>(a, o);
+        <<<grid, Cfg<CFG>::kThreadsPerCta, Cfg<CFG>::template smem_bytes<T>(), s>>>(a, o);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
 }
 
 template <typename T, int CFG>
-cudaError_t launch_block_cfg(const DevLayout& L, const SpmvOperands& o, cudaStream_t s) {
+cudaError_t launch_block_cfg(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, int32_t b0, int32_t b1) {
     const bool c = L.s_slot != nullptr, id = L.s_out == nullptr;
-    if (c && id) return launch_block<T, CFG, true, true>(L, o, s);
-    if (c) return launch_block<T, CFG, true, false>(L, o, s);
-    if (id) return launch_block<T, CFG, false, true>(L, o, s);
-    return launch_block<T, CFG, false, false>(L, o, s);
+    if (c && id) return launch_block<T, CFG, true, true>(L, o, s, b0, b1);
+    if (c) return launch_block<T, CFG, true, false>(L, o, s, b0, b1);
+    if (id) return launch_block<T, CFG, false, true>(L, o, s, b0, b1);
+    return launch_block<T, CFG, false, false>(L, o, s, b0, b1);
 }
 
 template <typename T>
-cudaError_t launch_block_any(const DevLayout& L, const SpmvOperands& o, cudaStream_t s) {
+cudaError_t launch_block_any(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, int32_t b0, int32_t b1) {
     switch (L.cfg) {
-        case 0: return launch_block_cfg<T, 0>(L, o, s);
-        case 1: return launch_block_cfg<T, 1>(L, o, s);
-        case 2: return launch_block_cfg<T, 2>(L, o, s);
-        case 3: return launch_block_cfg<T, 3>(L, o, s);
-        case 4: return launch_block_cfg<T, 4>(L, o, s);
-        case 5: return launch_block_cfg<T, 5>(L, o, s);
-        case 6: return launch_block_cfg<T, 6>(L, o, s);
-        case 7: return launch_block_cfg<T, 7>(L, o, s);
+        case 0: return launch_block_cfg<T, 0>(L, o, s, b0, b1);
+        case 1: return launch_block_cfg<T, 1>(L, o, s, b0, b1);
+        case 2: return launch_block_cfg<T, 2>(L, o, s, b0, b1);
+        case 3: return launch_block_cfg<T, 3>(L, o, s, b0, b1);
+        case 4: return launch_block_cfg<T, 4>(L, o, s, b0, b1);
+        case 5: return launch_block_cfg<T, 5>(L, o, s, b0, b1);
+        case 6: return launch_block_cfg<T, 6>(L, o, s, b0, b1);
+        case 7: return launch_block_cfg<T, 7>(L, o, s, b0, b1);
         default: return cudaErrorInvalidValue;
     }
 }
 static_assert(kNumBlockCfgs == 8, "update launch_block_any / occupancy dispatch");
 
 template <typename T>
-cudaError_t launch_all(const DevLayout& L, const SpmvOperands& o, cudaStream_t s) {
+cudaError_t launch_all(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, int32_t b0, int32_t b1, bool vec) {
     cudaError_t e = cudaSuccess;
-    if (L.nb > 0) {
-        e = launch_block_any<T>(L, o, s);
+    if (b1 > b0) {
+        e = launch_block_any<T>(L, o, s, b0, b1);
         if (e != cudaSuccess) return e;
     }
-    if (L.nV > 0) {
+    if (vec && L.nV > 0) {
         VecArgs a{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, L.nV};
         if (L.v_slot) spmv_vector_kernel<T, true><<<L.grid_v, kThreads, 0, s>>>(a, o);
         else spmv_vector_kernel<T, false><<<L.grid_v, kThreads, 0, s>>>(a, o);
@@ -577,7 +587,12 @@ int block_kernel_ctas_per_sm(int dtype, int cfg) {
 int device_sm_count() { return num_sms(); }
 
 cudaError_t launch_spmv(const DevLayout& L, int dtype, const SpmvOperands& o, cudaStream_t s) {
-    return dtype == DSPMV_F32 ? launch_all<float>(L, o, s) : launch_all<double>(L, o, s);
+    return launch_spmv_part(L, dtype, o, s, 0, L.nb, true);
+}
+
+cudaError_t launch_spmv_part(const DevLayout& L, int dtype, const SpmvOperands& o, cudaStream_t s, int32_t b0,
+                             int32_t b1, bool vec) {
+    return dtype == DSPMV_F32 ? launch_all<float>(L, o, s, b0, b1, vec) : launch_all<double>(L, o, s, b0, b1, vec);
 }
 
 cudaError_t launch_pack(int dtype, const void* x, const int32_t* map, void* out, int64_t n, cudaStream_t s) {

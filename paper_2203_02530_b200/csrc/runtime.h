@@ -43,12 +43,19 @@ struct SpmvOperands {
     void* my_part = nullptr;           // this op's partial for combined rows
     const void* other_part = nullptr;  // the other op's partial
     unsigned* ticket = nullptr;        // per combined row, epoch counter
+    // streamed x (dspmv_apply_host): row block b waits until
+    // xflag[desc[15] of b] >= epoch, i.e. its x chunks have landed
+    const unsigned* xflag = nullptr;
+    unsigned epoch = 0;
 };
 
 // kernels.cu
 int block_kernel_smem_bytes(int dtype, int cfg);
 int block_kernel_ctas_per_sm(int dtype, int cfg);
 cudaError_t launch_spmv(const DevLayout& L, int dtype, const SpmvOperands& o, cudaStream_t s);
+// row blocks [b0, b1) of the S group, plus the V group (long rows) if vec
+cudaError_t launch_spmv_part(const DevLayout& L, int dtype, const SpmvOperands& o, cudaStream_t s, int32_t b0,
+                             int32_t b1, bool vec);
 cudaError_t launch_pack(int dtype, const void* x, const int32_t* map, void* out, int64_t n,
                         cudaStream_t s);
 cudaError_t launch_copy(int dtype, const void* src, void* dst, int64_t n, cudaStream_t s);
@@ -126,6 +133,20 @@ struct Plan {
     std::vector<void*> ipc_opened;     // peer mappings to close
     bool poisoned = false;
     int live_scheds = 0;
+    // streamed host input for dspmv_apply_host (built at plan time): x
+    // arrives in K chunks; y_L launch group k (S blocks [grp[k], grp[k+1]))
+    // reads x chunks <= k only
+    struct HostPipe {
+        int K = 0;
+        std::vector<int64_t> x_chunk;  // [K+1] element boundaries
+        std::vector<int32_t> grp;      // [K+1] S-block boundaries
+        int pack_chunk = -1;           // x chunk holding max(pack_map) (-1 unknown, -2 none)
+        unsigned* d_xflag = nullptr;   // [K] epoch written after chunk k lands
+        cudaStream_t h2d = nullptr;
+        std::vector<cudaEvent_t> ev_x;
+        cudaEvent_t ev_in = nullptr;
+    } pipe;
+    bool streaming = false;            // inside dspmv_apply_host with pinned x/y
 };
 
 // One halo-exchange group of a schedule, issued once both its PostSend and
