@@ -30,6 +30,7 @@ def _worker(rank, world, port, mat, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import gen
+        import numpy as np
         from paper_2203_02530_b200 import dspmv as D
         from tests.gpu_helpers import derive_ops
         torch.cuda.set_device(0)
@@ -43,6 +44,10 @@ def _worker(rank, world, port, mat, q):
             n = 30000
             rb = D.dspmv_partition(n, world)
             rp, col, val = gen.powerlaw(n, (int(rb[rank]), int(rb[rank + 1])))
+        elif mat == "7pt":                       # >= 2 MB of x per rank: pipelined apply_host
+            n = 64 * 64 * 128
+            rb = D.dspmv_partition(n, world)
+            rp, col, val = gen.stencil("7pt", (64, 64, 128), (int(rb[rank]), int(rb[rank + 1])))
         else:
             n = 24 ** 3
             rb = D.dspmv_partition(n, world)
@@ -59,6 +64,15 @@ def _worker(rank, world, port, mat, q):
             dist.barrier()
             D.dspmv_apply(s, x, y)
             ys.append(y.cpu().numpy().copy())
+        # the end-to-end path (pinned host x/y) gives the same bits
+        xh = x.cpu().pin_memory()
+        yh = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
+        for _ in range(2):
+            yh.fill_(float("nan"))
+            dist.barrier()
+            D.dspmv_apply_host(s, xh, yh)
+            if not np.array_equal(yh.numpy(), ys[0]):
+                raise AssertionError("apply_host differs from apply")
         D.dspmv_schedule_destroy(s)
         D.dspmv_plan_destroy(plan)
         D.dspmv_comm_destroy(comm)
@@ -69,7 +83,7 @@ def _worker(rank, world, port, mat, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,mat", [(2, "pl"), (3, "27pt")])
+@pytest.mark.parametrize("world,mat", [(2, "pl"), (3, "27pt"), (2, "7pt")])
 def test_multiprocess_fused_put_on_one_gpu(world, mat):
     import gen
     from oracle import spmv as O1
@@ -90,6 +104,9 @@ def test_multiprocess_fused_put_on_one_gpu(world, mat):
     if mat == "pl":
         n = 30000
         rp, col, val = gen.powerlaw(n)
+    elif mat == "7pt":
+        n = 64 * 64 * 128
+        rp, col, val = gen.stencil("7pt", (64, 64, 128))
     else:
         n = 24 ** 3
         rp, col, val = gen.stencil("27pt", (24, 24, 24))
