@@ -342,3 +342,70 @@ def enumerate_derived(n_streams=2, edges=EDGES):
             key = canonical(ops)
             seen.setdefault(key, ops)
     return list(seen.values())
+
+
+# ------------------------------------------------------ orderable syncs
+def _sync_move(ops, u, iu, v_stream):
+    """Next synchronisation step for an unmet edge u -> v (tab:sync): a
+    cudaEventRecord on u's stream if no event recorded there after u yet,
+    else the wait (CES for a CPU v, CSWE on v's stream for a GPU v) on the
+    latest such event."""
+    su = ops[iu][1]
+    evs = [op[2] for t, op in enumerate(ops) if op[0] == "CER" and op[1] == su and t > iu]
+    if not evs:
+        n_ev = sum(1 for op in ops if op[0] == "CER")
+        return ("CER", su, n_ev)
+    return ("CES", evs[-1]) if v_stream is None else ("CSWE", v_stream, evs[-1])
+
+
+def orderable_moves(ops, n_streams, edges=None):
+    """Legal next ops of a prefix when synchronisation operations are moves
+    of their own ("some prefixes may require synchronization
+    operations before proceeding to the next vertex"; DESIGN.md R-N5, the
+    "first-unmet" reading of SURVEY Appendix A).  For every frontier vertex v
+    (all DAG predecessors in the prefix) and stream choice s (first-use
+    bijection pruning): v itself if every edge u -> v is already
+    enforced, else the next sync step of the first unmet predecessor."""
+    if not ops:
+        return [("start",)]
+    if edges is None:
+        edges = dag_of(ops)[1]
+        vertices = dag_of(ops)[0]
+    else:
+        vertices = VERTICES
+    done = {op[0] for op in ops if base(op[0]) in VERTICES}
+    used = len({op[1] for op in ops
+                if (base(op[0]) in GPU_VERTICES) or op[0] in ("CER", "CSWE")})
+    moves = []
+    for v in vertices:
+        pv = preds(v, edges)
+        if v in done or not all(u in done for u in pv):
+            continue
+        opts = range(min(used + 1, n_streams)) if base(v) in GPU_VERTICES else [None]
+        for s in opts:
+            vop = (v, s) if s is not None else (v,)
+            m = vop
+            for u in pv:
+                iu = next(t for t, op in enumerate(ops) if op[0] == u)
+                if not edge_satisfied(ops + [vop], iu, len(ops)):
+                    m = _sync_move(ops, u, iu, s)
+                    break
+            if m not in moves:
+                moves.append(m)
+    return moves
+
+
+def enumerate_orderable(n_streams=2, edges=EDGES):
+    """Every distinct complete schedule reachable through orderable_moves,
+    deduplicated by the canonical form (brute-force DFS)."""
+    seen = {}
+
+    def dfs(ops):
+        if ops and ops[-1][0] == "end":
+            seen.setdefault(canonical(ops), ops)
+            return
+        for m in orderable_moves(ops, n_streams, edges):
+            dfs(ops + [m])
+
+    dfs([])
+    return list(seen.values())

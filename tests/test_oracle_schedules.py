@@ -121,3 +121,36 @@ def test_validator_rejects_structural_errors():
     bad = list(good)
     bad[ces] = ("CES", 99)                                   # unrecorded event
     assert not S.validate(bad, 2)[0]
+
+
+def _orderable_golden():
+    out = []
+    for line in open(os.path.join(GOLDEN, "orderable_counts.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        a, b = line.split()
+        out.append((a, int(b)))
+    return out
+
+
+@pytest.mark.parametrize("reading,count", _orderable_golden())
+def test_orderable_sync_counts_match_appendix_a(reading, count):
+    """Syncs as moves of their own (R-N5 "first-unmet"): the
+    number of distinct schedules equals the surveyor's independent count."""
+    edges = {"A+both": S.EDGES, "A+PostSend->WaitRecv": S.EDGES_A + [("PostSend", "WaitRecv")]}[reading]
+    assert len(S.enumerate_orderable(2, edges)) == count
+
+
+def test_orderable_space_covers_the_derived_space_and_is_valid():
+    """Every traversal + stream binding of the derived space is reached (the
+    syncs may differ: an event already recorded after u is reused), and every
+    orderable schedule is valid."""
+    orderable = S.enumerate_orderable(2)
+
+    def proj(o):
+        return tuple(op for op in S.canonical(o) if op[0] in S.VERTICES)
+    keys = {proj(o) for o in orderable}
+    assert all(proj(o) in keys for o in S.enumerate_derived(2))
+    assert all(S.validate(o, 2) == (True, "", "") for o in orderable)
+    # a sync placed away from its consumer exists (what the derived space lacks)
+    assert any(o[i][0] == "CER" and o[i + 1][0] not in ("CES", "CSWE") for o in orderable for i in range(len(o) - 1))
