@@ -310,6 +310,17 @@ dspmv_status dspmv_schedule_derive_peers(const int32_t* order, const int32_t* st
 dspmv_status dspmv_schedule_dag(const int32_t* offsets, int n_offsets, int32_t* kinds, int32_t* peers, int cap_v,
                                 int* n_v, int32_t* edges, int cap_e, int* n_e);
 
+/* Host-only.  Orderable synchronisation (DESIGN.md R-N5): the
+ * legal next ops after `prefix` (a schedule prefix of the DAG of `offsets`,
+ * n_offsets = 0 -> coarse).  For every frontier vertex v and stream choice
+ * (first-use bijection pruning) the move is v itself if every
+ * edge u->v is enforced, else the next sync step of the first unmet
+ * predecessor u: CER on u's stream (event id = number of CERs so far) if none
+ * was recorded there after u, else CES (CPU v) / CSWE on v's stream (GPU v)
+ * on the latest such event.  Empty prefix -> START.  Duplicates removed. */
+dspmv_status dspmv_schedule_moves(const int32_t* offsets, int n_offsets, const dspmv_op* prefix, int n_prefix,
+                                  int n_streams, dspmv_op* out, int cap, int* n_out);
+
 /* Host-only.  External schedule text format: one op per line
  * "<name> <kind> [stream=<i>] [event=<id>] [peer=<d>]", kind in {Cpu, BoundGpu,
  * EventRecord, EventSync, StreamWaitEvent}; names start, Pack, y_L,

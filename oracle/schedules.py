@@ -358,7 +358,7 @@ def _sync_move(ops, u, iu, v_stream):
     return ("CES", evs[-1]) if v_stream is None else ("CSWE", v_stream, evs[-1])
 
 
-def orderable_moves(ops, n_streams, edges=None):
+def orderable_moves(ops, n_streams, edges=None, vertices=None):
     """Legal next ops of a prefix when synchronisation operations are moves
     of their own ("some prefixes may require synchronization
     operations before proceeding to the next vertex"; DESIGN.md R-N5, the
@@ -368,10 +368,9 @@ def orderable_moves(ops, n_streams, edges=None):
     enforced, else the next sync step of the first unmet predecessor."""
     if not ops:
         return [("start",)]
-    if edges is None:
-        edges = dag_of(ops)[1]
-        vertices = dag_of(ops)[0]
-    else:
+    if edges is None:                 # the coarse DAG unless given (a prefix may
+        vertices, edges = VERTICES, EDGES   # not show its granularity yet)
+    elif vertices is None:
         vertices = VERTICES
     done = {op[0] for op in ops if base(op[0]) in VERTICES}
     used = len({op[1] for op in ops

@@ -318,6 +318,102 @@ extern "C" dspmv_status dspmv_schedule_dag(const int32_t* offsets, int n_offsets
     return DSPMV_OK;
 }
 
+extern "C" dspmv_status dspmv_schedule_moves(const int32_t* offsets, int n_offsets, const dspmv_op* prefix,
+                                            int n_prefix, int n_streams, dspmv_op* out, int cap, int* n_out) {
+    if (!n_out || n_prefix < 0 || (n_prefix > 0 && !prefix) || n_offsets < 0 || (n_offsets > 0 && !offsets))
+        return fail(DSPMV_ERR_ARG, "bad argument");
+    if (n_streams < 1 || n_streams > DSPMV_MAX_STREAMS) return fail(DSPMV_ERR_ARG, "n_streams out of range");
+    std::vector<dspmv_op> moves;
+    auto emit = [&](const dspmv_op& m) {
+        for (const dspmv_op& x : moves)
+            if (x.kind == m.kind && x.stream == m.stream && x.event == m.event && x.peer == m.peer) return;
+        moves.push_back(m);
+    };
+    if (n_prefix == 0) {
+        emit({DSPMV_OP_START, 0, 0, 0});
+    } else {
+        std::vector<DagVertex> present;
+        for (int i = 0; i < n_offsets; ++i) {
+            if (offsets[i] == 0) return fail(DSPMV_ERR_ARG, "offsets must be non-zero");
+            present.push_back({DSPMV_OP_PACK, offsets[i]});
+        }
+        Dag g;
+        std::string why;
+        if (!build_dag(present, g, why)) return fail(DSPMV_ERR_ARG, why);
+        // replay the prefix
+        HB hb(g);
+        std::vector<int> where(g.v.size(), -1);
+        std::vector<int> ev_stream(DSPMV_MAX_EVENTS, -1), ev_pos(DSPMV_MAX_EVENTS, -1), ev_order;
+        int used = 0, n_ev = 0;
+        for (int t = 0; t < n_prefix; ++t) {
+            const dspmv_op& o = prefix[t];
+            if (is_dag_vertex(o.kind)) {
+                const int id = g.find(o.kind, o.peer);
+                if (id < 0 || where[id] >= 0) return fail(DSPMV_ERR_ARG, "prefix vertex not in the DAG or repeated");
+                if (is_gpu_vertex(o.kind) && (o.stream < 0 || o.stream >= n_streams))
+                    return fail(DSPMV_ERR_ARG, "prefix stream out of range");
+                where[id] = t;
+                hb.vertex(id, o.stream);
+                if (is_gpu_vertex(o.kind)) used = std::max(used, o.stream + 1);
+            } else if (o.kind == DSPMV_OP_EVENT_RECORD || o.kind == DSPMV_OP_EVENT_SYNC ||
+                       o.kind == DSPMV_OP_STREAM_WAIT_EVENT) {
+                if (o.event < 0 || o.event >= DSPMV_MAX_EVENTS) return fail(DSPMV_ERR_ARG, "prefix event out of range");
+                if (o.kind != DSPMV_OP_EVENT_SYNC) {
+                    if (o.stream < 0 || o.stream >= n_streams) return fail(DSPMV_ERR_ARG, "prefix stream out of range");
+                    used = std::max(used, o.stream + 1);
+                }
+                if (o.kind == DSPMV_OP_EVENT_RECORD) {
+                    ev_stream[o.event] = o.stream;
+                    ev_pos[o.event] = t;
+                    ev_order.push_back(o.event);
+                    ++n_ev;
+                }
+                hb.sync(o);
+            } else {
+                return fail(DSPMV_ERR_ARG, "bad prefix op");
+            }
+        }
+        // frontier vertices x stream choices (first-use pruning); the move is the
+        // vertex if every in-edge is enforced, else the next sync step of the
+        // first unmet predecessor (DESIGN.md R-N5)
+        for (size_t v = 0; v < g.v.size(); ++v) {
+            if (hb.done[v]) continue;
+            bool ready = true;
+            for (const auto& e : g.edges)
+                if (e[1] == int(v) && !hb.done[e[0]]) ready = false;
+            if (!ready) continue;
+            const int k = g.v[v].kind;
+            const int ns = is_gpu_vertex(k) ? std::min(used + 1, n_streams) : 1;
+            for (int sv = 0; sv < ns; ++sv) {
+                const int s_v = is_gpu_vertex(k) ? sv : -1;
+                int unmet = -1;
+                for (const auto& e : g.edges)
+                    if (e[1] == int(v) && !hb.enforced(e[0], s_v)) {
+                        unmet = e[0];
+                        break;
+                    }
+                if (unmet < 0) {
+                    emit({k, s_v < 0 ? 0 : s_v, 0, g.v[v].peer});
+                    continue;
+                }
+                const int su = hb.stream_of[unmet];
+                int ev = -1;  // latest event recorded on su after u
+                for (int q = int(ev_order.size()) - 1; q >= 0 && ev < 0; --q) {
+                    const int e = ev_order[q];
+                    if (ev_stream[e] == su && ev_pos[e] > where[unmet]) ev = e;
+                }
+                if (ev < 0) emit({DSPMV_OP_EVENT_RECORD, su, n_ev, 0});
+                else if (s_v < 0) emit({DSPMV_OP_EVENT_SYNC, 0, ev, 0});
+                else emit({DSPMV_OP_STREAM_WAIT_EVENT, s_v, ev, 0});
+            }
+        }
+    }
+    *n_out = int(moves.size());
+    if (int(moves.size()) > cap) return fail(DSPMV_ERR_ARG, "output capacity too small");
+    std::copy(moves.begin(), moves.end(), out);
+    return DSPMV_OK;
+}
+
 extern "C" dspmv_status dspmv_schedule_derive_peers(const int32_t* order, const int32_t* streams,
                                                     const int32_t* peers, int n_vertices, int n_streams,
                                                     dspmv_op* out, int cap, int* n_out) {

@@ -116,6 +116,7 @@ _sig("dspmv_schedule_validate", [_P, _I, _I])
 _sig("dspmv_schedule_derive", [_P, _P, _I, _P, _I, _P])
 _sig("dspmv_schedule_derive_peers", [_P, _P, _P, _I, _I, _P, _I, _P])
 _sig("dspmv_schedule_dag", [_P, _I, _P, _P, _I, _P, _P, _I, _P])
+_sig("dspmv_schedule_moves", [_P, _I, _P, _I, _I, _P, _I, _P])
 _sig("dspmv_schedule_parse", [ctypes.c_char_p, _P, _I, _P, _P])
 _sig("dspmv_schedule_format", [_P, _I, _P, ctypes.c_size_t])
 _sig("dspmv_schedule_create", [_P, _P, _I, _I, _P])
@@ -402,6 +403,18 @@ def dspmv_schedule_dag(offsets=()):
                                   peers.ctypes.data, nv.value, ctypes.byref(nv), edges.ctypes.data, ne.value,
                                   ctypes.byref(ne)))
     return list(zip(kinds.tolist(), peers.tolist())), [tuple(e) for e in edges.tolist()]
+
+
+def dspmv_schedule_moves(prefix, n_streams: int, offsets=()) -> np.ndarray:
+    """Legal next ops after a schedule prefix with orderable syncs (R-N5)."""
+    offs = np.ascontiguousarray(list(offsets), np.int32)
+    a = _ops_array(prefix) if len(prefix) else np.zeros((0, 4), np.int32)
+    out = np.zeros((4 * DSPMV_MAX_OPS, 4), np.int32)
+    n = _I()
+    _check(lib.dspmv_schedule_moves(offs.ctypes.data if len(offs) else None, len(offs),
+                                    a.ctypes.data if len(a) else None, len(a), n_streams, out.ctypes.data,
+                                    len(out), ctypes.byref(n)))
+    return out[:n.value].copy()
 
 
 def vertex_label(kind: int, peer: int = 0) -> str:

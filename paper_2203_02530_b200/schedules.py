@@ -143,6 +143,25 @@ def enumerate_derived(n_streams: int = 2, space: Space = COARSE):
     return list(seen.values())
 
 
+def enumerate_orderable(n_streams: int = 2, space: Space = COARSE):
+    """Every distinct schedule when synchronisation operations are moves of
+    their own (DESIGN.md R-N5; ``dspmv_schedule_moves``), as
+    canonical ops arrays.  Coarse DAG, two streams: 4,780 schedules."""
+    seen = {}
+
+    def dfs(prefix):
+        if prefix and prefix[-1][0] == D.DSPMV_OP_END:
+            key = canonical_key(prefix)
+            if key not in seen:
+                seen[key] = canonical_ops(prefix)
+            return
+        for m in D.dspmv_schedule_moves(prefix, n_streams, space.offsets).tolist():
+            dfs(prefix + [tuple(m)])
+
+    dfs([])
+    return list(seen.values())
+
+
 def describe(ops) -> str:
     """Compact one-line description: vertices in order with streams."""
     parts = []

@@ -361,3 +361,35 @@ def test_library_dag_equals_oracle_dag(offsets):
     assert {(names[u], names[v]) for u, v, dead in edges if dead} == set(Dl)
     for v in V:
         assert [a for a, b in got if b == v] == S.preds(v, E)
+
+
+def test_orderable_moves_and_space_match_oracle():
+    """dspmv_schedule_moves (vector clocks) offers exactly the oracle's
+    orderable_moves (happens-before graph) along every prefix, and the two
+    enumerations give the same 4,780 schedules (R-N5)."""
+    from paper_2203_02530_b200 import schedules as PS
+    lib_space = PS.enumerate_orderable(2)
+    assert len(lib_space) == 4780
+    ora = S.enumerate_orderable(2)
+    assert {PS.canonical_key(o) for o in lib_space} == {PS.canonical_key(to_lib(o)) for o in ora}
+    rng = random.Random(1)
+    for o in rng.sample(ora, 200):
+        for t in range(len(o)):
+            want = {tuple(m) for m in to_lib(S.orderable_moves(o[:t], 2))}
+            got = {tuple(m) for m in D.dspmv_schedule_moves(to_lib(o[:t]), 2).tolist()}
+            assert got == want, (o[:t], got, want)
+        D.dspmv_schedule_validate(to_lib(o), 2)
+
+
+def test_orderable_moves_per_destination_match_oracle():
+    V, E, _ = S.fine_dag([-1, 1])
+    rng = random.Random(4)
+    for _ in range(40):
+        ops = []
+        while not ops or ops[-1][0] != "end":
+            want = S.orderable_moves(ops, 2, E, V)
+            got = {tuple(m) for m in D.dspmv_schedule_moves(to_lib(ops), 2, [-1, 1]).tolist()}
+            assert got == {tuple(m) for m in to_lib(want)}, ops
+            ops = ops + [rng.choice(want)]
+        assert S.validate(ops, 2) == (True, "", "")
+        D.dspmv_schedule_validate(to_lib(ops), 2)
