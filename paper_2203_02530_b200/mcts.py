@@ -27,7 +27,10 @@ Phases (SPEC.md S:204-304 semantics):
 
 The tree walks any ``schedules.Space``: the coarse DAG (default) or the
 per-destination DAG of a set of peer offsets, whose traversal
-space is too large to enumerate.
+space is too large to enumerate.  ``syncs="orderable"`` makes the
+synchronisation operations tree moves of their own (DESIGN.md
+R-N5: ``dspmv_schedule_moves``) instead of deriving them when a traversal is
+complete.
 """
 from __future__ import annotations
 
@@ -62,11 +65,10 @@ def exploit_value(child, parent) -> float:
 
 
 class Node:
-    __slots__ = ("vertex", "stream", "parent", "children", "n", "t_min", "t_max",
-                 "fully_explored", "depth")
+    __slots__ = ("move", "parent", "children", "n", "t_min", "t_max", "fully_explored", "depth")
 
-    def __init__(self, vertex, stream, parent):
-        self.vertex, self.stream, self.parent = vertex, stream, parent
+    def __init__(self, move, parent):
+        self.move, self.parent = move, parent
         self.children = None            # materialised lazily
         self.n = 0
         self.t_min = math.inf
@@ -76,8 +78,8 @@ class Node:
 
     def prefix(self):
         out, nd = [], self
-        while nd is not None and nd.vertex is not None:
-            out.append((nd.vertex, nd.stream))
+        while nd is not None and nd.move is not None:
+            out.append(nd.move)
             nd = nd.parent
         return out[::-1]
 
@@ -108,19 +110,35 @@ def ops_of(prefix, n_streams: int, space: Space = COARSE) -> np.ndarray:
 class MCTS:
     """measure(ops) -> seconds benchmarks one complete schedule."""
 
-    def __init__(self, measure, n_streams: int = 2, seed: int = 2203, space: Space = COARSE):
+    def __init__(self, measure, n_streams: int = 2, seed: int = 2203, space: Space = COARSE,
+                 syncs: str = "derived"):
+        if syncs not in ("derived", "orderable"):
+            raise ValueError("syncs must be 'derived' or 'orderable'")
         self.measure = measure
         self.n_streams = n_streams
         self.space = space
+        self.syncs = syncs
         self.rng = random.Random(seed)
-        self.root = Node(None, None, None)
+        self.root = Node(None, None)
         self.dataset = {}               # canonical key -> {"ops", "times"}
         self.iterations = 0
 
     # -- tree helpers
+    def moves(self, prefix):
+        if self.syncs == "derived":
+            return legal_moves(prefix, self.n_streams, self.space)
+        if prefix and prefix[-1][0] == D.DSPMV_OP_END:
+            return []
+        return [tuple(m) for m in D.dspmv_schedule_moves(prefix, self.n_streams, self.space.offsets).tolist()]
+
+    def ops(self, prefix) -> np.ndarray:
+        if self.syncs == "derived":
+            return ops_of(prefix, self.n_streams, self.space)
+        return np.array(prefix, np.int32)
+
     def _materialise(self, node):
         if node.children is None:
-            node.children = [Node(v, s, node) for v, s in legal_moves(node.prefix(), self.n_streams, self.space)]
+            node.children = [Node(m, node) for m in self.moves(node.prefix())]
         return node.children
 
     def select(self):
@@ -155,7 +173,7 @@ class MCTS:
                 break
             path_end = self.rng.choice(kids)
         prefix = path_end.prefix()
-        ops = ops_of(prefix, self.n_streams, self.space)
+        ops = self.ops(prefix)
         t = float(self.measure(ops))
         rec = self.dataset.setdefault(canonical_key(ops), {"ops": ops, "times": []})
         rec["times"].append(t)

@@ -98,9 +98,10 @@ def _space(ops) -> Space:
 
 def op_names(ops) -> list:
     """Names of every op: vertices by name (per-destination ones as
-    "Pack[+1]"), syncs as CER-after-u / CES-b4-v / CSWE-b4-v (u = first DAG
-    predecessor of the consumer v on the recorded stream, edge order; a second
-    wait before the same v gets ':u')."""
+    "Pack[+1]"), syncs as CER-after-u / CES-b4-v / CSWE-b4-v (P:607; v = the
+    vertex after the wait, u = the latest DAG predecessor of v on the recorded
+    stream, else its latest GPU vertex; a second wait before the same v gets
+    ':u')."""
     ops = np.asarray(ops).tolist()
     sp = _space(ops)
     names = [None] * len(ops)
@@ -109,18 +110,27 @@ def op_names(ops) -> list:
         if k < 10:
             names[t] = sp.names[sp.index[(k, p)]]
             where[sp.index[(k, p)]] = (t, s)
+    def next_vertex(t0):
+        kv, pv = next((kk, pp) for kk, _, _, pp in ops[t0 + 1:] if kk < 10)
+        return sp.index[(kv, pv)]
+
     for t, (k, s, e, _) in enumerate(ops):
         if k != D.DSPMV_OP_EVENT_RECORD:
             continue
-        kv, pv = next((kk, pp) for kk, _, _, pp in ops[t + 1:] if kk < 10)
-        v = sp.index[(kv, pv)]
-        u = next((uu for (uu, vv) in sp.edges if vv == v and uu in sp.gpu and where[uu][1] == s
-                  and where[uu][0] < t), None)
+        waits = [tt for tt in range(t + 1, len(ops)) if ops[tt][0] in (11, 12) and ops[tt][2] == e]
+        # the event is named after the latest DAG predecessor, on its stream,
+        # of the vertex its first wait guards (with derived syncs the CER
+        # directly precedes that wait; with orderable syncs (R-N5) it may come
+        # earlier), else after the latest GPU vertex on its stream
+        v = next_vertex(waits[0]) if waits else next_vertex(t)
+        on_s = [i for i in sp.gpu if i in where and where[i][1] == s and where[i][0] < t]
+        preds_v = [i for i in on_s if (i, v) in sp.edges]
+        u = max(preds_v or on_s, key=lambda i: where[i][0], default=None)
         uname = sp.names[u] if u is not None else "?"
         names[t] = f"CER-after-{uname}"
-        w = next(tt for tt in range(t + 1, len(ops)) if ops[tt][0] in (11, 12) and ops[tt][2] == e)
-        base = ("CES-b4-" if ops[w][0] == D.DSPMV_OP_EVENT_SYNC else "CSWE-b4-") + sp.names[v]
-        names[w] = base if base not in names else f"{base}:{uname}"
+        for w in waits:
+            base = ("CES-b4-" if ops[w][0] == D.DSPMV_OP_EVENT_SYNC else "CSWE-b4-") + sp.names[next_vertex(w)]
+            names[w] = base if base not in names else f"{base}:{uname}"
     return names
 
 

@@ -195,6 +195,8 @@ def main():
     ap.add_argument("--out", default="gpurun_out/rules.json")
     ap.add_argument("--granularity", default="coarse", choices=["coarse", "fine"])
     ap.add_argument("--budget", type=int, default=800, help="fine: MCTS / random-rollout samples")
+    ap.add_argument("--syncs", default="derived", choices=["derived", "orderable"],
+                    help="orderable: syncs are moves of their own (R-N5; 4,780 coarse schedules)")
     a = ap.parse_args()
     if a.comm is not None:
         return main_distributed(a)
@@ -202,7 +204,7 @@ def main():
         return main_fine(a)
     comms, plans, xs, ys = setup(a.workload, a.ranks)
     measure = make_measure(plans, xs, ys)
-    space = PS.enumerate_derived(2)
+    space = PS.enumerate_orderable(2) if a.syncs == "orderable" else PS.enumerate_derived(2)
     t0 = time.perf_counter()
     times = np.array([measure(o) for o in space])
     sweep_s = time.perf_counter() - t0
@@ -211,7 +213,7 @@ def main():
     clf, mln, hist = R.train_tree(X, labels)
     rs = R.rulesets(clf, cols)
     out = {
-        "workload": a.workload, "ranks": a.ranks, "n_schedules": len(space),
+        "workload": a.workload, "ranks": a.ranks, "syncs": a.syncs, "n_schedules": len(space),
         "sweep_wall_s": round(sweep_s, 2),
         "fastest_us": float(times.min() * 1e6), "slowest_us": float(times.max() * 1e6),
         "fast_slow_ratio": float(times.max() / times.min()),
@@ -228,7 +230,7 @@ def main():
     # Table V protocol: MCTS subsets vs the exhaustive space
     acc = {}
     for iters in (50, 100, 200, 400):
-        m = M.MCTS(measure, n_streams=2, seed=2203).run(iters)
+        m = M.MCTS(measure, n_streams=2, seed=2203, syncs=a.syncs).run(iters)
         recs = m.records()
         sub_ops = [o for o, _ in recs]
         sub_t = np.array([t for _, t in recs])

@@ -97,3 +97,13 @@ def test_mcts_on_the_per_destination_space():
     for ops, _ in a.records():
         D.dspmv_schedule_validate(ops, 2)
         assert PS.Space.of_ops(ops).offsets == [-1, 1]
+
+
+def test_mcts_with_orderable_syncs_covers_the_4780_space():
+    """Syncs as tree moves (R-N5): the exhaustive search visits
+    exactly the 4,780 orderable schedules and finds the cost minimum."""
+    m = M.MCTS(cost, n_streams=2, seed=11, syncs="orderable").run(10 ** 6)
+    assert m.root.fully_explored
+    space = PS.enumerate_orderable(2)
+    assert set(m.dataset) == {PS.canonical_key(o) for o in space}
+    assert m.best()[1] == min(cost(o) for o in space)

