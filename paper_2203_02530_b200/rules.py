@@ -13,7 +13,8 @@ P:475-628) -- CPU-side analysis of the sweep / MCTS dataset.
 * ``features``      ordering feature "u before v" for every pair of named
   operations (inserted syncs included, named CER-after-u / CES-b4-v /
   CSWE-b4-v as in P:607), stream feature "u same stream as v" for every pair
-  of GPU vertices; constant columns dropped.
+  of GPU vertices; constant columns dropped.  A pair involving an
+  op that some schedules lack reads "not (u before v)" when 0.
 * ``train_tree``    scikit-learn CART, gini, class_weight=balanced,
   max_depth = max_leaf_nodes - 1, hyper-parameters by Algorithm 1
   (tab:tree-params P:542-555, alg:dt-params P:564-583).
@@ -157,7 +158,17 @@ def features(schedules):
             else:
                 X[i, j] = 1 if (u in stream and v in stream and stream[u] == stream[v]) else 0
     keep = [j for j in range(len(cols)) if X[:, j].min() != X[:, j].max()]
-    return X[:, keep], [cols[j] for j in keep]
+    # an ordering feature between ops that some schedules lack (sync ops) is
+    # 0 both when v comes first and when either is absent: its negation reads
+    # "not (u before v)", marked by the kind "before?"
+    always = set.intersection(*(set(pos) for pos, _ in rows)) if rows else set()
+    out_cols = []
+    for j in keep:
+        kind, u, v = cols[j]
+        if kind == "before" and not (u in always and v in always):
+            kind = "before?"
+        out_cols.append((kind, u, v))
+    return X[:, keep], out_cols
 
 
 # -------------------------------------------------------------------- tree
@@ -192,6 +203,8 @@ def rule_text(col, value: int) -> str:
     kind, u, v = col
     if kind == "before":
         return f"{u} before {v}" if value else f"{v} before {u}"
+    if kind == "before?":
+        return f"{u} before {v}" if value else f"not ({u} before {v})"
     return f"{u} same stream as {v}" if value else f"{u} different stream than {v}"
 
 
