@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--schedule", default="best", choices=["best", "paper1"])
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--space", default="derived", choices=["derived", "orderable"],
+                    help="sweep space: derived syncs (768 schedules) or orderable syncs "
+                         "(4,780, DESIGN.md R-N5)")
     ap.add_argument("--no-sweep", action="store_true",
                     help="skip the schedule sweep (use the class-1 'best' schedule)")
     ap.add_argument("--caller-stream0", type=int, default=1,
@@ -303,7 +306,7 @@ def run_ours(a):
     sweep = None
     if not a.no_sweep:
         sweep = schedule_sweep(D, plan, x, y, stream, world, rank, dist if world > 1 else None,
-                               barrier)
+                               barrier, space=a.space)
         ops = sweep.pop("_best_ops")
         ranked = sweep.pop("_ranked_ops")
         sched_desc = "fastest of sweep: " + sweep["fastest"]
@@ -581,8 +584,9 @@ def choose_exchange(D, mk, n, lo, hi, npdt, world, dist):
     return plans[best], label, {"us_per_apply_class1_schedule": note, "chosen": best}
 
 
-def schedule_sweep(D, plan, x, y, stream, world, rank, dist, barrier, t_measure=0.01):
-    """Every derived schedule of the DAG (768 under DESIGN.md R-Q13), measured
+def schedule_sweep(D, plan, x, y, stream, world, rank, dist, barrier, t_measure=0.01, space="derived"):
+    """Every schedule of the DAG (768 with derived syncs under DESIGN.md R-Q13,
+    4,780 with orderable syncs, R-N5), measured
     with the paper's protocol: repeat samples until t_measure =
     0.01 s, time = max over ranks of t_measure / n_samples.  Rank 0 calibrates
     n_samples and broadcasts it so every rank runs the same number of NCCL
@@ -591,7 +595,7 @@ def schedule_sweep(D, plan, x, y, stream, world, rank, dist, barrier, t_measure=
 
     import torch
     from paper_2203_02530_b200 import schedules as PS
-    all_ops = PS.enumerate_derived(2)
+    all_ops = PS.enumerate_orderable(2) if space == "orderable" else PS.enumerate_derived(2)
     times = []
     t_start = time.perf_counter()
     for ops in all_ops:
@@ -621,7 +625,8 @@ def schedule_sweep(D, plan, x, y, stream, world, rank, dist, barrier, t_measure=
     ib, iw = int(times.argmin()), int(times.argmax())
     q = np.percentile(times, [10, 50, 90])
     return {
-        "n_schedules": len(all_ops), "protocol": "P:461-464, t_measure 0.01 s, max over ranks",
+        "n_schedules": len(all_ops), "space": space,
+        "protocol": "P:461-464, t_measure 0.01 s, max over ranks",
         "fastest_ms": round(times[ib] * 1e3, 5), "slowest_ms": round(times[iw] * 1e3, 5),
         "p10_p50_p90_ms": [round(v * 1e3, 5) for v in q],
         "fast_slow_ratio": round(times[iw] / times[ib], 4),
