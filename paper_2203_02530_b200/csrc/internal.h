@@ -23,22 +23,24 @@ dspmv_status fail(dspmv_status st, const std::string& msg);
 struct BlockCfg {
     int tile, rowmax, warps, stages, min_ctas;  // min_ctas: __launch_bounds__ occupancy
     int chunk;                                  // x gathers in flight per lane (one lane per row)
+    int lane_max;                               // rows with <= lane_max nnz: one lane per row
 };
 constexpr BlockCfg kBlockCfgs[] = {
-    // tile  rowmax warps stages min_ctas chunk  (rowmax = 32 x warps: one row per lane)
-    {2048, 256, 8, 2, 4, 8},    // 0  fp32 short rows
-    {1024, 128, 4, 2, 6, 8},    // 1
-    {2048, 256, 8, 3, 2, 8},    // 2
-    {1024, 128, 4, 3, 5, 8},    // 3  fp64 short / irregular rows (default)
-    {768, 96, 3, 3, 7, 8},      // 4
-    {2048, 64, 2, 3, 3, 32},    // 5  long rows: 2 warps, 3 stages, 3 CTAs/SM
-    {4096, 128, 4, 2, 2, 32},   // 6  long uniform rows, one lane per row
-    {3072, 96, 3, 2, 3, 32},    // 7  long rows: 3 warps, 3 CTAs/SM
+    // tile  rowmax warps stages min_ctas chunk lane_max  (rowmax = 32 x warps: one row per lane)
+    {2048, 256, 8, 2, 4, 8, 8},     // 0  fp32 short rows
+    {1024, 128, 4, 2, 6, 8, 8},     // 1
+    {2048, 256, 8, 3, 2, 8, 8},     // 2
+    {1024, 128, 4, 3, 5, 8, 8},     // 3  fp64 short / irregular rows (default)
+    {768, 96, 3, 3, 7, 8, 8},       // 4
+    {4096, 256, 8, 2, 2, 16, 32},   // 5  long uniform rows: 8 warps, one lane per row up to 32 nnz
+    {4096, 128, 4, 2, 2, 32, 32},   // 6  long rows, 4 warps, 32 gathers in flight
+    {3072, 96, 3, 2, 3, 32, 32},    // 7  long rows: 3 warps, 3 CTAs/SM
 };
 constexpr int kNumBlockCfgs = sizeof(kBlockCfgs) / sizeof(kBlockCfgs[0]);
 constexpr int kDefaultBlockCfg = 3;   // short rows (one lane per row)
 constexpr int kShortRowBlockCfgF32 = 0;  // fp32 short rows: bigger blocks (measured 85 % vs 77 %)
-constexpr int kLongRowBlockCfg = 6;   // long, uniform rows: one lane per row, 32 gathers in flight
+constexpr int kLongRowBlockCfgF64 = 5;  // long, uniform rows, fp64: 8 warps, one lane per row (C3 91.6 % vs 86 %)
+constexpr int kLongRowBlockCfg = 6;     // long, uniform rows, fp32: 4 warps, 32 gathers in flight (89 % vs 79 %)
 constexpr int kAutoReserveSms = 8;    // SMs left to NCCL/pack when nranks > 1 (free on B200: y_L
                                       // time unchanged with 148-16 SMs)
 constexpr int kTileMin = 1024;        // smallest tile among the auto-chosen configs

@@ -148,7 +148,7 @@ int auto_block_cfg(const int32_t* rowptr, int32_t nrows, int vthr, int esize) {
     }
     if (rows == 0) return kDefaultBlockCfg;
     const double avg = double(nnz) / double(rows);
-    if (2 * nnz_short < nnz && avg >= 20.0) return kLongRowBlockCfg;
+    if (2 * nnz_short < nnz && avg >= 20.0) return esize == 8 ? kLongRowBlockCfgF64 : kLongRowBlockCfg;
     return esize == 4 ? kShortRowBlockCfgF32 : kDefaultBlockCfg;
 }
 
@@ -166,12 +166,12 @@ void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, cons
     // class c = log2(lanes per row), the smallest c with len <= 8 * 2^c.  Within
     // windows of kBinWindow S rows the rows are stable-partitioned by class, so
     // a block never mixes classes and y writes stay local to the window.
-    // one-lane configurations (chunk >= 16) keep rows up to `chunk` nnz in class 0
+    // rows up to the configuration's lane_max nnz stay in class 0 (one lane per row)
     static const int max_class_env = [] {
         const char* v = std::getenv("DSPMV_MAX_CLASS");
         return v ? std::atoi(v) : kMaxClass;
     }();
-    const int one_lane_len = std::max(8, cfg.chunk);
+    const int one_lane_len = cfg.lane_max;
     auto row_class = [&](int32_t i) {
         const int32_t len = rowptr[i + 1] - rowptr[i];
         if (len <= one_lane_len) return 0;

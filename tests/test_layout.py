@@ -7,14 +7,14 @@ import pytest
 import gen
 from paper_2203_02530_b200 import dspmv as D
 
-TILE = {0: 2048, 1: 1024, 2: 2048, 3: 1024, 4: 768, 5: 2048, 6: 4096, 7: 3072}
-ROWMAX = {0: 256, 1: 128, 2: 256, 3: 128, 4: 96, 5: 64, 6: 128, 7: 96}
-WARPS = {0: 8, 1: 4, 2: 8, 3: 4, 4: 3, 5: 2, 6: 4, 7: 3}
-CHUNK = {0: 8, 1: 8, 2: 8, 3: 8, 4: 8, 5: 32, 6: 32, 7: 32}
+TILE = {0: 2048, 1: 1024, 2: 2048, 3: 1024, 4: 768, 5: 4096, 6: 4096, 7: 3072}
+ROWMAX = {0: 256, 1: 128, 2: 256, 3: 128, 4: 96, 5: 256, 6: 128, 7: 96}
+WARPS = {0: 8, 1: 4, 2: 8, 3: 4, 4: 3, 5: 8, 6: 4, 7: 3}
+LANE_MAX = {0: 8, 1: 8, 2: 8, 3: 8, 4: 8, 5: 32, 6: 32, 7: 32}
 
 
 def _cls(length, cfg):
-    if length <= max(8, CHUNK[cfg]):
+    if length <= LANE_MAX[cfg]:
         return 0
     c = 0
     while c < 5 and length > (8 << c):
@@ -75,6 +75,7 @@ def test_layout_invariants(mat, cfg, vthr):
 
 def test_auto_config_choice():
     assert D.dspmv_layout_host(gen.stencil("7pt", (16, 16, 16))[0])[3] == 3
-    assert D.dspmv_layout_host(gen.stencil("27pt", (16, 16, 16))[0])[3] == 6
+    assert D.dspmv_layout_host(gen.stencil("27pt", (16, 16, 16))[0])[3] == 5
+    assert D.dspmv_layout_host(gen.stencil("27pt", (16, 16, 16))[0], dtype=D.DSPMV_F32)[3] == 6
     assert D.dspmv_layout_host(gen.powerlaw(20000)[0])[3] == 3
     assert D.dspmv_layout_host(gen.stencil("7pt", (16, 16, 16))[0], dtype=D.DSPMV_F32)[3] == 0
