@@ -34,6 +34,13 @@ $(BUILD)/kernels_prof.o: $(SRC)/kernels.cu $(SRC)/runtime.h $(SRC)/internal.h in
 $(OUT)/libdspmv_prof.so: $(BUILD)/kernels_prof.o $(BUILD)/api.o $(BUILD)/planner.o $(BUILD)/schedule.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -L$(NCCL_HOME)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_HOME)/lib
 
+# diagnostic variants of the gather (DIAG=1: none, DIAG=2: row-local), never the product
+$(BUILD)/kernels_diag$(DIAG).o: $(SRC)/kernels.cu $(SRC)/runtime.h $(SRC)/internal.h include/dspmv.h | $(BUILD)
+	$(NVCC) $(NVFLAGS) -DDSPMV_DIAG_GATHER=$(DIAG) -c $< -o $@ 2> /dev/null
+
+$(OUT)/libdspmv_diag$(DIAG).so: $(BUILD)/kernels_diag$(DIAG).o $(BUILD)/api.o $(BUILD)/planner.o $(BUILD)/schedule.o
+	$(NVCC) $(ARCH) -shared -o $@ $^ -L$(NCCL_HOME)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_HOME)/lib
+
 ifeq ($(PROFILE),1)
 all: $(OUT)/libdspmv_prof.so
 endif

@@ -225,7 +225,15 @@ __device__ __forceinline__ void block_rows(const St& S, int lgL_rt, int w0, int 
                 T xv[CH];
 #pragma unroll
                 for (int k = 0; k < CH; ++k)
-                    if (q + k * L < e1) xv[k] = ldg_x<kNoL1>(x + S.col[q + k * L], xpol);
+                    if (q + k * L < e1) {
+#ifdef DSPMV_DIAG_GATHER
+                        // diagnostic builds: 1 = no gather (x value = column id), 2 = local gather x[row]
+                        if (DSPMV_DIAG_GATHER == 1) xv[k] = T(S.col[q + k * L]);
+                        else xv[k] = ldg_x<kNoL1>(x + (r & 0xfffff), xpol);
+#else
+                        xv[k] = ldg_x<kNoL1>(x + S.col[q + k * L], xpol);
+#endif
+                    }
 #pragma unroll
                 for (int k = 0; k < CH; ++k)
                     if (q + k * L < e1) acc = add_rn(acc, mul_rn(S.val[q + k * L], xv[k]));
