@@ -625,6 +625,13 @@ dspmv_status begin_apply(Schedule& s, cudaStream_t caller) {
     if (cudaGetDevice(&cur) != cudaSuccess || cur != p.device) CUDA_TRY(cudaSetDevice(p.device));
     if (!s.compiled) ST_TRY(compile_exchange(s));
     if (s.step0) CUDA_TRY(cudaEventRecord(s.step0, caller));
+    // timestamp aliasing (runtime.h): nothing on the caller stream yet; END is
+    // recorded after the host's last wait, so it is never aliased here
+    s.origin = caller;
+    s.origin_dirty = p.streaming || !s.step0;
+    s.origin_tail = -1;
+    s.end_alias = -1;
+    std::fill(s.t0_alias.begin(), s.t0_alias.end(), 0);
     ++p.epoch;
     CUDA_TRY(cudaEventRecord(p.ev_start, caller));
     // schedule stream 0 may be the caller's stream itself (no cross-stream
@@ -722,8 +729,12 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
     const bool on_stream = gpu || o.kind == DSPMV_OP_EVENT_RECORD || o.kind == DSPMV_OP_STREAM_WAIT_EVENT;
     cudaStream_t st = on_stream ? (o.stream == 0 ? p.cur_stream0 : p.streams[o.stream]) : nullptr;
     const bool timed = gpu && s.timing && s.t0[t];
-    if (timed) CUDA_TRY(cudaEventRecord(s.t0[t], st));
+    if (timed) {
+        if (st == s.origin && !s.origin_dirty) s.t0_alias[t] = 1;  // same position as START
+        else CUDA_TRY(cudaEventRecord(s.t0[t], st));
+    }
     const bool timed_x = !gpu && s.timing && s.t0[t];  // a Post: time the exchange it issues
+    const uint64_t launches0 = g_launches.load(std::memory_order_relaxed);
     cudaError_t e = cudaSuccess;
     switch (o.kind) {
         case DSPMV_OP_START:
@@ -767,13 +778,17 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
             break;
         case DSPMV_OP_EVENT_SYNC:
             e = host_wait(s.ev[o.event]);
+            s.origin_dirty = true;  // later work is enqueued after a host wait
             break;
         case DSPMV_OP_STREAM_WAIT_EVENT:
             e = cudaStreamWaitEvent(st, s.ev[o.event], 0);
+            if (st == s.origin) s.origin_dirty = true;
             break;
         default:
             return fail(DSPMV_ERR_SCHEDULE, "bad op");
     }
+    if (o.kind == DSPMV_OP_WAIT_SEND || o.kind == DSPMV_OP_WAIT_RECV) s.origin_dirty = true;
+    if (st == s.origin && g_launches.load(std::memory_order_relaxed) != launches0) s.origin_dirty = true;
     if (e != cudaSuccess) {
         p.poisoned = true;
         const char* sync_names[] = {"CER", "CES", "CSWE"};
@@ -781,7 +796,10 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
                                                      : std::string(sync_names[(o.kind - DSPMV_OP_EVENT_RECORD) % 3]);
         return fail(DSPMV_ERR_CUDA, "op " + std::to_string(t) + " (" + nm + "): " + cudaGetErrorString(e));
     }
-    if (timed) CUDA_TRY(cudaEventRecord(s.t1[t], st));
+    if (timed) {
+        CUDA_TRY(cudaEventRecord(s.t1[t], st));
+        if (st == s.origin) s.origin_dirty = true;
+    }
     return DSPMV_OK;
 }
 
@@ -825,12 +843,24 @@ dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t ori
     } while (0)
     if (s.step0) CAP_TRY(cudaEventRecordWithFlags(s.step0, origin, cudaEventRecordExternal));
     CAP_TRY(cudaEventRecord(s.gev[0], origin));
+    // timestamp aliasing (runtime.h): track what lands on the origin stream
+    bool odirty = !s.step0, others = false;
+    int otail = -1;
+    std::vector<char> a0(s.ops.size(), 0);
+    for (int& v : s.ev_on) v = 0;
+    // an event recorded on another stream before any node landed there marks
+    // the fork point: waiting on it moves nothing
+    bool ev_trivial[DSPMV_MAX_EVENTS] = {};
     for (cudaStream_t q : all)
         if (!is_origin(q)) CAP_TRY(cudaStreamWaitEvent(q, s.gev[0], 0));
-    auto all_wait = [&](cudaEvent_t ev) -> cudaError_t {
+    // every stream waits on ev; the stream ev was recorded on (from, if
+    // known) needs no wait on itself
+    auto all_wait = [&](cudaEvent_t ev, cudaStream_t from, bool trivial) -> cudaError_t {
         for (cudaStream_t q : all) {
+            if (q == from) continue;
             cudaError_t e = cudaStreamWaitEvent(q, ev, 0);
             if (e != cudaSuccess) return e;
+            if (is_origin(q) && !trivial) odirty = true, otail = -1;
         }
         return cudaSuccess;
     };
@@ -841,14 +871,24 @@ dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t ori
         cudaStream_t q = (gpu || o.kind == DSPMV_OP_EVENT_RECORD || o.kind == DSPMV_OP_STREAM_WAIT_EVENT)
                              ? st[o.stream] : nullptr;
         const bool timed = gpu && s.timing && s.t0[t];
-        if (timed) CAP_TRY(cudaEventRecordWithFlags(s.t0[t], q, cudaEventRecordExternal));
+        if (timed) {
+            if (is_origin(q) && !odirty) a0[t] = 1;  // same position as START
+            else CAP_TRY(cudaEventRecordWithFlags(s.t0[t], q, cudaEventRecordExternal));
+            if (!is_origin(q)) others = true;
+        }
         switch (o.kind) {
             case DSPMV_OP_PACK:
             case DSPMV_OP_SPMV_LOCAL:
             case DSPMV_OP_UNPACK:
-            case DSPMV_OP_SPMV_REMOTE:
+            case DSPMV_OP_SPMV_REMOTE: {
+                const uint64_t l0 = g_launches.load();
                 CAP_TRY(launch_gpu_vertex(s, t, x, y, q));
+                if (g_launches.load() != l0) {
+                    if (is_origin(q)) odirty = true, otail = -1;
+                    else others = true;
+                }
                 break;
+            }
             case DSPMV_OP_POST_SEND:
             case DSPMV_OP_POST_RECV: {
                 ExGroup& g = s.groups[s.op_group[t]];
@@ -861,28 +901,42 @@ dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t ori
                     if (r != DSPMV_OK) return abort_capture(r);
                 }
                 if (tx) CAP_TRY(cudaEventRecordWithFlags(s.t1[t], xs, cudaEventRecordExternal));
+                if (tx || p.has_peers) {
+                    if (is_origin(xs)) odirty = true, otail = -1;
+                    else others = true;
+                }
                 break;
             }
             case DSPMV_OP_WAIT_SEND:
             case DSPMV_OP_WAIT_RECV: {
                 const ExGroup& g = s.groups[s.op_group[t]];
-                if (!g.empty()) CAP_TRY(all_wait(g.ev));
+                if (!g.empty()) CAP_TRY(all_wait(g.ev, nullptr, false));
                 break;
             }
             case DSPMV_OP_EVENT_RECORD:
                 CAP_TRY(cudaEventRecord(s.ev[o.event], q));
+                s.ev_on[o.event] = o.stream + 1;
+                ev_trivial[o.event] = !is_origin(q) && !others;
                 break;
             case DSPMV_OP_EVENT_SYNC:
-                CAP_TRY(all_wait(s.ev[o.event]));
+                CAP_TRY(all_wait(s.ev[o.event], s.ev_on[o.event] ? st[s.ev_on[o.event] - 1] : nullptr,
+                                 ev_trivial[o.event]));
                 break;
             case DSPMV_OP_STREAM_WAIT_EVENT:
                 CAP_TRY(cudaStreamWaitEvent(q, s.ev[o.event], 0));
+                if (is_origin(q) && !ev_trivial[o.event]) odirty = true, otail = -1;
                 break;
             default:
                 break;
         }
-        if (timed) CAP_TRY(cudaEventRecordWithFlags(s.t1[t], q, cudaEventRecordExternal));
+        if (timed) {
+            CAP_TRY(cudaEventRecordWithFlags(s.t1[t], q, cudaEventRecordExternal));
+            if (is_origin(q)) odirty = true, otail = t;
+        }
     }
+    // END directly behind an op's end event on origin, with no node on any
+    // other stream: that event is END (no second record)
+    const int ealias = (s.step1 && otail >= 0 && !others) ? otail : -1;
     // join every stream back into the origin
     int k = 1;
     for (cudaStream_t q : all) {
@@ -891,7 +945,7 @@ dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t ori
         CAP_TRY(cudaStreamWaitEvent(origin, s.gev[k], 0));
         ++k;
     }
-    if (s.step1) CAP_TRY(cudaEventRecordWithFlags(s.step1, origin, cudaEventRecordExternal));
+    if (s.step1 && ealias < 0) CAP_TRY(cudaEventRecordWithFlags(s.step1, origin, cudaEventRecordExternal));
 #undef CAP_TRY
     cudaGraph_t g = nullptr;
     CUDA_TRY(cudaStreamEndCapture(origin, &g));
@@ -905,6 +959,10 @@ dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t ori
     s.gx = x;
     s.gy = y;
     s.g_timing = s.timing;
+    if (s.timing) {
+        s.g_t0_alias = a0;
+        s.g_end_alias = ealias;
+    }
     return DSPMV_OK;
 }
 
@@ -1496,6 +1554,9 @@ dspmv_status dspmv_schedule_set_timing(dspmv_schedule_t s, int enable) {
     if (s->timing) {
         s->t0.assign(s->ops.size(), nullptr);
         s->t1.assign(s->ops.size(), nullptr);
+        s->t0_alias.assign(s->ops.size(), 0);
+        s->g_t0_alias.assign(s->ops.size(), 0);
+        s->end_alias = s->g_end_alias = -1;
         // enable == 1: every GPU vertex; otherwise a bit mask (1 << kind)
         const unsigned mask = enable == 1 ? ~0u : unsigned(enable);
         if (mask & 1u) {  // bit of START: whole apply, START..END on the caller stream
@@ -1516,12 +1577,12 @@ dspmv_status dspmv_schedule_set_timing(dspmv_schedule_t s, int enable) {
 dspmv_status dspmv_schedule_op_times(dspmv_schedule_t s, float* ms, int n) {
     if (!s || !ms) return fail(DSPMV_ERR_ARG, "null argument");
     if (!s->timing || !s->timed_valid) return fail(DSPMV_ERR_STATE, "timing not enabled or no apply yet");
-    if (s->step1) CUDA_TRY(cudaEventSynchronize(s->step1));  // recorded at END, may still be queued
+    if (s->step1) CUDA_TRY(cudaEventSynchronize(s->end_event()));  // recorded at END, may still be queued
     for (int t = 0; t < n && t < int(s->ops.size()); ++t) {
         ms[t] = 0.f;
-        if (s->t0[t]) CUDA_TRY(cudaEventElapsedTime(&ms[t], s->t0[t], s->t1[t]));
+        if (s->t0[t]) CUDA_TRY(cudaEventElapsedTime(&ms[t], s->begin_event(t), s->t1[t]));
     }
-    if (s->step0 && n > 0) CUDA_TRY(cudaEventElapsedTime(&ms[0], s->step0, s->step1));
+    if (s->step0 && n > 0) CUDA_TRY(cudaEventElapsedTime(&ms[0], s->step0, s->end_event()));
     return DSPMV_OK;
 }
 
@@ -1529,17 +1590,18 @@ dspmv_status dspmv_schedule_op_timeline(dspmv_schedule_t s, float* begin_ms, flo
     if (!s || !begin_ms || !end_ms) return fail(DSPMV_ERR_ARG, "null argument");
     if (!s->timing || !s->timed_valid || !s->step0)
         return fail(DSPMV_ERR_STATE, "timeline needs timing with the START bit and an apply");
-    CUDA_TRY(cudaEventSynchronize(s->step1));
+    CUDA_TRY(cudaEventSynchronize(s->end_event()));
     for (int t = 0; t < n && t < int(s->ops.size()); ++t) {
         begin_ms[t] = end_ms[t] = -1.f;
         if (s->t0[t]) {
-            CUDA_TRY(cudaEventElapsedTime(&begin_ms[t], s->step0, s->t0[t]));
+            if (s->t0_alias[t]) begin_ms[t] = 0.f;
+            else CUDA_TRY(cudaEventElapsedTime(&begin_ms[t], s->step0, s->t0[t]));
             CUDA_TRY(cudaEventElapsedTime(&end_ms[t], s->step0, s->t1[t]));
         }
     }
     if (n > 0) {
         begin_ms[0] = 0.f;
-        CUDA_TRY(cudaEventElapsedTime(&end_ms[0], s->step0, s->step1));
+        CUDA_TRY(cudaEventElapsedTime(&end_ms[0], s->step0, s->end_event()));
     }
     return DSPMV_OK;
 }
@@ -1581,6 +1643,10 @@ dspmv_status dspmv_apply_graph(dspmv_schedule_t s, const void* x, void* y, dspmv
         return fail(DSPMV_ERR_CUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
     }
     g_launches.fetch_add(s->graph_kernels, std::memory_order_relaxed);
+    if (s->timing) {
+        s->t0_alias = s->g_t0_alias;
+        s->end_alias = s->g_end_alias;
+    }
     s->timed_valid = s->timing;
     return DSPMV_OK;
 }
@@ -1683,7 +1749,10 @@ dspmv_status dspmv_apply_group(const dspmv_schedule_t* scheds, int nranks, const
             return fail(DSPMV_ERR_ARG, "every rank must run the same schedule (P:460)");
         plans[r] = p;
     }
-    for (int r = 0; r < nranks; ++r) ST_TRY(begin_apply(*scheds[r], static_cast<cudaStream_t>(stream)));
+    for (int r = 0; r < nranks; ++r) {
+        ST_TRY(begin_apply(*scheds[r], static_cast<cudaStream_t>(stream)));
+        scheds[r]->origin_dirty = true;  // the ranks share the caller stream: no timestamp aliasing
+    }
     std::vector<Schedule*> ss(scheds, scheds + nranks);
     const int n_ops = int(scheds[0]->ops.size());
     for (int t = 0; t < n_ops; ++t) {

@@ -189,6 +189,23 @@ struct Schedule {
     uint64_t graph_kernels = 0;        // kernel nodes per graph launch (launch counter)
     cudaEvent_t gev[DSPMV_MAX_STREAMS + 2] = {};  // fork / join helpers
     bool timed_valid = false;
+    // Timestamp aliasing.  A timing event recorded right behind another one
+    // on the same stream costs ~2.3 us on B200
+    // (profiles/r1_ubench_graph_events.txt), so an event that would sit at
+    // the same stream position as one already recorded reuses it: an op's
+    // begin event directly after START is START's event (t0_alias), and in a
+    // graph whose other streams carry no nodes, END directly after an op's end
+    // event is that event (end_alias).  Same timestamps, fewer records.
+    std::vector<char> t0_alias, g_t0_alias;   // current apply / captured graph
+    int end_alias = -1, g_end_alias = -1;
+    // enqueue tracking while an apply is issued / captured
+    cudaStream_t origin = nullptr;     // the caller's stream (START / END)
+    bool origin_dirty = true;          // work or a wait on origin since START
+    bool others_dirty = true;          // nodes on any other stream (graph)
+    int origin_tail = -1;              // op whose end event is the last item on origin
+    int ev_on[DSPMV_MAX_EVENTS] = {};  // schedule event -> stream it was recorded on (+1)
+    cudaEvent_t begin_event(int t) const { return t0_alias[t] ? step0 : t0[t]; }
+    cudaEvent_t end_event() const { return end_alias >= 0 ? t1[end_alias] : step1; }
 };
 
 }  // namespace dspmv

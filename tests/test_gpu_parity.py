@@ -453,3 +453,48 @@ def test_apply_graph_equals_host_mode(name):
             D.dspmv_schedule_destroy(s)
         D.dspmv_plan_destroy(plan)
         D.dspmv_comm_destroy(comm)
+
+
+def test_timestamp_aliasing_keeps_times_consistent():
+    """An op-begin event at START's stream position reuses START's event, and
+    in a graph END reuses y_L's end event when nothing follows it (runtime.h,
+    timestamp aliasing): timings stay ordered and y stays bitwise = O1."""
+    n, (rp, col, val) = gen.config_matrix("c2", mz=32)
+    x = gen.x_values((0, n))
+    yref = O1.o1_spmv(rp, col, val, x)
+    comm = D.dspmv_comm_create(D.dspmv_comm_unique_id(), 1, 0, 0)
+    plan = D.dspmv_plan_create(comm, n, rp, col, val, caller_stream0=True)
+    stream = torch.cuda.Stream()
+    order = ["start", "y_L", "Pack", "PostSend", "PostRecv", "WaitRecv", "Unpack", "WaitSend", "y_R", "end"]
+    kinds = [D.VERTEX_NAMES.index(v) for v in order]
+    cases = {"y_L first on the caller stream": [0] * 10,
+             "y_L first on the caller stream, Pack on stream 1": [1 if v == "Pack" else 0 for v in order],
+             "y_L on stream 1": [1 if v == "y_L" else 0 for v in order]}
+    scheds = []
+    try:
+        xd = torch.from_numpy(x).cuda()
+        for name, streams in cases.items():
+            ops = D.dspmv_schedule_derive(kinds, streams, 2)
+            iyl = [i for i, o in enumerate(ops) if o[0] == D.DSPMV_OP_SPMV_LOCAL][0]
+            s = D.dspmv_schedule_create(plan, ops, 2)
+            scheds.append(s)
+            D.dspmv_schedule_set_timing(s, (1 << D.DSPMV_OP_SPMV_LOCAL) | (1 << D.DSPMV_OP_START))
+            for mode, fn in (("host", D.dspmv_apply), ("graph", D.dspmv_apply_graph)):
+                yd = torch.full_like(xd, float("nan"))
+                for _ in range(3):
+                    fn(s, xd, yd, stream)
+                stream.synchronize()
+                assert np.array_equal(yd.cpu().numpy(), yref), (name, mode)
+                t = D.dspmv_schedule_op_times(s)
+                b, e = D.dspmv_schedule_op_timeline(s)
+                assert t[iyl] > 0 and t[0] >= t[iyl] - 1e-6, (name, mode, t[0], t[iyl])
+                assert 0.0 <= b[iyl] <= e[iyl] <= e[0] + 1e-6, (name, mode, b[iyl], e[iyl], e[0])
+                if streams[1] == 0:
+                    assert b[iyl] == 0.0, (name, mode)          # begin aliased to START
+                    if mode == "graph":
+                        assert e[iyl] == e[0], (name, mode)     # END aliased to y_L's end
+    finally:
+        for s in scheds:
+            D.dspmv_schedule_destroy(s)
+        D.dspmv_plan_destroy(plan)
+        D.dspmv_comm_destroy(comm)
