@@ -26,6 +26,8 @@ ORDERS = [
 def _case(name):
     if name == "7pt96":
         return 96 ** 3, gen.stencil("7pt", (96, 96, 96))
+    if name == "7pt97":  # odd n: x bytes not a multiple of 16
+        return 97 ** 3, gen.stencil("7pt", (97, 97, 97))
     if name == "pl400k":
         n = 400000
         return n, gen.powerlaw(n)
@@ -33,7 +35,7 @@ def _case(name):
 
 
 @pytest.mark.parametrize("dtype", [D.DSPMV_F64, D.DSPMV_F32], ids=["f64", "f32"])
-@pytest.mark.parametrize("name", ["7pt96", "pl400k"])
+@pytest.mark.parametrize("name", ["7pt96", "7pt97", "pl400k"])
 def test_apply_host_pipelined_equals_device_apply(name, dtype):
     n, (rp, col, val) = _case(name)
     tdt = torch.float32 if dtype == D.DSPMV_F32 else torch.float64
