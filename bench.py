@@ -511,7 +511,8 @@ def run_ours(a):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": ncu_traffic(a.workload, world),
-                         "kernel": "spmv_block_kernel (y_L, SPMV_LOCAL op)",
+                         "kernel": ("spmv_stream_kernel" if info.get("s_kernel_local") == D.DSPMV_SKERNEL_STREAM
+                                    else "spmv_block_kernel") + " (y_L, SPMV_LOCAL op)",
                          "alg_bytes_per_launch": int(yl_bytes),
                          "avg_launch_ms": round(yl_ms_avg, 6), "max_rank_launch_ms": round(yl_ms_max, 6),
                          "peak_source": peak_src},

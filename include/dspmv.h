@@ -131,10 +131,21 @@ typedef struct {
                                   IPC handles exchanged at plan time for NCCL comms)
                                   and publishes an epoch flag; the exchange waits on the
                                   flags with stream memory operations               */
-    int32_t reserved[3];
+    int32_t s_kernel;          /* kernel of the rows with <= vector_threshold nnz:
+                                  DSPMV_SKERNEL_AUTO (0, default): CSR-stream when the
+                                  row lengths are irregular (coefficient of variation
+                                  > 0.5), else the row-block kernel; a forced block_cfg
+                                  implies the row-block kernel.  DSPMV_SKERNEL_BLOCK:
+                                  TMA-staged row blocks.  DSPMV_SKERNEL_STREAM: a warp
+                                  per row-aligned tile of <= 256 nnz gathers 8 x values
+                                  per lane (coalesced col/val loads), then one lane per
+                                  row sums its products in stored order (bitwise the
+                                  serial CSR loop)                              */
+    int32_t reserved[2];
 } dspmv_plan_opts;
 
 enum { DSPMV_EXCHANGE_COPY = 0, DSPMV_EXCHANGE_PUT = 1 };
+enum { DSPMV_SKERNEL_AUTO = 0, DSPMV_SKERNEL_BLOCK = 1, DSPMV_SKERNEL_STREAM = 2 };
 
 void dspmv_plan_opts_default(dspmv_plan_opts* opts);
 
@@ -166,6 +177,7 @@ typedef struct {
     int32_t grid_local, grid_remote;          /* persistent grid of the block kernel   */
     int32_t rank, nranks, dtype, ready;
     int64_t device_bytes;
+    int32_t s_kernel_local, s_kernel_remote;  /* DSPMV_SKERNEL_BLOCK / _STREAM in use    */
 } dspmv_plan_info;
 dspmv_status dspmv_plan_info_get(dspmv_plan_t plan, dspmv_plan_info* out);
 

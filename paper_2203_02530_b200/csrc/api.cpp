@@ -127,6 +127,13 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
         const int reserve = p.opts.reserve_sms >= 0 ? p.opts.reserve_sms : (p.comm->nranks > 1 ? kAutoReserveSms : 0);
         const int usable = std::max(1, sms - reserve);
         D.grid_s = std::max(1, std::min(L.nb, per_sm * usable));
+        if (L.stream) {
+            D.stream = true;
+            D.ntiles = int32_t(L.s_tiles.size() / 2);
+            ST_TRY(dev_upload(p, &D.s_tiles, L.s_tiles.data(), L.s_tiles.size()));
+            const int tpsm = stream_kernel_ctas_per_sm(p.dtype);
+            D.grid_t = std::max(1, std::min((D.ntiles + kStreamWarps - 1) / kStreamWarps, tpsm * usable));
+        }
     }
     if (L.nV > 0) {
         ST_TRY(dev_upload(p, &D.v_rowptr, L.v_rowptr.data(), L.v_rowptr.size()));
@@ -138,6 +145,15 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
     }
     D.combine = L.s_has_slot || L.v_has_slot;
     return DSPMV_OK;
+}
+
+// S-group kernel of a matrix: forced by opts.s_kernel, else the row-block
+// kernel when a block configuration is forced, else chosen by row lengths.
+bool use_stream(const dspmv_plan_opts& o, const int32_t* rowptr, int32_t nrows, int vthr) {
+    if (o.s_kernel == DSPMV_SKERNEL_STREAM) return true;
+    if (o.s_kernel == DSPMV_SKERNEL_BLOCK || o.block_cfg >= 0) return false;
+    if (const char* ev = std::getenv("DSPMV_SKERNEL")) return std::atoi(ev) == DSPMV_SKERNEL_STREAM;  // sweeps
+    return auto_stream(rowptr, nrows, vthr);
 }
 
 // Streamed host input of dspmv_apply_host (plan time, host only).  x is cut
@@ -687,6 +703,11 @@ cudaError_t launch_gpu_vertex(Schedule& s, int t, const void* x, void* y, cudaSt
             // apply_host pipeline: one launch; the producer warp of each CTA
             // waits for the x chunk flag of a block before staging it
             auto& H = p.pipe;
+            if (p.L.stream) {  // CSR-stream tiles have no per-block x chunk: wait for all of x
+                e = cudaStreamWaitEvent(st, H.ev_x[H.K - 1], 0);
+                if (e == cudaSuccess) e = launch_spmv(p.L, p.dtype, op, st);
+                break;
+            }
             op.xflag = H.d_xflag;
             op.epoch = p.epoch;
             e = launch_spmv_part(p.L, p.dtype, op, st, 0, p.L.nb, false);
@@ -1173,7 +1194,8 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
         Layout L;
         const int c = cfg >= 0 ? cfg : auto_block_cfg(h.al_rowptr.data(), int32_t(h.n_local()), vthr, p->esize);
         build_layout(h.al_rowptr.data(), int32_t(h.n_local()), h.al_col.data(), h.al_val.data(), p->esize, nullptr,
-                     nR > 0 ? slotL.data() : nullptr, vthr, kBlockCfgs[c], L);
+                     nR > 0 ? slotL.data() : nullptr, vthr, kBlockCfgs[c], L,
+                     use_stream(opts, h.al_rowptr.data(), int32_t(h.n_local()), vthr));
         build_host_pipe(*p, L);   // also stores each block's x chunk in desc[15]
         if ((st = upload_layout(*p, L, c, p->L)) != DSPMV_OK) return bail(st);
     }
@@ -1183,7 +1205,7 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
         Layout R;
         const int c = cfg >= 0 ? cfg : auto_block_cfg(h.ar_rowptr.data(), nR, vthr, p->esize);
         build_layout(h.ar_rowptr.data(), nR, h.ar_col.data(), h.ar_val.data(), p->esize, h.ar_rows.data(),
-                     slotR.data(), vthr, kBlockCfgs[c], R);
+                     slotR.data(), vthr, kBlockCfgs[c], R, use_stream(opts, h.ar_rowptr.data(), nR, vthr));
         if ((st = upload_layout(*p, R, c, p->R)) != DSPMV_OK) return bail(st);
     }
     const size_t hsz = h.halo_gid.size();
@@ -1294,6 +1316,8 @@ dspmv_status dspmv_plan_info_get(dspmv_plan_t plan, dspmv_plan_info* out) {
     out->grid_remote = plan->R.grid_s;
     out->ready = plan->ready;
     out->device_bytes = plan->device_bytes;
+    out->s_kernel_local = plan->L.stream ? DSPMV_SKERNEL_STREAM : DSPMV_SKERNEL_BLOCK;
+    out->s_kernel_remote = plan->R.stream ? DSPMV_SKERNEL_STREAM : DSPMV_SKERNEL_BLOCK;
     return DSPMV_OK;
 }
 

@@ -47,6 +47,9 @@ constexpr int kTileMin = 1024;        // smallest tile among the auto-chosen con
 constexpr int kTileMax = 2048;     // vector_threshold upper bound (a row fits a block)
 constexpr int kPad = 8;            // device arrays padded (aligned over-read)
 constexpr int kDescInts = 16;      // per-block descriptor: r0 r1 p0 p1 flag wb[0..warps]
+constexpr int kStreamTile = 256;   // CSR-stream tile: nnz per warp pass (8 per lane)
+constexpr int kStreamRows = 64;    // CSR-stream tile: rows
+constexpr int kStreamWarps = 8;    // CSR-stream CTA: warps (one tile each)
 constexpr int kDefaultVectorThreshold = 256;  // rows above: warp-per-row kernel
 constexpr int kMaxClass = 5;       // row classes: 2^c lanes per row, c = 0..5
 constexpr int kBinWindow = 4096;   // rows are binned by class within such windows
@@ -92,15 +95,24 @@ struct Layout {
     std::vector<int32_t> v_rowptr, v_col, v_out, v_slot;
     std::vector<uint8_t> v_val;
     bool v_has_slot = false;
+    // CSR-stream form of the S group (irregular row lengths): row-aligned
+    // tiles [r0, r1) of <= kStreamTile nnz and <= kStreamRows rows, S rows in
+    // matrix-row order (no class binning)
+    bool stream = false;
+    std::vector<int32_t> s_tiles;      // 2 per tile
 };
 // out_row / slot nullable: identity / no combine.
 // Plan-time choice of the row-block configuration for one matrix: measured
 // on B200 (K1 table), one-lane-per-row matrices (7-pt stencils,
 // power-law) run best with cfg 3, long uniform rows (27-pt) with cfg 0.
 int auto_block_cfg(const int32_t* rowptr, int32_t nrows, int vthr, int esize);
+// Plan-time choice of the S-group kernel: CSR-stream for irregular row
+// lengths (coefficient of variation > 0.5, e.g. the power-law G2), the
+// TMA-staged row-block kernel otherwise (stencils, banded)
+bool auto_stream(const int32_t* rowptr, int32_t nrows, int vthr);
 void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, const uint8_t* val,
                   int esize, const int32_t* out_row, const int32_t* slot, int vthr,
-                  const BlockCfg& cfg, Layout& L);
+                  const BlockCfg& cfg, Layout& L, bool stream = false);
 
 // -------------------------------------------------------------- schedules
 // A DAG vertex instance: kind + peer offset (0 = coarse / not an exchange vertex)

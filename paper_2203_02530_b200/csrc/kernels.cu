@@ -14,6 +14,11 @@
 //                      products and sums rounded separately (the rounding of
 //                      the oracle's O1 loop), then release the slot on its
 //                      "empty" mbarrier.  No CTA-wide barrier in the loop.
+//   spmv_stream_kernel the same rows for irregular matrices (CSR-stream): a
+//                      warp per row-aligned tile of <= 256 nnz loads col/val
+//                      coalesced, keeps 8 x gathers per lane in flight, writes
+//                      the products to shared memory, then one lane per row
+//                      sums them in stored order (bitwise the O1 loop)
 //   spmv_vector_kernel rows with > vector_threshold nnz: one warp per row,
 //                      unrolled coalesced loads, warp-shuffle reduction.
 //   pack_kernel        sendbuf[k] = x[pack_map[k]]
@@ -363,6 +368,66 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
     }
 }
 
+struct StreamArgs {
+    const int32_t* rowptr;
+    const int32_t* col;
+    const void* val;
+    const int32_t* out;
+    const int32_t* slot;
+    const int32_t* tiles;   // [r0, r1) per tile, S-row indices
+    int32_t ntiles;
+};
+
+// CSR-stream (irregular row lengths).  Lane l of a warp takes entries
+// l, l+32, .., l+224 of its tile: every col/val load is one coalesced 128-B
+// (256-B) access and the 8 x gathers of a lane are independent, so they are
+// all in flight at once -- the access order in which the gathers run at the
+// measured random-gather rate (C4).  The products, each rounded,
+// go to shared memory; lane j then sums row j's products in stored order from
+// +0 (the oracle's loop), so y is bitwise O1 on every row.
+template <typename T, bool kCombine, bool kIdentity>
+__global__ void __launch_bounds__(kStreamWarps * 32) spmv_stream_kernel(StreamArgs a, SpmvOperands o) {
+    __shared__ T prod[kStreamWarps][kStreamTile];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const T* __restrict__ val = static_cast<const T*>(a.val);
+    const T* __restrict__ x = static_cast<const T*>(o.x);
+    T* __restrict__ y = static_cast<T*>(o.y);
+    T* pr = prod[w];
+    const uint64_t xpol = policy_evict_last();
+    for (int t = blockIdx.x * kStreamWarps + w; t < a.ntiles; t += gridDim.x * kStreamWarps) {
+        const int2 tr = __ldg(reinterpret_cast<const int2*>(a.tiles) + t);
+        const int32_t p0 = __ldg(a.rowptr + tr.x), m = __ldg(a.rowptr + tr.y) - p0;
+        int32_t c[kStreamTile / 32];
+        T v[kStreamTile / 32], xv[kStreamTile / 32];
+#pragma unroll
+        for (int k = 0; k < kStreamTile / 32; ++k) {
+            const int q = lane + 32 * k;
+            c[k] = q < m ? __ldcs(a.col + p0 + q) : 0;
+            v[k] = q < m ? __ldcs(val + p0 + q) : T(0);
+        }
+#pragma unroll
+        for (int k = 0; k < kStreamTile / 32; ++k) xv[k] = lane + 32 * k < m ? ldg_x<true>(x + c[k], xpol) : T(0);
+#pragma unroll
+        for (int k = 0; k < kStreamTile / 32; ++k) pr[lane + 32 * k] = mul_rn(v[k], xv[k]);
+        __syncwarp();
+        for (int32_t r = tr.x + lane; r < tr.y; r += 32) {
+            const int32_t e0 = __ldg(a.rowptr + r) - p0, e1 = __ldg(a.rowptr + r + 1) - p0;
+            T acc = T(0);
+            for (int32_t q = e0; q < e1; ++q) acc = add_rn(acc, pr[q]);
+            const int32_t orow = kIdentity ? r : a.out[r];
+            if (kCombine) {
+                const int32_t k = a.slot[r];
+                if (k >= 0) {
+                    combine<T>(acc, k, orow, o);
+                    continue;
+                }
+            }
+            __stcs(y + orow, acc);
+        }
+        __syncwarp();
+    }
+}
+
 template <typename T, bool kCombine>
 __global__ void __launch_bounds__(kThreads) spmv_vector_kernel(VecArgs a, SpmvOperands o) {
     const int lane = threadIdx.x & 31;
@@ -530,9 +595,27 @@ cudaError_t launch_block_any(const DevLayout& L, const SpmvOperands& o, cudaStre
 static_assert(kNumBlockCfgs == 8, "update launch_block_any / occupancy dispatch");
 
 template <typename T>
+cudaError_t launch_stream(const DevLayout& L, const SpmvOperands& o, cudaStream_t s) {
+    StreamArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_out, L.s_slot, L.s_tiles, L.ntiles};
+    const bool c = L.s_slot != nullptr, id = L.s_out == nullptr;
+    const dim3 grid(L.grid_t), block(kStreamWarps * 32);
+    if (c && id) spmv_stream_kernel<T, true, true><<<grid, block, 0, s>>>(a, o);
+    else if (c) spmv_stream_kernel<T, true, false><<<grid, block, 0, s>>>(a, o);
+    else if (id) spmv_stream_kernel<T, false, true><<<grid, block, 0, s>>>(a, o);
+    else spmv_stream_kernel<T, false, false><<<grid, block, 0, s>>>(a, o);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t launch_all(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, int32_t b0, int32_t b1, bool vec) {
     cudaError_t e = cudaSuccess;
-    if (b1 > b0) {
+    if (L.stream) {  // CSR-stream S group: all tiles in one launch (b0 / b1 ignored)
+        if (b1 > b0 && L.ntiles > 0) {
+            e = launch_stream<T>(L, o, s);
+            if (e != cudaSuccess) return e;
+        }
+    } else if (b1 > b0) {
         e = launch_block_any<T>(L, o, s, b0, b1);
         if (e != cudaSuccess) return e;
     }
@@ -586,6 +669,15 @@ int prof_read(unsigned long long* out, int n, bool reset) {
     (void)out; (void)n; (void)reset;
     return 0;
 #endif
+}
+
+int stream_kernel_ctas_per_sm(int dtype) {
+    int n = 0;
+    if (dtype == DSPMV_F32)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_stream_kernel<float, false, true>, kStreamWarps * 32, 0);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_stream_kernel<double, false, true>, kStreamWarps * 32, 0);
+    return n > 0 ? n : 1;
 }
 
 int block_kernel_ctas_per_sm(int dtype, int cfg) {

@@ -152,11 +152,28 @@ int auto_block_cfg(const int32_t* rowptr, int32_t nrows, int vthr, int esize) {
     return esize == 4 ? kShortRowBlockCfgF32 : kDefaultBlockCfg;
 }
 
+bool auto_stream(const int32_t* rowptr, int32_t nrows, int vthr) {
+    double s1 = 0, s2 = 0;
+    int64_t rows = 0;
+    for (int32_t i = 0; i < nrows; ++i) {
+        const double len = rowptr[i + 1] - rowptr[i];
+        if (len > vthr) continue;
+        s1 += len;
+        s2 += len * len;
+        ++rows;
+    }
+    if (rows < 2 || s1 <= 0) return false;
+    const double mean = s1 / double(rows), var = s2 / double(rows) - mean * mean;
+    return var > 0.25 * mean * mean;   // CV > 0.5
+}
+
 void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, const uint8_t* val,
                   int esize, const int32_t* out_row, const int32_t* slot, int vthr,
-                  const BlockCfg& cfg, Layout& L) {
+                  const BlockCfg& cfg, Layout& L, bool stream) {
     L = Layout();
     L.nrows = nrows;
+    L.stream = stream;
+    if (stream) vthr = std::min(vthr, kStreamTile);   // a CSR-stream tile holds any S row
     std::vector<int32_t> srows, vrows;
     srows.reserve(nrows);
     for (int32_t i = 0; i < nrows; ++i) {
@@ -174,7 +191,7 @@ void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, cons
     const int one_lane_len = cfg.lane_max;
     auto row_class = [&](int32_t i) {
         const int32_t len = rowptr[i + 1] - rowptr[i];
-        if (len <= one_lane_len) return 0;
+        if (stream || len <= one_lane_len) return 0;   // CSR-stream: matrix-row order
         int c = 0;
         while (c < kMaxClass && len > (8 << c)) ++c;
         return std::min(c, max_class_env);
@@ -255,6 +272,18 @@ void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, cons
         L.s_desc.insert(L.s_desc.end(), d, d + kDescInts);
     }
     L.nb = int32_t(L.s_desc.size() / kDescInts);
+    if (stream) {
+        // CSR-stream tiles: greedy runs of rows with <= kStreamTile nnz and
+        // <= kStreamRows rows (every S row has <= vthr <= kStreamTile nnz)
+        L.s_tiles.clear();
+        for (int32_t t0 = 0; t0 < L.nS;) {
+            int32_t t1 = t0;
+            while (t1 < L.nS && t1 - t0 < kStreamRows && L.s_rowptr[t1 + 1] - L.s_rowptr[t0] <= kStreamTile) ++t1;
+            L.s_tiles.push_back(t0);
+            L.s_tiles.push_back(t1);
+            t0 = t1;
+        }
+    }
 }
 
 }  // namespace dspmv

@@ -34,6 +34,11 @@ struct DevLayout {
     void* v_val = nullptr;
     int32_t* v_out = nullptr;
     int32_t* v_slot = nullptr;
+    // CSR-stream S group (Layout::stream): tiles instead of TMA row blocks
+    bool stream = false;
+    int32_t ntiles = 0;
+    int grid_t = 0;
+    int32_t* s_tiles = nullptr;
 };
 
 // Operands of one SpMV op (y_L or y_R) for the kernels.
@@ -52,6 +57,7 @@ struct SpmvOperands {
 // kernels.cu
 int block_kernel_smem_bytes(int dtype, int cfg);
 int block_kernel_ctas_per_sm(int dtype, int cfg);
+int stream_kernel_ctas_per_sm(int dtype);
 cudaError_t launch_spmv(const DevLayout& L, int dtype, const SpmvOperands& o, cudaStream_t s);
 // row blocks [b0, b1) of the S group, plus the V group (long rows) if vec
 cudaError_t launch_spmv_part(const DevLayout& L, int dtype, const SpmvOperands& o, cudaStream_t s, int32_t b0,

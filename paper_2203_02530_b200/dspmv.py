@@ -31,6 +31,7 @@ STATUS_NAMES = ["OK", "ERR_ARG", "ERR_RANGE", "ERR_SCHEDULE", "ERR_DEADLOCK", "E
 DSPMV_F64, DSPMV_F32 = 0, 1
 DSPMV_COMM_NCCL, DSPMV_COMM_LOCAL, DSPMV_COMM_HOST = 0, 1, 2
 DSPMV_EXCHANGE_COPY, DSPMV_EXCHANGE_PUT = 0, 1
+DSPMV_SKERNEL_AUTO, DSPMV_SKERNEL_BLOCK, DSPMV_SKERNEL_STREAM = 0, 1, 2
 (DSPMV_OP_START, DSPMV_OP_PACK, DSPMV_OP_SPMV_LOCAL, DSPMV_OP_POST_SEND, DSPMV_OP_POST_RECV,
  DSPMV_OP_WAIT_SEND, DSPMV_OP_WAIT_RECV, DSPMV_OP_UNPACK, DSPMV_OP_SPMV_REMOTE, DSPMV_OP_END,
  DSPMV_OP_EVENT_RECORD, DSPMV_OP_EVENT_SYNC, DSPMV_OP_STREAM_WAIT_EVENT) = range(13)
@@ -54,7 +55,7 @@ class dspmv_plan_opts(ctypes.Structure):
                 ("keep_host", ctypes.c_int32), ("comm_priority", ctypes.c_int32),
                 ("block_cfg", ctypes.c_int32), ("caller_stream0", ctypes.c_int32),
                 ("reserve_sms", ctypes.c_int32), ("exchange", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 3)]
+                ("s_kernel", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
 
 
 class dspmv_plan_info(ctypes.Structure):
@@ -68,7 +69,8 @@ class dspmv_plan_info(ctypes.Structure):
                 ("grid_local", ctypes.c_int32), ("grid_remote", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
                 ("dtype", ctypes.c_int32), ("ready", ctypes.c_int32),
-                ("device_bytes", ctypes.c_int64)]
+                ("device_bytes", ctypes.c_int64),
+                ("s_kernel_local", ctypes.c_int32), ("s_kernel_remote", ctypes.c_int32)]
 
 
 class dspmv_op(ctypes.Structure):
@@ -232,7 +234,7 @@ def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_
                       vector_threshold: int = -1, keep_host: bool = False,
                       comm_priority: bool = True, block_cfg: int = -1,
                       caller_stream0: bool | None = None, reserve_sms: int | None = None,
-                      exchange: int = DSPMV_EXCHANGE_COPY):
+                      exchange: int = DSPMV_EXCHANGE_COPY, s_kernel: int = DSPMV_SKERNEL_AUTO):
     """rowptr int64[n_local+1], col int32[nnz] (global ids), val float64/32."""
     rowptr = np.ascontiguousarray(rowptr, np.int64)
     col = np.ascontiguousarray(col_global, np.int32)
@@ -249,6 +251,7 @@ def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_
     if reserve_sms is not None:
         o.reserve_sms = int(reserve_sms)
     o.exchange = int(exchange)
+    o.s_kernel = int(s_kernel)
     h = _P()
     _check(lib.dspmv_plan_create(comm, n_global, len(rowptr) - 1, rowptr.ctypes.data,
                                  col.ctypes.data, val.ctypes.data, ctypes.byref(o),

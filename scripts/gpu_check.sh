@@ -12,7 +12,7 @@ timeout 300 python bench.py --impl reference --steps 20 --warmup 2 > $OUT/bench_
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
     python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-sweep > $OUT/ncu_launch_$TAG.log 2>&1; echo "ncu1 exit $?" >> $OUT/ncu_launch_$TAG.log
 for w in c2 c3 c4; do
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmv_block -s 2 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"spmv_(block|stream)" -s 2 -c 1 \
     -o $OUT/prof_${w}_$TAG -f python bench.py --workload $w --steps 2 --warmup 1 --no-cpu-baseline --no-sweep > $OUT/ncu_full_${w}_$TAG.log 2>&1; echo "ncu $w exit $?" >> $OUT/ncu_full_${w}_$TAG.log
 done
 echo done

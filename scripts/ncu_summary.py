@@ -56,7 +56,7 @@ def main():
     json.dump({"report": rep, "kernels": kernels}, open(out, "w"), indent=1)
     print(json.dumps(kernels, indent=1)[:3000])
     if key:
-        yl = [k for k in kernels if "spmv_block_kernel" in k["kernel"]]
+        yl = [k for k in kernels if "spmv_block_kernel" in k["kernel"] or "spmv_stream_kernel" in k["kernel"]]
         if yl:
             tp = "profiles/ncu_traffic.json"
             try:

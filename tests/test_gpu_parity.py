@@ -498,3 +498,55 @@ def test_timestamp_aliasing_keeps_times_consistent():
             D.dspmv_schedule_destroy(s)
         D.dspmv_plan_destroy(plan)
         D.dspmv_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("name", ["pl20k", "rand300", "7pt32", "27pt20"])
+@pytest.mark.parametrize("P", [1, 3])
+def test_stream_kernel_bitwise_vs_oracle(name, P):
+    """CSR-stream S group (DSPMV_SKERNEL_STREAM): every row of <= 256 nnz is
+    summed in stored order by one lane from rounded products, so y equals the
+    oracle's O2 loops bit for bit on every row whose A_L and A_R parts both go
+    to the stream kernel (whole row <= 256 nnz); longer rows (warp-per-row
+    kernel) within the R-Q11 tolerance."""
+    n, (rp, col, val) = _mat(name)
+    x = gen.x_values((0, n))
+    run = LocalRun(n, rp, col, val, P, s_kernel=D.DSPMV_SKERNEL_STREAM)
+    try:
+        y = run.apply(run.schedule(derive_ops()), x, reps=2)
+        assert all(D.dspmv_plan_info_get(p)["s_kernel_local"] == D.DSPMV_SKERNEL_STREAM for p in run.plans)
+    finally:
+        run.close()
+    plans = O2.plan_all(rp, col, n, P)
+    yref = O2.simulate(plans, val, x, [(v,) for v in S.topological_orders(S.EDGES)[0]])
+    short = np.diff(rp) <= 256
+    assert np.array_equal(y[short], yref[short])
+    assert within_tol(y, yref, O1.o1_absdot(rp, col, val, x), 1e-12)
+
+
+def test_stream_kernel_auto_choice_and_fp32():
+    """Auto choice: the power-law matrix (irregular rows) runs the CSR-stream
+    kernel, the 7-pt stencil the row-block kernel; a forced block_cfg keeps
+    the row-block kernel.  fp32 CSR-stream within the R-Q12 tolerance."""
+    comm = D.dspmv_comm_create(D.dspmv_comm_unique_id(), 1, 0, 0)
+    try:
+        for name, want in (("pl20k", D.DSPMV_SKERNEL_STREAM), ("7pt32", D.DSPMV_SKERNEL_BLOCK)):
+            n, (rp, col, val) = _mat(name)
+            plan = D.dspmv_plan_create(comm, n, rp, col, val)
+            assert D.dspmv_plan_info_get(plan)["s_kernel_local"] == want, name
+            D.dspmv_plan_destroy(plan)
+        n, (rp, col, val) = _mat("pl20k")
+        plan = D.dspmv_plan_create(comm, n, rp, col, val, block_cfg=3)
+        assert D.dspmv_plan_info_get(plan)["s_kernel_local"] == D.DSPMV_SKERNEL_BLOCK
+        D.dspmv_plan_destroy(plan)
+    finally:
+        D.dspmv_comm_destroy(comm)
+    n, (rp, col, val) = _mat("pl20k")
+    v32 = val.astype(np.float32)
+    x32 = gen.x_values((0, n)).astype(np.float32)
+    run = LocalRun(n, rp, col, v32, 2, dtype=D.DSPMV_F32, s_kernel=D.DSPMV_SKERNEL_STREAM)
+    try:
+        y = run.apply(run.schedule(derive_ops()), x32)
+    finally:
+        run.close()
+    xr, vr = x32.astype(np.float64), v32.astype(np.float64)
+    assert within_tol(y, O1.o1_spmv(rp, col, vr, xr), O1.o1_absdot(rp, col, vr, xr), 1e-5)
