@@ -131,7 +131,8 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
             D.stream = true;
             D.ntiles = int32_t(L.s_tiles.size() / 2);
             ST_TRY(dev_upload(p, &D.s_tiles, L.s_tiles.data(), L.s_tiles.size()));
-            const int tpsm = stream_kernel_ctas_per_sm(p.dtype);
+            int tpsm = stream_kernel_ctas_per_sm(p.dtype);
+            if (const char* ev = std::getenv("DSPMV_STREAM_CTAS")) tpsm = std::max(1, std::min(tpsm, std::atoi(ev)));  // sweeps
             D.grid_t = std::max(1, std::min((D.ntiles + kStreamWarps - 1) / kStreamWarps, tpsm * usable));
         }
     }
