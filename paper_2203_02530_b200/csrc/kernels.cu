@@ -368,71 +368,10 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
     }
 }
 
-struct StreamArgs {
-    const int32_t* rowptr;
-    const int32_t* col;
-    const void* val;
-    const int32_t* out;
-    const int32_t* slot;
-    const int32_t* tiles;   // [r0, r1) per tile, S-row indices
-    int32_t ntiles;
-};
-
-// CSR-stream (irregular row lengths).  Lane l of a warp takes entries
-// l, l+32, .., l+224 of its tile: every col/val load is one coalesced 128-B
-// (256-B) access and the 8 x gathers of a lane are independent, so they are
-// all in flight at once -- the access order in which the gathers run at the
-// measured random-gather rate (DESIGN.md, C4).  The products, each rounded,
-// go to shared memory; lane j then sums row j's products in stored order from
-// +0 (the oracle's loop, P:273), so y is bitwise O1 on every row.
-template <typename T, bool kCombine, bool kIdentity>
-__global__ void __launch_bounds__(kStreamWarps * 32) spmv_stream_kernel(StreamArgs a, SpmvOperands o) {
-    __shared__ T prod[kStreamWarps][kStreamTile];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const T* __restrict__ val = static_cast<const T*>(a.val);
-    const T* __restrict__ x = static_cast<const T*>(o.x);
-    T* __restrict__ y = static_cast<T*>(o.y);
-    T* pr = prod[w];
-    const uint64_t xpol = policy_evict_last();
-    for (int t = blockIdx.x * kStreamWarps + w; t < a.ntiles; t += gridDim.x * kStreamWarps) {
-        const int2 tr = __ldg(reinterpret_cast<const int2*>(a.tiles) + t);
-        const int32_t p0 = __ldg(a.rowptr + tr.x), m = __ldg(a.rowptr + tr.y) - p0;
-        int32_t c[kStreamTile / 32];
-        T v[kStreamTile / 32], xv[kStreamTile / 32];
-#pragma unroll
-        for (int k = 0; k < kStreamTile / 32; ++k) {
-            const int q = lane + 32 * k;
-            c[k] = q < m ? __ldcs(a.col + p0 + q) : 0;
-            v[k] = q < m ? __ldcs(val + p0 + q) : T(0);
-        }
-#pragma unroll
-        for (int k = 0; k < kStreamTile / 32; ++k) xv[k] = lane + 32 * k < m ? ldg_x<true>(x + c[k], xpol) : T(0);
-#pragma unroll
-        for (int k = 0; k < kStreamTile / 32; ++k) pr[lane + 32 * k] = mul_rn(v[k], xv[k]);
-        __syncwarp();
-        for (int32_t r = tr.x + lane; r < tr.y; r += 32) {
-            const int32_t e0 = __ldg(a.rowptr + r) - p0, e1 = __ldg(a.rowptr + r + 1) - p0;
-            T acc = T(0);
-            for (int32_t q = e0; q < e1; ++q) acc = add_rn(acc, pr[q]);
-            const int32_t orow = kIdentity ? r : a.out[r];
-            if (kCombine) {
-                const int32_t k = a.slot[r];
-                if (k >= 0) {
-                    combine<T>(acc, k, orow, o);
-                    continue;
-                }
-            }
-            __stcs(y + orow, acc);
-        }
-        __syncwarp();
-    }
-}
-
+// Rows > vector_threshold: warp w of nw takes rows w, w + nw, ...
 template <typename T, bool kCombine>
-__global__ void __launch_bounds__(kThreads) spmv_vector_kernel(VecArgs a, SpmvOperands o) {
+__device__ __forceinline__ void vector_rows(const VecArgs& a, const SpmvOperands& o, int w, int nw) {
     const int lane = threadIdx.x & 31;
-    const int w = (blockIdx.x * kThreads + threadIdx.x) >> 5;
-    const int nw = (gridDim.x * kThreads) >> 5;
     const T* __restrict__ val = static_cast<const T*>(a.val);
     const T* __restrict__ x = static_cast<const T*>(o.x);
     const uint64_t xpol = policy_evict_last();
@@ -467,6 +406,80 @@ __global__ void __launch_bounds__(kThreads) spmv_vector_kernel(VecArgs a, SpmvOp
         }
     }
 }
+
+template <typename T, bool kCombine>
+__global__ void __launch_bounds__(kThreads) spmv_vector_kernel(VecArgs a, SpmvOperands o) {
+    vector_rows<T, kCombine>(a, o, (blockIdx.x * kThreads + threadIdx.x) >> 5, (gridDim.x * kThreads) >> 5);
+}
+
+struct StreamArgs {
+    const int32_t* rowptr;
+    const int32_t* col;
+    const void* val;
+    const int32_t* out;
+    const int32_t* slot;
+    const int32_t* tiles;   // [r0, r1) per tile, S-row indices
+    int32_t ntiles;
+    VecArgs v;              // rows > vector_threshold (nV = 0: none / launched apart)
+};
+
+// CSR-stream (irregular row lengths).  Lane l of a warp takes entries
+// l, l+32, .., l+224 of its tile: every col/val load is one coalesced 128-B
+// (256-B) access and the 8 x gathers of a lane are independent, so they are
+// all in flight at once -- the access order in which the gathers run at the
+// measured random-gather rate (DESIGN.md, C4).  The products, each rounded,
+// go to shared memory; lane j then sums row j's products in stored order from
+// +0 (the oracle's loop, P:273), so y is bitwise O1 on every row.
+template <typename T, bool kCombine, bool kIdentity>
+__global__ void __launch_bounds__(kStreamWarps * 32) spmv_stream_kernel(StreamArgs a, SpmvOperands o) {
+    __shared__ T prod[kStreamWarps][kStreamTile];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const T* __restrict__ val = static_cast<const T*>(a.val);
+    const T* __restrict__ x = static_cast<const T*>(o.x);
+    T* __restrict__ y = static_cast<T*>(o.y);
+    T* pr = prod[w];
+    // the long rows (> vector_threshold) first, a warp per row, so they do not
+    // trail the tiles (and need no second launch)
+    if (a.v.nV > 0) {
+        if (a.v.slot) vector_rows<T, true>(a.v, o, blockIdx.x * kStreamWarps + w, gridDim.x * kStreamWarps);
+        else vector_rows<T, false>(a.v, o, blockIdx.x * kStreamWarps + w, gridDim.x * kStreamWarps);
+    }
+    const uint64_t xpol = policy_evict_last();
+    for (int t = blockIdx.x * kStreamWarps + w; t < a.ntiles; t += gridDim.x * kStreamWarps) {
+        const int2 tr = __ldg(reinterpret_cast<const int2*>(a.tiles) + t);
+        const int32_t p0 = __ldg(a.rowptr + tr.x), m = __ldg(a.rowptr + tr.y) - p0;
+        int32_t c[kStreamTile / 32];
+        T v[kStreamTile / 32], xv[kStreamTile / 32];
+#pragma unroll
+        for (int k = 0; k < kStreamTile / 32; ++k) {
+            const int q = lane + 32 * k;
+            c[k] = q < m ? __ldcs(a.col + p0 + q) : 0;
+            v[k] = q < m ? __ldcs(val + p0 + q) : T(0);
+        }
+#pragma unroll
+        for (int k = 0; k < kStreamTile / 32; ++k) xv[k] = lane + 32 * k < m ? ldg_x<true>(x + c[k], xpol) : T(0);
+        __syncwarp();  // keeps ptxas from pairing each gather with its multiply: all 8 stay in flight
+#pragma unroll
+        for (int k = 0; k < kStreamTile / 32; ++k) pr[lane + 32 * k] = mul_rn(v[k], xv[k]);
+        __syncwarp();
+        for (int32_t r = tr.x + lane; r < tr.y; r += 32) {
+            const int32_t e0 = __ldg(a.rowptr + r) - p0, e1 = __ldg(a.rowptr + r + 1) - p0;
+            T acc = T(0);
+            for (int32_t q = e0; q < e1; ++q) acc = add_rn(acc, pr[q]);
+            const int32_t orow = kIdentity ? r : a.out[r];
+            if (kCombine) {
+                const int32_t k = a.slot[r];
+                if (k >= 0) {
+                    combine<T>(acc, k, orow, o);
+                    continue;
+                }
+            }
+            __stcs(y + orow, acc);
+        }
+        __syncwarp();
+    }
+}
+
 
 template <typename T>
 __global__ void pack_kernel(const T* __restrict__ x, const int32_t* __restrict__ map, T* __restrict__ out,
@@ -595,8 +608,9 @@ cudaError_t launch_block_any(const DevLayout& L, const SpmvOperands& o, cudaStre
 static_assert(kNumBlockCfgs == 8, "update launch_block_any / occupancy dispatch");
 
 template <typename T>
-cudaError_t launch_stream(const DevLayout& L, const SpmvOperands& o, cudaStream_t s) {
-    StreamArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_out, L.s_slot, L.s_tiles, L.ntiles};
+cudaError_t launch_stream(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, bool vec) {
+    StreamArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_out, L.s_slot, L.s_tiles, L.ntiles,
+                 VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}};
     const bool c = L.s_slot != nullptr, id = L.s_out == nullptr;
     const dim3 grid(L.grid_t), block(kStreamWarps * 32);
     if (c && id) spmv_stream_kernel<T, true, true><<<grid, block, 0, s>>>(a, o);
@@ -610,10 +624,11 @@ cudaError_t launch_stream(const DevLayout& L, const SpmvOperands& o, cudaStream_
 template <typename T>
 cudaError_t launch_all(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, int32_t b0, int32_t b1, bool vec) {
     cudaError_t e = cudaSuccess;
-    if (L.stream) {  // CSR-stream S group: all tiles in one launch (b0 / b1 ignored)
+    if (L.stream) {  // CSR-stream S group: all tiles (b0 / b1 ignored) and the long rows, one launch
         if (b1 > b0 && L.ntiles > 0) {
-            e = launch_stream<T>(L, o, s);
+            e = launch_stream<T>(L, o, s, vec);
             if (e != cudaSuccess) return e;
+            vec = false;
         }
     } else if (b1 > b0) {
         e = launch_block_any<T>(L, o, s, b0, b1);
