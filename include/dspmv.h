@@ -240,6 +240,16 @@ dspmv_status dspmv_host_plan_set_requests(dspmv_host_plan_t hp, const int32_t* c
 dspmv_status dspmv_layout_host(const int64_t* rowptr, int32_t nrows, int dtype, int cfg, int vthr,
                                int32_t* s_rows, int32_t* n_s, int32_t* desc, int32_t* n_blocks,
                                int32_t* v_rows, int32_t* n_v, int32_t* cfg_used);
+/* Host-only, test hook: the CSR-stream form of the same matrix -- whether
+ * s_kernel (DSPMV_SKERNEL_*; AUTO = by row-length variation, as
+ * dspmv_plan_create decides) selects it (*stream_used), the tiles
+ * (int32[2*n_tiles]: [r0, r1) in S-row indices, <= 256 nnz and <= 64 rows
+ * each; S rows in matrix order) and the V-group rows (int32[nV], rows of
+ * more than min(vthr, 256) nnz).  Tiles and V rows are returned whatever
+ * *stream_used says.  Pass NULL outputs to get sizes. */
+dspmv_status dspmv_stream_layout_host(const int64_t* rowptr, int32_t nrows, int vthr, int s_kernel,
+                                      int32_t* tiles, int32_t* n_tiles, int32_t* v_rows, int32_t* n_v,
+                                      int32_t* stream_used);
 
 /* ------------------------------------------------------------ schedules
  * A schedule is a traversal of the program DAG with every GPU

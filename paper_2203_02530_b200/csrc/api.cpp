@@ -1493,6 +1493,36 @@ dspmv_status dspmv_layout_host(const int64_t* rowptr, int32_t nrows, int dtype, 
     return DSPMV_OK;
 }
 
+dspmv_status dspmv_stream_layout_host(const int64_t* rowptr, int32_t nrows, int vthr, int s_kernel,
+                                      int32_t* tiles, int32_t* n_tiles, int32_t* v_rows, int32_t* n_v,
+                                      int32_t* stream_used) {
+    if (!rowptr || nrows < 0 || !n_tiles || !n_v) return fail(DSPMV_ERR_ARG, "null argument");
+    if (vthr < 0) vthr = kDefaultVectorThreshold;
+    std::vector<int32_t> rp(static_cast<size_t>(nrows) + 1);
+    for (int32_t i = 0; i <= nrows; ++i) {
+        const int64_t v = rowptr[i] - rowptr[0];
+        if (v >= (int64_t(1) << 31)) return fail(DSPMV_ERR_RANGE, "nnz >= 2^31");
+        rp[i] = int32_t(v);
+    }
+    dspmv_plan_opts o;
+    dspmv_plan_opts_default(&o);
+    o.s_kernel = s_kernel;
+    std::vector<int32_t> col(size_t(rp[nrows]), 0), ident(static_cast<size_t>(nrows));
+    for (int32_t i = 0; i < nrows; ++i) ident[i] = i;
+    Layout L;
+    build_layout(rp.data(), nrows, col.data(), nullptr, 8, ident.data(), nullptr, vthr,
+                 kBlockCfgs[kDefaultBlockCfg], L, true);
+    const int32_t nt = int32_t(L.s_tiles.size() / 2);
+    const bool fit = (!tiles || *n_tiles >= nt) && (!v_rows || *n_v >= L.nV);
+    if (tiles && fit) std::copy(L.s_tiles.begin(), L.s_tiles.end(), tiles);
+    if (v_rows && fit) std::copy(L.v_out.begin(), L.v_out.end(), v_rows);
+    *n_tiles = nt;
+    *n_v = L.nV;
+    if (stream_used) *stream_used = use_stream(o, rp.data(), nrows, vthr) ? 1 : 0;
+    if (!fit) return fail(DSPMV_ERR_ARG, "output arrays too small");
+    return DSPMV_OK;
+}
+
 dspmv_status dspmv_host_plan_destroy(dspmv_host_plan_t hp) {
     if (!hp) return fail(DSPMV_ERR_ARG, "null host plan");
     delete hp;

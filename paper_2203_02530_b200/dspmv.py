@@ -114,6 +114,7 @@ _sig("dspmv_rank_plan_build_host", [_I, _I, _I64, _I64, _P, _P, _P, _I, _P])
 _sig("dspmv_host_plan_requests", [_P, _I, _P, ctypes.c_size_t, _P])
 _sig("dspmv_host_plan_set_requests", [_P, _P, _P])
 _sig("dspmv_layout_host", [_P, ctypes.c_int32, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P])
+_sig("dspmv_stream_layout_host", [_P, ctypes.c_int32, _I, _I, _P, _P, _P, _P, _P])
 _sig("dspmv_schedule_validate", [_P, _I, _I])
 _sig("dspmv_schedule_derive", [_P, _P, _I, _P, _I, _P])
 _sig("dspmv_schedule_derive_peers", [_P, _P, _P, _I, _I, _P, _I, _P])
@@ -362,6 +363,20 @@ def dspmv_layout_host(rowptr, dtype=DSPMV_F64, cfg: int = -1, vthr: int = -1):
                                  desc.ctypes.data, ctypes.byref(nb), v_rows.ctypes.data, ctypes.byref(nv),
                                  ctypes.byref(cu)))
     return s_rows[:ns.value], desc[:nb.value * 16].reshape(-1, 16), v_rows[:nv.value], cu.value
+
+
+def dspmv_stream_layout_host(rowptr, vthr: int = -1, s_kernel: int = DSPMV_SKERNEL_AUTO):
+    """(tiles[nt,2], v_rows, stream_used) of the planner's CSR-stream layout."""
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    nr = len(rowptr) - 1
+    nt, nv, su = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_int32(0)
+    _check(lib.dspmv_stream_layout_host(rowptr.ctypes.data, nr, vthr, s_kernel, None, ctypes.byref(nt), None,
+                                        ctypes.byref(nv), ctypes.byref(su)))
+    tiles = np.zeros(max(nt.value, 1) * 2, np.int32)
+    v_rows = np.zeros(max(nv.value, 1), np.int32)
+    _check(lib.dspmv_stream_layout_host(rowptr.ctypes.data, nr, vthr, s_kernel, tiles.ctypes.data, ctypes.byref(nt),
+                                        v_rows.ctypes.data, ctypes.byref(nv), ctypes.byref(su)))
+    return tiles[:2 * nt.value].reshape(-1, 2), v_rows[:nv.value], bool(su.value)
 
 
 def dspmv_schedule_validate(ops, n_streams: int):

@@ -79,3 +79,45 @@ def test_auto_config_choice():
     assert D.dspmv_layout_host(gen.stencil("27pt", (16, 16, 16))[0], dtype=D.DSPMV_F32)[3] == 6
     assert D.dspmv_layout_host(gen.powerlaw(20000)[0])[3] == 3
     assert D.dspmv_layout_host(gen.stencil("7pt", (16, 16, 16))[0], dtype=D.DSPMV_F32)[3] == 0
+
+
+@pytest.mark.parametrize("mat", list(MATS))
+@pytest.mark.parametrize("vthr", [-1, 0, 16, 1024])
+def test_stream_layout_invariants(mat, vthr):
+    """CSR-stream tiles (K1b): S rows (<= min(vthr, 256) nnz) in
+    matrix order, cut greedily into contiguous row-aligned tiles of <= 256
+    nnz and <= 64 rows that cover every S row once; the rest are V rows."""
+    rp = MATS[mat]()
+    lens = np.diff(rp)
+    cap = min(256 if vthr < 0 else vthr, 256)
+    tiles, v_rows, _ = D.dspmv_stream_layout_host(rp, vthr=vthr)
+    s_rows = np.flatnonzero(lens <= cap)
+    assert np.array_equal(v_rows, np.flatnonzero(lens > cap))
+    ns = len(s_rows)
+    if ns == 0:
+        assert len(tiles) == 0
+        return
+    assert tiles[0, 0] == 0 and tiles[-1, 1] == ns
+    assert np.array_equal(tiles[1:, 0], tiles[:-1, 1])          # contiguous, no gap or overlap
+    slen = lens[s_rows]
+    cum = np.concatenate([[0], np.cumsum(slen)])
+    for r0, r1 in tiles:
+        assert r1 > r0 and r1 - r0 <= 64
+        assert cum[r1] - cum[r0] <= 256
+        if r1 < ns:  # greedy: the next row would break a limit
+            assert r1 - r0 == 64 or cum[r1 + 1] - cum[r0] > 256
+
+
+def test_stream_kernel_auto_choice_host():
+    """Row-length coefficient of variation > 0.5 selects CSR-stream: the
+    power-law generator (G2) yes, stencils no; forced choices win."""
+    pick = lambda rp, k=D.DSPMV_SKERNEL_AUTO: D.dspmv_stream_layout_host(rp, s_kernel=k)[2]
+    pl = MATS["pl"]()
+    assert pick(pl)
+    assert not pick(MATS["7pt"]()) and not pick(MATS["27pt"]())
+    assert not pick(gen.stencil("7pt", (16, 16, 16))[0]) and not pick(gen.config_matrix("c1")[1][0])
+    assert not pick(pl, D.DSPMV_SKERNEL_BLOCK)
+    assert pick(MATS["7pt"](), D.DSPMV_SKERNEL_STREAM)
+    lens = np.diff(pl).astype(float)
+    lens = lens[lens <= 256]
+    assert lens.std() > 0.5 * lens.mean()   # the criterion, computed independently
