@@ -1,7 +1,8 @@
 """Small runs of every kernel path for compute-sanitizer (memcheck /
 racecheck / synccheck): stencil (one lane per row), 27-pt (4 lanes/row),
-power-law (all classes + warp-per-row), 3 LOCAL ranks (pack, exchange,
-unpack, combine), fp32, per-destination schedules."""
+power-law through the CSR-stream kernel (its auto choice) and through the
+row-block kernel (all classes) + warp-per-row, 3 LOCAL ranks (pack,
+exchange, unpack, combine), fp32, per-destination schedules."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -13,18 +14,19 @@ from tests.gpu_helpers import LocalRun, derive_ops, oracle_ops_to_lib
 V, E, _ = S.fine_dag([-1, 1])
 FINE = oracle_ops_to_lib(S.derive(S.topological_orders(E, V)[5], {v: i % 2 for i, v in enumerate(V)}))
 
-cases = [("7pt", 16 ** 3, gen.stencil("7pt", (16, 16, 16))),
-         ("27pt", 12 ** 3, gen.stencil("27pt", (12, 12, 12))),
-         ("pl", 6000, gen.powerlaw(6000))]
-for name, n, (rp, col, val) in cases:
+cases = [("7pt", 16 ** 3, gen.stencil("7pt", (16, 16, 16)), D.DSPMV_SKERNEL_AUTO),
+         ("27pt", 12 ** 3, gen.stencil("27pt", (12, 12, 12)), D.DSPMV_SKERNEL_AUTO),
+         ("pl", 6000, gen.powerlaw(6000), D.DSPMV_SKERNEL_AUTO),
+         ("pl-block", 6000, gen.powerlaw(6000), D.DSPMV_SKERNEL_BLOCK)]
+for name, n, (rp, col, val), sk in cases:
     for P in (1, 3):
         for dt in (D.DSPMV_F64, D.DSPMV_F32):
             for ex in (D.DSPMV_EXCHANGE_COPY, D.DSPMV_EXCHANGE_PUT):
                 v = val.astype(np.float32) if dt == D.DSPMV_F32 else val
                 for gran, ops in (("coarse", derive_ops()), ("fine", FINE)):
-                    if gran == "fine" and name == "pl":
+                    if gran == "fine" and name.startswith("pl"):
                         continue                      # power-law: every rank is a peer, offsets +-1, +-2
-                    run = LocalRun(n, rp, col, v, P, dtype=dt, exchange=ex)
+                    run = LocalRun(n, rp, col, v, P, dtype=dt, exchange=ex, s_kernel=sk)
                     y = run.apply(run.schedule(ops), gen.x_values((0, n)), reps=2)
                     run.close()
                     assert np.isfinite(y).all()
