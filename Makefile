@@ -34,7 +34,8 @@ $(BUILD)/kernels_prof.o: $(SRC)/kernels.cu $(SRC)/runtime.h $(SRC)/internal.h in
 $(OUT)/libdspmv_prof.so: $(BUILD)/kernels_prof.o $(BUILD)/api.o $(BUILD)/planner.o $(BUILD)/schedule.o
 	$(NVCC) $(ARCH) -shared -o $@ $^ -L$(NCCL_HOME)/lib -l:libnccl.so.2 -Xlinker -rpath,$(NCCL_HOME)/lib
 
-# diagnostic variants of the gather (DIAG=1: none, DIAG=2: row-local), never the product
+# diagnostic variants (DIAG=1: no gather, DIAG=2: row-local gather, DIAG=3: CSR-stream without
+# row sums, DIAG=4: CSR-stream without gathers), never the product
 $(BUILD)/kernels_diag$(DIAG).o: $(SRC)/kernels.cu $(SRC)/runtime.h $(SRC)/internal.h include/dspmv.h | $(BUILD)
 	$(NVCC) $(NVFLAGS) -DDSPMV_DIAG_GATHER=$(DIAG) -c $< -o $@ 2> /dev/null
 

@@ -457,15 +457,26 @@ __global__ void __launch_bounds__(kStreamWarps * 32) spmv_stream_kernel(StreamAr
             v[k] = q < m ? __ldcs(val + p0 + q) : T(0);
         }
 #pragma unroll
-        for (int k = 0; k < kStreamTile / 32; ++k) xv[k] = lane + 32 * k < m ? ldg_x<true>(x + c[k], xpol) : T(0);
+        for (int k = 0; k < kStreamTile / 32; ++k) {
+#if defined(DSPMV_DIAG_GATHER) && DSPMV_DIAG_GATHER == 4
+            xv[k] = T(c[k]);  // diagnostic build 4: no gathers (cost of the streaming + row sums)
+#else
+            xv[k] = lane + 32 * k < m ? ldg_x<true>(x + c[k], xpol) : T(0);
+#endif
+        }
         __syncwarp();  // keeps ptxas from pairing each gather with its multiply: all 8 stay in flight
 #pragma unroll
         for (int k = 0; k < kStreamTile / 32; ++k) pr[lane + 32 * k] = mul_rn(v[k], xv[k]);
         __syncwarp();
         for (int32_t r = tr.x + lane; r < tr.y; r += 32) {
+#if defined(DSPMV_DIAG_GATHER) && DSPMV_DIAG_GATHER == 3
+            // diagnostic build 3: no row sums (cost of the gather phase alone)
+            const T acc = pr[r - tr.x];
+#else
             const int32_t e0 = __ldg(a.rowptr + r) - p0, e1 = __ldg(a.rowptr + r + 1) - p0;
             T acc = T(0);
             for (int32_t q = e0; q < e1; ++q) acc = add_rn(acc, pr[q]);
+#endif
             const int32_t orow = kIdentity ? r : a.out[r];
             if (kCombine) {
                 const int32_t k = a.slot[r];
