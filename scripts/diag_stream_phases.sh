@@ -1,7 +1,7 @@
 #!/bin/bash
 # CSR-stream kernel on C4: product vs no row sums (DIAG=3) vs no gathers (DIAG=1)
 OUT=gpurun_out; mkdir -p $OUT
-for v in diag4; do
+for v in ""; do
   DSPMV_LIB=$v timeout 300 python bench.py --workload c4 --steps 50 --warmup 5 --no-cpu-baseline --no-sweep --execution host > $OUT/sp_$v.json 2>/dev/null
   python -c "
 import json
