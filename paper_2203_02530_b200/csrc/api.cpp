@@ -171,9 +171,23 @@ void build_host_pipe(Plan& p, Layout& L) {
     // boundary costs a copy-engine drain, the last chunk's rows trail the copy
     int kmax = 4;
     if (const char* ev = std::getenv("DSPMV_HOST_CHUNKS")) kmax = std::max(1, std::min(64, std::atoi(ev)));  // tuning
-    const int K = int(std::min<int64_t>(kmax, bytes / (int64_t(1) << 20)));
+    int K = int(std::min<int64_t>(kmax, bytes / (int64_t(1) << 20)));
+    std::vector<double> frac;   // chunk end fractions (uniform by default)
+    for (int k = 1; k < K; ++k) frac.push_back(double(k) / K);
+    if (const char* ev = std::getenv("DSPMV_HOST_SPLIT")) {  // tuning: "0.4,0.7,0.9"
+        frac.clear();
+        for (const char* q = ev; *q;) {
+            char* e = nullptr;
+            const double f = std::strtod(q, &e);
+            if (e == q) break;
+            if (f > 0 && f < 1 && (frac.empty() || f > frac.back())) frac.push_back(f);
+            q = *e == ',' ? e + 1 : e;
+        }
+        K = int(frac.size()) + 1;
+    }
     H.x_chunk.assign(K + 1, 0);
-    for (int k = 1; k < K; ++k) H.x_chunk[k] = std::min<int64_t>(n, (int64_t(k) * n / K + 255) / 256 * 256);
+    for (int k = 1; k < K; ++k)
+        H.x_chunk[k] = std::min<int64_t>(n, (int64_t(frac[k - 1] * double(n)) + 255) / 256 * 256);
     H.x_chunk[K] = n;
     auto chunk_of = [&](int64_t c) {
         return int(std::upper_bound(H.x_chunk.begin(), H.x_chunk.end(), c) - H.x_chunk.begin()) - 1;
