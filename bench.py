@@ -413,6 +413,7 @@ def run_ours(a):
     t_wall0 = time.perf_counter()
     step_ms_rank = 0.0
     tl_begin, tl_end = [], []
+    step_list = []
     for k in range(a.steps):
         D.dspmv_l2_flush(device, stream)
         evs[k][0].record(stream)
@@ -421,6 +422,7 @@ def run_ours(a):
         t = D.dspmv_schedule_op_times(sched)
         yl_ms += float(t[iyl])
         step_ms_rank += float(t[0])   # START..END events recorded on `stream` by the library
+        step_list.append(float(t[0]))
         if world > 1:
             x_us.append(max(float(t[i]) for i in iposts) * 1e3)
         b_, e_ = D.dspmv_schedule_op_timeline(sched)
@@ -435,6 +437,8 @@ def run_ours(a):
     py_step_ms = allmax(sum(e0.elapsed_time(e1) for e0, e1 in evs)) / a.steps
     total_ms = allmax(step_ms_rank)
     ms_per_step = total_ms / a.steps
+    # per-step distribution (median, min, p90), max over ranks of each statistic
+    step_stats = [round(allmax(float(np.percentile(step_list, q))) * 1e3, 2) for q in (50, 0, 90)]
     yl_ms_avg = yl_ms / a.steps
     yl_ms_max = allmax(yl_ms_avg)
     nnz_total = allsum(float(nnz_rank))
@@ -507,6 +511,7 @@ def run_ours(a):
                                                 round(float(np.median(tl_end)) * 1e3, 2)],
                 "step_hbm_gbs_algorithmic": round(step_gbs, 1),
                 "wall_s_timed_region": round(t_wall, 3),
+                "step_us_median_min_p90": step_stats,
             },
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
