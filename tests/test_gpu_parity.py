@@ -550,3 +550,31 @@ def test_stream_kernel_auto_choice_and_fp32():
         run.close()
     xr, vr = x32.astype(np.float64), v32.astype(np.float64)
     assert within_tol(y, O1.o1_spmv(rp, col, vr, xr), O1.o1_absdot(rp, col, vr, xr), 1e-5)
+
+
+def test_stream_kernel_edge_cases():
+    """CSR-stream with no S rows at all (every row > 256 nnz: the long-row
+    kernel alone), with runs of empty rows (tiles whose rows sum to +0), and
+    a 1-row matrix."""
+    rng = np.random.default_rng(3)
+    cases = []
+    n = 600                                            # every row 300 nnz
+    cols = np.stack([np.sort(rng.choice(n, 300, replace=False)) for _ in range(n)]).ravel().astype(np.int32)
+    cases.append((n, np.arange(n + 1, dtype=np.int64) * 300, cols, rng.uniform(-1, 1, cols.size)))
+    n = 5000                                           # 4000 empty rows in a row, then short rows
+    lens = np.r_[np.zeros(4000, np.int64), rng.integers(1, 12, 1000)]
+    rp = np.r_[0, np.cumsum(lens)].astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in lens]).astype(np.int32)
+    cases.append((n, rp, cols, rng.uniform(-1, 1, cols.size)))
+    cases.append((1, np.array([0, 1], np.int64), np.array([0], np.int32), np.array([2.5])))
+    for n, rp, col, val in cases:
+        x = gen.x_values((0, n))
+        run = LocalRun(n, rp, col, val, 1, s_kernel=D.DSPMV_SKERNEL_STREAM)
+        try:
+            y = run.apply(run.schedule(derive_ops()), x)
+        finally:
+            run.close()
+        yref = O1.o1_spmv(rp, col, val, x)
+        short = np.diff(rp) <= 256
+        assert np.array_equal(y[short], yref[short]) and not np.any(np.signbit(y[np.diff(rp) == 0]))
+        assert within_tol(y, yref, O1.o1_absdot(rp, col, val, x), 1e-12)
