@@ -1,5 +1,6 @@
 #!/bin/bash
-# CSR-stream with TMA-staged col/val (DSPMV_STREAM_TMA=1) vs the product kernel on C4, + parity
+# CSR-stream with TMA-staged col/val (DSPMV_STREAM_TMA=1) vs the product kernel on C4, + parity.
+# The TMA variant was measured (profiles/r1_stream_kernel_c4_sweep.txt) and removed; the knob is now a no-op.
 OUT=gpurun_out; mkdir -p $OUT
 DSPMV_STREAM_TMA=1 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "stream or irregular" > $OUT/pytest_tma.log 2>&1; echo "exit $?" >> $OUT/pytest_tma.log
 for v in 0 1; do
