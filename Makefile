@@ -47,7 +47,7 @@ all: $(OUT)/libdspmv_prof.so
 endif
 
 oracle/libo1.so: oracle/o1.c
-	gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -o $@ $< -lm
+	gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp -fPIC -shared -o $@ $< -lm
 
 gen/libgenc.so: gen/genc.c
 	gcc -O2 -ffp-contract=off -fPIC -shared -o $@ $< -lm

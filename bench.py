@@ -658,9 +658,21 @@ def cpu_baseline(workload_name, budget_s=10.0, world=1):
         reps += 1
     dt = time.perf_counter() - t0
     nnz = int(rp[-1])
+    # the same loop over rows on all host cores (OpenMP, static)
+    O1.o1_spmv_omp(rp, col, val, x)  # warm
+    reps_m, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s / 2:
+        O1.o1_spmv_omp(rp, col, val, x)
+        reps_m += 1
+    dt_m = time.perf_counter() - t0
+    threads = O1.o1_threads()
     return {"value": round(2.0 * nnz * reps / dt / 1e9, 4), "unit": "GFLOP/s", "cores": 1,
             "kind": "oracle",
             "sample": f"full {desc}: {reps} O1 SpMVs ({nnz} nnz each) in {dt:.2f} s, 1 thread",
+            "all_cores": {"value": round(2.0 * nnz * reps_m / dt_m / 1e9, 4), "unit": "GFLOP/s",
+                          "cores": threads,
+                          "sample": f"full {desc}: {reps_m} O1 SpMVs, rows over {threads} OpenMP threads "
+                                    f"(static schedule) in {dt_m:.2f} s"},
             "cpu": _cpu_model()}
 
 

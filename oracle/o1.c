@@ -59,3 +59,25 @@ void o1_absdot(int64_t n_rows, const int64_t* rowptr, const int32_t* col,
         s[i] = acc;
     }
 }
+
+/* "the same plain loop with #pragma omp parallel for
+ * schedule(static) over rows on all host cores" -- the CPU baseline on every
+ * core.  Each row is still summed by one thread in stored order, so y is
+ * bitwise that of o1_spmv. */
+#include <omp.h>
+void o1_spmv_omp(int64_t n_rows, const int64_t* rowptr, const int32_t* col,
+                 const double* val, const double* x, double* y)
+{
+    const int64_t base = rowptr[0];
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n_rows; ++i) {
+        double acc = 0.0;
+        for (int64_t p = rowptr[i] - base; p < rowptr[i + 1] - base; ++p) {
+            double prod = val[p] * x[col[p]];
+            acc = acc + prod;
+        }
+        y[i] = acc;
+    }
+}
+
+int o1_omp_threads(void) { return omp_get_max_threads(); }

@@ -23,7 +23,7 @@ def build() -> str:
     """Compile o1.c (plain -O2, no FMA contraction, no fast-math)."""
     src = os.path.join(_HERE, "o1.c")
     if (not os.path.exists(_SO)) or os.path.getmtime(_SO) < os.path.getmtime(src):
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math",
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
                                "-fPIC", "-shared", "-o", _SO, src, "-lm"])
     return _SO
 
@@ -34,12 +34,13 @@ def _load():
         build()
         lib = ctypes.CDLL(_SO)
         P = ctypes.c_void_p
-        for name in ("o1_spmv", "o1_absdot"):
+        for name in ("o1_spmv", "o1_absdot", "o1_spmv_omp"):
             f = getattr(lib, name)
             f.argtypes = [ctypes.c_int64, P, P, P, P, P]
             f.restype = None
         lib.o1_spmv_rows.argtypes = [ctypes.c_int64, P, P, P, P, P, P]
         lib.o1_spmv_rows.restype = None
+        lib.o1_omp_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -61,6 +62,27 @@ def o1_spmv(rowptr, col, val, x) -> np.ndarray:
         lib.o1_spmv(n, rowptr.ctypes.data, col.ctypes.data, val.ctypes.data,
                     x.ctypes.data, y.ctypes.data)
     return y
+
+
+def o1_spmv_omp(rowptr, col, val, x) -> np.ndarray:
+    """The O1 loop with its rows split over all host cores (OpenMP, static
+    schedule; SURVEY 8(d) CPU baseline); bitwise equal to o1_spmv."""
+    lib = _load()
+    rowptr = _c(rowptr, np.int64)
+    col = _c(col, np.int32)
+    val = _c(val, np.float64)
+    x = _c(x, np.float64)
+    n = len(rowptr) - 1
+    y = np.empty(n, np.float64)
+    if n:
+        lib.o1_spmv_omp(n, rowptr.ctypes.data, col.ctypes.data, val.ctypes.data,
+                        x.ctypes.data, y.ctypes.data)
+    return y
+
+
+def o1_threads() -> int:
+    """Threads o1_spmv_omp uses (OpenMP max threads)."""
+    return int(_load().o1_omp_threads())
 
 
 def o1_spmv_rows(rows, rowptr, col, val, x) -> np.ndarray:

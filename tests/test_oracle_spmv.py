@@ -136,3 +136,16 @@ def test_exact_mode_partial_sums_fit():
     assert s.max() < 2 ** 24
     y32 = O1.o1_spmv(rp, col, val.astype(np.float32).astype(np.float64), x)
     assert np.array_equal(y32, O1.o1_spmv(rp, col, val, x))
+
+
+def test_o1_openmp_rows_equal_serial_bitwise():
+    """The all-cores CPU baseline (the O1 loop under
+    `omp parallel for schedule(static)` over rows) sums every row in one
+    thread in stored order, so it equals the serial O1 bit for bit."""
+    mats = [gen.powerlaw(20000), gen.stencil("27pt", (14, 14, 14)),
+            gen.random_csr(300, 0.05, seed=11, empty_rows=(0, 1, 150, 299), dense_rows=(7, 200))]
+    for rp, col, val in mats:
+        n = len(rp) - 1
+        x = gen.x_values((0, n))
+        assert np.array_equal(O1.o1_spmv_omp(rp, col, val, x), O1.o1_spmv(rp, col, val, x))
+    assert O1.o1_threads() >= 1
