@@ -149,3 +149,96 @@ def test_o1_openmp_rows_equal_serial_bitwise():
         x = gen.x_values((0, n))
         assert np.array_equal(O1.o1_spmv_omp(rp, col, val, x), O1.o1_spmv(rp, col, val, x))
     assert O1.o1_threads() >= 1
+
+
+# --------------------------------------------------------------------------
+# Independent pins for o1_absdot, the scale s_i = sum_j |a_ij x_j| of every
+# tolerance assertion (BASELINE.json north_star).  The |y| <= s bound above is
+# one-sided: an over-large s (an accumulator not reset per row, sum|a| max|x|)
+# would pass it and silently loosen every parity test.  These pin s from the
+# other side with a library routine and with closed forms.
+
+def _scipy_absdot(rp, col, val, x, n):
+    A = sp.csr_matrix((np.abs(val), col, rp - rp[0]), shape=(len(rp) - 1, n))
+    return A @ np.abs(x)
+
+
+@pytest.mark.parametrize("name", ["rand", "pl", "27pt", "5pt"])
+def test_absdot_exact_mode_equals_scipy_abs_product(name):
+    """Exact mode (integers, R-Q23): |A| @ |x| by scipy is exact, so O1's s
+    must equal it bitwise, row by row (including empty rows, where s = 0)."""
+    if name == "rand":
+        n = 300
+        rp, col, val = gen.random_csr(n, 0.05, seed=3, exact=True,
+                                      empty_rows=(0, 17, 299), dense_rows=(5,))
+    elif name == "pl":
+        n = 20000
+        rp, col, val = gen.powerlaw(n, exact=True)
+    elif name == "27pt":
+        n = 9 * 8 * 7
+        rp, col, val = gen.stencil("27pt", (9, 8, 7))
+    else:
+        n = 33 * 31
+        rp, col, val = gen.stencil("5pt", (33, 31, 1))
+    x = gen.x_values((0, n), exact=True)
+    s = O1.o1_absdot(rp, col, val, x)
+    assert np.array_equal(s, _scipy_absdot(rp, col, val, x, n))
+
+
+@pytest.mark.parametrize("n,dens", [(64, 0.5), (300, 0.05), (2000, 0.01)])
+def test_absdot_float_mode_within_rounding_of_scipy(n, dens):
+    """Float mode: both sides sum k nonnegative terms, so each is within
+    gamma_k = k u/(1 - k u) (u = 2^-53) of the exact value; the two differ by
+    at most 2 gamma_k s_i."""
+    rp, col, val = gen.random_csr(n, dens, seed=23, exact=False, dense_rows=(1,))
+    x = gen.x_values((0, n))
+    s = O1.o1_absdot(rp, col, val, x)
+    ref = _scipy_absdot(rp, col, val, x, n)
+    k = np.diff(rp).astype(np.float64)
+    u = 2.0 ** -53
+    g = k * u / (1 - k * u)
+    assert np.all(np.abs(s - ref) <= 2 * g * ref)
+    assert np.all(s > 0) or np.all(s[k > 0] > 0)
+
+
+def test_absdot_nonnegative_inputs_equal_y():
+    """Closed form: with a_ij >= 0 and x_j >= 0, |a_ij x_j| = a_ij x_j, so s is
+    the same sum in the same order as y -- bitwise equal to O1's y."""
+    n = 500
+    rp, col, val = gen.random_csr(n, 0.03, seed=5, exact=False, empty_rows=(3,))
+    val = np.abs(val)
+    x = np.abs(gen.x_values((0, n)))
+    assert np.array_equal(O1.o1_absdot(rp, col, val, x), O1.o1_spmv(rp, col, val, x))
+
+
+def test_absdot_cancellation_rows():
+    """Closed forms: a row (+1, -1) against x = (1, 1) gives y = 0 but s = 2; an
+    empty row gives s = 0; a row (2, -3, 5) against (1, -1, 2) has all products
+    positive, so s = y = 15; a row (2, 3) against (1, -1) gives y = -1, s = 5."""
+    rp = np.array([0, 2, 2, 5, 7], np.int64)
+    col = np.array([0, 1, 0, 1, 2, 0, 1], np.int32)
+    val = np.array([1.0, -1.0, 2.0, -3.0, 5.0, 2.0, 3.0])
+    x = np.array([1.0, -1.0, 2.0])
+    s = O1.o1_absdot(rp, col, val, np.array([1.0, 1.0, 1.0]))
+    assert s[0] == 2.0 and s[1] == 0.0
+    s = O1.o1_absdot(rp, col, val, x)
+    y = O1.o1_spmv(rp, col, val, x)
+    assert s.tolist() == [2.0, 0.0, 15.0, 5.0]
+    assert y.tolist() == [2.0, 0.0, 15.0, -1.0]
+
+
+def test_absdot_is_per_row_and_scales_with_x():
+    """Row-locality (a sample of rows equals the same rows of the full s after
+    permuting the row order) and homogeneity s(A, c x) = |c| s(A, x) for c a
+    power of two (exact)."""
+    n = 4096
+    rp, col, val = gen.powerlaw(n)
+    x = gen.x_values((0, n))
+    s = O1.o1_absdot(rp, col, val, x)
+    perm = np.random.default_rng(1).permutation(n)
+    lens = np.diff(rp)[perm]
+    rp2 = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    col2 = np.concatenate([col[rp[i]:rp[i + 1]] for i in perm])
+    val2 = np.concatenate([val[rp[i]:rp[i + 1]] for i in perm])
+    assert np.array_equal(O1.o1_absdot(rp2, col2, val2, x), s[perm])
+    assert np.array_equal(O1.o1_absdot(rp, col, val, -0.25 * x), 0.25 * s)
