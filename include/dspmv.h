@@ -113,7 +113,10 @@ typedef struct {
                                   (2^c lanes per row, c by row length).
                                   -1 = default (256); valid 0..1024                     */
     int32_t keep_host;         /* 1: keep host copies of A_L/A_R for dspmv_plan_export  */
-    int32_t comm_priority;     /* 1 (default): comm + stream 0 at the highest priority   */
+    int32_t comm_priority;     /* 1 (default): the internal comm stream at the highest
+                                  priority.  All schedule streams share the lowest
+                                  priority, so they are interchangeable (the stream
+                                  bijection of the design space)             */
     int32_t block_cfg;         /* row-block kernel configuration (tile nnz / consumer
                                   warps / TMA stages), -1 = chosen per matrix from its
                                   row lengths; K1                         */
@@ -141,11 +144,48 @@ typedef struct {
                                   per lane (coalesced col/val loads), then one lane per
                                   row sums its products in stored order (bitwise the
                                   serial CSR loop)                              */
-    int32_t reserved[2];
+    int32_t pack_mode;         /* DSPMV_PACK_GATHER (0, default): Pack gathers
+                                  sendbuf[k] = x[pack_map[k]].
+                                  DSPMV_PACK_ALIAS_IF_CONTIGUOUS: when every
+                                  destination's send list is a run of consecutive
+                                  local rows (stencil planes), the
+                                  NCCL sends read straight from x and Pack launches
+                                  nothing; otherwise as GATHER.  COPY exchange only
+                                  (PUT already fuses the gather with the store).
+                                  dspmv_plan_info.pack_alias reports the outcome    */
+    int32_t accumulate_mode;   /* DSPMV_ACC_TICKET (0, default): y = y_L + y_R combined
+                                  by the second SpMV to finish each row (R-Q9).
+                                  DSPMV_ACC_EXPLICIT_IN_END (debug): y_L and y_R only
+                                  deposit their partials; END adds them
+                                  (y_i = fl(s_L,i + s_R,i)) in one kernel on
+                                  the caller's stream.  Same bits as TICKET.        */
+    int32_t debug_checks;      /* 1: COLLECTIVE calls verify their arguments agree
+                                  across ranks -- plan_create hashes (n_global,
+                                  nranks, dtype, modes), the first apply of a
+                                  schedule hashes its ops; a mismatch returns
+                                  DSPMV_ERR_ARG / DSPMV_ERR_SCHEDULE on every rank.
+                                  Default 0, or the env DSPMV_DEBUG_CHECKS.         */
+    int32_t reserved0;
+    /* Device memory of the plan (matrix layouts, buffers): alloc(bytes, device,
+       ctx) returns device memory on `device` or NULL (-> DSPMV_ERR_OOM);
+       free(ptr, bytes, device, ctx) releases it at plan_destroy (after the
+       device is idle for the plan).  NULL = cudaMalloc / cudaFree.  The Python
+       binding routes them to the framework's caching allocator.  Buffers peers map
+       through CUDA IPC (PUT receive buffers and flags) always use cudaMalloc. */
+    void* (*alloc)(size_t bytes, int device, void* ctx);
+    void (*free)(void* ptr, size_t bytes, int device, void* ctx);
+    void* alloc_ctx;
 } dspmv_plan_opts;
 
-enum { DSPMV_EXCHANGE_COPY = 0, DSPMV_EXCHANGE_PUT = 1 };
-enum { DSPMV_SKERNEL_AUTO = 0, DSPMV_SKERNEL_BLOCK = 1, DSPMV_SKERNEL_STREAM = 2 };
+enum { DSPMV_PACK_GATHER = 0, DSPMV_PACK_ALIAS_IF_CONTIGUOUS = 1 };
+enum { DSPMV_ACC_TICKET = 0, DSPMV_ACC_EXPLICIT_IN_END = 1 };
+
+enum { DSPMV_EXCHANGE_COPY = 0, DSPMV_EXCHANGE_PUT = 1,
+       /* timing baseline only (SURVEY 8(d) overlap efficiency, T_noexch): Post/Wait
+          run their synchronisation but move no data, so y is WRONG on rows with
+          remote entries.  Never a product mode. */
+       DSPMV_EXCHANGE_NONE = 2 };
+enum { DSPMV_SKERNEL_AUTO = 0, DSPMV_SKERNEL_BLOCK = 1, DSPMV_SKERNEL_STREAM = 2, DSPMV_SKERNEL_STREAM_TMA = 3 };
 
 void dspmv_plan_opts_default(dspmv_plan_opts* opts);
 
@@ -177,7 +217,9 @@ typedef struct {
     int32_t grid_local, grid_remote;          /* persistent grid of the block kernel   */
     int32_t rank, nranks, dtype, ready;
     int64_t device_bytes;
-    int32_t s_kernel_local, s_kernel_remote;  /* DSPMV_SKERNEL_BLOCK / _STREAM in use    */
+    int32_t s_kernel_local, s_kernel_remote;  /* DSPMV_SKERNEL_BLOCK / _STREAM(_TMA)     */
+    int32_t pack_alias;              /* 1: sends read x directly, Pack is empty    */
+    int32_t accumulate_mode;         /* DSPMV_ACC_* in use                         */
 } dspmv_plan_info;
 dspmv_status dspmv_plan_info_get(dspmv_plan_t plan, dspmv_plan_info* out);
 
@@ -398,8 +440,13 @@ dspmv_status dspmv_apply_host(dspmv_schedule_t sched, const void* x_host, void* 
  * device-side join of all streams on that event, the NCCL exchange is captured
  * on the comm stream, and START/END fork from / join into `stream`; each call
  * then launches the graph.  Stream-ordered: returns immediately, y is complete
- * when `stream` reaches this point.  Same results as dspmv_apply.  Not for
- * LOCAL groups with > 1 rank or the PUT exchange; `stream` must not be NULL. */
+ * when `stream` reaches this point.  Same results as dspmv_apply.  PUT
+ * exchange: the apply's epoch lives in device memory (bumped by the graph's
+ * first node), the fused Pack+put kernels pick the receive-buffer parity from
+ * it and the wait on the sources' flags is a kernel (traps after ~30 s
+ * instead of hanging on a dead peer), so the fused exchange runs without any
+ * host round trip.  LOCAL groups with > 1 rank use
+ * dspmv_apply_graph_group; `stream` must not be NULL. */
 dspmv_status dspmv_apply_graph(dspmv_schedule_t sched, const void* x_local, void* y_local,
                                dspmv_stream_t stream);
 /* LOCAL comms: all nranks ranks of one in-process group in lock-step (op k on
@@ -407,6 +454,18 @@ dspmv_status dspmv_apply_graph(dspmv_schedule_t sched, const void* x_local, void
 dspmv_status dspmv_apply_group(const dspmv_schedule_t* scheds, int nranks,
                                const void* const* x_local, void* const* y_local,
                                dspmv_stream_t stream);
+
+/* COLLECTIVE over a LOCAL group, from one host thread: the schedules of ranks
+ * 0..nranks-1 captured in lock-step into ONE CUDA graph -- every rank's ops
+ * on that rank's own streams, host syncs turned into device-side joins as in
+ * dspmv_apply_graph, the exchange as device copies ordered after the
+ * senders' Pack kernels (COPY) or flag-wait kernels on the device epoch
+ * (PUT) -- and launched on `stream` (non-default).  Stream-ordered: returns
+ * without waiting.  Re-captured when a schedule, x/y pointer or the timing
+ * setting changes.  The graph is held by scheds[0]; destroy the group's
+ * schedules together. */
+dspmv_status dspmv_apply_graph_group(const dspmv_schedule_t* scheds, int nranks, const void* const* x,
+                                     void* const* y, dspmv_stream_t stream);
 
 /* ------------------------------------------------------------- utilities */
 /* Read a device scratch buffer of 2x the L2 size (allocated on first use)

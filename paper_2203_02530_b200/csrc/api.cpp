@@ -59,33 +59,48 @@ int prof_read(unsigned long long* out, int n, bool reset);
 
 namespace {
 
+#define ST_TRY(expr)                       \
+    do {                                   \
+        dspmv_status _s = (expr);          \
+        if (_s != DSPMV_OK) return _s;     \
+    } while (0)
+
 ncclDataType_t nccl_type(int dtype) { return dtype == DSPMV_F32 ? ncclFloat32 : ncclFloat64; }
+
+// Device memory of a plan: the caller's allocator (opts.alloc, e.g. torch's
+// caching allocator) unless `ipc` (buffers peers map through CUDA IPC need
+// their own cudaMalloc allocation) or no allocator was given.
+dspmv_status raw_alloc(Plan& p, void** dst, size_t bytes, bool ipc) {
+    *dst = nullptr;
+    const bool cb = !ipc && p.opts.alloc && p.opts.free;
+    if (cb) {
+        *dst = p.opts.alloc(bytes, p.device, p.opts.alloc_ctx);
+        if (!*dst) return fail(DSPMV_ERR_OOM, "allocator callback returned NULL for " + std::to_string(bytes) + " bytes");
+    } else if (cudaMalloc(dst, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        *dst = nullptr;
+        return fail(DSPMV_ERR_OOM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+    }
+    p.allocs.push_back({*dst, bytes, cb});
+    p.device_bytes += int64_t(bytes);
+    return DSPMV_OK;
+}
 
 template <typename T>
 dspmv_status dev_upload(Plan& p, T** dst, const T* src, size_t n) {
     *dst = nullptr;
     if (n == 0) return DSPMV_OK;
     void* d = nullptr;
-    if (cudaMalloc(&d, n * sizeof(T)) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(DSPMV_ERR_OOM, "cudaMalloc of " + std::to_string(n * sizeof(T)) + " bytes failed");
-    }
-    p.allocs.push_back(d);
-    p.device_bytes += int64_t(n * sizeof(T));
+    ST_TRY(raw_alloc(p, &d, n * sizeof(T), false));
     if (src) CUDA_TRY(cudaMemcpy(d, src, n * sizeof(T), cudaMemcpyHostToDevice));
     *dst = static_cast<T*>(d);
     return DSPMV_OK;
 }
 
-dspmv_status dev_alloc(Plan& p, void** dst, size_t bytes, bool zero) {
+dspmv_status dev_alloc(Plan& p, void** dst, size_t bytes, bool zero, bool ipc = false) {
     *dst = nullptr;
     if (bytes == 0) return DSPMV_OK;
-    if (cudaMalloc(dst, bytes) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(DSPMV_ERR_OOM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
-    }
-    p.allocs.push_back(*dst);
-    p.device_bytes += int64_t(bytes);
+    ST_TRY(raw_alloc(p, dst, bytes, ipc));
     if (zero) CUDA_TRY(cudaMemset(*dst, 0, bytes));
     return DSPMV_OK;
 }
@@ -102,11 +117,8 @@ struct DevScratch {
     }
 };
 
-#define ST_TRY(expr)                       \
-    do {                                   \
-        dspmv_status _s = (expr);          \
-        if (_s != DSPMV_OK) return _s;     \
-    } while (0)
+
+static bool stream_tma_default();
 
 dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
     D = DevLayout();
@@ -129,11 +141,20 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
         D.grid_s = std::max(1, std::min(L.nb, per_sm * usable));
         if (L.stream) {
             D.stream = true;
+            set_x_persist_limit();
             D.ntiles = int32_t(L.s_tiles.size() / 2);
             ST_TRY(dev_upload(p, &D.s_tiles, L.s_tiles.data(), L.s_tiles.size()));
             int tpsm = stream_kernel_ctas_per_sm(p.dtype);
             if (const char* ev = std::getenv("DSPMV_STREAM_CTAS")) tpsm = std::max(1, std::min(tpsm, std::atoi(ev)));  // sweeps
             D.grid_t = std::max(1, std::min((D.ntiles + kStreamWarps - 1) / kStreamWarps, tpsm * usable));
+            if (p.opts.s_kernel == DSPMV_SKERNEL_STREAM_TMA ||
+                (p.opts.s_kernel == DSPMV_SKERNEL_AUTO && stream_tma_default())) {
+                D.stream_tma = true;
+                D.ntblocks = int32_t(L.s_tdesc.size() / kDescInts);
+                ST_TRY(dev_upload(p, &D.s_tdesc, L.s_tdesc.data(), L.s_tdesc.size()));
+                const int bpsm = stream_tma_kernel_ctas_per_sm(p.dtype);
+                D.grid_tt = std::max(1, std::min(D.ntblocks, bpsm * usable));
+            }
         }
     }
     if (L.nV > 0) {
@@ -148,10 +169,20 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
     return DSPMV_OK;
 }
 
+// Irregular matrices: the TMA-producer CSR-stream variant by default
+// (DSPMV_STREAM_TMA=0/1 overrides, for sweeps)
+static bool stream_tma_default() {
+    static const int v = [] {
+        const char* ev = std::getenv("DSPMV_STREAM_TMA");
+        return ev ? std::atoi(ev) : 0;
+    }();
+    return v != 0;
+}
+
 // S-group kernel of a matrix: forced by opts.s_kernel, else the row-block
 // kernel when a block configuration is forced, else chosen by row lengths.
 bool use_stream(const dspmv_plan_opts& o, const int32_t* rowptr, int32_t nrows, int vthr) {
-    if (o.s_kernel == DSPMV_SKERNEL_STREAM) return true;
+    if (o.s_kernel == DSPMV_SKERNEL_STREAM || o.s_kernel == DSPMV_SKERNEL_STREAM_TMA) return true;
     if (o.s_kernel == DSPMV_SKERNEL_BLOCK || o.block_cfg >= 0) return false;
     if (const char* ev = std::getenv("DSPMV_SKERNEL")) return std::atoi(ev) == DSPMV_SKERNEL_STREAM;  // sweeps
     return auto_stream(rowptr, nrows, vthr);
@@ -212,8 +243,24 @@ dspmv_status finalize_send(Plan& p) {
     for (int q = 0; q < p.host.nranks; ++q)
         p.has_peers |= (p.host.recv_count[q] > 0 || p.host.send_count[q] > 0);
     const size_t s = p.host.pack_map.size();
+    // DSPMV_PACK_ALIAS_IF_CONTIGUOUS: every destination's
+    // send list a run of consecutive local rows -> send from x, no Pack kernel
+    p.pack_alias = false;
+    if (p.opts.pack_mode == DSPMV_PACK_ALIAS_IF_CONTIGUOUS && !p.put_mode && s > 0) {
+        const RankPlan& h = p.host;
+        bool ok = true;
+        p.alias_off.assign(size_t(h.nranks), 0);
+        for (int q = 0; q < h.nranks && ok; ++q) {
+            const int32_t c = h.send_count[q], d = h.send_displ[q];
+            if (c <= 0) continue;
+            const int32_t b = h.pack_map[d];
+            for (int32_t k = 1; k < c && ok; ++k) ok = h.pack_map[d + k] == b + k;
+            p.alias_off[q] = b;
+        }
+        p.pack_alias = ok;
+    }
     ST_TRY(dev_upload(p, &p.d_pack_map, p.host.pack_map.data(), s));
-    ST_TRY(dev_alloc(p, &p.d_sendbuf, s * p.esize, true));
+    if (!p.pack_alias) ST_TRY(dev_alloc(p, &p.d_sendbuf, s * p.esize, true));
     p.ready = true;
     return DSPMV_OK;
 }
@@ -488,18 +535,26 @@ dspmv_status wait_group(Plan& p, const ExGroup& g) {
 dspmv_status issue_group_nccl(Plan& p, ExGroup& g) {
     g.issued = true;
     if (g.empty()) return DSPMV_OK;
+    if (p.skip_exchange) {  // DSPMV_EXCHANGE_NONE: timing baseline, no data moves
+        CUDA_TRY(cudaEventRecord(g.ev, p.comm_stream));
+        return DSPMV_OK;
+    }
     const RankPlan& h = p.host;
     const ncclDataType_t ty = nccl_type(p.dtype);
     char* rb = static_cast<char*>(p.d_recvbuf);
     char* sb = static_cast<char*>(p.d_sendbuf);
+    if (p.pack_alias && p.streaming && p.pipe.pack_chunk >= 0 && !g.send_to.empty())
+        CUDA_TRY(cudaStreamWaitEvent(p.comm_stream, p.pipe.ev_x[p.pipe.pack_chunk], 0));
     ncclResult_t gr = ncclSuccess;
     NCCL_TRY(ncclGroupStart());
     for (int q : g.recv_from)
         NCCL_GROUP_CALL(gr, ncclRecv(rb + size_t(h.recv_displ[q]) * p.esize, h.recv_count[q], ty, q, p.comm->nccl,
                                      p.comm_stream));
-    for (int q : g.send_to)
-        NCCL_GROUP_CALL(gr, ncclSend(sb + size_t(h.send_displ[q]) * p.esize, h.send_count[q], ty, q, p.comm->nccl,
-                                     p.comm_stream));
+    for (int q : g.send_to) {
+        const char* src = p.pack_alias ? static_cast<const char*>(p.cur_x) + size_t(p.alias_off[q]) * p.esize
+                                       : sb + size_t(h.send_displ[q]) * p.esize;
+        NCCL_GROUP_CALL(gr, ncclSend(src, h.send_count[q], ty, q, p.comm->nccl, p.comm_stream));
+    }
     NCCL_TRY(ncclGroupEnd());
     NCCL_TRY(gr);
     CUDA_TRY(cudaEventRecord(g.ev, p.comm_stream));
@@ -546,6 +601,18 @@ dspmv_status issue_group_put(Plan& p, ExGroup& g) {
     return DSPMV_OK;
 }
 
+// PUT inside a captured graph: the wait on the sources' flags is a kernel
+// comparing against the device epoch (a stream memory operation would freeze
+// the epoch of the apply that was captured).
+dspmv_status issue_group_put_graph(Plan& p, ExGroup& g) {
+    g.issued = true;
+    if (g.empty()) return DSPMV_OK;
+    if (g.recv_from.size() > size_t(kMaxWaitPeers)) return fail(DSPMV_ERR_ARG, "too many peers for the graph wait");
+    CUDA_TRY(launch_wait_flags(p.d_flags, g.recv_from.data(), int(g.recv_from.size()), p.d_epoch, p.comm_stream));
+    CUDA_TRY(cudaEventRecord(g.ev, p.comm_stream));
+    return DSPMV_OK;
+}
+
 // LOCAL group: group gi of every rank (lock-step, so all ranks have posted it).
 dspmv_status issue_group_local(const std::vector<Schedule*>& ss, int gi) {
     if (!ss.empty() && ss[0]->plan->put_mode) {
@@ -558,10 +625,14 @@ dspmv_status issue_group_local(const std::vector<Schedule*>& ss, int gi) {
         g.issued = true;
         const RankPlan& h = pr.host;
         for (int q : g.recv_from) {
+            if (pr.skip_exchange) break;
             const Plan* src = ss[q]->plan;
-            const size_t off_src = size_t(src->host.send_displ[h.rank]) * pr.esize;
+            const char* from = src->pack_alias
+                                   ? static_cast<const char*>(src->cur_x) + size_t(src->alias_off[h.rank]) * pr.esize
+                                   : static_cast<const char*>(src->d_sendbuf) +
+                                         size_t(src->host.send_displ[h.rank]) * pr.esize;
             CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(pr.d_recvbuf) + size_t(h.recv_displ[q]) * pr.esize,
-                                     static_cast<const char*>(src->d_sendbuf) + off_src,
+                                     from,
                                      size_t(h.recv_count[q]) * pr.esize, cudaMemcpyDeviceToDevice, pr.comm_stream));
         }
         if (!g.empty()) CUDA_TRY(cudaEventRecord(g.ev, pr.comm_stream));
@@ -664,6 +735,13 @@ dspmv_status begin_apply(Schedule& s, cudaStream_t caller) {
     s.end_alias = -1;
     std::fill(s.t0_alias.begin(), s.t0_alias.end(), 0);
     ++p.epoch;
+    if (p.d_epoch) {   // PUT: the kernels read the epoch from device memory
+        auto wv = write_value32();
+        if (!wv) return fail(DSPMV_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+        const CUresult r = wv(reinterpret_cast<CUstream>(caller), reinterpret_cast<CUdeviceptr>(p.d_epoch), p.epoch,
+                              CU_STREAM_WRITE_VALUE_DEFAULT);
+        if (r != CUDA_SUCCESS) return fail(DSPMV_ERR_CUDA, "cuStreamWriteValue32 failed (" + std::to_string(int(r)) + ")");
+    }
     CUDA_TRY(cudaEventRecord(p.ev_start, caller));
     // schedule stream 0 may be the caller's stream itself (no cross-stream
     // wait for its work); the others wait on the caller's START point
@@ -682,22 +760,21 @@ cudaError_t launch_gpu_vertex(Schedule& s, int t, const void* x, void* y, cudaSt
     switch (s.ops[t].kind) {
         case DSPMV_OP_PACK: {
             const int q = s.op_peer[t];  // -2: every destination; -1: nothing to send
-            if (q == -1) break;
+            if (q == -1 || p.pack_alias) break;
             if (p.streaming && p.pipe.pack_chunk >= 0) {  // x still arriving (apply_host)
                 e = cudaStreamWaitEvent(st, p.pipe.ev_x[p.pipe.pack_chunk], 0);
                 if (e != cudaSuccess) break;
             }
             if (p.put_mode) {
-                void* const* dst = p.d_seg_dst + (p.epoch & 1u) * p.put_nseg;
                 if (q == -2) {
-                    PutArgs a{x, p.d_pack_map, 0, int64_t(p.host.pack_map.size()), p.d_seg_begin, dst, p.d_seg_flag,
-                              p.put_nseg, p.epoch, p.d_put_counter + p.put_nseg};
+                    PutArgs a{x, p.d_pack_map, 0, int64_t(p.host.pack_map.size()), p.d_seg_begin, p.d_seg_dst,
+                              p.d_seg_flag, p.put_nseg, p.put_nseg, p.d_epoch, p.d_put_counter + p.put_nseg};
                     e = launch_pack_put(p.dtype, a, st);
                 } else {
                     const int j = s.op_seg[t];
                     const int64_t k0 = p.host.send_displ[q];
-                    PutArgs a{x, p.d_pack_map, k0, k0 + p.host.send_count[q], p.d_seg_begin + j, dst + j,
-                              p.d_seg_flag + j, 1, p.epoch, p.d_put_counter + j};
+                    PutArgs a{x, p.d_pack_map, k0, k0 + p.host.send_count[q], p.d_seg_begin + j, p.d_seg_dst + j,
+                              p.d_seg_flag + j, 1, p.put_nseg, p.d_epoch, p.d_put_counter + j};
                     e = launch_pack_put(p.dtype, a, st);
                 }
             } else if (q == -2) {
@@ -710,7 +787,7 @@ cudaError_t launch_gpu_vertex(Schedule& s, int t, const void* x, void* y, cudaSt
             break;
         }
         case DSPMV_OP_SPMV_LOCAL: {
-            SpmvOperands op{x, y, p.d_partL, p.d_partR, p.d_ticket};
+            SpmvOperands op{x, y, p.d_partL, p.explicit_acc, p.d_partR, p.d_ticket};
             if (!p.streaming) {
                 e = launch_spmv(p.L, p.dtype, op, st);
                 break;
@@ -736,8 +813,15 @@ cudaError_t launch_gpu_vertex(Schedule& s, int t, const void* x, void* y, cudaSt
         case DSPMV_OP_UNPACK: {
             const int q = s.op_peer[t];
             if (q == -1) break;
-            const char* src = static_cast<const char*>(p.d_recvbuf) +
-                              (p.put_mode && (p.epoch & 1u) ? p.recv_stride * size_t(p.esize) : 0);
+            if (p.put_mode) {   // receive-buffer parity of this apply, from the device epoch
+                const size_t off = q == -2 ? 0 : size_t(p.host.recv_displ[q]) * p.esize;
+                const int64_t cnt = q == -2 ? int64_t(p.host.halo_gid.size()) : p.host.recv_count[q];
+                e = launch_copy_parity(p.dtype, static_cast<const char*>(p.d_recvbuf) + off,
+                                       p.recv_stride * size_t(p.esize), p.d_epoch,
+                                       static_cast<char*>(p.d_xhalo) + off, cnt, st);
+                break;
+            }
+            const char* src = static_cast<const char*>(p.d_recvbuf);
             if (q == -2) {
                 e = launch_copy(p.dtype, src, p.d_xhalo, int64_t(p.host.halo_gid.size()), st);
             } else {
@@ -747,7 +831,7 @@ cudaError_t launch_gpu_vertex(Schedule& s, int t, const void* x, void* y, cudaSt
             break;
         }
         case DSPMV_OP_SPMV_REMOTE: {
-            SpmvOperands op{p.d_xhalo, y, p.d_partR, p.d_partL, p.d_ticket};
+            SpmvOperands op{p.d_xhalo, y, p.d_partR, p.explicit_acc, p.d_partL, p.d_ticket};
             e = launch_spmv(p.R, p.dtype, op, st);
             break;
         }
@@ -839,6 +923,58 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
     return DSPMV_OK;
 }
 
+// DSPMV_ACC_EXPLICIT_IN_END: after END every GPU vertex has completed,
+// so one kernel on the caller's stream adds the deposited partials.
+dspmv_status end_combine(Schedule& s, void* y, cudaStream_t st) {
+    Plan& p = *s.plan;
+    if (!p.explicit_acc || p.host.ar_rows.empty()) return DSPMV_OK;
+    CUDA_TRY(launch_combine_end(p.dtype, p.d_partL, p.d_partR, p.d_ar_rows, y, int64_t(p.host.ar_rows.size()), st));
+    if (s.origin == st) s.origin_dirty = true;
+    return DSPMV_OK;
+}
+
+// FNV-1a over bytes
+uint64_t fnv1a(const void* data, size_t n, uint64_t h = 1469598103934665603ull) {
+    const unsigned char* b = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    return h;
+}
+
+// opts.debug_checks: does every rank hold the same value?  NCCL: all-reduce
+// MIN of (h, ~h) -- equal everywhere iff min(h) == ~min(~h) = max(h); HOST:
+// the caller's allgather; LOCAL: compared over the group's plans.
+dspmv_status ranks_agree(Plan& p, uint64_t h, bool* same) {
+    *same = true;
+    Comm& c = *p.comm;
+    if (c.nranks == 1) return DSPMV_OK;
+    if (c.kind == DSPMV_COMM_NCCL) {
+        DevScratch d;
+        CUDA_TRY(cudaMalloc(&d.p, 16));
+        const uint64_t hv[2] = {h, ~h};
+        CUDA_TRY(cudaMemcpyAsync(d.p, hv, 16, cudaMemcpyHostToDevice, p.comm_stream));
+        NCCL_TRY(ncclAllReduce(d.p, d.p, 2, ncclUint64, ncclMin, c.nccl, p.comm_stream));
+        uint64_t r[2];
+        CUDA_TRY(cudaMemcpyAsync(r, d.p, 16, cudaMemcpyDeviceToHost, p.comm_stream));
+        CUDA_TRY(cudaStreamSynchronize(p.comm_stream));
+        *same = r[0] == ~r[1];
+    } else if (c.kind == DSPMV_COMM_HOST) {
+        std::vector<uint64_t> all(size_t(c.nranks));
+        if (c.allgather(&h, all.data(), 8, c.allgather_ctx) != 0) return fail(DSPMV_ERR_ARG, "allgather failed");
+        for (uint64_t v : all) *same &= v == h;
+    }
+    return DSPMV_OK;
+}
+
+dspmv_status check_schedule_hash(Schedule& s) {
+    Plan& p = *s.plan;
+    if (!p.opts.debug_checks || s.hash_checked || p.comm->kind == DSPMV_COMM_LOCAL) return DSPMV_OK;
+    bool same = true;
+    ST_TRY(ranks_agree(p, fnv1a(s.ops.data(), s.ops.size() * sizeof(dspmv_op), fnv1a(&s.n_streams, 4)), &same));
+    if (!same) return fail(DSPMV_ERR_SCHEDULE, "debug check: the ranks apply different schedules (P:460)");
+    s.hash_checked = true;
+    return DSPMV_OK;
+}
+
 // ------------------------------------------------ GPU-resident schedules
 // Capture the schedule into a CUDA graph (NEXT-3 (iii)): GPU vertices,
 // CER and CSWE are captured as they are; a host synchronisation point (CES,
@@ -848,20 +984,43 @@ dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
 // captured on the comm stream; START/END are the fork from / join into the
 // caller's stream.  Timed ops record external events, so op times and the
 // timeline work unchanged.
-dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t origin) {
-    Plan& p = *s.plan;
-    if (p.put_mode && p.has_peers)
-        return fail(DSPMV_ERR_ARG, "apply_graph: the PUT exchange carries a per-apply epoch; use dspmv_apply");
-    if (p.comm->kind == DSPMV_COMM_LOCAL && p.host.nranks > 1)
-        return fail(DSPMV_ERR_ARG, "apply_graph: LOCAL groups with > 1 rank run with dspmv_apply_group");
-    if (!s.compiled) ST_TRY(compile_exchange(s));
-    for (auto& e : s.gev)
-        if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    const int ns = s.n_streams;
-    std::vector<cudaStream_t> st(ns);
-    for (int i = 0; i < ns; ++i) st[i] = (i == 0 && p.opts.caller_stream0) ? origin : p.streams[i];
-    std::vector<cudaStream_t> all(st);
-    if (p.has_peers) all.push_back(p.comm_stream);
+// One capture serves a single rank (dspmv_apply_graph) or every rank of a
+// LOCAL group in lock-step (dspmv_apply_graph_group: one graph, each rank's
+// ops on that rank's own streams, so the ranks' branches run concurrently).
+// The graph and the pointers it was captured for are stored on ss[0].
+dspmv_status capture_graph(const std::vector<Schedule*>& ss, const std::vector<const void*>& xs,
+                           const std::vector<void*>& ys, cudaStream_t origin) {
+    const int R = int(ss.size());
+    const bool group = R > 1;
+    Schedule& s0 = *ss[0];
+    for (Schedule* sp : ss) {
+        if (!sp->compiled) ST_TRY(compile_exchange(*sp));
+        for (auto& e : sp->gev)
+            if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    // per rank: schedule streams (stream 0 may be the origin for one rank
+    // only), all streams incl. the comm stream, Pack-done events (COPY groups)
+    struct RankCap {
+        std::vector<cudaStream_t> st, all;
+        bool ev_trivial[DSPMV_MAX_EVENTS] = {};
+        std::vector<cudaEvent_t> pack_ev;   // by destination rank, recorded after its Pack
+    };
+    std::vector<RankCap> rc(R);
+    for (int r = 0; r < R; ++r) {
+        Plan& p = *ss[r]->plan;
+        const int ns = ss[r]->n_streams;
+        rc[r].st.resize(ns);
+        for (int i = 0; i < ns; ++i) rc[r].st[i] = (i == 0 && p.opts.caller_stream0 && !group) ? origin : p.streams[i];
+        rc[r].all = rc[r].st;
+        if (p.has_peers) rc[r].all.push_back(p.comm_stream);
+        if (group && !p.put_mode) {
+            if (p.g_pack_ev.empty()) {
+                p.g_pack_ev.assign(size_t(p.host.nranks), nullptr);
+                for (auto& e : p.g_pack_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            }
+            rc[r].pack_ev.assign(size_t(p.host.nranks), nullptr);
+        }
+    }
     auto is_origin = [&](cudaStream_t q) { return q == origin; };
     const uint64_t launches0 = g_launches.load();
     CUDA_TRY(cudaStreamBeginCapture(origin, cudaStreamCaptureModeThreadLocal));
@@ -877,22 +1036,35 @@ dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t ori
         if (_e != cudaSuccess)                                                                 \
             return abort_capture(fail(DSPMV_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e))); \
     } while (0)
-    if (s.step0) CAP_TRY(cudaEventRecordWithFlags(s.step0, origin, cudaEventRecordExternal));
-    CAP_TRY(cudaEventRecord(s.gev[0], origin));
-    // timestamp aliasing (runtime.h): track what lands on the origin stream
-    bool odirty = !s.step0, others = false;
+    for (Schedule* sp : ss)
+        if (sp->step0) CAP_TRY(cudaEventRecordWithFlags(sp->step0, origin, cudaEventRecordExternal));
+    // PUT: the first node advances the device epoch (the host executor writes
+    // it at START instead); every Pack / Unpack / flag wait of this graph
+    // reads it, so one captured graph serves every apply
+    bool any_epoch = false;
+    for (Schedule* sp : ss)
+        if (sp->plan->d_epoch) {
+            CAP_TRY(launch_epoch_bump(sp->plan->d_epoch, origin));
+            any_epoch = true;
+        }
+    CAP_TRY(cudaEventRecord(s0.gev[0], origin));
+    // timestamp aliasing (runtime.h), single rank only: track what lands on
+    // the origin stream
+    bool odirty = !s0.step0 || any_epoch || group, others = false;
     int otail = -1;
-    std::vector<char> a0(s.ops.size(), 0);
-    for (int& v : s.ev_on) v = 0;
-    // an event recorded on another stream before any node landed there marks
-    // the fork point: waiting on it moves nothing
-    bool ev_trivial[DSPMV_MAX_EVENTS] = {};
-    for (cudaStream_t q : all)
-        if (!is_origin(q)) CAP_TRY(cudaStreamWaitEvent(q, s.gev[0], 0));
-    // every stream waits on ev; the stream ev was recorded on (from, if
-    // known) needs no wait on itself
-    auto all_wait = [&](cudaEvent_t ev, cudaStream_t from, bool trivial) -> cudaError_t {
-        for (cudaStream_t q : all) {
+    std::vector<std::vector<char>> a0(R);
+    for (int r = 0; r < R; ++r) {
+        a0[r].assign(ss[r]->ops.size(), 0);
+        for (int& v : ss[r]->ev_on) v = 0;
+        for (cudaStream_t q : rc[r].all)
+            if (!is_origin(q)) CAP_TRY(cudaStreamWaitEvent(q, s0.gev[0], 0));
+        for (ExGroup& g : ss[r]->groups) g.ps = g.pr = g.issued = false;
+        ss[r]->plan->cur_x = xs[r];
+    }
+    // every stream of rank r waits on ev; the stream ev was recorded on
+    // (from, if known) needs no wait on itself
+    auto all_wait = [&](int r, cudaEvent_t ev, cudaStream_t from, bool trivial) -> cudaError_t {
+        for (cudaStream_t q : rc[r].all) {
             if (q == from) continue;
             cudaError_t e = cudaStreamWaitEvent(q, ev, 0);
             if (e != cudaSuccess) return e;
@@ -900,106 +1072,187 @@ dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t ori
         }
         return cudaSuccess;
     };
-    for (ExGroup& g : s.groups) g.ps = g.pr = g.issued = false;
-    for (int t = 0; t < int(s.ops.size()); ++t) {
-        const dspmv_op& o = s.ops[t];
-        const bool gpu = is_gpu_vertex(o.kind);
-        cudaStream_t q = (gpu || o.kind == DSPMV_OP_EVENT_RECORD || o.kind == DSPMV_OP_STREAM_WAIT_EVENT)
-                             ? st[o.stream] : nullptr;
-        const bool timed = gpu && s.timing && s.t0[t];
-        if (timed) {
-            if (is_origin(q) && !odirty) a0[t] = 1;  // same position as START
-            else CAP_TRY(cudaEventRecordWithFlags(s.t0[t], q, cudaEventRecordExternal));
-            if (!is_origin(q)) others = true;
+    const int n_ops = int(s0.ops.size());
+    for (int t = 0; t < n_ops; ++t) {
+        for (int r = 0; r < R; ++r) {
+            Schedule& s = *ss[r];
+            Plan& p = *s.plan;
+            const dspmv_op& o = s.ops[t];
+            const bool gpu = is_gpu_vertex(o.kind);
+            cudaStream_t q = (gpu || o.kind == DSPMV_OP_EVENT_RECORD || o.kind == DSPMV_OP_STREAM_WAIT_EVENT)
+                                 ? rc[r].st[o.stream] : nullptr;
+            const bool timed = gpu && s.timing && s.t0[t];
+            if (timed) {
+                if (is_origin(q) && !odirty) a0[r][t] = 1;  // same position as START
+                else CAP_TRY(cudaEventRecordWithFlags(s.t0[t], q, cudaEventRecordExternal));
+                if (!is_origin(q)) others = true;
+            }
+            switch (o.kind) {
+                case DSPMV_OP_PACK:
+                case DSPMV_OP_SPMV_LOCAL:
+                case DSPMV_OP_UNPACK:
+                case DSPMV_OP_SPMV_REMOTE: {
+                    const uint64_t l0 = g_launches.load();
+                    CAP_TRY(launch_gpu_vertex(s, t, xs[r], ys[r], q));
+                    if (g_launches.load() != l0) {
+                        if (is_origin(q)) odirty = true, otail = -1;
+                        else others = true;
+                    }
+                    // LOCAL COPY group: the receivers' copies wait for this Pack
+                    if (o.kind == DSPMV_OP_PACK && !rc[r].pack_ev.empty() && s.op_peer[t] != -1) {
+                        const int qd = s.op_peer[t];
+                        cudaEvent_t ev = p.g_pack_ev[qd == -2 ? 0 : qd];
+                        CAP_TRY(cudaEventRecord(ev, q));
+                        for (int d = 0; d < p.host.nranks; ++d)
+                            if (qd == -2 || d == qd) rc[r].pack_ev[d] = ev;
+                    }
+                    break;
+                }
+                case DSPMV_OP_POST_SEND:
+                case DSPMV_OP_POST_RECV: {
+                    ExGroup& g = s.groups[s.op_group[t]];
+                    (o.kind == DSPMV_OP_POST_SEND ? g.ps : g.pr) = true;
+                    const bool tx = s.timing && s.t0[t];
+                    cudaStream_t xs_ = p.has_peers ? p.comm_stream : origin;  // comm joins only with peers
+                    if (tx) CAP_TRY(cudaEventRecordWithFlags(s.t0[t], xs_, cudaEventRecordExternal));
+                    if (g.ps && g.pr && !g.issued && (!group || p.put_mode)) {
+                        // captured on the comm stream: the NCCL group, or (PUT) a
+                        // kernel waiting for the sources' epoch flags
+                        dspmv_status st_ = p.put_mode ? issue_group_put_graph(p, g) : issue_group_nccl(p, g);
+                        if (st_ != DSPMV_OK) return abort_capture(st_);
+                    }
+                    if (tx && !group) CAP_TRY(cudaEventRecordWithFlags(s.t1[t], xs_, cudaEventRecordExternal));
+                    if (tx || p.has_peers) {
+                        if (is_origin(xs_)) odirty = true, otail = -1;
+                        else others = true;
+                    }
+                    break;
+                }
+                case DSPMV_OP_WAIT_SEND:
+                case DSPMV_OP_WAIT_RECV: {
+                    const ExGroup& g = s.groups[s.op_group[t]];
+                    if (!g.empty()) CAP_TRY(all_wait(r, g.ev, nullptr, false));
+                    break;
+                }
+                case DSPMV_OP_EVENT_RECORD:
+                    CAP_TRY(cudaEventRecord(s.ev[o.event], q));
+                    s.ev_on[o.event] = o.stream + 1;
+                    rc[r].ev_trivial[o.event] = !is_origin(q) && !others;
+                    break;
+                case DSPMV_OP_EVENT_SYNC:
+                    CAP_TRY(all_wait(r, s.ev[o.event], s.ev_on[o.event] ? rc[r].st[s.ev_on[o.event] - 1] : nullptr,
+                                     rc[r].ev_trivial[o.event]));
+                    break;
+                case DSPMV_OP_STREAM_WAIT_EVENT:
+                    CAP_TRY(cudaStreamWaitEvent(q, s.ev[o.event], 0));
+                    if (is_origin(q) && !rc[r].ev_trivial[o.event]) odirty = true, otail = -1;
+                    break;
+                default:
+                    break;
+            }
+            if (timed) {
+                CAP_TRY(cudaEventRecordWithFlags(s.t1[t], q, cudaEventRecordExternal));
+                if (is_origin(q)) odirty = true, otail = t;
+            }
         }
-        switch (o.kind) {
-            case DSPMV_OP_PACK:
-            case DSPMV_OP_SPMV_LOCAL:
-            case DSPMV_OP_UNPACK:
-            case DSPMV_OP_SPMV_REMOTE: {
-                const uint64_t l0 = g_launches.load();
-                CAP_TRY(launch_gpu_vertex(s, t, x, y, q));
-                if (g_launches.load() != l0) {
-                    if (is_origin(q)) odirty = true, otail = -1;
-                    else others = true;
+        // LOCAL COPY group, lock-step: group gi is posted on every rank at op t
+        if (group && !s0.plan->put_mode) {
+            const int gi = s0.op_group[t];
+            if (gi >= 0 && s0.groups[gi].ps && s0.groups[gi].pr && !s0.groups[gi].issued) {
+                for (int r = 0; r < R; ++r) {
+                    Plan& pr = *ss[r]->plan;
+                    ExGroup& g = ss[r]->groups[gi];
+                    g.issued = true;
+                    const RankPlan& h = pr.host;
+                    for (int q : g.recv_from) {
+                        if (pr.skip_exchange) break;
+                        if (cudaEvent_t ev = rc[q].pack_ev.empty() ? nullptr : rc[q].pack_ev[h.rank])
+                            CAP_TRY(cudaStreamWaitEvent(pr.comm_stream, ev, 0));
+                        const Plan* src = ss[q]->plan;
+                        const char* from = src->pack_alias
+                                               ? static_cast<const char*>(xs[q]) + size_t(src->alias_off[h.rank]) * pr.esize
+                                               : static_cast<const char*>(src->d_sendbuf) +
+                                                     size_t(src->host.send_displ[h.rank]) * pr.esize;
+                        CAP_TRY(cudaMemcpyAsync(static_cast<char*>(pr.d_recvbuf) + size_t(h.recv_displ[q]) * pr.esize,
+                                                from, size_t(h.recv_count[q]) * pr.esize, cudaMemcpyDeviceToDevice,
+                                                pr.comm_stream));
+                    }
+                    if (!g.empty()) CAP_TRY(cudaEventRecord(g.ev, pr.comm_stream));
                 }
-                break;
             }
-            case DSPMV_OP_POST_SEND:
-            case DSPMV_OP_POST_RECV: {
-                ExGroup& g = s.groups[s.op_group[t]];
-                (o.kind == DSPMV_OP_POST_SEND ? g.ps : g.pr) = true;
-                const bool tx = s.timing && s.t0[t];
-                cudaStream_t xs = p.has_peers ? p.comm_stream : origin;  // comm joins the capture only with peers
-                if (tx) CAP_TRY(cudaEventRecordWithFlags(s.t0[t], xs, cudaEventRecordExternal));
-                if (g.ps && g.pr && !g.issued) {
-                    dspmv_status r = issue_group_nccl(p, g);  // captured on the comm stream
-                    if (r != DSPMV_OK) return abort_capture(r);
-                }
-                if (tx) CAP_TRY(cudaEventRecordWithFlags(s.t1[t], xs, cudaEventRecordExternal));
-                if (tx || p.has_peers) {
-                    if (is_origin(xs)) odirty = true, otail = -1;
-                    else others = true;
-                }
-                break;
-            }
-            case DSPMV_OP_WAIT_SEND:
-            case DSPMV_OP_WAIT_RECV: {
-                const ExGroup& g = s.groups[s.op_group[t]];
-                if (!g.empty()) CAP_TRY(all_wait(g.ev, nullptr, false));
-                break;
-            }
-            case DSPMV_OP_EVENT_RECORD:
-                CAP_TRY(cudaEventRecord(s.ev[o.event], q));
-                s.ev_on[o.event] = o.stream + 1;
-                ev_trivial[o.event] = !is_origin(q) && !others;
-                break;
-            case DSPMV_OP_EVENT_SYNC:
-                CAP_TRY(all_wait(s.ev[o.event], s.ev_on[o.event] ? st[s.ev_on[o.event] - 1] : nullptr,
-                                 ev_trivial[o.event]));
-                break;
-            case DSPMV_OP_STREAM_WAIT_EVENT:
-                CAP_TRY(cudaStreamWaitEvent(q, s.ev[o.event], 0));
-                if (is_origin(q) && !ev_trivial[o.event]) odirty = true, otail = -1;
-                break;
-            default:
-                break;
         }
-        if (timed) {
-            CAP_TRY(cudaEventRecordWithFlags(s.t1[t], q, cudaEventRecordExternal));
-            if (is_origin(q)) odirty = true, otail = t;
+        if (group) {   // timed Posts of a group: the exchange interval on each comm stream
+            for (int r = 0; r < R; ++r) {
+                Schedule& s = *ss[r];
+                const int k = s.ops[t].kind;
+                if ((k == DSPMV_OP_POST_SEND || k == DSPMV_OP_POST_RECV) && s.timing && s.t0[t])
+                    CAP_TRY(cudaEventRecordWithFlags(s.t1[t], s.plan->has_peers ? s.plan->comm_stream : origin,
+                                                     cudaEventRecordExternal));
+            }
         }
     }
+    bool any_explicit = false;
+    for (Schedule* sp : ss) any_explicit |= sp->plan->explicit_acc;
     // END directly behind an op's end event on origin, with no node on any
     // other stream: that event is END (no second record)
-    const int ealias = (s.step1 && otail >= 0 && !others) ? otail : -1;
+    const int ealias = (!group && s0.step1 && otail >= 0 && !others && !any_explicit) ? otail : -1;
     // join every stream back into the origin
     int k = 1;
-    for (cudaStream_t q : all) {
-        if (is_origin(q)) continue;
-        CAP_TRY(cudaEventRecord(s.gev[k], q));
-        CAP_TRY(cudaStreamWaitEvent(origin, s.gev[k], 0));
-        ++k;
+    for (int r = 0; r < R; ++r) {
+        Schedule& s = *ss[r];
+        for (cudaStream_t q : rc[r].all) {
+            if (is_origin(q)) continue;
+            cudaEvent_t ev = s.gev[k];   // k <= DSPMV_MAX_STREAMS + 1
+            CAP_TRY(cudaEventRecord(ev, q));
+            CAP_TRY(cudaStreamWaitEvent(origin, ev, 0));
+            ++k;
+        }
+        k = 1;
     }
-    if (s.step1 && ealias < 0) CAP_TRY(cudaEventRecordWithFlags(s.step1, origin, cudaEventRecordExternal));
+    for (int r = 0; r < R; ++r) {
+        if (ss[r]->plan->explicit_acc) {
+            const dspmv_status cst = end_combine(*ss[r], ys[r], origin);
+            if (cst != DSPMV_OK) return abort_capture(cst);
+        }
+    }
+    for (Schedule* sp : ss)
+        if (sp->step1 && ealias < 0) CAP_TRY(cudaEventRecordWithFlags(sp->step1, origin, cudaEventRecordExternal));
 #undef CAP_TRY
     cudaGraph_t g = nullptr;
     CUDA_TRY(cudaStreamEndCapture(origin, &g));
     // captured launches run with each graph launch, not now
-    s.graph_kernels = g_launches.load() - launches0;
-    g_launches.fetch_sub(s.graph_kernels);
-    if (s.gexec) cudaGraphExecDestroy(s.gexec), s.gexec = nullptr;
-    const cudaError_t ie = cudaGraphInstantiate(&s.gexec, g, 0);
+    s0.graph_kernels = g_launches.load() - launches0;
+    g_launches.fetch_sub(s0.graph_kernels);
+    if (s0.gexec) cudaGraphExecDestroy(s0.gexec), s0.gexec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&s0.gexec, g, 0);
     cudaGraphDestroy(g);
     if (ie != cudaSuccess) return fail(DSPMV_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie));
-    s.gx = x;
-    s.gy = y;
-    s.g_timing = s.timing;
-    if (s.timing) {
-        s.g_t0_alias = a0;
-        s.g_end_alias = ealias;
+    s0.gx = xs[0];
+    s0.gy = ys[0];
+    s0.g_group.clear();
+    if (group)
+        for (int r = 0; r < R; ++r) {
+            s0.g_group.push_back(ss[r]);
+            s0.g_group_ptrs.push_back(xs[r]);
+            s0.g_group_ptrs.push_back(ys[r]);
+        }
+    for (int r = 0; r < R; ++r) {
+        Schedule& s = *ss[r];
+        s.g_timing = s.timing;
+        if (s.timing) {
+            s.g_t0_alias = a0[r];
+            s.g_end_alias = ealias;
+        }
     }
     return DSPMV_OK;
+}
+
+dspmv_status capture_graph(Schedule& s, const void* x, void* y, cudaStream_t origin) {
+    Plan& p = *s.plan;
+    if (p.comm->kind == DSPMV_COMM_LOCAL && p.host.nranks > 1)
+        return fail(DSPMV_ERR_ARG, "apply_graph: LOCAL groups with > 1 rank run with dspmv_apply_graph_group");
+    s.g_group_ptrs.clear();
+    return capture_graph(std::vector<Schedule*>{&s}, std::vector<const void*>{x}, std::vector<void*>{y}, origin);
 }
 
 std::mutex g_flush_mu;
@@ -1128,12 +1381,17 @@ void dspmv_plan_opts_default(dspmv_plan_opts* o) {
     o->exchange = DSPMV_EXCHANGE_COPY;
     if (const char* ev = std::getenv("DSPMV_CALLER_STREAM0")) o->caller_stream0 = std::atoi(ev);
     if (const char* ev = std::getenv("DSPMV_RESERVE_SMS")) o->reserve_sms = std::atoi(ev);
+    if (const char* ev = std::getenv("DSPMV_DEBUG_CHECKS")) o->debug_checks = std::atoi(ev);
 }
 
 static void free_plan_device(Plan& p) {
     for (void* a : p.ipc_opened) cudaIpcCloseMemHandle(a);
     p.ipc_opened.clear();
-    for (void* a : p.allocs) cudaFree(a);
+    if (!p.allocs.empty()) cudaDeviceSynchronize();   // nothing of the plan in flight
+    for (const auto& a : p.allocs) {
+        if (a.cb) p.opts.free(a.ptr, a.bytes, p.device, p.opts.alloc_ctx);
+        else cudaFree(a.ptr);
+    }
     p.allocs.clear();
     for (auto& s : p.streams)
         if (s) cudaStreamDestroy(s), s = nullptr;
@@ -1142,6 +1400,9 @@ static void free_plan_device(Plan& p) {
     for (auto& e : p.pipe.ev_x)
         if (e) cudaEventDestroy(e), e = nullptr;
     if (p.pipe.ev_in) cudaEventDestroy(p.pipe.ev_in), p.pipe.ev_in = nullptr;
+    for (auto& e : p.g_pack_ev)
+        if (e) cudaEventDestroy(e);
+    p.g_pack_ev.clear();
     if (p.ev_start) cudaEventDestroy(p.ev_start), p.ev_start = nullptr;
 }
 
@@ -1185,12 +1446,14 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
     p->nnz_L = int64_t(h.al_col.size());
     p->nnz_R = int64_t(h.ar_col.size());
 
-    // streams: schedule streams + comm stream (highest priority if requested)
+    // streams: schedule streams + comm stream (highest priority if requested).
+    // Every schedule stream gets the same priority: the design space treats
+    // the streams as interchangeable (stream-bijection pruning), so
+    // no schedule stream may be privileged.
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     for (int i = 0; i < DSPMV_MAX_STREAMS; ++i) {
-        const int prio = (opts.comm_priority && i == 0) ? hi : lo;
-        if (cudaStreamCreateWithPriority(&p->streams[i], cudaStreamNonBlocking, prio) != cudaSuccess)
+        if (cudaStreamCreateWithPriority(&p->streams[i], cudaStreamNonBlocking, lo) != cudaSuccess)
             return bail(fail(DSPMV_ERR_CUDA, "cudaStreamCreateWithPriority failed"));
     }
     if (cudaStreamCreateWithPriority(&p->comm_stream, cudaStreamNonBlocking, opts.comm_priority ? hi : lo) !=
@@ -1213,6 +1476,7 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
                      use_stream(opts, h.al_rowptr.data(), int32_t(h.n_local()), vthr));
         build_host_pipe(*p, L);   // also stores each block's x chunk in desc[15]
         if ((st = upload_layout(*p, L, c, p->L)) != DSPMV_OK) return bail(st);
+        p->L.x_bytes = h.n_local() * p->esize;
     }
     {
         std::vector<int32_t> slotR(nR);
@@ -1222,22 +1486,27 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
         build_layout(h.ar_rowptr.data(), nR, h.ar_col.data(), h.ar_val.data(), p->esize, h.ar_rows.data(),
                      slotR.data(), vthr, kBlockCfgs[c], R, use_stream(opts, h.ar_rowptr.data(), nR, vthr));
         if ((st = upload_layout(*p, R, c, p->R)) != DSPMV_OK) return bail(st);
+        p->R.x_bytes = int64_t(h.halo_gid.size()) * p->esize;
     }
     const size_t hsz = h.halo_gid.size();
     p->put_mode = opts.exchange == DSPMV_EXCHANGE_PUT;
-    if (opts.exchange != DSPMV_EXCHANGE_COPY && opts.exchange != DSPMV_EXCHANGE_PUT)
+    p->skip_exchange = opts.exchange == DSPMV_EXCHANGE_NONE;
+    if (opts.exchange != DSPMV_EXCHANGE_COPY && opts.exchange != DSPMV_EXCHANGE_PUT &&
+        opts.exchange != DSPMV_EXCHANGE_NONE)
         return bail(fail(DSPMV_ERR_ARG, "bad exchange mode"));
     // PUT: two receive buffers (apply parity) -- a rank may run one apply ahead
     // parity stride padded to 256 B so both halves stay 16-B aligned for Unpack
     p->recv_stride = ((hsz * p->esize + 255) / 256 * 256) / p->esize;
     if ((st = dev_alloc(*p, &p->d_recvbuf,
-                        p->put_mode ? std::max<size_t>(2 * p->recv_stride * p->esize, 256) : hsz * p->esize, true)) !=
-        DSPMV_OK)
+                        p->put_mode ? std::max<size_t>(2 * p->recv_stride * p->esize, 256) : hsz * p->esize, true,
+                        p->put_mode)) != DSPMV_OK)
         return bail(st);
     if (p->put_mode) {
         // own allocation (IPC-exportable); at least one word so every rank has a handle
-        if ((st = dev_alloc(*p, reinterpret_cast<void**>(&p->d_flags), size_t(comm->nranks) * 4, true)) != DSPMV_OK)
+        if ((st = dev_alloc(*p, reinterpret_cast<void**>(&p->d_flags), size_t(comm->nranks) * 4, true, true)) !=
+            DSPMV_OK)
             return bail(st);
+        if ((st = dev_alloc(*p, reinterpret_cast<void**>(&p->d_epoch), 4, true)) != DSPMV_OK) return bail(st);
         // last-CTA counters: one per destination segment (per-destination Pack) + one
         if ((st = dev_alloc(*p, reinterpret_cast<void**>(&p->d_put_counter), size_t(comm->nranks + 1) * 4, true)) !=
             DSPMV_OK)
@@ -1247,6 +1516,14 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
     if ((st = dev_alloc(*p, &p->d_partL, size_t(nR) * p->esize, true)) != DSPMV_OK) return bail(st);
     if ((st = dev_alloc(*p, &p->d_partR, size_t(nR) * p->esize, true)) != DSPMV_OK) return bail(st);
     if ((st = dev_alloc(*p, reinterpret_cast<void**>(&p->d_ticket), size_t(nR) * 4, true)) != DSPMV_OK)
+        return bail(st);
+    p->explicit_acc = opts.accumulate_mode == DSPMV_ACC_EXPLICIT_IN_END;
+    if (opts.accumulate_mode != DSPMV_ACC_TICKET && !p->explicit_acc)
+        return bail(fail(DSPMV_ERR_ARG, "bad accumulate_mode"));
+    if (opts.pack_mode != DSPMV_PACK_GATHER && opts.pack_mode != DSPMV_PACK_ALIAS_IF_CONTIGUOUS)
+        return bail(fail(DSPMV_ERR_ARG, "bad pack_mode"));
+    if (p->explicit_acc && nR > 0 &&
+        (st = dev_upload(*p, &p->d_ar_rows, h.ar_rows.data(), h.ar_rows.size())) != DSPMV_OK)
         return bail(st);
     if (!opts.keep_host) {
         std::vector<int32_t>().swap(h.al_rowptr);
@@ -1259,11 +1536,18 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
 
     // phase 2: request lists -> send counts + pack maps
     if (comm->kind == DSPMV_COMM_NCCL || comm->kind == DSPMV_COMM_HOST) {
-        if (comm->kind == DSPMV_COMM_HOST && !p->put_mode)
+        if (comm->kind == DSPMV_COMM_HOST && !p->put_mode && !p->skip_exchange)
             return bail(fail(DSPMV_ERR_ARG, "plans on a HOST comm need exchange = DSPMV_EXCHANGE_PUT"));
         st = comm->kind == DSPMV_COMM_NCCL ? exchange_requests_nccl(*p) : exchange_requests_allgather(*p);
         if (st != DSPMV_OK) return bail(st);
         if ((st = finalize_send(*p)) != DSPMV_OK) return bail(st);
+        if (opts.debug_checks) {   // COLLECTIVE arguments agree across ranks
+            const int64_t key[6] = {n_global, comm->nranks, opts.dtype, opts.exchange, opts.pack_mode,
+                                    opts.accumulate_mode};
+            bool same = true;
+            if ((st = ranks_agree(*p, fnv1a(key, sizeof(key)), &same)) != DSPMV_OK) return bail(st);
+            if (!same) return bail(fail(DSPMV_ERR_ARG, "debug check: plan_create arguments differ across ranks"));
+        }
         if (p->put_mode && comm->nranks > 1 && (st = setup_put_nccl(*p)) != DSPMV_OK) return bail(st);
     } else {
         LocalGroup& g = *comm->group;
@@ -1331,8 +1615,13 @@ dspmv_status dspmv_plan_info_get(dspmv_plan_t plan, dspmv_plan_info* out) {
     out->grid_remote = plan->R.grid_s;
     out->ready = plan->ready;
     out->device_bytes = plan->device_bytes;
-    out->s_kernel_local = plan->L.stream ? DSPMV_SKERNEL_STREAM : DSPMV_SKERNEL_BLOCK;
-    out->s_kernel_remote = plan->R.stream ? DSPMV_SKERNEL_STREAM : DSPMV_SKERNEL_BLOCK;
+    auto skern = [](const DevLayout& D) {
+        return D.stream ? (D.stream_tma ? DSPMV_SKERNEL_STREAM_TMA : DSPMV_SKERNEL_STREAM) : DSPMV_SKERNEL_BLOCK;
+    };
+    out->s_kernel_local = skern(plan->L);
+    out->s_kernel_remote = skern(plan->R);
+    out->pack_alias = plan->pack_alias ? 1 : 0;
+    out->accumulate_mode = plan->explicit_acc ? DSPMV_ACC_EXPLICIT_IN_END : DSPMV_ACC_TICKET;
     return DSPMV_OK;
 }
 
@@ -1682,7 +1971,9 @@ dspmv_status dspmv_apply(dspmv_schedule_t s, const void* x, void* y, dspmv_strea
     if (p.comm->kind == DSPMV_COMM_LOCAL && p.host.nranks > 1)
         return fail(DSPMV_ERR_ARG, "LOCAL groups with >1 rank use dspmv_apply_group");
     if (p.host.n_local() > 0 && (!x || !y)) return fail(DSPMV_ERR_ARG, "null x/y");
+    ST_TRY(check_schedule_hash(*s));
     ST_TRY(begin_apply(*s, static_cast<cudaStream_t>(stream)));
+    p.cur_x = x;
     const bool local = p.comm->kind == DSPMV_COMM_LOCAL;
     for (int t = 0; t < int(s->ops.size()); ++t) {
         ST_TRY(exec_op(*s, t, x, y, local));
@@ -1690,6 +1981,7 @@ dspmv_status dspmv_apply(dspmv_schedule_t s, const void* x, void* y, dspmv_strea
         if (local && gi >= 0 && s->groups[gi].ps && s->groups[gi].pr && !s->groups[gi].issued)
             ST_TRY(issue_group_local({s}, gi));
     }
+    ST_TRY(end_combine(*s, y, static_cast<cudaStream_t>(stream)));
     if (s->step1) CUDA_TRY(cudaEventRecord(s->step1, static_cast<cudaStream_t>(stream)));
     s->timed_valid = s->timing;
     return DSPMV_OK;
@@ -1705,18 +1997,70 @@ dspmv_status dspmv_apply_graph(dspmv_schedule_t s, const void* x, void* y, dspmv
     if (cudaGetDevice(&cur) != cudaSuccess || cur != p.device) CUDA_TRY(cudaSetDevice(p.device));
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     if (!cs) return fail(DSPMV_ERR_ARG, "apply_graph needs a non-default stream");
-    if (!s->gexec || s->gx != x || s->gy != y || s->g_timing != s->timing) ST_TRY(capture_graph(*s, x, y, cs));
+    ST_TRY(check_schedule_hash(*s));
+    if (!s->gexec || !s->g_group.empty() || s->gx != x || s->gy != y || s->g_timing != s->timing)
+        ST_TRY(capture_graph(*s, x, y, cs));
     const cudaError_t e = cudaGraphLaunch(s->gexec, cs);
     if (e != cudaSuccess) {
         p.poisoned = true;
         return fail(DSPMV_ERR_CUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
     }
+    if (p.d_epoch) ++p.epoch;   // the graph bumped the device copy (keeps host-mode applies in step)
     g_launches.fetch_add(s->graph_kernels, std::memory_order_relaxed);
     if (s->timing) {
         s->t0_alias = s->g_t0_alias;
         s->end_alias = s->g_end_alias;
     }
     s->timed_valid = s->timing;
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_apply_graph_group(const dspmv_schedule_t* scheds, int nranks, const void* const* x,
+                                     void* const* y, dspmv_stream_t stream) {
+    if (!scheds || nranks < 1 || !x || !y) return fail(DSPMV_ERR_ARG, "null argument");
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    if (!cs) return fail(DSPMV_ERR_ARG, "apply_graph_group needs a non-default stream");
+    std::vector<Schedule*> ss(nranks);
+    std::vector<const void*> xs(x, x + nranks);
+    std::vector<void*> ys(y, y + nranks);
+    for (int r = 0; r < nranks; ++r) {
+        if (!scheds[r]) return fail(DSPMV_ERR_ARG, "null schedule");
+        Plan* p = scheds[r]->plan;
+        if (p->comm->kind != DSPMV_COMM_LOCAL || p->comm->nranks != nranks || p->comm->rank != r)
+            return fail(DSPMV_ERR_ARG, "schedules must be ranks 0..n-1 of one LOCAL group");
+        if (r > 0 && p->comm->group != scheds[0]->plan->comm->group) return fail(DSPMV_ERR_ARG, "mixed groups");
+        if (scheds[r]->ops.size() != scheds[0]->ops.size() ||
+            std::memcmp(scheds[r]->ops.data(), scheds[0]->ops.data(), sizeof(dspmv_op) * scheds[0]->ops.size()))
+            return fail(DSPMV_ERR_ARG, "every rank must run the same schedule (P:460)");
+        if (p->poisoned) return fail(DSPMV_ERR_STATE, "plan is poisoned by an earlier error");
+        if (!p->ready) return fail(DSPMV_ERR_STATE, "plan not ready");
+        if (p->host.n_local() > 0 && (!x[r] || !y[r])) return fail(DSPMV_ERR_ARG, "null x/y");
+        ss[r] = scheds[r];
+    }
+    Schedule& s0 = *ss[0];
+    CUDA_TRY(cudaSetDevice(s0.plan->device));
+    bool fresh = s0.gexec && s0.g_group.size() == size_t(nranks);
+    for (int r = 0; fresh && r < nranks; ++r)
+        fresh = s0.g_group[r] == ss[r] && s0.g_group_ptrs[2 * r] == x[r] && s0.g_group_ptrs[2 * r + 1] == y[r] &&
+                ss[r]->g_timing == ss[r]->timing;
+    if (!fresh) {
+        s0.g_group_ptrs.clear();
+        ST_TRY(capture_graph(ss, xs, ys, cs));
+    }
+    const cudaError_t e = cudaGraphLaunch(s0.gexec, cs);
+    if (e != cudaSuccess) {
+        for (Schedule* sp : ss) sp->plan->poisoned = true;
+        return fail(DSPMV_ERR_CUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
+    }
+    g_launches.fetch_add(s0.graph_kernels, std::memory_order_relaxed);
+    for (Schedule* sp : ss) {
+        ++sp->plan->epoch;
+        if (sp->timing) {
+            sp->t0_alias = sp->g_t0_alias;
+            sp->end_alias = sp->g_end_alias;
+        }
+        sp->timed_valid = sp->timing;
+    }
     return DSPMV_OK;
 }
 
@@ -1821,6 +2165,7 @@ dspmv_status dspmv_apply_group(const dspmv_schedule_t* scheds, int nranks, const
     for (int r = 0; r < nranks; ++r) {
         ST_TRY(begin_apply(*scheds[r], static_cast<cudaStream_t>(stream)));
         scheds[r]->origin_dirty = true;  // the ranks share the caller stream: no timestamp aliasing
+        plans[r]->cur_x = x[r];
     }
     std::vector<Schedule*> ss(scheds, scheds + nranks);
     const int n_ops = int(scheds[0]->ops.size());
@@ -1832,6 +2177,7 @@ dspmv_status dspmv_apply_group(const dspmv_schedule_t* scheds, int nranks, const
             ST_TRY(issue_group_local(ss, gi));
     }
     for (int r = 0; r < nranks; ++r) {
+        ST_TRY(end_combine(*scheds[r], y[r], static_cast<cudaStream_t>(stream)));
         if (scheds[r]->step1) CUDA_TRY(cudaEventRecord(scheds[r]->step1, static_cast<cudaStream_t>(stream)));
         scheds[r]->timed_valid = scheds[r]->timing;
     }

@@ -50,6 +50,11 @@ constexpr int kDescInts = 16;      // per-block descriptor: r0 r1 p0 p1 flag wb[
 constexpr int kStreamTile = 256;   // CSR-stream tile: nnz per warp pass (8 per lane)
 constexpr int kStreamRows = 64;    // CSR-stream tile: rows
 constexpr int kStreamWarps = 8;    // CSR-stream CTA: warps (one tile each)
+// CSR-stream with a TMA producer (spmv_stream_tma_kernel): a block is kStreamWarps
+// consecutive tiles, staged whole (col, val, rowptr slice) by one producer warp
+constexpr int kSTBlockNnz = kStreamWarps * kStreamTile;    // 2048
+constexpr int kSTBlockRows = kStreamWarps * kStreamRows;   // 512
+constexpr int kSTStages = 3;                               // ring slots per CTA
 constexpr int kDefaultVectorThreshold = 256;  // rows above: warp-per-row kernel
 constexpr int kMaxClass = 5;       // row classes: 2^c lanes per row, c = 0..5
 constexpr int kBinWindow = 4096;   // rows are binned by class within such windows
@@ -100,6 +105,9 @@ struct Layout {
     // matrix-row order (no class binning)
     bool stream = false;
     std::vector<int32_t> s_tiles;      // 2 per tile
+    // the same tiles grouped kStreamWarps at a time for the TMA-producer
+    // variant: r0 r1 p0 p1 flag tb[0..kStreamWarps] per block (kDescInts)
+    std::vector<int32_t> s_tdesc;
 };
 // out_row / slot nullable: identity / no combine.
 // Plan-time choice of the row-block configuration for one matrix: measured

@@ -283,6 +283,23 @@ void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, cons
             L.s_tiles.push_back(t1);
             t0 = t1;
         }
+        // TMA-producer blocks: kStreamWarps consecutive tiles (tile w of a
+        // block is consumer warp w's), flag = any row needs the combine
+        L.s_tdesc.clear();
+        const int32_t nt = int32_t(L.s_tiles.size() / 2);
+        for (int32_t b = 0; b < nt; b += kStreamWarps) {
+            const int32_t e = std::min(nt, b + kStreamWarps);
+            int32_t d[kDescInts] = {};
+            d[0] = L.s_tiles[2 * b];
+            d[1] = L.s_tiles[2 * (e - 1) + 1];
+            d[2] = L.s_rowptr[d[0]];
+            d[3] = L.s_rowptr[d[1]];
+            bool flag = false;
+            for (int32_t r = d[0]; r < d[1]; ++r) flag |= L.s_slot[r] >= 0;
+            d[4] = flag ? 1 : 0;
+            for (int w = 0; w <= kStreamWarps; ++w) d[5 + w] = b + w < e ? L.s_tiles[2 * (b + w)] : d[1];
+            L.s_tdesc.insert(L.s_tdesc.end(), d, d + kDescInts);
+        }
     }
 }
 

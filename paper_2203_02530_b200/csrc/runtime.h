@@ -39,6 +39,12 @@ struct DevLayout {
     int32_t ntiles = 0;
     int grid_t = 0;
     int32_t* s_tiles = nullptr;
+    // TMA-producer variant of the CSR-stream kernel (Layout::s_tdesc)
+    bool stream_tma = false;
+    int32_t ntblocks = 0;
+    int grid_tt = 0;
+    int32_t* s_tdesc = nullptr;
+    int64_t x_bytes = 0;               // bytes of the x operand (L2 access-policy window)
 };
 
 // Operands of one SpMV op (y_L or y_R) for the kernels.
@@ -46,6 +52,7 @@ struct SpmvOperands {
     const void* x = nullptr;           // x_L (caller) or x_halo
     void* y = nullptr;                 // caller's y
     void* my_part = nullptr;           // this op's partial for combined rows
+    bool explicit_acc = false;         // deposit only; END combines (DSPMV_ACC_EXPLICIT_IN_END)
     const void* other_part = nullptr;  // the other op's partial
     unsigned* ticket = nullptr;        // per combined row, epoch counter
     // streamed x (dspmv_apply_host): row block b waits until
@@ -58,29 +65,47 @@ struct SpmvOperands {
 int block_kernel_smem_bytes(int dtype, int cfg);
 int block_kernel_ctas_per_sm(int dtype, int cfg);
 int stream_kernel_ctas_per_sm(int dtype);
+int stream_tma_kernel_ctas_per_sm(int dtype);
+void set_x_persist_limit();   // experiment DSPMV_X_PERSIST (plan time)
 cudaError_t launch_spmv(const DevLayout& L, int dtype, const SpmvOperands& o, cudaStream_t s);
 // row blocks [b0, b1) of the S group, plus the V group (long rows) if vec
 cudaError_t launch_spmv_part(const DevLayout& L, int dtype, const SpmvOperands& o, cudaStream_t s, int32_t b0,
                              int32_t b1, bool vec);
 cudaError_t launch_pack(int dtype, const void* x, const int32_t* map, void* out, int64_t n,
                         cudaStream_t s);
+// DSPMV_ACC_EXPLICIT_IN_END: y[rows[k]] = partL[k] + partR[k], k < n
+cudaError_t launch_combine_end(int dtype, const void* partL, const void* partR, const int32_t* rows, void* y,
+                               int64_t n, cudaStream_t s);
 cudaError_t launch_copy(int dtype, const void* src, void* dst, int64_t n, cudaStream_t s);
 cudaError_t launch_flush(void* buf, size_t bytes, cudaStream_t s);
 // fused Pack + put (DSPMV_EXCHANGE_PUT): entries [seg_begin[j], seg_begin[j+1])
 // go to seg_dst[j] (peer receive buffer, this apply's parity); the last CTA
 // publishes `epoch` to every seg_flag[j] with a system-scope release.
+// The apply's epoch lives in device memory (*epoch, written by the host
+// executor at START or bumped by the first node of a captured graph), so one
+// captured graph serves every apply: the kernel picks the receive-buffer
+// parity (epoch & 1) and publishes the epoch itself.
 struct PutArgs {
     const void* x;
     const int32_t* pack_map;
     int64_t k0, n;              // send-list entries [k0, n)
     const int64_t* seg_begin;   // [nseg + 1]
-    void* const* seg_dst;       // [nseg]
+    void* const* seg_dst;       // [2][seg_stride]: parity 0 / parity 1 destinations
     unsigned* const* seg_flag;  // [nseg]
-    int nseg;
-    unsigned epoch;
+    int nseg, seg_stride;
+    const unsigned* epoch;
     unsigned* counter;          // last-CTA detection, self-resetting
 };
 cudaError_t launch_pack_put(int dtype, const PutArgs& a, cudaStream_t s);
+// PUT Unpack: dst = (recvbuf + (epoch & 1) * parity_bytes)[0, n)
+cudaError_t launch_copy_parity(int dtype, const void* recv, size_t parity_bytes, const unsigned* epoch, void* dst,
+                               int64_t n, cudaStream_t s);
+// PUT exchange inside a graph: wait until flags[peers[i]] >= *epoch for all i
+// (system-scope acquire); traps after ~30 s so a dead peer cannot hang the GPU
+cudaError_t launch_wait_flags(const unsigned* flags, const int* peers, int n, const unsigned* epoch,
+                              cudaStream_t s);
+cudaError_t launch_epoch_bump(unsigned* epoch, cudaStream_t s);
+constexpr int kMaxWaitPeers = 64;
 
 struct Plan;
 
@@ -122,15 +147,31 @@ struct Plan {
     cudaStream_t comm_stream = nullptr;
     cudaStream_t cur_stream0 = nullptr;  // stream of schedule stream 0 in this apply
     cudaEvent_t ev_start = nullptr;
-    std::vector<void*> allocs;
+    struct Alloc {
+        void* ptr;
+        size_t bytes;
+        bool cb;                       // from opts.alloc (else cudaMalloc)
+    };
+    std::vector<Alloc> allocs;
     int64_t device_bytes = 0;
     bool ready = false;                // phase 2 done (send lists, pack map)
     bool has_peers = false;            // anything to send or receive
     // DSPMV_EXCHANGE_PUT state
     bool put_mode = false;
+    bool skip_exchange = false;        // DSPMV_EXCHANGE_NONE (timing baseline)
+    // DSPMV_PACK_ALIAS_IF_CONTIGUOUS in effect: destination q's send list is
+    // x[alias_off[q] .. + send_count[q]), sent straight from x (no Pack kernel)
+    bool pack_alias = false;
+    std::vector<int64_t> alias_off;
+    const void* cur_x = nullptr;       // x of the apply being issued / captured
+    // DSPMV_ACC_EXPLICIT_IN_END: local row of each combined row (device)
+    int32_t* d_ar_rows = nullptr;
+    bool explicit_acc = false;
+    std::vector<cudaEvent_t> g_pack_ev;  // LOCAL group graphs: Pack done, per destination
     size_t recv_stride = 0;            // elements between the two receive buffers
     unsigned epoch = 0;                // applies so far (parity selects the receive buffer)
     unsigned* d_flags = nullptr;       // [P] epoch written by each source rank
+    unsigned* d_epoch = nullptr;       // this apply's epoch, device copy (PUT)
     unsigned* d_put_counter = nullptr;
     int put_nseg = 0;
     int64_t* d_seg_begin = nullptr;    // [nseg + 1]
@@ -189,12 +230,15 @@ struct Schedule {
     // per (x, y) into a CUDA graph with host synchronisation turned into
     // device-side joins
     cudaGraphExec_t gexec = nullptr;
+    std::vector<struct Schedule*> g_group;     // LOCAL group graph: the ranks' schedules (on rank 0's)
+    std::vector<const void*> g_group_ptrs;     // x_r, y_r the group graph was captured for
     const void* gx = nullptr;
     void* gy = nullptr;
     bool g_timing = false;
     uint64_t graph_kernels = 0;        // kernel nodes per graph launch (launch counter)
     cudaEvent_t gev[DSPMV_MAX_STREAMS + 2] = {};  // fork / join helpers
     bool timed_valid = false;
+    bool hash_checked = false;         // opts.debug_checks: ops agreed across ranks
     // Timestamp aliasing.  A timing event recorded right behind another one
     // on the same stream costs ~2.3 us on B200
     // (profiles/r1_ubench_graph_events.txt), so an event that would sit at

@@ -30,8 +30,10 @@ STATUS_NAMES = ["OK", "ERR_ARG", "ERR_RANGE", "ERR_SCHEDULE", "ERR_DEADLOCK", "E
                 "ERR_CUDA", "ERR_NCCL", "ERR_OOM"]
 DSPMV_F64, DSPMV_F32 = 0, 1
 DSPMV_COMM_NCCL, DSPMV_COMM_LOCAL, DSPMV_COMM_HOST = 0, 1, 2
-DSPMV_EXCHANGE_COPY, DSPMV_EXCHANGE_PUT = 0, 1
-DSPMV_SKERNEL_AUTO, DSPMV_SKERNEL_BLOCK, DSPMV_SKERNEL_STREAM = 0, 1, 2
+DSPMV_EXCHANGE_COPY, DSPMV_EXCHANGE_PUT, DSPMV_EXCHANGE_NONE = 0, 1, 2
+DSPMV_SKERNEL_AUTO, DSPMV_SKERNEL_BLOCK, DSPMV_SKERNEL_STREAM, DSPMV_SKERNEL_STREAM_TMA = 0, 1, 2, 3
+DSPMV_PACK_GATHER, DSPMV_PACK_ALIAS_IF_CONTIGUOUS = 0, 1
+DSPMV_ACC_TICKET, DSPMV_ACC_EXPLICIT_IN_END = 0, 1
 (DSPMV_OP_START, DSPMV_OP_PACK, DSPMV_OP_SPMV_LOCAL, DSPMV_OP_POST_SEND, DSPMV_OP_POST_RECV,
  DSPMV_OP_WAIT_SEND, DSPMV_OP_WAIT_RECV, DSPMV_OP_UNPACK, DSPMV_OP_SPMV_REMOTE, DSPMV_OP_END,
  DSPMV_OP_EVENT_RECORD, DSPMV_OP_EVENT_SYNC, DSPMV_OP_STREAM_WAIT_EVENT) = range(13)
@@ -50,12 +52,19 @@ class DspmvError(RuntimeError):
         super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 9 else status}: {msg}")
 
 
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p)
+
+
 class dspmv_plan_opts(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int32), ("vector_threshold", ctypes.c_int32),
                 ("keep_host", ctypes.c_int32), ("comm_priority", ctypes.c_int32),
                 ("block_cfg", ctypes.c_int32), ("caller_stream0", ctypes.c_int32),
                 ("reserve_sms", ctypes.c_int32), ("exchange", ctypes.c_int32),
-                ("s_kernel", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
+                ("s_kernel", ctypes.c_int32), ("pack_mode", ctypes.c_int32),
+                ("accumulate_mode", ctypes.c_int32), ("debug_checks", ctypes.c_int32),
+                ("reserved0", ctypes.c_int32),
+                ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", ctypes.c_void_p)]
 
 
 class dspmv_plan_info(ctypes.Structure):
@@ -70,7 +79,8 @@ class dspmv_plan_info(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
                 ("dtype", ctypes.c_int32), ("ready", ctypes.c_int32),
                 ("device_bytes", ctypes.c_int64),
-                ("s_kernel_local", ctypes.c_int32), ("s_kernel_remote", ctypes.c_int32)]
+                ("s_kernel_local", ctypes.c_int32), ("s_kernel_remote", ctypes.c_int32),
+                ("pack_alias", ctypes.c_int32), ("accumulate_mode", ctypes.c_int32)]
 
 
 class dspmv_op(ctypes.Structure):
@@ -131,6 +141,7 @@ _sig("dspmv_apply", [_P, _P, _P, _P])
 _sig("dspmv_apply_host", [_P, _P, _P, _P])
 _sig("dspmv_apply_graph", [_P, _P, _P, _P])
 _sig("dspmv_apply_group", [_P, _I, _P, _P, _P])
+_sig("dspmv_apply_graph_group", [_P, _I, _P, _P, _P])
 _sig("dspmv_l2_flush", [_I, _P])
 _sig("dspmv_launch_count", [_P])
 _sig("dspmv_profile_counters", [_P, _I, _I, _P])
@@ -193,13 +204,17 @@ def dspmv_comm_create(uid: bytes, nranks: int, rank: int, device: int):
     buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
     h = _P()
     _check(lib.dspmv_comm_create(buf, nranks, rank, device, ctypes.byref(h)))
+    h._device = device
     return h
 
 
 def dspmv_comm_create_local(nranks: int, device: int):
     hs = (_P * nranks)()
     _check(lib.dspmv_comm_create_local(nranks, device, hs))
-    return [_P(h) for h in hs]
+    out = [_P(h) for h in hs]
+    for h in out:
+        h._device = device
+    return out
 
 
 def dspmv_comm_create_host(nranks: int, rank: int, device: int, allgather):
@@ -218,6 +233,7 @@ def dspmv_comm_create_host(nranks: int, rank: int, device: int, allgather):
     h = _P()
     _check(lib.dspmv_comm_create_host(nranks, rank, device, cb, None, ctypes.byref(h)))
     h._cb = cb
+    h._device = device
     return h
 
 
@@ -231,12 +247,33 @@ def dspmv_comm_info(comm):
     return n.value, r.value, k.value
 
 
+def _torch_alloc(nbytes, device, ctx):
+    try:
+        import torch
+        return torch.cuda.caching_allocator_alloc(int(nbytes), int(device))
+    except Exception:  # noqa: BLE001 -- the library reports ERR_OOM
+        return None
+
+
+def _torch_free(ptr, nbytes, device, ctx):
+    import torch
+    torch.cuda.caching_allocator_delete(ptr)
+
+
+_TORCH_ALLOC = ALLOC_FN(_torch_alloc)
+_TORCH_FREE = FREE_FN(_torch_free)
+
+
 def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_F64,
                       vector_threshold: int = -1, keep_host: bool = False,
                       comm_priority: bool = True, block_cfg: int = -1,
                       caller_stream0: bool | None = None, reserve_sms: int | None = None,
-                      exchange: int = DSPMV_EXCHANGE_COPY, s_kernel: int = DSPMV_SKERNEL_AUTO):
-    """rowptr int64[n_local+1], col int32[nnz] (global ids), val float64/32."""
+                      exchange: int = DSPMV_EXCHANGE_COPY, s_kernel: int = DSPMV_SKERNEL_AUTO,
+                      pack_mode: int = DSPMV_PACK_GATHER, accumulate_mode: int = DSPMV_ACC_TICKET,
+                      debug_checks: bool | None = None, torch_alloc: bool = True):
+    """rowptr int64[n_local+1], col int32[nnz] (global ids), val float64/32.
+    torch_alloc: the plan's device memory comes from torch's caching allocator
+    (dspmv_plan_opts.alloc/free); False = cudaMalloc inside the library."""
     rowptr = np.ascontiguousarray(rowptr, np.int64)
     col = np.ascontiguousarray(col_global, np.int32)
     val = np.ascontiguousarray(val, np.float32 if dtype == DSPMV_F32 else np.float64)
@@ -253,11 +290,24 @@ def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_
         o.reserve_sms = int(reserve_sms)
     o.exchange = int(exchange)
     o.s_kernel = int(s_kernel)
+    o.pack_mode = int(pack_mode)
+    o.accumulate_mode = int(accumulate_mode)
+    if debug_checks is not None:
+        o.debug_checks = int(debug_checks)
+    if torch_alloc:
+        o.alloc, o.free = _TORCH_ALLOC, _TORCH_FREE
     h = _P()
     _check(lib.dspmv_plan_create(comm, n_global, len(rowptr) - 1, rowptr.ctypes.data,
                                  col.ctypes.data, val.ctypes.data, ctypes.byref(o),
                                  ctypes.byref(h)))
+    info = dspmv_plan_info_get(h)
+    # what apply-time argument checks need (dtype, rows, device)
+    h._meta = (dtype, int(info["row_end"] - info["row_begin"]), _comm_device(comm))
     return h
+
+
+def _comm_device(comm):
+    return getattr(comm, "_device", None)
 
 
 def dspmv_plan_destroy(plan):
@@ -460,7 +510,33 @@ def dspmv_schedule_create(plan, ops, n_streams: int):
     h = _P()
     _check(lib.dspmv_schedule_create(plan, a.ctypes.data, len(a), n_streams, ctypes.byref(h)))
     h._n_ops = len(a)
+    h._meta = getattr(plan, "_meta", None)
     return h
+
+
+def _check_vec(sched, v, name, host: bool):
+    """Tensors passed to an apply must match the plan: dtype, >= n_local
+    elements, contiguous, on the plan's device (device applies) or in host
+    memory (apply_host).  Raw pointers / numpy arrays pass unchecked except
+    numpy dtype and length."""
+    meta = getattr(sched, "_meta", None)
+    if meta is None or v is None or isinstance(v, int):
+        return
+    dtype, n_local, device = meta
+    want = "float32" if dtype == DSPMV_F32 else "float64"
+    if isinstance(v, np.ndarray):
+        if v.dtype != np.dtype(want) or v.size < n_local or not v.flags.c_contiguous:
+            raise DspmvError(DSPMV_ERR_ARG, f"{name}: need a contiguous {want} array of >= {n_local} elements")
+        return
+    if not hasattr(v, "data_ptr"):
+        return
+    if str(v.dtype).split(".")[-1] != want or v.numel() < n_local or not v.is_contiguous():
+        raise DspmvError(DSPMV_ERR_ARG, f"{name}: need a contiguous {want} tensor of >= {n_local} elements, "
+                                        f"got {v.dtype} {tuple(v.shape)}")
+    if host and v.is_cuda:
+        raise DspmvError(DSPMV_ERR_ARG, f"{name}: apply_host takes host memory")
+    if not host and n_local > 0 and (not v.is_cuda or (device is not None and v.device.index != device)):
+        raise DspmvError(DSPMV_ERR_ARG, f"{name}: must be on cuda:{device}")
 
 
 def dspmv_schedule_destroy(sched):
@@ -490,25 +566,46 @@ def dspmv_schedule_op_timeline(sched, n: int | None = None):
 
 def dspmv_apply(sched, x, y, stream=None):
     """x, y: device buffers (torch tensors or raw pointers)."""
+    _check_vec(sched, x, "x", False)
+    _check_vec(sched, y, "y", False)
     _check(lib.dspmv_apply(sched, _ptr(x), _ptr(y), _stream(stream)))
 
 
 def dspmv_apply_graph(sched, x, y, stream):
     """GPU-resident (CUDA-graph) execution; stream-ordered, non-blocking."""
+    _check_vec(sched, x, "x", False)
+    _check_vec(sched, y, "y", False)
     _check(lib.dspmv_apply_graph(sched, _ptr(x), _ptr(y), _stream(stream)))
 
 
 def dspmv_apply_host(sched, x_host, y_host, stream=None):
     """x_host, y_host: host buffers (numpy or pinned torch CPU tensors)."""
+    _check_vec(sched, x_host, "x_host", True)
+    _check_vec(sched, y_host, "y_host", True)
     _check(lib.dspmv_apply_host(sched, _ptr(x_host), _ptr(y_host), _stream(stream)))
 
 
 def dspmv_apply_group(scheds, xs, ys, stream=None):
     n = len(scheds)
+    for s, x, y in zip(scheds, xs, ys):
+        _check_vec(s, x, "x", False)
+        _check_vec(s, y, "y", False)
     sa = (_P * n)(*[s.value for s in scheds])
     xa = (_P * n)(*[_ptr(x) for x in xs])
     ya = (_P * n)(*[_ptr(y) for y in ys])
     _check(lib.dspmv_apply_group(sa, n, xa, ya, _stream(stream)))
+
+
+def dspmv_apply_graph_group(scheds, xs, ys, stream):
+    """LOCAL group as ONE CUDA graph (every rank's branch concurrent); stream-ordered."""
+    n = len(scheds)
+    for s, x, y in zip(scheds, xs, ys):
+        _check_vec(s, x, "x", False)
+        _check_vec(s, y, "y", False)
+    sa = (_P * n)(*[s.value for s in scheds])
+    xa = (_P * n)(*[_ptr(x) for x in xs])
+    ya = (_P * n)(*[_ptr(y) for y in ys])
+    _check(lib.dspmv_apply_graph_group(sa, n, xa, ya, _stream(stream)))
 
 
 def dspmv_l2_flush(device: int = 0, stream=None):

@@ -43,7 +43,8 @@ class LocalRun:
     """P LOCAL ranks on cuda:0 holding the row blocks of one global matrix."""
 
     def __init__(self, n, rp, col, val, P, dtype=D.DSPMV_F64, vector_threshold=-1,
-                 keep_host=False, block_cfg=-1, exchange=D.DSPMV_EXCHANGE_COPY, s_kernel=D.DSPMV_SKERNEL_AUTO):
+                 keep_host=False, block_cfg=-1, exchange=D.DSPMV_EXCHANGE_COPY, s_kernel=D.DSPMV_SKERNEL_AUTO,
+                 **opts):
         self.n, self.P, self.dtype = n, P, dtype
         self.tdt = torch.float32 if dtype == D.DSPMV_F32 else torch.float64
         self.rb = D.dspmv_partition(n, P)
@@ -56,7 +57,7 @@ class LocalRun:
             self.plans.append(D.dspmv_plan_create(self.comms[r], n, rpr, col[lo:hi], val[lo:hi],
                                                   dtype=dtype, vector_threshold=vector_threshold,
                                                   keep_host=keep_host, block_cfg=block_cfg, s_kernel=s_kernel,
-                                                  exchange=exchange))
+                                                  exchange=exchange, **opts))
         self.scheds = []
 
     def schedule(self, ops, n_streams=2):

@@ -500,9 +500,10 @@ def test_timestamp_aliasing_keeps_times_consistent():
         D.dspmv_comm_destroy(comm)
 
 
+@pytest.mark.parametrize("skern", [D.DSPMV_SKERNEL_STREAM, D.DSPMV_SKERNEL_STREAM_TMA])
 @pytest.mark.parametrize("name", ["pl20k", "rand300", "7pt32", "27pt20"])
 @pytest.mark.parametrize("P", [1, 3])
-def test_stream_kernel_bitwise_vs_oracle(name, P):
+def test_stream_kernel_bitwise_vs_oracle(name, P, skern):
     """CSR-stream S group (DSPMV_SKERNEL_STREAM): every row of <= 256 nnz is
     summed in stored order by one lane from rounded products, so y equals the
     oracle's O2 loops bit for bit on every row whose A_L and A_R parts both go
@@ -510,10 +511,10 @@ def test_stream_kernel_bitwise_vs_oracle(name, P):
     kernel) within the R-Q11 tolerance."""
     n, (rp, col, val) = _mat(name)
     x = gen.x_values((0, n))
-    run = LocalRun(n, rp, col, val, P, s_kernel=D.DSPMV_SKERNEL_STREAM)
+    run = LocalRun(n, rp, col, val, P, s_kernel=skern)
     try:
         y = run.apply(run.schedule(derive_ops()), x, reps=2)
-        assert all(D.dspmv_plan_info_get(p)["s_kernel_local"] == D.DSPMV_SKERNEL_STREAM for p in run.plans)
+        assert all(D.dspmv_plan_info_get(p)["s_kernel_local"] == skern for p in run.plans)
     finally:
         run.close()
     plans = O2.plan_all(rp, col, n, P)
@@ -552,7 +553,8 @@ def test_stream_kernel_auto_choice_and_fp32():
     assert within_tol(y, O1.o1_spmv(rp, col, vr, xr), O1.o1_absdot(rp, col, vr, xr), 1e-5)
 
 
-def test_stream_kernel_edge_cases():
+@pytest.mark.parametrize("skern", [D.DSPMV_SKERNEL_STREAM, D.DSPMV_SKERNEL_STREAM_TMA])
+def test_stream_kernel_edge_cases(skern):
     """CSR-stream with no S rows at all (every row > 256 nnz: the long-row
     kernel alone), with runs of empty rows (tiles whose rows sum to +0), and
     a 1-row matrix."""
@@ -569,7 +571,7 @@ def test_stream_kernel_edge_cases():
     cases.append((1, np.array([0, 1], np.int64), np.array([0], np.int32), np.array([2.5])))
     for n, rp, col, val in cases:
         x = gen.x_values((0, n))
-        run = LocalRun(n, rp, col, val, 1, s_kernel=D.DSPMV_SKERNEL_STREAM)
+        run = LocalRun(n, rp, col, val, 1, s_kernel=skern)
         try:
             y = run.apply(run.schedule(derive_ops()), x)
         finally:
