@@ -152,7 +152,8 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
                 D.stream_tma = true;
                 D.ntblocks = int32_t(L.s_tdesc.size() / kDescInts);
                 ST_TRY(dev_upload(p, &D.s_tdesc, L.s_tdesc.data(), L.s_tdesc.size()));
-                const int bpsm = stream_tma_kernel_ctas_per_sm(p.dtype);
+                D.st_variant = stream_tma_variant();
+                const int bpsm = stream_tma_kernel_ctas_per_sm(p.dtype, D.st_variant);
                 D.grid_tt = std::max(1, std::min(D.ntblocks, bpsm * usable));
             }
         }

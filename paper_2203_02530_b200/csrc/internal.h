@@ -54,7 +54,7 @@ constexpr int kStreamWarps = 8;    // CSR-stream CTA: warps (one tile each)
 // consecutive tiles, staged whole (col, val, rowptr slice) by one producer warp
 constexpr int kSTBlockNnz = kStreamWarps * kStreamTile;    // 2048
 constexpr int kSTBlockRows = kStreamWarps * kStreamRows;   // 512
-constexpr int kSTStages = 3;                               // ring slots per CTA
+constexpr int kDefaultStVariant = 2;   // kernels.cu kStVariants: 3 slots, 2 CTAs/SM, pipelined
 constexpr int kDefaultVectorThreshold = 256;  // rows above: warp-per-row kernel
 constexpr int kMaxClass = 5;       // row classes: 2^c lanes per row, c = 0..5
 constexpr int kBinWindow = 4096;   // rows are binned by class within such windows

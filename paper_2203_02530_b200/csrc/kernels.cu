@@ -32,6 +32,7 @@
 // fl(a+b) = fl(b+a), so y is bitwise identical for every schedule.
 // SpMV is not a dense contraction: no tensor cores (north_star).
 #include <cuda/atomic>
+#include <atomic>
 #include <cuda_runtime.h>
 #include <cstdlib>
 
@@ -152,12 +153,41 @@ __device__ __forceinline__ float ldg_x(const float* p, uint64_t pol) {
     return v;
 }
 
+// x still arriving (dspmv_apply_host pipeline, SpmvOperands::xflag): the
+// producer lane acquires the chunk flag and the mbarrier hands that on to the
+// consumers, but the read-only (.nc) path requires x to be immutable for the
+// whole kernel -- so the streamed-x instantiation (kCoh) gathers with plain
+// weak global loads (L1 not allocated), which the acquire chain orders.
+template <bool kNoL1, bool kCoh>
+__device__ __forceinline__ double load_x(const double* p, uint64_t pol) {
+    if constexpr (kCoh) {
+        double v;
+        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+        return v;
+    } else {
+        return ldg_x<kNoL1>(p, pol);
+    }
+}
+template <bool kNoL1, bool kCoh>
+__device__ __forceinline__ float load_x(const float* p, uint64_t pol) {
+    if constexpr (kCoh) {
+        float v;
+        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+        return v;
+    } else {
+        return ldg_x<kNoL1>(p, pol);
+    }
+}
+
 template <typename T> __device__ __forceinline__ T mul_rn(T a, T b);
 template <> __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 template <> __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 template <typename T> __device__ __forceinline__ T add_rn(T a, T b);
 template <> __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 template <> __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+template <typename T> __device__ __forceinline__ T fma_rn(T a, T b, T c);
+template <> __device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+template <> __device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 
 struct BlockArgs {
     const int32_t* rowptr;
@@ -213,7 +243,7 @@ struct Cfg {
 // entry, then a shuffle tree over the L lanes -- tolerance, R-Q10).  Lanes
 // of consecutive rows read consecutive columns for banded rows, so the x
 // gathers coalesce; up to 8 gathers per lane are in flight per chunk.
-template <typename T, bool kIdentity, bool kOneLane, int CH, bool kNoL1, typename St>
+template <typename T, bool kIdentity, bool kOneLane, int CH, bool kNoL1, bool kCoh, typename St>
 __device__ __forceinline__ void block_rows(const St& S, int lgL_rt, int w0, int w1, int a0, int ra0,
                                            bool blk_combine, int lane, const T* __restrict__ x,
                                            T* __restrict__ y, const int32_t* __restrict__ out,
@@ -238,7 +268,7 @@ __device__ __forceinline__ void block_rows(const St& S, int lgL_rt, int w0, int 
                         if (DSPMV_DIAG_GATHER == 1) xv[k] = T(S.col[q + k * L]);
                         else xv[k] = ldg_x<kNoL1>(x + (r & 0xfffff), xpol);
 #else
-                        xv[k] = ldg_x<kNoL1>(x + S.col[q + k * L], xpol);
+                        xv[k] = load_x<kNoL1, kCoh>(x + S.col[q + k * L], xpol);
 #endif
                     }
 #pragma unroll
@@ -261,7 +291,7 @@ __device__ __forceinline__ void block_rows(const St& S, int lgL_rt, int w0, int 
     }
 }
 
-template <typename T, int CFG, bool kCombine, bool kIdentity>
+template <typename T, int CFG, bool kCombine, bool kIdentity, bool kCoh>
 __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_ctas)
     spmv_block_kernel(BlockArgs a, SpmvOperands o) {
     using C = Cfg<CFG>;
@@ -354,11 +384,11 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
 
         const int lgL = S.hdr[4] >> 8;
         if (lgL == 0)
-            block_rows<T, kIdentity, true, kBlockCfgs[CFG].chunk, C::kNoL1>(S, 0, w0, w1, a0, ra0, blk_combine,
-                                                                            lane, x, y, out, slot, o, xpol);
+            block_rows<T, kIdentity, true, kBlockCfgs[CFG].chunk, C::kNoL1, kCoh>(S, 0, w0, w1, a0, ra0, blk_combine,
+                                                                                  lane, x, y, out, slot, o, xpol);
         else
-            block_rows<T, kIdentity, false, 8, C::kNoL1>(S, lgL, w0, w1, a0, ra0, blk_combine, lane, x, y, out, slot,
-                                                         o, xpol);
+            block_rows<T, kIdentity, false, 8, C::kNoL1, kCoh>(S, lgL, w0, w1, a0, ra0, blk_combine, lane, x, y, out,
+                                                               slot, o, xpol);
         __syncwarp();
 #ifdef DSPMV_PROFILE
         if (lane == 0) {
@@ -370,7 +400,11 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
     }
 }
 
-// Rows > vector_threshold: warp w of nw takes rows w, w + nw, ...
+// Rows > vector_threshold: warp w of nw takes rows w, w + nw, ...  Each lane
+// accumulates every 32nd product with a fused multiply-add (one rounding per
+// term, __fma_rn), then a shuffle tree adds the 32 lane sums: a different
+// summation order and rounding than the oracle's loop, checked by the R-Q11
+// tolerance (DESIGN.md R-Q10).
 template <typename T, bool kCombine>
 __device__ __forceinline__ void vector_rows(const VecArgs& a, const SpmvOperands& o, int w, int nw) {
     const int lane = threadIdx.x & 31;
@@ -390,11 +424,11 @@ __device__ __forceinline__ void vector_rows(const VecArgs& a, const SpmvOperands
                 v[u] = __ldcs(val + p + 32 * u);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc += v[u] * ldg_x<true>(x + c[u], xpol);
+            for (int u = 0; u < 4; ++u) acc = fma_rn(v[u], ldg_x<true>(x + c[u], xpol), acc);
         }
-        for (; p < p1; p += 32) acc += __ldcs(val + p) * ldg_x<true>(x + __ldcs(a.col + p), xpol);
+        for (; p < p1; p += 32) acc = fma_rn(__ldcs(val + p), ldg_x<true>(x + __ldcs(a.col + p), xpol), acc);
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        for (int off = 16; off > 0; off >>= 1) acc = add_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
         if (lane == 0) {
             const int32_t orow = a.out[i];
             if (kCombine) {
@@ -511,9 +545,19 @@ struct __align__(16) StStage {
     int32_t rp[kSTBlockRows + kPad];
     int32_t hdr[kDescInts];
 };
-template <typename T>
+// Variants (measured on C4, K1c): ring slots, CTAs per SM, and
+// whether a consumer warp issues the gathers of its next block before it
+// sums the rows of the current one (the gather latency then overlaps the
+// stored-order row sums instead of following them).
+struct StVariant {
+    int stages, min_ctas;
+    bool pipe;
+};
+constexpr StVariant kStVariants[] = {{3, 2, false}, {2, 4, false}, {3, 2, true}, {2, 3, true}};
+constexpr int kNumStVariants = 4;
+template <typename T, int V>
 constexpr int st_smem_bytes() {
-    return kSTStages * int(sizeof(StStage<T>)) + 2 * kSTStages * 8;
+    return kStVariants[V].stages * int(sizeof(StStage<T>)) + 2 * kStVariants[V].stages * 8;
 }
 
 struct StreamTmaArgs {
@@ -527,16 +571,83 @@ struct StreamTmaArgs {
     VecArgs v;              // rows > vector_threshold (nV = 0: none / launched apart)
 };
 
+// One consumer warp's tile of a staged block: tile rows [t0, t1), entries
+// [e0, e1) of the stage (<= kStreamTile).
+struct StTile {
+    int32_t a0, ra0, t0, t1, e0, e1;
+    bool combine;
+    int32_t ro[2], rs[2];   // output row / combine slot of rows t0 + lane (+ 32), loaded early
+};
+
 template <typename T, bool kCombine, bool kIdentity>
-__global__ void __launch_bounds__((kStreamWarps + 1) * 32, 2)
+__device__ __forceinline__ StTile st_tile(const StStage<T>& S, int warp, int lane, const int32_t* __restrict__ out,
+                                          const int32_t* __restrict__ slot) {
+    StTile t;
+    t.a0 = S.hdr[2];
+    t.ra0 = S.hdr[3];
+    t.combine = kCombine && (S.hdr[4] & 1) != 0;
+    t.t0 = S.hdr[5 + warp];
+    t.t1 = S.hdr[6 + warp];
+    t.e0 = S.rp[t.t0 - t.ra0] - t.a0;
+    t.e1 = S.rp[t.t1 - t.ra0] - t.a0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int32_t r = t.t0 + lane + 32 * j;
+        const bool ok = r < t.t1;
+        t.ro[j] = kIdentity ? r : (ok ? __ldg(out + r) : 0);
+        t.rs[j] = (t.combine && ok) ? __ldg(slot + r) : -1;
+    }
+    return t;
+}
+
+template <typename T, int K>
+__device__ __forceinline__ void st_gather(const StStage<T>& S, const StTile& t, int lane, const T* __restrict__ x,
+                                          uint64_t xpol, T (&xv)[K]) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int q = t.e0 + lane + 32 * k;
+        xv[k] = q < t.e1 ? ldg_x<true>(x + S.col[q], xpol) : T(0);
+    }
+}
+
+template <typename T, int K>
+__device__ __forceinline__ void st_products(StStage<T>& S, const StTile& t, int lane, const T (&xv)[K]) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int q = t.e0 + lane + 32 * k;
+        if (q < t.e1) S.val[q] = mul_rn(S.val[q], xv[k]);
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void st_rowsums(const StStage<T>& S, const StTile& t, int lane, T* __restrict__ y,
+                                           const SpmvOperands& o) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int32_t r = t.t0 + lane + 32 * j;
+        if (r >= t.t1) break;
+        const int32_t q0 = S.rp[r - t.ra0] - t.a0, q1 = S.rp[r + 1 - t.ra0] - t.a0;
+        T acc = T(0);
+        for (int32_t q = q0; q < q1; ++q) acc = add_rn(acc, S.val[q]);
+        if (t.rs[j] >= 0) {
+            combine<T>(acc, t.rs[j], t.ro[j], o);
+            continue;
+        }
+        __stcs(y + t.ro[j], acc);
+    }
+}
+
+template <typename T, bool kCombine, bool kIdentity, int V>
+__global__ void __launch_bounds__((kStreamWarps + 1) * 32, kStVariants[V].min_ctas)
     spmv_stream_tma_kernel(StreamTmaArgs a, SpmvOperands o) {
+    constexpr int NS = kStVariants[V].stages;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     StStage<T>* st = reinterpret_cast<StStage<T>*>(smem_raw);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + kSTStages * sizeof(StStage<T>));
-    uint64_t* empty = full + kSTStages;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + NS * sizeof(StStage<T>));
+    uint64_t* empty = full + NS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kSTStages; ++i) {
+        for (int i = 0; i < NS; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], kStreamWarps);
         }
@@ -550,8 +661,8 @@ __global__ void __launch_bounds__((kStreamWarps + 1) * 32, 2)
             const uint64_t pol = policy_evict_first();
             int it = 0;
             for (int b = blockIdx.x; b < a.nb; b += gridDim.x, ++it) {
-                const int s = it % kSTStages;
-                const int u = it / kSTStages;
+                const int s = it % NS;
+                const int u = it / NS;
                 if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
                 const int4* d = reinterpret_cast<const int4*>(a.desc + size_t(b) * kDescInts);
                 const int4 d0 = __ldg(d), d1 = __ldg(d + 1), d2 = __ldg(d + 2), d3 = __ldg(d + 3);
@@ -589,45 +700,53 @@ __global__ void __launch_bounds__((kStreamWarps + 1) * 32, 2)
     T* __restrict__ y = static_cast<T*>(o.y);
     const uint64_t xpol = policy_evict_last();
     constexpr int K = kStreamTile / 32;
-    int it = 0;
-    for (int b = blockIdx.x; b < a.nb; b += gridDim.x, ++it) {
-        const int s = it % kSTStages;
-        const int u = it / kSTStages;
-        mbar_wait(&full[s], u & 1);
-        StStage<T>& S = st[s];
-        const int32_t a0 = S.hdr[2], ra0 = S.hdr[3];
-        const bool blk_combine = kCombine && (S.hdr[4] & 1) != 0;
-        const int32_t t0 = S.hdr[5 + warp], t1 = S.hdr[6 + warp];
-        const int32_t e0 = S.rp[t0 - ra0] - a0, e1 = S.rp[t1 - ra0] - a0;
+    if constexpr (!kStVariants[V].pipe) {
+        int it = 0;
+        for (int b = blockIdx.x; b < a.nb; b += gridDim.x, ++it) {
+            const int s = it % NS;
+            mbar_wait(&full[s], (it / NS) & 1);
+            StStage<T>& S = st[s];
+            const StTile t = st_tile<T, kCombine, kIdentity>(S, warp, lane, a.out, a.slot);
+            T xv[K];
+            st_gather<T, K>(S, t, lane, x, xpol, xv);
+            __syncwarp();
+            st_products<T, K>(S, t, lane, xv);
+            __syncwarp();
+            st_rowsums<T>(S, t, lane, y, o);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+    } else {
+        // software pipeline: block b's gathers were issued during block
+        // (b - grid)'s row sums
+        int it = 0, b = blockIdx.x;
         T xv[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const int q = e0 + lane + 32 * k;
-            xv[k] = q < e1 ? ldg_x<true>(x + S.col[q], xpol) : T(0);
+        StTile t{};
+        if (b < a.nb) {
+            mbar_wait(&full[0], 0);
+            t = st_tile<T, kCombine, kIdentity>(st[0], warp, lane, a.out, a.slot);
+            st_gather<T, K>(st[0], t, lane, x, xpol, xv);
         }
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const int q = e0 + lane + 32 * k;
-            if (q < e1) S.val[q] = mul_rn(S.val[q], xv[k]);
-        }
-        __syncwarp();
-        for (int32_t r = t0 + lane; r < t1; r += 32) {
-            const int32_t q0 = S.rp[r - ra0] - a0, q1 = S.rp[r + 1 - ra0] - a0;
-            T acc = T(0);
-            for (int32_t q = q0; q < q1; ++q) acc = add_rn(acc, S.val[q]);
-            const int32_t orow = kIdentity ? r : a.out[r];
-            if (blk_combine) {
-                const int32_t k = a.slot[r];
-                if (k >= 0) {
-                    combine<T>(acc, k, orow, o);
-                    continue;
-                }
+        while (b < a.nb) {
+            const int s = it % NS;
+            StStage<T>& S = st[s];
+            __syncwarp();
+            st_products<T, K>(S, t, lane, xv);
+            __syncwarp();
+            const StTile cur = t;
+            const int bn = b + gridDim.x;
+            if (bn < a.nb) {   // next block's gathers in flight during this block's row sums
+                const int sn = (it + 1) % NS;
+                mbar_wait(&full[sn], ((it + 1) / NS) & 1);
+                t = st_tile<T, kCombine, kIdentity>(st[sn], warp, lane, a.out, a.slot);
+                st_gather<T, K>(st[sn], t, lane, x, xpol, xv);
             }
-            __stcs(y + orow, acc);
+            st_rowsums<T>(S, cur, lane, y, o);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            b = bn;
+            ++it;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
     }
 }
 
@@ -733,40 +852,54 @@ __global__ void flush_kernel(const uint4* __restrict__ buf, int64_t n16, unsigne
     if (acc == salt) sink[0] = acc;
 }
 
-int g_num_sms = 0;
+// SM count of the current device, cached per device (plans on several
+// devices in one process size their grids for their own device)
+std::atomic<int> g_num_sms[64];
 
 int num_sms() {
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    }
-    return g_num_sms;
-}
-
-template <typename T, int CFG, bool C, bool I>
-cudaError_t prep_block_kernel() {
-    static bool done[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 64 && done[dev]) return cudaSuccess;
+    if (dev < 0 || dev >= 64) dev = 0;
+    int n = g_num_sms[dev].load(std::memory_order_relaxed);
+    if (n <= 0) {
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+        g_num_sms[dev].store(n, std::memory_order_relaxed);
+    }
+    return n;
+}
+
+template <typename T, int CFG, bool C, bool I, bool H = false>
+cudaError_t prep_block_kernel() {
+    static std::atomic<bool> done[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && done[dev].load(std::memory_order_acquire)) return cudaSuccess;
     const int smem = Cfg<CFG>::template smem_bytes<T>();
-    cudaError_t e = cudaFuncSetAttribute(spmv_block_kernel<T, CFG, C, I>,
+    cudaError_t e = cudaFuncSetAttribute(spmv_block_kernel<T, CFG, C, I, H>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(spmv_block_kernel<T, CFG, C, I>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e == cudaSuccess && dev < 64) done[dev] = true;
+    e = cudaFuncSetAttribute(spmv_block_kernel<T, CFG, C, I, H>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e == cudaSuccess && dev < 64) done[dev].store(true, std::memory_order_release);
     return e;
 }
 
 template <typename T, int CFG, bool C, bool I>
 cudaError_t launch_block(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, int32_t b0, int32_t b1) {
-    cudaError_t e = prep_block_kernel<T, CFG, C, I>();
-    if (e != cudaSuccess) return e;
     BlockArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_desc, L.s_out, L.s_slot, b0, b1};
     const int grid = std::min(L.grid_s, b1 - b0);
-    spmv_block_kernel<T, CFG, C, I>
+    cudaError_t e;
+    if (o.xflag) {   // x streamed in: the coherent-load instantiation
+        e = prep_block_kernel<T, CFG, C, I, true>();
+        if (e != cudaSuccess) return e;
+        spmv_block_kernel<T, CFG, C, I, true>
+            <<<grid, Cfg<CFG>::kThreadsPerCta, Cfg<CFG>::template smem_bytes<T>(), s>>>(a, o);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return cudaGetLastError();
+    }
+    e = prep_block_kernel<T, CFG, C, I>();
+    if (e != cudaSuccess) return e;
+    spmv_block_kernel<T, CFG, C, I, false>
         <<<grid, Cfg<CFG>::kThreadsPerCta, Cfg<CFG>::template smem_bytes<T>(), s>>>(a, o);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
@@ -847,44 +980,61 @@ cudaError_t launch_stream(const DevLayout& L, const SpmvOperands& o, cudaStream_
     return cudaGetLastError();
 }
 
-template <typename T, bool C, bool I>
+int st_variant() {   // DSPMV_STMA_VARIANT (sweeps); default kDefaultStVariant
+    static const int v = [] {
+        const char* ev = std::getenv("DSPMV_STMA_VARIANT");
+        const int k = ev ? std::atoi(ev) : kDefaultStVariant;
+        return (k >= 0 && k < kNumStVariants) ? k : kDefaultStVariant;
+    }();
+    return v;
+}
+
+template <typename T, bool C, bool I, int V>
 cudaError_t prep_stream_tma() {
-    static bool done[64] = {};
+    static std::atomic<bool> done[64];
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 64 && done[dev]) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(spmv_stream_tma_kernel<T, C, I>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, st_smem_bytes<T>());
+    if (dev < 64 && done[dev].load(std::memory_order_acquire)) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(spmv_stream_tma_kernel<T, C, I, V>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, st_smem_bytes<T, V>());
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(spmv_stream_tma_kernel<T, C, I>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e == cudaSuccess && dev < 64) done[dev] = true;
+    e = cudaFuncSetAttribute(spmv_stream_tma_kernel<T, C, I, V>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e == cudaSuccess && dev < 64) done[dev].store(true, std::memory_order_release);
     return e;
+}
+
+template <typename T, bool C, bool I, int V>
+cudaError_t launch_stream_tma_v(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, bool vec) {
+    cudaError_t e = prep_stream_tma<T, C, I, V>();
+    if (e != cudaSuccess) return e;
+    StreamTmaArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_tdesc, L.s_out, L.s_slot, L.ntblocks,
+                    VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}};
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(L.grid_tt);
+    cfg.blockDim = dim3((kStreamWarps + 1) * 32);
+    cfg.dynamicSmemBytes = st_smem_bytes<T, V>();
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    if (x_persist_fraction() > 0 && L.x_bytes > 0) {
+        x_window(at[0], o.x, L.x_bytes);
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+    }
+    e = cudaLaunchKernelEx(&cfg, spmv_stream_tma_kernel<T, C, I, V>, a, o);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <typename T, bool C, bool I>
 cudaError_t launch_stream_tma_ci(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, bool vec) {
-    cudaError_t e = prep_stream_tma<T, C, I>();
-    if (e != cudaSuccess) return e;
-    StreamTmaArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_tdesc, L.s_out, L.s_slot, L.ntblocks,
-                    VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}};
-    if (x_persist_fraction() > 0 && L.x_bytes > 0) {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(L.grid_tt);
-        cfg.blockDim = dim3((kStreamWarps + 1) * 32);
-        cfg.dynamicSmemBytes = st_smem_bytes<T>();
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        x_window(at[0], o.x, L.x_bytes);
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, spmv_stream_tma_kernel<T, C, I>, a, o);
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        return e != cudaSuccess ? e : cudaGetLastError();
+    switch (L.st_variant) {
+        case 0: return launch_stream_tma_v<T, C, I, 0>(L, o, s, vec);
+        case 1: return launch_stream_tma_v<T, C, I, 1>(L, o, s, vec);
+        case 2: return launch_stream_tma_v<T, C, I, 2>(L, o, s, vec);
+        default: return launch_stream_tma_v<T, C, I, 3>(L, o, s, vec);
     }
-    spmv_stream_tma_kernel<T, C, I><<<L.grid_tt, (kStreamWarps + 1) * 32, st_smem_bytes<T>(), s>>>(a, o);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return cudaGetLastError();
 }
+static_assert(kNumStVariants == 4, "update launch_stream_tma_ci / occupancy dispatch");
 
 template <typename T>
 cudaError_t launch_stream_tma(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, bool vec) {
@@ -893,6 +1043,15 @@ cudaError_t launch_stream_tma(const DevLayout& L, const SpmvOperands& o, cudaStr
     if (c) return launch_stream_tma_ci<T, true, false>(L, o, s, vec);
     if (id) return launch_stream_tma_ci<T, false, true>(L, o, s, vec);
     return launch_stream_tma_ci<T, false, false>(L, o, s, vec);
+}
+
+template <typename T, int V>
+int stma_occupancy() {
+    int n = 0;
+    if (prep_stream_tma<T, false, true, V>() == cudaSuccess)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_stream_tma_kernel<T, false, true, V>,
+                                                      (kStreamWarps + 1) * 32, st_smem_bytes<T, V>());
+    return n > 0 ? n : 1;
 }
 
 template <typename T>
@@ -922,7 +1081,7 @@ template <typename T, int CFG>
 int occupancy() {
     int n = 0;
     if (prep_block_kernel<T, CFG, true, false>() != cudaSuccess) return 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_block_kernel<T, CFG, true, false>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_block_kernel<T, CFG, true, false, false>,
                                                   Cfg<CFG>::kThreadsPerCta, Cfg<CFG>::template smem_bytes<T>());
     return n > 0 ? n : 1;
 }
@@ -969,18 +1128,24 @@ int stream_kernel_ctas_per_sm(int dtype) {
     return n > 0 ? n : 1;
 }
 
-int stream_tma_kernel_ctas_per_sm(int dtype) {
-    int n = 0;
+int stream_tma_kernel_ctas_per_sm(int dtype, int variant) {
     if (dtype == DSPMV_F32) {
-        if (prep_stream_tma<float, false, true>() == cudaSuccess)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_stream_tma_kernel<float, false, true>,
-                                                          (kStreamWarps + 1) * 32, st_smem_bytes<float>());
-    } else if (prep_stream_tma<double, false, true>() == cudaSuccess) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_stream_tma_kernel<double, false, true>,
-                                                      (kStreamWarps + 1) * 32, st_smem_bytes<double>());
+        switch (variant) {
+            case 0: return stma_occupancy<float, 0>();
+            case 1: return stma_occupancy<float, 1>();
+            case 2: return stma_occupancy<float, 2>();
+            default: return stma_occupancy<float, 3>();
+        }
     }
-    return n > 0 ? n : 1;
+    switch (variant) {
+        case 0: return stma_occupancy<double, 0>();
+        case 1: return stma_occupancy<double, 1>();
+        case 2: return stma_occupancy<double, 2>();
+        default: return stma_occupancy<double, 3>();
+    }
 }
+
+int stream_tma_variant() { return st_variant(); }
 
 void set_x_persist_limit() {
     if (x_persist_fraction() <= 0) return;

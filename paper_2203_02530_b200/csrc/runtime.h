@@ -41,6 +41,7 @@ struct DevLayout {
     int32_t* s_tiles = nullptr;
     // TMA-producer variant of the CSR-stream kernel (Layout::s_tdesc)
     bool stream_tma = false;
+    int st_variant = 0;                // kStVariants index (kernels.cu)
     int32_t ntblocks = 0;
     int grid_tt = 0;
     int32_t* s_tdesc = nullptr;
@@ -65,7 +66,8 @@ struct SpmvOperands {
 int block_kernel_smem_bytes(int dtype, int cfg);
 int block_kernel_ctas_per_sm(int dtype, int cfg);
 int stream_kernel_ctas_per_sm(int dtype);
-int stream_tma_kernel_ctas_per_sm(int dtype);
+int stream_tma_kernel_ctas_per_sm(int dtype, int variant);
+int stream_tma_variant();   // kStVariants index in use (DSPMV_STMA_VARIANT)
 void set_x_persist_limit();   // experiment DSPMV_X_PERSIST (plan time)
 cudaError_t launch_spmv(const DevLayout& L, int dtype, const SpmvOperands& o, cudaStream_t s);
 // row blocks [b0, b1) of the S group, plus the V group (long rows) if vec

@@ -320,13 +320,14 @@ def main_fine(a):
         D.dspmv_comm_destroy(c)
 
 
-def analyse(space, times, measure_sub, workload, ranks, sweep_s):
+def analyse(space, times, measure_sub, workload, ranks, sweep_s, syncs="derived", execution=None):
     labels, ranges, bounds = R.class_labels(times)
     X, cols = R.features(space)
     clf, mln, hist = R.train_tree(X, labels)
     rs = R.rulesets(clf, cols)
     out = {
-        "workload": workload, "ranks": ranks, "n_schedules": len(space), "sweep_wall_s": round(sweep_s, 2),
+        "workload": workload, "ranks": ranks, "syncs": syncs, "execution_model": execution,
+        "n_schedules": len(space), "sweep_wall_s": round(sweep_s, 2),
         "fastest_us": float(times.min() * 1e6), "slowest_us": float(times.max() * 1e6),
         "fast_slow_ratio": float(times.max() / times.min()),
         "sorted_times_us": [round(float(t) * 1e6, 3) for t in np.sort(times)],
@@ -340,7 +341,7 @@ def analyse(space, times, measure_sub, workload, ranks, sweep_s):
     }
     acc = {}
     for iters in (50, 100, 200, 400):
-        m = M.MCTS(measure_sub, n_streams=2, seed=2203).run(iters)
+        m = M.MCTS(measure_sub, n_streams=2, seed=2203, syncs=syncs).run(iters)
         recs = m.records()
         sub_t = np.array([t for _, t in recs])
         acc[str(iters)] = {"distinct": len(recs),
@@ -354,10 +355,14 @@ def main_distributed(a):
     dist, world, rank, comm, plan, x, y = setup_distributed(a.workload, a.comm)
     measure = make_measure_distributed(dist, rank, plan, x, y)
     if rank == 0:
-        space = PS.enumerate_derived(2)
+        space = PS.enumerate_orderable(2) if a.syncs == "orderable" else PS.enumerate_derived(2)
         t0 = time.perf_counter()
         times = np.array([measure(o) for o in space])
-        out = analyse(space, times, measure, a.workload, world, time.perf_counter() - t0)
+        model = (f"SPMD: {world} processes, one rank each, "
+                 + ("NCCL communicator, NCCL send/recv exchange" if a.comm == "nccl" else
+                    "HOST communicator (gloo bootstrap), fused Pack+put exchange over CUDA IPC")
+                 + f", {torch.cuda.device_count()} GPU(s) visible")
+        out = analyse(space, times, measure, a.workload, world, time.perf_counter() - t0, a.syncs, model)
         measure(None)                                     # release the other ranks
         json.dump(out, open(a.out, "w"), indent=1)
         print(json.dumps({k: v for k, v in out.items() if k != "sorted_times_us"}, indent=1))

@@ -129,6 +129,7 @@ def test_plan_memory_from_torch_caching_allocator():
             y = torch.empty_like(x)
             D.dspmv_apply(s, x, y)
             ys.append(y.cpu().numpy())
+            del y
             D.dspmv_schedule_destroy(s)
             D.dspmv_plan_destroy(plan)
             torch.cuda.synchronize()
