@@ -55,8 +55,20 @@ def step_convolve(a, r: int) -> np.ndarray:
     return c
 
 
-def class_labels(times, radius: int | None = None, percentile: float = 98.0):
-    """Labels (1 = fastest) for `times` (any order) and the class ranges."""
+def class_labels(times, radius: int | None = None, percentile: float = 98.0, threshold: str = "signal",
+                 mad_k: float = 3.0):
+    """Labels (1 = fastest) for `times` (any order) and the class ranges.
+
+    threshold -- which peaks of the step convolution become class boundaries:
+      "signal" (R-N2, default): prominence >= the `percentile` of the
+               convolution signal;
+      "peaks"  (the literal P:508 wording): prominence >= the `percentile` of
+               the peaks' own prominences;
+      "mad"    (noise floor): log prominence >= median + mad_k * 1.4826 * MAD
+               of the peaks' log prominences -- robust when many classes
+               exist, where the two percentile readings drop real boundaries."""
+    if threshold not in ("signal", "peaks", "mad"):
+        raise ValueError("threshold must be 'signal', 'peaks' or 'mad'")
     from scipy.signal import find_peaks, peak_prominences
     t = np.asarray(times, np.float64)
     order = np.argsort(t, kind="stable")
@@ -74,9 +86,19 @@ def class_labels(times, radius: int | None = None, percentile: float = 98.0):
             with warnings.catch_warnings():
                 warnings.simplefilter("ignore")
                 prom = peak_prominences(np.where(np.isfinite(valid), valid, np.nanmin(c)), peaks)[0]
-            # R-N2: a peak is kept when its prominence is >= the 98th
-            # percentile of the convolution signal (noise peaks stay below it)
-            thr = np.percentile(c[~np.isnan(c)], percentile)
+            if threshold == "signal":
+                # R-N2: a peak is kept when its prominence is >= the 98th
+                # percentile of the convolution signal (noise peaks stay below it)
+                thr = np.percentile(c[~np.isnan(c)], percentile)
+            elif threshold == "peaks":
+                thr = np.percentile(prom, percentile)
+            else:
+                # noise floor on a log scale: noise peaks spread over orders of
+                # magnitude, class boundaries stand out above them
+                lp = np.log(prom[prom > 0]) if np.any(prom > 0) else np.zeros(1)
+                med = float(np.median(lp))
+                mad = 1.4826 * float(np.median(np.abs(lp - med)))
+                thr = float(np.exp(med + mad_k * mad))
             bounds = sorted(int(p) for p, q in zip(peaks, prom) if q >= thr and q > 0)
     lab_sorted = np.ones(n, np.int64)
     for b in bounds:

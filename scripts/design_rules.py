@@ -348,6 +348,9 @@ def analyse(space, times, measure_sub, workload, ranks, sweep_s, syncs="derived"
                            "accuracy": R.class_accuracy([o for o, _ in recs], sub_t, space, times),
                            "best_found_us": float(sub_t.min() * 1e6)}
     out["mcts_table_v"] = acc
+    # class counts under the three readings of P:508 (DESIGN.md R-N2)
+    out["classes_by_threshold"] = {th: len(R.class_labels(times, threshold=th)[1])
+                                   for th in ("signal", "peaks", "mad")}
     return out
 
 

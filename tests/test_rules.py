@@ -88,3 +88,26 @@ def test_features_on_orderable_schedules():
         assert None not in nm and len(set(nm)) == len(nm), nm
     X, cols = R.features(space[:600])
     assert X.shape[0] == 600 and X.shape[1] > 10
+
+
+def test_labels_many_separated_classes_mad_threshold():
+    """Nine classes separated by >= 40 sigma jumps: the percentile readings of
+    P:508 keep too few boundaries (R-N2 keeps the 98th percentile of the
+    signal, the literal reading 2 % of the peaks); the log-MAD noise floor
+    recovers all nine, and stays at 1 / 2 / 5 classes on single-cluster,
+    two-cluster and uniform five-cluster data."""
+    rng = np.random.default_rng(0)
+    sig = 1e-3
+    t9 = np.concatenate([1 + k * 40 * sig * (1 + 0.5 * k) + rng.normal(0, sig, 230) for k in range(9)])
+    lab, ranges, bounds = R.class_labels(t9, threshold="mad")
+    assert len(ranges) == 9
+    order = np.argsort(t9)
+    assert np.array_equal(lab[order], np.repeat(np.arange(1, 10), 230))
+    assert len(R.class_labels(t9, threshold="signal")[1]) < 9
+    assert len(R.class_labels(1 + rng.normal(0, sig, 2000), threshold="mad")[1]) == 1
+    t2 = np.concatenate([1 + rng.normal(0, sig, 1000), 2 + rng.normal(0, sig, 1000)])
+    assert len(R.class_labels(t2, threshold="mad")[1]) == 2
+    t5 = np.concatenate([1 + k * 0.05 + rng.uniform(0, 0.01, 400) for k in range(5)])
+    assert len(R.class_labels(t5, threshold="mad")[1]) == 5
+    with pytest.raises(ValueError):
+        R.class_labels(t5, threshold="bogus")
