@@ -418,6 +418,7 @@ def pick_mode(ctx, sched, x, y, pref, exchange):
             ctx.torch.cuda.synchronize()
         except Exception as e:  # noqa: BLE001 -- falls back to the host mode, reported
             graph_ok, note = False, f"graph capture failed, host mode used: {e}"
+            print(f"[bench rank {ctx.rank}] {note}", file=sys.stderr, flush=True)
     graph_ok = ctx.alland(graph_ok)
     if not graph_ok:
         return D.dspmv_apply, "host", note
@@ -714,8 +715,9 @@ def rerank(ctx, plan, x, y, ranked, k, mode_pref, ex_mode):
                 for _ in range(3):
                     fn(sc, x, y, ctx.stream)
                 ctx.torch.cuda.synchronize()
-            except Exception:  # noqa: BLE001 -- mode unavailable for this schedule
+            except Exception as e:  # noqa: BLE001 -- mode unavailable for this schedule
                 ok = False
+                print(f"[bench rank {ctx.rank}] rerank candidate {ci} {mname}: {e}", file=sys.stderr, flush=True)
             if not ctx.alland(ok):
                 continue
             st = time_steps(ctx, sc, fn, x, y, 30)[0]
