@@ -412,16 +412,17 @@ def pick_mode(ctx, sched, x, y, pref, exchange):
     graph_ok = pref != "host"
     note = None
     if graph_ok:
-        try:
-            for _ in range(3):
-                D.dspmv_apply_graph(sched, x, y, ctx.stream)
-            ctx.torch.cuda.synchronize()
+        try:   # capture only: every rank agrees before any rank launches (PUT epochs)
+            D.dspmv_apply_graph_prepare(sched, x, y, ctx.stream)
         except Exception as e:  # noqa: BLE001 -- falls back to the host mode, reported
             graph_ok, note = False, f"graph capture failed, host mode used: {e}"
             print(f"[bench rank {ctx.rank}] {note}", file=sys.stderr, flush=True)
     graph_ok = ctx.alland(graph_ok)
     if not graph_ok:
         return D.dspmv_apply, "host", note
+    for _ in range(3):
+        D.dspmv_apply_graph(sched, x, y, ctx.stream)
+    ctx.torch.cuda.synchronize()
     if pref == "graph":
         return D.dspmv_apply_graph, "graph", note
     tms = {}
@@ -668,10 +669,19 @@ def overlap_efficiency(ctx, plan, plan_none, ops, mode, x, y, t_best):
     def t_of(p, o):
         s = D.dspmv_schedule_create(p, o, 2)
         D.dspmv_schedule_set_timing(s, timing_mask(ctx.world))
+        f = fn
+        if f is D.dspmv_apply_graph:   # agree on the graph before any rank launches one
+            ok = True
+            try:
+                D.dspmv_apply_graph_prepare(s, x, y, ctx.stream)
+            except Exception:  # noqa: BLE001 -- this measurement then runs host-synchronised
+                ok = False
+            if not ctx.alland(ok):
+                f = D.dspmv_apply
         try:
             for _ in range(5):
-                fn(s, x, y, ctx.stream)
-            st = time_steps(ctx, s, fn, x, y, 50)[0]
+                f(s, x, y, ctx.stream)
+            st = time_steps(ctx, s, f, x, y, 50)[0]
             return ctx.allmax(sum(st) / len(st))
         finally:
             D.dspmv_schedule_destroy(s)
@@ -710,16 +720,20 @@ def rerank(ctx, plan, x, y, ranked, k, mode_pref, ex_mode):
         sc = D.dspmv_schedule_create(plan, cand, 2)
         D.dspmv_schedule_set_timing(sc, timing_mask(ctx.world))
         for mname, fn in modes:
+            # every rank must run the same applies (PUT epochs): capture first,
+            # agree, then run
             ok = True
-            try:
-                for _ in range(3):
-                    fn(sc, x, y, ctx.stream)
-                ctx.torch.cuda.synchronize()
-            except Exception as e:  # noqa: BLE001 -- mode unavailable for this schedule
-                ok = False
-                print(f"[bench rank {ctx.rank}] rerank candidate {ci} {mname}: {e}", file=sys.stderr, flush=True)
+            if mname == "graph":
+                try:
+                    D.dspmv_apply_graph_prepare(sc, x, y, ctx.stream)
+                except Exception as e:  # noqa: BLE001 -- mode unavailable for this schedule
+                    ok = False
+                    print(f"[bench rank {ctx.rank}] rerank candidate {ci} graph: {e}", file=sys.stderr, flush=True)
             if not ctx.alland(ok):
                 continue
+            for _ in range(3):
+                fn(sc, x, y, ctx.stream)
+            ctx.torch.cuda.synchronize()
             st = time_steps(ctx, sc, fn, x, y, 30)[0]
             tot = ctx.allmax(sum(st) / 30)
             log.append([ci, mname, round(tot * 1e3, 2)])

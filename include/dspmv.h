@@ -449,6 +449,12 @@ dspmv_status dspmv_apply_host(dspmv_schedule_t sched, const void* x_host, void* 
  * dspmv_apply_graph_group; `stream` must not be NULL. */
 dspmv_status dspmv_apply_graph(dspmv_schedule_t sched, const void* x_local, void* y_local,
                                dspmv_stream_t stream);
+/* Capture (or re-capture) the graph dspmv_apply_graph would launch for these
+ * x/y, without launching it.  Not collective: lets SPMD callers agree that
+ * every rank can run the graph before any rank launches one (an apply some
+ * ranks run and others do not would desynchronise the PUT epochs). */
+dspmv_status dspmv_apply_graph_prepare(dspmv_schedule_t sched, const void* x_local, void* y_local,
+                                       dspmv_stream_t stream);
 /* LOCAL comms: all nranks ranks of one in-process group in lock-step (op k on
  * every rank before op k+1).  scheds[r], x[r], y[r] belong to rank r. */
 dspmv_status dspmv_apply_group(const dspmv_schedule_t* scheds, int nranks,

@@ -198,12 +198,14 @@ void build_host_pipe(Plan& p, Layout& L) {
     const int64_t n = p.host.n_local();
     const int64_t bytes = n * p.esize;
     if (L.nb < 2 || bytes < (int64_t(2) << 20)) return;   // small: one transfer is as good
-    // 4 chunks measured best on C2 (scripts/diag_pcie5.py: K = 1 / 2 / 4 / 8 / 12 ->
-    // 0.647 / 0.527 / 0.487 / 0.510 / 0.560 ms per apply_host): each chunk
-    // boundary costs a copy-engine drain, the last chunk's rows trail the copy
-    int kmax = 4;
-    if (const char* ev = std::getenv("DSPMV_HOST_CHUNKS")) kmax = std::max(1, std::min(64, std::atoi(ev)));  // tuning
-    int K = int(std::min<int64_t>(kmax, bytes / (int64_t(1) << 20)));
+    // ~4 MiB chunks, at most 16: measured best on C2 (16.8 MB of x: K = 1 / 2 / 4 / 8
+    // / 12 -> 0.647 / 0.527 / 0.487 / 0.510 / 0.560 ms per apply_host) and on C3
+    // (134 MB: K = 4 / 8 / 16 / 32 -> 3.98 / 3.67 / 3.60 / 3.72 ms,
+    // profiles/r2_e2e_chunks_c3.txt): each chunk boundary costs a copy-engine
+    // drain, the last chunk's rows trail the copy
+    int K = int(std::max<int64_t>(2, std::min<int64_t>(16, bytes / (int64_t(4) << 20))));
+    if (const char* ev = std::getenv("DSPMV_HOST_CHUNKS"))   // tuning
+        K = int(std::min<int64_t>(std::max(1, std::min(64, std::atoi(ev))), bytes / (int64_t(1) << 20)));
     std::vector<double> frac;   // chunk end fractions (uniform by default)
     for (int k = 1; k < K; ++k) frac.push_back(double(k) / K);
     if (const char* ev = std::getenv("DSPMV_HOST_SPLIT")) {  // tuning: "0.4,0.7,0.9"
@@ -591,6 +593,17 @@ PFN_cuStreamWriteValue32_v11070 write_value32() {
 dspmv_status issue_group_put(Plan& p, ExGroup& g) {
     g.issued = true;
     if (g.empty()) return DSPMV_OK;
+    if (p.comm->kind == DSPMV_COMM_HOST) {
+        // peers may be other processes on this same GPU: their contexts
+        // time-slice the device, and a context parked on a stream semaphore
+        // wait is not switched out for the context that would release it --
+        // so the wait is a (preemptible) spin kernel instead
+        if (g.recv_from.size() > size_t(kMaxWaitPeers)) return fail(DSPMV_ERR_ARG, "too many peers for the flag wait");
+        CUDA_TRY(launch_wait_flags(p.d_flags, g.recv_from.data(), int(g.recv_from.size()), nullptr, p.comm_stream,
+                                   p.epoch));
+        CUDA_TRY(cudaEventRecord(g.ev, p.comm_stream));
+        return DSPMV_OK;
+    }
     auto wv = wait_value32();
     if (!wv) return fail(DSPMV_ERR_CUDA, "cuStreamWaitValue32 unavailable");
     for (int q : g.recv_from) {
@@ -2062,6 +2075,20 @@ dspmv_status dspmv_apply_graph_group(const dspmv_schedule_t* scheds, int nranks,
         }
         sp->timed_valid = sp->timing;
     }
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_apply_graph_prepare(dspmv_schedule_t s, const void* x, void* y, dspmv_stream_t stream) {
+    if (!s) return fail(DSPMV_ERR_ARG, "null schedule");
+    Plan& p = *s->plan;
+    if (p.poisoned) return fail(DSPMV_ERR_STATE, "plan is poisoned by an earlier error");
+    if (!p.ready) return fail(DSPMV_ERR_STATE, "plan not ready");
+    if (p.host.n_local() > 0 && (!x || !y)) return fail(DSPMV_ERR_ARG, "null x/y");
+    CUDA_TRY(cudaSetDevice(p.device));
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    if (!cs) return fail(DSPMV_ERR_ARG, "apply_graph needs a non-default stream");
+    if (!s->gexec || !s->g_group.empty() || s->gx != x || s->gy != y || s->g_timing != s->timing)
+        ST_TRY(capture_graph(*s, x, y, cs));
     return DSPMV_OK;
 }
 

@@ -806,8 +806,8 @@ struct WaitPeers {
     int p[kMaxWaitPeers];
 };
 
-__global__ void wait_flags_kernel(const unsigned* flags, WaitPeers peers, int n, const unsigned* ep) {
-    const unsigned want = *ep;
+__global__ void wait_flags_kernel(const unsigned* flags, WaitPeers peers, int n, const unsigned* ep, unsigned ep_val) {
+    const unsigned want = ep ? *ep : ep_val;
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -1221,12 +1221,12 @@ cudaError_t launch_copy_parity(int dtype, const void* recv, size_t parity_bytes,
 }
 
 cudaError_t launch_wait_flags(const unsigned* flags, const int* peers, int n, const unsigned* epoch,
-                              cudaStream_t s) {
+                              cudaStream_t s, unsigned epoch_val) {
     if (n <= 0) return cudaSuccess;
     if (n > kMaxWaitPeers) return cudaErrorInvalidValue;
     WaitPeers w{};
     for (int i = 0; i < n; ++i) w.p[i] = peers[i];
-    wait_flags_kernel<<<1, 32, 0, s>>>(flags, w, n, epoch);
+    wait_flags_kernel<<<1, 32, 0, s>>>(flags, w, n, epoch, epoch_val);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
 }

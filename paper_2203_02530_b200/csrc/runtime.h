@@ -104,8 +104,9 @@ cudaError_t launch_copy_parity(int dtype, const void* recv, size_t parity_bytes,
                                int64_t n, cudaStream_t s);
 // PUT exchange inside a graph: wait until flags[peers[i]] >= *epoch for all i
 // (system-scope acquire); traps after ~30 s so a dead peer cannot hang the GPU
+// (epoch == nullptr: compare against epoch_val, the host executor's epoch)
 cudaError_t launch_wait_flags(const unsigned* flags, const int* peers, int n, const unsigned* epoch,
-                              cudaStream_t s);
+                              cudaStream_t s, unsigned epoch_val = 0);
 cudaError_t launch_epoch_bump(unsigned* epoch, cudaStream_t s);
 constexpr int kMaxWaitPeers = 64;
 

@@ -140,6 +140,7 @@ _sig("dspmv_schedule_op_timeline", [_P, _P, _P, _I])
 _sig("dspmv_apply", [_P, _P, _P, _P])
 _sig("dspmv_apply_host", [_P, _P, _P, _P])
 _sig("dspmv_apply_graph", [_P, _P, _P, _P])
+_sig("dspmv_apply_graph_prepare", [_P, _P, _P, _P])
 _sig("dspmv_apply_group", [_P, _I, _P, _P, _P])
 _sig("dspmv_apply_graph_group", [_P, _I, _P, _P, _P])
 _sig("dspmv_l2_flush", [_I, _P])
@@ -576,6 +577,13 @@ def dspmv_apply_graph(sched, x, y, stream):
     _check_vec(sched, x, "x", False)
     _check_vec(sched, y, "y", False)
     _check(lib.dspmv_apply_graph(sched, _ptr(x), _ptr(y), _stream(stream)))
+
+
+def dspmv_apply_graph_prepare(sched, x, y, stream):
+    """Capture the graph for x/y without launching it (SPMD: agree first)."""
+    _check_vec(sched, x, "x", False)
+    _check_vec(sched, y, "y", False)
+    _check(lib.dspmv_apply_graph_prepare(sched, _ptr(x), _ptr(y), _stream(stream)))
 
 
 def dspmv_apply_host(sched, x_host, y_host, stream=None):
