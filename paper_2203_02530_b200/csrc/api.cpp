@@ -101,7 +101,13 @@ dspmv_status dev_alloc(Plan& p, void** dst, size_t bytes, bool zero, bool ipc = 
     *dst = nullptr;
     if (bytes == 0) return DSPMV_OK;
     ST_TRY(raw_alloc(p, dst, bytes, ipc));
-    if (zero) CUDA_TRY(cudaMemset(*dst, 0, bytes));
+    if (zero) {
+        // cudaMemset runs on the legacy stream, which does not order the
+        // library's non-blocking streams (nor peers writing over IPC): wait
+        // for it, or a flag written later could be zeroed after the fact
+        CUDA_TRY(cudaMemset(*dst, 0, bytes));
+        CUDA_TRY(cudaDeviceSynchronize());
+    }
     return DSPMV_OK;
 }
 

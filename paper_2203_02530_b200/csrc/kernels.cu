@@ -125,6 +125,19 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
     return v;
 }
 
+// Streamed x (dspmv_apply_host): wait until the copy stream has published this
+// apply's epoch for the chunk; trap after ~30 s rather than hang the device.
+__device__ __forceinline__ void wait_xflag(const unsigned* flag, unsigned epoch) {
+    unsigned long long t0 = 0;
+    while (ld_acquire_gpu(flag) < epoch) {
+        __nanosleep(256);
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (!t0) t0 = t;
+        else if (t - t0 > 30ull * 1000000000ull) __trap();
+    }
+}
+
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -329,9 +342,7 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
 #endif
                 const int4* d = reinterpret_cast<const int4*>(a.desc + size_t(b) * kDescInts);
                 const int4 d0 = __ldg(d), d1 = __ldg(d + 1), d2 = __ldg(d + 2), d3 = __ldg(d + 3);
-                if (o.xflag) {  // streamed x: wait until x chunks <= desc[15] have landed
-                    while (ld_acquire_gpu(o.xflag + d3.w) < o.epoch) __nanosleep(256);
-                }
+                if (o.xflag) wait_xflag(o.xflag + d3.w, o.epoch);  // streamed x: chunks <= desc[15] landed
                 const int32_t r0 = d0.x, r1 = d0.y, p0 = d0.z, p1 = d0.w;
                 const int32_t a0 = p0 & ~3, a1 = (p1 + 3) & ~3;
                 const int32_t ra0 = r0 & ~3, ra1 = (r1 + 1 + 3) & ~3;
@@ -666,9 +677,7 @@ __global__ void __launch_bounds__((kStreamWarps + 1) * 32, kStVariants[V].min_ct
                 if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
                 const int4* d = reinterpret_cast<const int4*>(a.desc + size_t(b) * kDescInts);
                 const int4 d0 = __ldg(d), d1 = __ldg(d + 1), d2 = __ldg(d + 2), d3 = __ldg(d + 3);
-                if (o.xflag) {
-                    while (ld_acquire_gpu(o.xflag + d3.w) < o.epoch) __nanosleep(256);
-                }
+                if (o.xflag) wait_xflag(o.xflag + d3.w, o.epoch);
                 const int32_t r0 = d0.x, r1 = d0.y, p0 = d0.z, p1 = d0.w;
                 const int32_t a0 = p0 & ~3, a1 = (p1 + 3) & ~3;
                 const int32_t ra0 = r0 & ~3, ra1 = (r1 + 1 + 3) & ~3;
