@@ -72,7 +72,7 @@ __device__ __forceinline__ uint32_t sa(const void* p) { return static_cast<uint3
 // (the TMA destination must be 128-B aligned: each lane's 64 B land in a 128-B slot)
 template <int S>
 __global__ void __launch_bounds__(128) tma_gather(const __grid_constant__ CUtensorMap tm, const int* __restrict__ idx,
-                                                  long long m, double* out) {
+                                                  long long m, double* out, int bw) {
     extern __shared__ __align__(128) unsigned char dsm[];
     double (*buf)[S][32 * 16] = reinterpret_cast<double (*)[S][32 * 16]>(dsm);
     uint64_t (*bar)[S] = reinterpret_cast<uint64_t (*)[S]>(dsm + sizeof(double) * 4 * S * 32 * 16);
@@ -97,10 +97,10 @@ __global__ void __launch_bounds__(128) tma_gather(const __grid_constant__ CUtens
         for (int k = 0; k < 4; ++k) {
             const int c = base + k < m ? __ldcs(idx + base + k) : 0;
             cc[s][k] = c;
-            r[k] = c >> 1;
+            r[k] = c / bw;
         }
         if (lane == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bar[w][s])), "r"(32 * 64)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bar[w][s])), "r"(32 * 32 * bw)
                          : "memory");
         __syncwarp();
         asm volatile(
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(128) tma_gather(const __grid_constant__ CUtens
             asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
                          : "=r"(ok) : "r"(sa(&bar[w][s])), "r"(par) : "memory");
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc += buf[w][s][lane * 16 + k * 2 + (cc[s][k] & 1)];
+        for (int k = 0; k < 4; ++k) acc += buf[w][s][lane * 16 + k * bw + (cc[s][k] % bw)];
         __syncwarp();
         if (j + S < nchunks) issue(j + S, s);
     }
@@ -133,6 +133,9 @@ __global__ void __launch_bounds__(128) tma_gather(const __grid_constant__ CUtens
 int main(int argc, char** argv) {
     const long long m = (argc > 1 ? atoll(argv[1]) : 134) * 1000000LL;
     const long long xmb = argc > 2 ? atoll(argv[2]) : 64;
+    const int bw = argc > 3 ? atoi(argv[3]) : 2;      // box width (doubles per gathered row)
+    const int bh = argc > 4 ? atoi(argv[4]) : 1;      // box height in the tensor map
+    const int mode = argc > 5 ? atoi(argv[5]) : 2;    // 0: lsu only, 1: tma only, 2: both
     const int n = int(xmb * 1024 * 1024 / 8);
     double* x;
     int* idx;
@@ -154,9 +157,9 @@ int main(int argc, char** argv) {
     cudaDriverEntryPointQueryResult q;
     CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q));
     CUtensorMap tm;
-    cuuint64_t dims[2] = {2, cuuint64_t(n / 2)};
-    cuuint64_t strides[1] = {16};
-    cuuint32_t box[2] = {2, 1};
+    cuuint64_t dims[2] = {cuuint64_t(bw), cuuint64_t(n / bw)};
+    cuuint64_t strides[1] = {cuuint64_t(bw) * 8};
+    cuuint32_t box[2] = {cuuint32_t(bw), cuuint32_t(bh)};
     cuuint32_t es[2] = {1, 1};
     CUresult r = ((EncFn)fp)(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, x, dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -185,7 +188,9 @@ int main(int argc, char** argv) {
         printf("%-28s x %4lld MB  %lld M gathers  %.3f ms  %.1f G gathers/s\n", name, xmb, m / 1000000, best,
                double(m) / (best * 1e-3) / 1e9);
     };
+    printf("box %d x %d\n", bw, bh);
     for (int ctas : {4, 8}) {
+        if (mode == 1) break;
         char nm[64];
         snprintf(nm, sizeof nm, "lsu nc.noL1 %d CTA/SM", ctas);
         timeit(nm, [&] { lsu_gather<<<sms * ctas, 256>>>(x, idx, m, out); });
@@ -195,9 +200,10 @@ int main(int argc, char** argv) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         char nm[64];
         snprintf(nm, sizeof nm, "tma gather4 S=%d %d CTA/SM", S, ctas);
-        timeit(nm, [&] { kern<<<sms * ctas, 128, smem>>>(tm, idx, m, out); });
+        timeit(nm, [&] { kern<<<sms * ctas, 128, smem>>>(tm, idx, m, out, bw); });
     };
     for (int ctas : {1, 2, 3}) {
+        if (mode == 0) break;
         run_tma(tma_gather<2>, 2, ctas);
         run_tma(tma_gather<4>, 4, ctas);
     }
