@@ -70,10 +70,12 @@ __device__ __forceinline__ uint32_t sa(const void* p) { return static_cast<uint3
 // TMA gather4: each warp owns a ring of S stages; a stage = 32 gather4 ops
 // (one per lane) = 128 gathers = 2 KB; lane 0 arms the stage's mbarrier.
 // (the TMA destination must be 128-B aligned: each lane's 64 B land in a 128-B slot)
-template <int S>
+template <int S, bool kTile = false>
 __global__ void __launch_bounds__(128) tma_gather(const __grid_constant__ CUtensorMap tm, const int* __restrict__ idx,
                                                   long long m, double* out, int bw) {
-    extern __shared__ __align__(128) unsigned char dsm[];
+    extern __shared__ __align__(128) unsigned char dsm_raw[];
+    // the dynamic shared-memory base is not guaranteed 128-B aligned: align by hand
+    unsigned char* dsm = dsm_raw + ((128 - (sa(dsm_raw) & 127)) & 127);
     double (*buf)[S][32 * 16] = reinterpret_cast<double (*)[S][32 * 16]>(dsm);
     uint64_t (*bar)[S] = reinterpret_cast<uint64_t (*)[S]>(dsm + sizeof(double) * 4 * S * 32 * 16);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -100,9 +102,18 @@ __global__ void __launch_bounds__(128) tma_gather(const __grid_constant__ CUtens
             r[k] = c / bw;
         }
         if (lane == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bar[w][s])), "r"(32 * 32 * bw)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bar[w][s])),
+                         "r"(kTile ? 32 * 8 * bw : 32 * 32 * bw)
                          : "memory");
         __syncwarp();
+        if constexpr (kTile) {   // control: one plain 2-D tile load (one row) per lane
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4}], [%2];" ::"r"(sa(&buf[w][s][lane * 16])),
+                "l"(&tm), "r"(sa(&bar[w][s])), "r"(0), "r"(r[0])
+                : "memory");
+            return;
+        }
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
             " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(sa(&buf[w][s][lane * 8])),
@@ -123,7 +134,7 @@ __global__ void __launch_bounds__(128) tma_gather(const __grid_constant__ CUtens
             asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
                          : "=r"(ok) : "r"(sa(&bar[w][s])), "r"(par) : "memory");
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc += buf[w][s][lane * 16 + k * bw + (cc[s][k] % bw)];
+        for (int k = 0; k < (kTile ? 1 : 4); ++k) acc += buf[w][s][lane * 16 + k * bw + (cc[s][k] % bw)];
         __syncwarp();
         if (j + S < nchunks) issue(j + S, s);
     }
@@ -196,12 +207,16 @@ int main(int argc, char** argv) {
         timeit(nm, [&] { lsu_gather<<<sms * ctas, 256>>>(x, idx, m, out); });
     }
     auto run_tma = [&](auto kern, int S, int ctas) {
-        const size_t smem = sizeof(double) * 4 * S * 32 * 16 + 8 * 4 * S;
+        const size_t smem = sizeof(double) * 4 * S * 32 * 16 + 8 * 4 * S + 128;
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         char nm[64];
         snprintf(nm, sizeof nm, "tma gather4 S=%d %d CTA/SM", S, ctas);
         timeit(nm, [&] { kern<<<sms * ctas, 128, smem>>>(tm, idx, m, out, bw); });
     };
+    if (mode == 3) {
+        run_tma(tma_gather<4, true>, 4, 2);
+        return 0;
+    }
     for (int ctas : {1, 2, 3}) {
         if (mode == 0) break;
         run_tma(tma_gather<2>, 2, ctas);
