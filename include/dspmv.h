@@ -218,7 +218,9 @@ typedef struct {
     int32_t rank, nranks, dtype, ready;
     int64_t device_bytes;
     int32_t s_kernel_local, s_kernel_remote;  /* DSPMV_SKERNEL_BLOCK / _STREAM(_TMA)     */
-    int32_t pack_alias;              /* 1: sends read x directly, Pack is empty    */
+    int32_t pack_alias;              /* 1: sends read x directly, Pack is empty
+                                        (host plans: 1 if ALIAS_IF_CONTIGUOUS would
+                                        alias this rank's send lists)             */
     int32_t accumulate_mode;         /* DSPMV_ACC_* in use                         */
 } dspmv_plan_info;
 dspmv_status dspmv_plan_info_get(dspmv_plan_t plan, dspmv_plan_info* out);

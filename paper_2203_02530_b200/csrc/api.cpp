@@ -254,20 +254,8 @@ dspmv_status finalize_send(Plan& p) {
     const size_t s = p.host.pack_map.size();
     // DSPMV_PACK_ALIAS_IF_CONTIGUOUS: every destination's
     // send list a run of consecutive local rows -> send from x, no Pack kernel
-    p.pack_alias = false;
-    if (p.opts.pack_mode == DSPMV_PACK_ALIAS_IF_CONTIGUOUS && !p.put_mode && s > 0) {
-        const RankPlan& h = p.host;
-        bool ok = true;
-        p.alias_off.assign(size_t(h.nranks), 0);
-        for (int q = 0; q < h.nranks && ok; ++q) {
-            const int32_t c = h.send_count[q], d = h.send_displ[q];
-            if (c <= 0) continue;
-            const int32_t b = h.pack_map[d];
-            for (int32_t k = 1; k < c && ok; ++k) ok = h.pack_map[d + k] == b + k;
-            p.alias_off[q] = b;
-        }
-        p.pack_alias = ok;
-    }
+    p.pack_alias = p.opts.pack_mode == DSPMV_PACK_ALIAS_IF_CONTIGUOUS && !p.put_mode && s > 0 &&
+                   pack_alias_offsets(p.host, p.alias_off);
     ST_TRY(dev_upload(p, &p.d_pack_map, p.host.pack_map.data(), s));
     if (!p.pack_alias) ST_TRY(dev_alloc(p, &p.d_sendbuf, s * p.esize, true));
     p.ready = true;
@@ -1728,6 +1716,8 @@ dspmv_status dspmv_host_plan_info(dspmv_host_plan_t hp, int rank, dspmv_plan_inf
     out->nnz_local = int64_t(h.al_col.size());
     out->nnz_remote = int64_t(h.ar_col.size());
     out->ready = 1;
+    std::vector<int64_t> off;
+    out->pack_alias = pack_alias_offsets(h, off) ? 1 : 0;   // would ALIAS_IF_CONTIGUOUS alias?
     return DSPMV_OK;
 }
 

@@ -83,6 +83,8 @@ dspmv_status plan_phase1(int64_t n_global, int nranks, int rank, int64_t n_local
                          int esize, RankPlan& out);
 // Phase 2 given every rank's halo: send counts/displ + pack map of rank p.
 void plan_phase2_from_requests(RankPlan& p, const std::vector<std::vector<int32_t>>& requests);
+// DSPMV_PACK_ALIAS_IF_CONTIGUOUS: every destination's send list consecutive?
+bool pack_alias_offsets(const RankPlan& h, std::vector<int64_t>& off);
 // requests[r] = global ids rank p must send to rank r (ascending)
 std::vector<int32_t> halo_segment_for(const RankPlan& r, int owner);
 

@@ -136,6 +136,23 @@ void plan_phase2_from_requests(RankPlan& p, const std::vector<std::vector<int32_
     }
 }
 
+// DSPMV_PACK_ALIAS_IF_CONTIGUOUS: true when the send list
+// to every destination is a run of consecutive local rows; off[q] is then
+// its first row (host-only, phase 2 done).
+bool pack_alias_offsets(const RankPlan& h, std::vector<int64_t>& off) {
+    off.assign(size_t(h.nranks), 0);
+    if (h.pack_map.empty() || h.send_count.empty()) return false;
+    for (int q = 0; q < h.nranks; ++q) {
+        const int32_t c = h.send_count[q], d = h.send_displ[q];
+        if (c <= 0) continue;
+        const int32_t b = h.pack_map[d];
+        for (int32_t k = 1; k < c; ++k)
+            if (h.pack_map[d + k] != b + k) return false;
+        off[q] = b;
+    }
+    return true;
+}
+
 // ---------------------------------------------------------------- layout
 int auto_block_cfg(const int32_t* rowptr, int32_t nrows, int vthr, int esize) {
     int64_t nnz = 0, nnz_short = 0, rows = 0;

@@ -99,3 +99,31 @@ def test_stencil_appendix_b_counts_library():
         assert (i["nnz_remote"], i["n_halo"], i["n_remote_rows"]) == (
             nb * (3 * m - 2) ** 2, nb * m * m, nb * m * m)
     D.dspmv_host_plan_destroy(hp)
+
+
+def test_pack_alias_detection_host():
+    """the contiguous-alias option applies exactly when every
+    destination's send list is a run of consecutive rows -- stencil slabs
+    (whole planes) yes, the power-law matrix no -- checked against the
+    oracle planner's pack maps."""
+    from oracle import plan as O2
+    from paper_2203_02530_b200 import dspmv as D
+    cases = [("7pt", 12 ** 3, gen.stencil("7pt", (12, 12, 12)), (2, 3, 4)),
+             ("27pt", 10 ** 3, gen.stencil("27pt", (10, 10, 10)), (2, 5)),
+             ("pl", 6000, gen.powerlaw(6000), (2, 3))]
+    for name, n, (rp, col, _), Ps in cases:
+        for P in Ps:
+            hp = D.dspmv_plan_build_host(P, n, rp, col)
+            try:
+                plans = O2.plan_all(rp, col, n, P)
+                for r in range(P):
+                    pm = np.asarray(plans[r]["pack_map"])
+                    sc = np.asarray(plans[r]["send_count"])
+                    sd = np.concatenate([[0], np.cumsum(sc)])
+                    want = int(len(pm) > 0 and all(np.all(np.diff(pm[sd[q]:sd[q + 1]]) == 1)
+                                                    for q in range(P) if sc[q] > 0))
+                    assert D.dspmv_host_plan_info(hp, r)["pack_alias"] == want, (name, P, r)
+                    if name != "pl" and len(pm):
+                        assert want == 1
+            finally:
+                D.dspmv_host_plan_destroy(hp)
