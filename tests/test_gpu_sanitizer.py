@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
 def test_compute_sanitizer_clean(tool):
     r = subprocess.run(["compute-sanitizer", "--tool", tool, "--error-exitcode", "9",
                         sys.executable, os.path.join(ROOT, "scripts", "sanitize.py")],
