@@ -125,6 +125,27 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
     return v;
 }
 
+template <typename T>
+__device__ __forceinline__ T ld_stream_ef(const T* p, uint64_t pol);
+template <>
+__device__ __forceinline__ int32_t ld_stream_ef(const int32_t* p, uint64_t pol) {
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+template <>
+__device__ __forceinline__ double ld_stream_ef(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+template <>
+__device__ __forceinline__ float ld_stream_ef(const float* p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 // Streamed x (dspmv_apply_host): wait until the copy stream has published this
 // apply's epoch for the chunk; trap after ~30 s rather than hang the device.
 __device__ __forceinline__ void wait_xflag(const unsigned* flag, unsigned epoch) {
@@ -492,6 +513,9 @@ __global__ void __launch_bounds__(kStreamWarps * 32) spmv_stream_kernel(StreamAr
         else vector_rows<T, false>(a.v, o, blockIdx.x * kStreamWarps + w, gridDim.x * kStreamWarps);
     }
     const uint64_t xpol = policy_evict_last();
+#if defined(DSPMV_K1B_EF)
+    const uint64_t mpol = policy_evict_first();
+#endif
     for (int t = blockIdx.x * kStreamWarps + w; t < a.ntiles; t += gridDim.x * kStreamWarps) {
         const int2 tr = __ldg(reinterpret_cast<const int2*>(a.tiles) + t);
         const int32_t p0 = __ldg(a.rowptr + tr.x), m = __ldg(a.rowptr + tr.y) - p0;
@@ -500,8 +524,14 @@ __global__ void __launch_bounds__(kStreamWarps * 32) spmv_stream_kernel(StreamAr
 #pragma unroll
         for (int k = 0; k < kStreamTile / 32; ++k) {
             const int q = lane + 32 * k;
+#if defined(DSPMV_K1B_EF)
+            // experiment: the matrix stream with an explicit L2 evict_first policy
+            c[k] = q < m ? ld_stream_ef(a.col + p0 + q, mpol) : 0;
+            v[k] = q < m ? ld_stream_ef(val + p0 + q, mpol) : T(0);
+#else
             c[k] = q < m ? __ldcs(a.col + p0 + q) : 0;
             v[k] = q < m ? __ldcs(val + p0 + q) : T(0);
+#endif
         }
 #pragma unroll
         for (int k = 0; k < kStreamTile / 32; ++k) {
@@ -512,6 +542,17 @@ __global__ void __launch_bounds__(kStreamWarps * 32) spmv_stream_kernel(StreamAr
 #endif
         }
         __syncwarp();  // keeps ptxas from pairing each gather with its multiply: all 8 stay in flight
+#if defined(DSPMV_DIAG_GATHER) && DSPMV_DIAG_GATHER == 5
+        // diagnostic build 5: no shared memory at all (each lane sums its 8
+        // products and stores one value per row slot): gathers + streaming only
+        {
+            T acc5 = T(0);
+#pragma unroll
+            for (int k = 0; k < kStreamTile / 32; ++k) acc5 = add_rn(acc5, mul_rn(v[k], xv[k]));
+            if (tr.x + lane < tr.y) __stcs(y + (kIdentity ? tr.x + lane : a.out[tr.x + lane]), acc5);
+            continue;
+        }
+#endif
 #pragma unroll
         for (int k = 0; k < kStreamTile / 32; ++k) pr[lane + 32 * k] = mul_rn(v[k], xv[k]);
         __syncwarp();
