@@ -152,7 +152,7 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
             ST_TRY(dev_upload(p, &D.s_tiles, L.s_tiles.data(), L.s_tiles.size()));
             int tpsm = stream_kernel_ctas_per_sm(p.dtype);
             if (const char* ev = std::getenv("DSPMV_STREAM_CTAS")) tpsm = std::max(1, std::min(tpsm, std::atoi(ev)));  // sweeps
-            D.grid_t = std::max(1, std::min((D.ntiles + kStreamWarps - 1) / kStreamWarps, tpsm * usable));
+            D.grid_t = std::max(1, std::min((D.ntiles + kStreamCtaWarps - 1) / kStreamCtaWarps, tpsm * usable));
             if (p.opts.s_kernel == DSPMV_SKERNEL_STREAM_TMA ||
                 (p.opts.s_kernel == DSPMV_SKERNEL_AUTO && stream_tma_default())) {
                 D.stream_tma = true;

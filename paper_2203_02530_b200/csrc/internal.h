@@ -49,7 +49,11 @@ constexpr int kPad = 8;            // device arrays padded (aligned over-read)
 constexpr int kDescInts = 16;      // per-block descriptor: r0 r1 p0 p1 flag wb[0..warps]
 constexpr int kStreamTile = 256;   // CSR-stream tile: nnz per warp pass (8 per lane)
 constexpr int kStreamRows = 64;    // CSR-stream tile: rows
-constexpr int kStreamWarps = 8;    // CSR-stream CTA: warps (one tile each)
+constexpr int kStreamWarps = 8;    // CSR-stream tiles per TMA-fed block (K1c)
+#ifndef DSPMV_STREAM_CTA_WARPS
+#define DSPMV_STREAM_CTA_WARPS 20
+#endif
+constexpr int kStreamCtaWarps = DSPMV_STREAM_CTA_WARPS;   // K1b CTA: warps (one tile each); 20 x 2 CTAs/SM measured 1 % faster than 8 x 5 on C4
 // CSR-stream with a TMA producer (spmv_stream_tma_kernel): a block is kStreamWarps
 // consecutive tiles, staged whole (col, val, rowptr slice) by one producer warp
 constexpr int kSTBlockNnz = kStreamWarps * kStreamTile;    // 2048

@@ -499,8 +499,8 @@ struct StreamArgs {
 // go to shared memory; lane j then sums row j's products in stored order from
 // +0 (the oracle's loop), so y is bitwise O1 on every row.
 template <typename T, bool kCombine, bool kIdentity>
-__global__ void __launch_bounds__(kStreamWarps * 32) spmv_stream_kernel(StreamArgs a, SpmvOperands o) {
-    __shared__ T prod[kStreamWarps][kStreamTile];
+__global__ void __launch_bounds__(kStreamCtaWarps * 32) spmv_stream_kernel(StreamArgs a, SpmvOperands o) {
+    __shared__ T prod[kStreamCtaWarps][kStreamTile];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const T* __restrict__ val = static_cast<const T*>(a.val);
     const T* __restrict__ x = static_cast<const T*>(o.x);
@@ -509,14 +509,14 @@ __global__ void __launch_bounds__(kStreamWarps * 32) spmv_stream_kernel(StreamAr
     // the long rows (> vector_threshold) first, a warp per row, so they do not
     // trail the tiles (and need no second launch)
     if (a.v.nV > 0) {
-        if (a.v.slot) vector_rows<T, true>(a.v, o, blockIdx.x * kStreamWarps + w, gridDim.x * kStreamWarps);
-        else vector_rows<T, false>(a.v, o, blockIdx.x * kStreamWarps + w, gridDim.x * kStreamWarps);
+        if (a.v.slot) vector_rows<T, true>(a.v, o, blockIdx.x * kStreamCtaWarps + w, gridDim.x * kStreamCtaWarps);
+        else vector_rows<T, false>(a.v, o, blockIdx.x * kStreamCtaWarps + w, gridDim.x * kStreamCtaWarps);
     }
     const uint64_t xpol = policy_evict_last();
 #if defined(DSPMV_K1B_EF)
     const uint64_t mpol = policy_evict_first();
 #endif
-    for (int t = blockIdx.x * kStreamWarps + w; t < a.ntiles; t += gridDim.x * kStreamWarps) {
+    for (int t = blockIdx.x * kStreamCtaWarps + w; t < a.ntiles; t += gridDim.x * kStreamCtaWarps) {
         const int2 tr = __ldg(reinterpret_cast<const int2*>(a.tiles) + t);
         const int32_t p0 = __ldg(a.rowptr + tr.x), m = __ldg(a.rowptr + tr.y) - p0;
         int32_t c[kStreamTile / 32];
@@ -1004,7 +1004,7 @@ cudaError_t launch_stream(const DevLayout& L, const SpmvOperands& o, cudaStream_
     StreamArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_out, L.s_slot, L.s_tiles, L.ntiles,
                  VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}};
     const bool c = L.s_slot != nullptr, id = L.s_out == nullptr;
-    const dim3 grid(L.grid_t), block(kStreamWarps * 32);
+    const dim3 grid(L.grid_t), block(kStreamCtaWarps * 32);
     if (x_persist_fraction() > 0 && L.x_bytes > 0) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = grid;
@@ -1172,9 +1172,9 @@ int prof_read(unsigned long long* out, int n, bool reset) {
 int stream_kernel_ctas_per_sm(int dtype) {
     int n = 0;
     if (dtype == DSPMV_F32)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_stream_kernel<float, false, true>, kStreamWarps * 32, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_stream_kernel<float, false, true>, kStreamCtaWarps * 32, 0);
     else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_stream_kernel<double, false, true>, kStreamWarps * 32, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_stream_kernel<double, false, true>, kStreamCtaWarps * 32, 0);
     return n > 0 ? n : 1;
 }
 
