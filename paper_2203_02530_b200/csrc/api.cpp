@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -850,9 +851,39 @@ cudaError_t launch_gpu_vertex(Schedule& s, int t, const void* x, void* y, cudaSt
 }
 
 // Execute op t of schedule s. `defer` = LOCAL group (exchange issued by caller).
+// NVTX ranges (DSPMV_NVTX=1): one host range per executed schedule op and
+// per apply, named after the paper's vertices and sync ops (SURVEY §5 tracing),
+// so an nsys/ncu timeline shows the traversal.  Header-only NVTX3: free when no
+// tool is attached, skipped entirely when the variable is unset.
+bool nvtx_on() {
+    static const bool on = [] {
+        const char* ev = std::getenv("DSPMV_NVTX");
+        return ev && std::atoi(ev) != 0;
+    }();
+    return on;
+}
+struct NvtxScope {
+    bool on;
+    explicit NvtxScope(bool enable, const std::string& name) : on(enable) {
+        if (on) nvtxRangePushA(name.c_str());
+    }
+    ~NvtxScope() {
+        if (on) nvtxRangePop();
+    }
+};
+std::string op_label(const dspmv_op& o) {
+    static const char* sync_names[] = {"CER", "CES", "CSWE"};
+    std::string nm = is_dag_vertex(o.kind) ? vertex_label(o.kind, o.peer)
+                                           : std::string(sync_names[(o.kind - DSPMV_OP_EVENT_RECORD) % 3]);
+    if (is_gpu_vertex(o.kind) || o.kind == DSPMV_OP_EVENT_RECORD || o.kind == DSPMV_OP_STREAM_WAIT_EVENT)
+        nm += "@s" + std::to_string(o.stream);
+    return nm;
+}
+
 dspmv_status exec_op(Schedule& s, int t, const void* x, void* y, bool defer) {
     Plan& p = *s.plan;
     const dspmv_op& o = s.ops[t];
+    NvtxScope nvtx_scope(nvtx_on(), nvtx_on() ? op_label(o) : std::string());
     const bool gpu = is_gpu_vertex(o.kind);
     const bool on_stream = gpu || o.kind == DSPMV_OP_EVENT_RECORD || o.kind == DSPMV_OP_STREAM_WAIT_EVENT;
     cudaStream_t st = on_stream ? (o.stream == 0 ? p.cur_stream0 : p.streams[o.stream]) : nullptr;
@@ -1982,6 +2013,7 @@ dspmv_status dspmv_apply(dspmv_schedule_t s, const void* x, void* y, dspmv_strea
         return fail(DSPMV_ERR_ARG, "LOCAL groups with >1 rank use dspmv_apply_group");
     if (p.host.n_local() > 0 && (!x || !y)) return fail(DSPMV_ERR_ARG, "null x/y");
     ST_TRY(check_schedule_hash(*s));
+    NvtxScope nvtx_scope(nvtx_on(), "dspmv_apply rank " + std::to_string(p.host.rank));
     ST_TRY(begin_apply(*s, static_cast<cudaStream_t>(stream)));
     p.cur_x = x;
     const bool local = p.comm->kind == DSPMV_COMM_LOCAL;
@@ -2008,6 +2040,7 @@ dspmv_status dspmv_apply_graph(dspmv_schedule_t s, const void* x, void* y, dspmv
     cudaStream_t cs = static_cast<cudaStream_t>(stream);
     if (!cs) return fail(DSPMV_ERR_ARG, "apply_graph needs a non-default stream");
     ST_TRY(check_schedule_hash(*s));
+    NvtxScope nvtx_scope(nvtx_on(), "dspmv_apply_graph rank " + std::to_string(p.host.rank));
     if (!s->gexec || !s->g_group.empty() || s->gx != x || s->gy != y || s->g_timing != s->timing)
         ST_TRY(capture_graph(*s, x, y, cs));
     const cudaError_t e = cudaGraphLaunch(s->gexec, cs);

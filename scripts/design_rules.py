@@ -186,6 +186,44 @@ def make_measure_distributed(dist, rank, plan, x, y, t_measure=0.01, n_meas=3):
     return measure
 
 
+def sweep_with_resume(space, measure, path):
+    """Measure every schedule of `space` in order; with `path` (JSONL), each
+    measured schedule is appended as {"i", "schedule", "t"} and flushed, and a
+    restarted sweep reuses the lines whose index and schedule text match, so a
+    sweep of the 4,780-schedule space survives a lost lease."""
+    done = {}
+    if path and os.path.exists(path):
+        for line in open(path):
+            try:
+                r = json.loads(line)
+            except ValueError:
+                continue                                  # a torn last line
+            done[int(r["i"])] = r
+    f = open(path, "a") if path else None
+    if f and os.path.getsize(path) > 0:
+        with open(path, "rb") as g:
+            g.seek(-1, os.SEEK_END)
+            if g.read(1) != b"\n":
+                f.write("\n")                          # end a torn last line
+    times = []
+    reused = 0
+    for i, ops in enumerate(space):
+        text = PS.describe(ops)
+        r = done.get(i)
+        if r is not None and r.get("schedule") == text:
+            times.append(float(r["t"]))
+            reused += 1
+            continue
+        t = measure(ops)
+        times.append(t)
+        if f:
+            f.write(json.dumps({"i": i, "schedule": text, "t": t}) + "\n")
+            f.flush()
+    if f:
+        f.close()
+    return np.array(times), reused
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="g3", choices=["g3", "c2", "c5", "c5b"])
@@ -197,6 +235,8 @@ def main():
     ap.add_argument("--budget", type=int, default=800, help="fine: MCTS / random-rollout samples")
     ap.add_argument("--syncs", default="derived", choices=["derived", "orderable"],
                     help="orderable: syncs are moves of their own (R-N5; 4,780 coarse schedules)")
+    ap.add_argument("--resume", default=None,
+                    help="JSONL checkpoint of the sweep: measured schedules are appended, a rerun skips them")
     a = ap.parse_args()
     if a.comm is not None:
         return main_distributed(a)
@@ -206,7 +246,7 @@ def main():
     measure = make_measure(plans, xs, ys)
     space = PS.enumerate_orderable(2) if a.syncs == "orderable" else PS.enumerate_derived(2)
     t0 = time.perf_counter()
-    times = np.array([measure(o) for o in space])
+    times, reused = sweep_with_resume(space, measure, a.resume)
     sweep_s = time.perf_counter() - t0
     labels, ranges, bounds = R.class_labels(times)
     X, cols = R.features(space)
@@ -360,7 +400,7 @@ def main_distributed(a):
     if rank == 0:
         space = PS.enumerate_orderable(2) if a.syncs == "orderable" else PS.enumerate_derived(2)
         t0 = time.perf_counter()
-        times = np.array([measure(o) for o in space])
+        times, reused = sweep_with_resume(space, measure, a.resume)
         model = (f"SPMD: {world} processes, one rank each, "
                  + ("NCCL communicator, NCCL send/recv exchange" if a.comm == "nccl" else
                     "HOST communicator (gloo bootstrap), fused Pack+put exchange over CUDA IPC")
