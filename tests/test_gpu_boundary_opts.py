@@ -234,3 +234,29 @@ def test_debug_checks_catch_schedules_that_differ_across_ranks():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: D.DSPMV_ERR_SCHEDULE, 1: D.DSPMV_ERR_SCHEDULE}, res
+
+
+def test_nvtx_ranges_do_not_change_results():
+    """DSPMV_NVTX=1 wraps every executed op and apply in an NVTX range
+    (SURVEY §5 tracing); the run under it gives the bits of a plain run."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np, torch, gen\n"
+        "from paper_2203_02530_b200 import dspmv as D\n"
+        "from tests.gpu_helpers import LocalRun, derive_ops\n"
+        "n, (rp, col, val) = gen.config_matrix('c1')\n"
+        "run = LocalRun(n, rp, col, val, 2)\n"
+        "y = run.apply(run.schedule(derive_ops()), gen.x_values((0, n), exact=True))\n"
+        "run.close()\n"
+        "np.save(sys.argv[1], y)\n" % ROOT)
+    outs = []
+    for env_on in ("0", "1"):
+        path = os.path.join("/tmp", f"nvtx_y_{os.getpid()}_{env_on}.npy")
+        r = subprocess.run([sys.executable, "-c", code, path], capture_output=True, text=True, timeout=300,
+                           env={**os.environ, "DSPMV_NVTX": env_on}, cwd=ROOT)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+        os.unlink(path)
+    assert np.array_equal(outs[0], outs[1])
