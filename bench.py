@@ -60,6 +60,16 @@ WORKLOADS = {
     "c4": ("powerlaw", 1 << 23, "BASELINE configs[3]: power-law 8,388,608 rows, avg 16 nnz/row, long tail, fp64"),
     "c5": ("7pt", (192, 192, 192), "BASELINE configs[4]: 3D 7-point Laplacian 192^3 (7,077,888 rows) fp64"),
 }
+# input values (SURVEY §5 config flags): x seed, float or exact-integer values (R-Q23)
+X_SEED = 2530
+EXACT = False
+
+
+def xvals(lo, hi):
+    import gen
+    return gen.x_values((lo, hi), seed=X_SEED, exact=EXACT)
+
+
 # measured random-gather ceiling of the x operand (scripts/ubench_gather_scope.cu,
 # profiles/r1_ubench_gather_scope.txt: 67 MB x, ld.global.nc.L1::no_allocate +
 # L2 evict_last hint, 148 SMs): the second roofline of irregular matrices
@@ -100,6 +110,10 @@ def parse():
     ap.add_argument("--exchange", default="auto", choices=["auto", "copy", "put"],
                     help="halo exchange: NCCL group (copy), fused Pack+put over peer memory "
                          "(put), or auto = time both at N>1 and keep the faster")
+    ap.add_argument("--value-mode", default="float", choices=["float", "exact"],
+                    help="exact: small-integer matrix values and x (R-Q23), every result exact; the parity "
+                         "self-check then requires bitwise equality")
+    ap.add_argument("--seed", type=int, default=2530, help="seed of the x values (counter-based, gen/)")
     ap.add_argument("--no-t1", action="store_true",
                     help="N>1: skip the 1-GPU run of the whole matrix on rank 0 (scaling efficiency)")
     return ap.parse_args()
@@ -116,7 +130,7 @@ def workload_rows(name, lo, hi):
     import gen
     kind, dims, _ = WORKLOADS[name]
     if kind == "powerlaw":
-        rp, col, val = gen.powerlaw(dims, (lo, hi))
+        rp, col, val = gen.powerlaw(dims, (lo, hi), exact=EXACT)
         return dims, rp, col, val
     rp, col, val = gen.stencil(kind, dims, (lo, hi))
     return dims[0] * dims[1] * dims[2], rp, col, val
@@ -180,7 +194,7 @@ def parity_sample(rp, col, val, lo, hi, n, npdt, seed=7, k=2048):
             pick = rng.choice(idx, size=min(256, idx.size), replace=False)
             rows |= set((np.searchsorted(rp - base, pick, side="right") - 1).tolist())
     rows = np.array(sorted(rows), np.int64)
-    x = gen.x_values((0, n)).astype(npdt).astype(np.float64)
+    x = xvals(0, n).astype(npdt).astype(np.float64)
     yref = np.empty(rows.size)
     scale = np.empty(rows.size)
     for t, i in enumerate(rows):
@@ -203,7 +217,8 @@ def check_parity(sample, y, rel):
     err = np.abs(yy - yref)
     # both sides round differently (any order within a row, R-Q10/Q11): within
     # rel * s_i, plus an fp64 rounding term of the numpy reference itself
-    ok = bool(np.all(err <= rel * scale + 1e-300) and np.all(np.isfinite(yy)))
+    ok = bool(np.all(err <= rel * scale) and np.all(np.isfinite(yy))) if rel > 0 else \
+        bool(np.array_equal(yy, yref))
     worst = float(np.max(err / np.maximum(scale, 1e-300))) if rows.size else 0.0
     return ok, worst
 
@@ -471,7 +486,7 @@ def measure(ctx, wname, headline, clocks=None, sched_from=None):
     # N>1 overlap baseline: the same plan with a zero-byte exchange (T_noexch)
     plan_none = mk(D.DSPMV_EXCHANGE_NONE) if (headline and world > 1) else None
     del col, valn
-    x = torch.from_numpy(gen.x_values((lo, hi)).astype(ctx.npdt)).cuda()
+    x = torch.from_numpy(xvals(lo, hi).astype(ctx.npdt)).cuda()
     y = torch.empty_like(x)
     torch.cuda.synchronize()
 
@@ -535,7 +550,7 @@ def measure(ctx, wname, headline, clocks=None, sched_from=None):
     y.fill_(float("nan"))
     apply_fn(sched, x, y, ctx.stream)
     torch.cuda.synchronize()
-    ok, worst = check_parity(sample, y, ctx.rel)
+    ok, worst = check_parity(sample, y, 0.0 if EXACT else ctx.rel)
     parity = {"ok": ctx.alland(ok), "rows_checked": int(ctx.allsum(float(0 if sample is None else len(sample[0])))),
               "max_err_over_scale": ctx.allmax(worst), "tolerance": ctx.rel,
               "reference": "numpy fp64 row products of sampled rows (first/last, remote, random) vs the "
@@ -621,7 +636,7 @@ def e2e_leg(ctx, sched, lo, hi, nnz_total, steps):
     x, the schedule, and the D2H of y inside every timed step."""
     import gen
     D, torch = ctx.D, ctx.torch
-    xh = torch.from_numpy(gen.x_values((lo, hi)).astype(ctx.npdt)).pin_memory()
+    xh = torch.from_numpy(xvals(lo, hi).astype(ctx.npdt)).pin_memory()
     yh = torch.empty_like(xh).pin_memory()
     k = max(3, min(steps, 100))
     for _ in range(3):
@@ -655,6 +670,25 @@ def e2e_leg(ctx, sched, lo, hi, nnz_total, steps):
                                "rates; pcie_frac = floor / e2e step time",
                        "source": pc["source"]}
     return out
+
+
+def build_ids():
+    """Content hashes of the library that ran and of its sources (the box has
+    no .git): ties a JSON line to a build."""
+    import hashlib
+
+    def h(paths):
+        d = hashlib.sha256()
+        for q in paths:
+            try:
+                d.update(open(q, "rb").read())
+            except OSError:
+                pass
+        return d.hexdigest()[:16]
+    from paper_2203_02530_b200 import dspmv as D
+    src = sorted(os.path.join(dp, f) for dp, _, fs in os.walk(os.path.join(ROOT, "paper_2203_02530_b200", "csrc"))
+                 for f in fs) + [os.path.join(ROOT, "include", "dspmv.h")]
+    return {"lib_sha16": h([D.LIB_PATH]), "src_sha16": h(src), "bench_sha16": h([os.path.abspath(__file__)])}
 
 
 def pcie_peak():
@@ -760,7 +794,7 @@ def choose_exchange(ctx, mk, lo, hi):
     import gen
     D, torch, dist = ctx.D, ctx.torch, ctx.dist
     ops = derive(D, BEST_ORDER, BEST_STREAMS)
-    x = torch.from_numpy(gen.x_values((lo, hi)).astype(ctx.npdt)).cuda()
+    x = torch.from_numpy(xvals(lo, hi).astype(ctx.npdt)).cuda()
     y = torch.empty_like(x)
     times, plans, errs = {}, {}, {}
     for name, ex in (("copy", D.DSPMV_EXCHANGE_COPY), ("put", D.DSPMV_EXCHANGE_PUT)):
@@ -868,7 +902,7 @@ def t1_run(ctx, wname, ops, mode):
             plan = D.dspmv_plan_create(comm1, n, rp, col, val.astype(ctx.npdt), dtype=ctx.dt,
                                        caller_stream0=bool(ctx.a.caller_stream0))
             del rp, col, val
-            x = torch.from_numpy(gen.x_values((0, n)).astype(ctx.npdt)).cuda()
+            x = torch.from_numpy(xvals(0, n).astype(ctx.npdt)).cuda()
             y = torch.empty_like(x)
             s = D.dspmv_schedule_create(plan, ops, 2)
             D.dspmv_schedule_set_timing(s, timing_mask(1))
@@ -949,6 +983,8 @@ def run_ours(a):
                 "step_hbm_gbs_algorithmic": head.pop("step_hbm_gbs_algorithmic"),
                 "yL_window_in_step_us_median": head.pop("yL_window_in_step_us_median"),
                 "wall_s_timed_region": head.pop("wall_s_timed_region"),
+                "values": {"mode": "exact" if EXACT else "float", "x_seed": X_SEED, "matrix_seed": 2203},
+                "build": build_ids(),
             },
             "roofline": head.pop("roofline"),
             "parity_ok": head["parity"]["ok"], "parity": head.pop("parity"),
@@ -981,7 +1017,7 @@ def cpu_baseline(workload_name, budget_s=10.0):
     from oracle import spmv as O1
     n, rp, col, val = workload_rows(workload_name, 0, workload_n(workload_name))
     desc = workload_desc(workload_name, 1)
-    x = gen.x_values((0, n))
+    x = xvals(0, n)
     O1.o1_spmv(rp, col, val, x)  # warm
     reps, t0 = 0, time.perf_counter()
     while time.perf_counter() - t0 < budget_s:
@@ -1030,7 +1066,7 @@ def run_reference(a, budget_s=90.0):
     n = workload_n(a.workload)
     probe = min(n, 1 << 18)
     _, rp, col, val = workload_rows(a.workload, 0, probe)
-    x = gen.x_values((0, n))
+    x = xvals(0, n)
     t0 = time.perf_counter()
     O1.o1_spmv(rp, col, val, x)
     t_probe = max(time.perf_counter() - t0, 1e-6)
@@ -1064,6 +1100,8 @@ def run_reference(a, budget_s=90.0):
 
 def main():
     a = parse()
+    global X_SEED, EXACT
+    X_SEED, EXACT = a.seed, a.value_mode == "exact"
     if a.impl == "reference":
         run_reference(a)
     else:
