@@ -498,11 +498,12 @@ def measure(ctx, wname, headline, clocks=None, sched_from=None):
         sweep = schedule_sweep(ctx, plan, x, y, space=space, out_path=a.sweep_out)
         ranked = sweep.pop("_ranked_ops")
         ranked_top = ranked[:16]
-        ops, best_mode, rerank_log = rerank(ctx, plan, x, y, ranked, a.rerank, mode_pref, ex_mode)
+        ops, best_mode, cs0, rerank_log = rerank(ctx, plan, x, y, ranked, a.rerank, mode_pref, ex_mode)
         sweep["rerank_us"] = rerank_log
         from paper_2203_02530_b200 import schedules as PS
         sched_desc = (f"best of the {min(a.rerank, len(ranked))} sweep-fastest (+1) re-timed per step "
-                      f"({best_mode} execution): " + PS.describe(ops))
+                      f"({best_mode} execution, stream 0 = {'caller' if cs0 else 'library'} stream): "
+                      + PS.describe(ops))
         if mode_pref == "auto":
             mode_pref = best_mode
     elif sched_from is not None:
@@ -513,18 +514,21 @@ def measure(ctx, wname, headline, clocks=None, sched_from=None):
         cands = list(head_ranked[:8]) if head_ranked else []
         if not any(np.array_equal(head_ops, c) for c in cands):
             cands.append(head_ops)
-        ops, best_mode, _ = rerank(ctx, plan, x, y, cands, len(cands), mode_pref, ex_mode)
+        ops, best_mode, cs0, _ = rerank(ctx, plan, x, y, cands, len(cands), mode_pref, ex_mode)
         sched_desc = (f"best of the headline sweep's {len(cands)} fastest, re-timed on this matrix "
-                      f"({best_mode} execution): " + PS.describe(ops))
+                      f"({best_mode} execution, stream 0 = {'caller' if cs0 else 'library'} stream): "
+                      + PS.describe(ops))
         if mode_pref == "auto":
             mode_pref = best_mode
     else:
         order = BEST_ORDER if a.schedule == "best" else PAPER1_ORDER
         streams = BEST_STREAMS if a.schedule == "best" else dict.fromkeys(BEST_STREAMS, 0)
         ops = derive(D, order, streams)
+        cs0 = 0
         sched_desc = a.schedule + ": " + " ".join(order) + f" streams={streams}"
     sched = D.dspmv_schedule_create(plan, ops, 2)
     D.dspmv_schedule_set_timing(sched, timing_mask(world))
+    D.dspmv_schedule_set_caller_stream0(sched, cs0)
     iyl = [i for i, o in enumerate(ops) if o[0] == D.DSPMV_OP_SPMV_LOCAL][0]
     iposts = [i for i, o in enumerate(ops) if o[0] in (D.DSPMV_OP_POST_SEND, D.DSPMV_OP_POST_RECV)] \
         if world > 1 else []
@@ -612,7 +616,7 @@ def measure(ctx, wname, headline, clocks=None, sched_from=None):
                     "per direction (B200_PROFILING.md), 900 GB/s spec"}
     # ---- overlap efficiency (N > 1): 1 - (T_best - T_noexch) / T_exch_alone
     if plan_none is not None:
-        rec["overlap"] = overlap_efficiency(ctx, plan, plan_none, ops, mode, x, y, ms_per_step)
+        rec["overlap"] = overlap_efficiency(ctx, plan, plan_none, ops, mode, x, y, ms_per_step, cs0)
     if plan_none is not None:
         D.dspmv_plan_destroy(plan_none)
 
@@ -623,6 +627,7 @@ def measure(ctx, wname, headline, clocks=None, sched_from=None):
         rec["e2e"] = e2e_leg(ctx, sched, lo, hi, nnz_total, steps)
         rec["_sched_ops"] = ops
         rec["_mode"] = mode
+        rec["_cs0"] = cs0
         rec["_ranked"] = ranked_top if sweep is not None else None
     D.dspmv_schedule_destroy(sched)
     D.dspmv_plan_destroy(plan)
@@ -702,7 +707,7 @@ def pcie_peak():
         return None
 
 
-def overlap_efficiency(ctx, plan, plan_none, ops, mode, x, y, t_best):
+def overlap_efficiency(ctx, plan, plan_none, ops, mode, x, y, t_best, cs0=0):
     """T_noexch = the headline schedule on a plan whose exchange
     moves no bytes (DSPMV_EXCHANGE_NONE, same syncs); T_exch_alone = the
     serial schedule (both Waits before any SpMV) minus the same serial
@@ -713,6 +718,7 @@ def overlap_efficiency(ctx, plan, plan_none, ops, mode, x, y, t_best):
     def t_of(p, o):
         s = D.dspmv_schedule_create(p, o, 2)
         D.dspmv_schedule_set_timing(s, timing_mask(ctx.world))
+        D.dspmv_schedule_set_caller_stream0(s, cs0)
         f = fn
         if f is D.dspmv_apply_graph:   # agree on the graph before any rank launches one
             ok = True
@@ -763,7 +769,11 @@ def rerank(ctx, plan, x, y, ranked, k, mode_pref, ex_mode):
     for ci, cand in enumerate(cands):
         sc = D.dspmv_schedule_create(plan, cand, 2)
         D.dspmv_schedule_set_timing(sc, timing_mask(ctx.world))
-        for mname, fn in modes:
+        # stream 0 bound to a library stream (the sweep's symmetric setting) or
+        # to the caller's stream (no fork for its first op): a timing choice
+        # made after the sweep, so the sweep's stream bijection still holds
+        for (mname, fn), cs0 in [(m, b) for m in modes for b in (0, 1)]:
+            D.dspmv_schedule_set_caller_stream0(sc, cs0)
             # every rank must run the same applies (PUT epochs): capture first,
             # agree, then run
             ok = True
@@ -780,11 +790,11 @@ def rerank(ctx, plan, x, y, ranked, k, mode_pref, ex_mode):
             ctx.torch.cuda.synchronize()
             st = time_steps(ctx, sc, fn, x, y, 30)[0]
             tot = ctx.allmax(sum(st) / 30)
-            log.append([ci, mname, round(tot * 1e3, 2)])
+            log.append([ci, mname, cs0, round(tot * 1e3, 2)])
             if best is None or tot < best[0]:
-                best = (tot, cand, mname)
+                best = (tot, cand, mname, cs0)
         D.dspmv_schedule_destroy(sc)
-    return best[1], best[2], log
+    return best[1], best[2], best[3], log
 
 
 def choose_exchange(ctx, mk, lo, hi):
@@ -888,7 +898,7 @@ def schedule_sweep(ctx, plan, x, y, t_measure=0.01, space="derived", out_path=No
     }
 
 
-def t1_run(ctx, wname, ops, mode):
+def t1_run(ctx, wname, ops, mode, cs0=0):
     """N>1 scaling efficiency: rank 0 alone runs the whole matrix on its GPU
     through a 1-rank communicator (same schedule and execution mode, 30
     flushed steps); the other ranks wait."""
@@ -906,6 +916,7 @@ def t1_run(ctx, wname, ops, mode):
             y = torch.empty_like(x)
             s = D.dspmv_schedule_create(plan, ops, 2)
             D.dspmv_schedule_set_timing(s, timing_mask(1))
+            D.dspmv_schedule_set_caller_stream0(s, cs0)
             fn = D.dspmv_apply_graph if mode == "graph" else D.dspmv_apply
             for _ in range(5):
                 D.dspmv_l2_flush(ctx.device, ctx.stream)
@@ -943,13 +954,13 @@ def run_ours(a):
     world, rank = ctx.world, ctx.rank
     clocks = Clocks(list(range(min(world, ctx.torch.cuda.device_count())))) if rank == 0 else None
     head = measure(ctx, a.workload, True, clocks)
-    ops, mode, ranked = head.pop("_sched_ops"), head.pop("_mode"), head.pop("_ranked")
+    ops, mode, ranked, cs0 = head.pop("_sched_ops"), head.pop("_mode"), head.pop("_ranked"), head.pop("_cs0")
     secs = {}
     for w in secondaries(a, world):
         secs[w] = measure(ctx, w, False, clocks, sched_from=(ops, mode, ranked))
     scaling = None
     if world > 1 and not a.no_t1:
-        t1 = t1_run(ctx, a.workload, ops, mode)
+        t1 = t1_run(ctx, a.workload, ops, mode, cs0)
         if rank == 0 and t1:
             scaling = {"T1_ms": round(t1, 6), "TP_ms": head["ms_per_step"], "P": world,
                        "efficiency": round(t1 / (world * head["ms_per_step"]), 4),

@@ -414,6 +414,13 @@ dspmv_status dspmv_schedule_destroy(dspmv_schedule_t sched);
  * records an event on the caller stream at START and at END.  After an
  * apply, ms[i] = device time of ops[i] (0 for untimed ops) and, with the
  * START bit, ms[0] = END - START on the caller stream (the whole apply). */
+/* Bind schedule stream 0 to the caller's stream for this schedule (mode 1),
+ * to a library stream (0), or follow the plan's opts.caller_stream0 (-1,
+ * default).  With 1, an op at the head of stream 0 needs no fork from the
+ * caller's stream (and START's timing event doubles as its begin event); the
+ * two schedule streams are then no longer interchangeable, so design-space
+ * sweeps keep 0 and apply 1 only when timing a chosen schedule. */
+dspmv_status dspmv_schedule_set_caller_stream0(dspmv_schedule_t sched, int mode);
 dspmv_status dspmv_schedule_set_timing(dspmv_schedule_t sched, int enable);
 dspmv_status dspmv_schedule_op_times(dspmv_schedule_t sched, float* ms, int n);
 /* Per-op timeline of the last apply (needs timing with the START bit):

@@ -754,8 +754,9 @@ dspmv_status begin_apply(Schedule& s, cudaStream_t caller) {
     CUDA_TRY(cudaEventRecord(p.ev_start, caller));
     // schedule stream 0 may be the caller's stream itself (no cross-stream
     // wait for its work); the others wait on the caller's START point
-    p.cur_stream0 = p.opts.caller_stream0 ? caller : p.streams[0];
-    for (int i = p.opts.caller_stream0 ? 1 : 0; i < s.n_streams; ++i)
+    const bool cs0 = s.caller_stream0 >= 0 ? s.caller_stream0 != 0 : p.opts.caller_stream0 != 0;
+    p.cur_stream0 = cs0 ? caller : p.streams[0];
+    for (int i = cs0 ? 1 : 0; i < s.n_streams; ++i)
         CUDA_TRY(cudaStreamWaitEvent(p.streams[i], p.ev_start, 0));
     for (ExGroup& g : s.groups) g.ps = g.pr = g.issued = false;
     return DSPMV_OK;
@@ -1049,7 +1050,8 @@ dspmv_status capture_graph(const std::vector<Schedule*>& ss, const std::vector<c
         Plan& p = *ss[r]->plan;
         const int ns = ss[r]->n_streams;
         rc[r].st.resize(ns);
-        for (int i = 0; i < ns; ++i) rc[r].st[i] = (i == 0 && p.opts.caller_stream0 && !group) ? origin : p.streams[i];
+        const bool cs0 = ss[r]->caller_stream0 >= 0 ? ss[r]->caller_stream0 != 0 : p.opts.caller_stream0 != 0;
+        for (int i = 0; i < ns; ++i) rc[r].st[i] = (i == 0 && cs0 && !group) ? origin : p.streams[i];
         rc[r].all = rc[r].st;
         if (p.has_peers) rc[r].all.push_back(p.comm_stream);
         if (group && !p.put_mode) {
@@ -1940,6 +1942,18 @@ dspmv_status dspmv_schedule_destroy(dspmv_schedule_t s) {
     destroy_timing(*s);
     s->plan->live_scheds--;
     delete s;
+    return DSPMV_OK;
+}
+
+dspmv_status dspmv_schedule_set_caller_stream0(dspmv_schedule_t s, int mode) {
+    if (!s) return fail(DSPMV_ERR_ARG, "null schedule");
+    if (mode < -1 || mode > 1) return fail(DSPMV_ERR_ARG, "mode must be -1, 0 or 1");
+    if (s->caller_stream0 != mode && s->gexec) {
+        CUDA_TRY(cudaSetDevice(s->plan->device));
+        cudaGraphExecDestroy(s->gexec);   // captured with the other stream binding
+        s->gexec = nullptr;
+    }
+    s->caller_stream0 = mode;
     return DSPMV_OK;
 }
 

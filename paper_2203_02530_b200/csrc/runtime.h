@@ -242,6 +242,7 @@ struct Schedule {
     cudaEvent_t gev[DSPMV_MAX_STREAMS + 2] = {};  // fork / join helpers
     bool timed_valid = false;
     bool hash_checked = false;         // opts.debug_checks: ops agreed across ranks
+    int caller_stream0 = -1;           // -1: the plan's opts.caller_stream0; 0 / 1: override
     // Timestamp aliasing.  A timing event recorded right behind another one
     // on the same stream costs ~2.3 us on B200
     // (profiles/r1_ubench_graph_events.txt), so an event that would sit at

@@ -135,6 +135,7 @@ _sig("dspmv_schedule_format", [_P, _I, _P, ctypes.c_size_t])
 _sig("dspmv_schedule_create", [_P, _P, _I, _I, _P])
 _sig("dspmv_schedule_destroy", [_P])
 _sig("dspmv_schedule_set_timing", [_P, _I])
+_sig("dspmv_schedule_set_caller_stream0", [_P, _I])
 _sig("dspmv_schedule_op_times", [_P, _P, _I])
 _sig("dspmv_schedule_op_timeline", [_P, _P, _P, _I])
 _sig("dspmv_apply", [_P, _P, _P, _P])
@@ -542,6 +543,11 @@ def _check_vec(sched, v, name, host: bool):
 
 def dspmv_schedule_destroy(sched):
     _check(lib.dspmv_schedule_destroy(sched))
+
+
+def dspmv_schedule_set_caller_stream0(sched, mode: int):
+    """1: schedule stream 0 is the caller's stream; 0: a library stream; -1: the plan's option."""
+    _check(lib.dspmv_schedule_set_caller_stream0(sched, int(mode)))
 
 
 def dspmv_schedule_set_timing(sched, enable):

@@ -260,3 +260,34 @@ def test_nvtx_ranges_do_not_change_results():
         outs.append(np.load(path))
         os.unlink(path)
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_schedule_caller_stream0_override():
+    """dspmv_schedule_set_caller_stream0: stream 0 bound to the caller's
+    stream or to a library stream, per schedule, in host and graph mode (the
+    cached graph is re-captured on a change): identical bits, = O1."""
+    n = 32 ** 3
+    rp, col, val = gen.stencil("7pt", (32, 32, 32))
+    comm = D.dspmv_comm_create(D.dspmv_comm_unique_id(), 1, 0, 0)
+    plan = D.dspmv_plan_create(comm, n, rp, col, val)
+    order = ["start", "y_L", "Pack", "PostSend", "PostRecv", "WaitRecv", "Unpack", "y_R", "WaitSend", "end"]
+    s = D.dspmv_schedule_create(plan, derive_ops(order, {"y_L": 0, "Pack": 1, "Unpack": 1, "y_R": 0}), 2)
+    D.dspmv_schedule_set_timing(s, True)
+    x = torch.from_numpy(gen.x_values((0, n))).cuda()
+    st = torch.cuda.Stream()
+    ref = O1.o1_spmv(rp, col, val, x.cpu().numpy())
+    try:
+        for mode in (0, 1, -1, 1, 0):
+            D.dspmv_schedule_set_caller_stream0(s, mode)
+            for fn in (D.dspmv_apply, D.dspmv_apply_graph):
+                y = torch.full_like(x, float("nan"))
+                fn(s, x, y, st)
+                torch.cuda.synchronize()
+                assert np.array_equal(y.cpu().numpy(), ref), (mode, fn.__name__)
+                assert D.dspmv_schedule_op_times(s)[0] > 0
+        with pytest.raises(D.DspmvError):
+            D.dspmv_schedule_set_caller_stream0(s, 2)
+    finally:
+        D.dspmv_schedule_destroy(s)
+        D.dspmv_plan_destroy(plan)
+        D.dspmv_comm_destroy(comm)
