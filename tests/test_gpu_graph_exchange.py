@@ -196,3 +196,37 @@ def test_multiprocess_put_graph(world):
     for k in range(len(res[0])):
         y = np.concatenate([np.array(res[r][k]) for r in range(world)])
         assert np.array_equal(y, yref), k
+
+
+@pytest.mark.parametrize("cfg,P,exchange,pack_mode", [
+    ("c5", 4, D.DSPMV_EXCHANGE_PUT, D.DSPMV_PACK_GATHER),
+    ("c5", 4, D.DSPMV_EXCHANGE_COPY, D.DSPMV_PACK_ALIAS_IF_CONTIGUOUS),
+    ("c4", 8, D.DSPMV_EXCHANGE_PUT, D.DSPMV_PACK_GATHER),
+], ids=["c5-put", "c5-alias", "c4-put-8"])
+def test_full_size_group_graph_vs_o1(cfg, P, exchange, pack_mode):
+    """BASELINE configs[4] (7-pt 192^3 over 4 ranks) and configs[3] (power-law
+    8M over 8 ranks, up to 7 peers) at full size, as ONE GPU-resident graph
+    per apply with the fused put or aliased sends: every row against the O1
+    oracle (the C loop runs the whole matrix in well under a second), over
+    both PUT receive-buffer parities."""
+    n, (rp, col, val) = gen.config_matrix(cfg)
+    x = gen.x_values((0, n))
+    yref = O1.o1_spmv(rp, col, val, x)
+    scale = O1.o1_absdot(rp, col, val, x)
+    run = LocalRun(n, rp, col, val, P, exchange=exchange, pack_mode=pack_mode)
+    xs, ys = run.xy(x)
+    stream = torch.cuda.Stream()
+    try:
+        ss = run.schedule(oracle_ops_to_lib(S.enumerate_derived(2, S.EDGES)[5]))
+        for _ in range(2):
+            for y in ys:
+                y.fill_(float("nan"))
+            D.dspmv_apply_graph_group(ss, xs, ys, stream)
+            torch.cuda.synchronize()
+            y = np.concatenate([t.cpu().numpy() for t in ys])
+            assert np.all(np.abs(y - yref) <= 1e-12 * scale)
+            short = np.diff(rp) <= 8        # one lane per row (stencil) / CSR-stream rows: bitwise O1
+            if cfg == "c5":
+                assert np.array_equal(y[short], yref[short])
+    finally:
+        run.close()
