@@ -245,6 +245,32 @@ void build_host_pipe(Plan& p, Layout& L) {
         L.s_desc[size_t(b) * kDescInts + 15] = pm;
     }
     H.K = K;
+    // y by copy engine: only where each group's blocks cover a contiguous,
+    // increasing run of rows that no other kernel writes (one rank, S rows in
+    // matrix order, no warp-per-row rows, no combined rows)
+    H.ycopy = false;
+    if (p.host.nranks == 1 && L.nV == 0 && L.s_identity && !L.stream && !L.s_has_slot) {
+        H.yrow.assign(size_t(K) + 1, 0);
+        H.nblk.assign(size_t(K), 0);
+        bool ok = true;
+        int32_t prev = -1;
+        for (int32_t b = 0; b < L.nb && ok; ++b) {
+            const int32_t* d = L.s_desc.data() + size_t(b) * kDescInts;
+            const int g = d[15];
+            ok = g >= prev;   // groups in block order
+            if (g != prev) {
+                for (int k = prev + 1; k <= g; ++k) H.yrow[k] = d[0];
+                prev = g;
+            }
+            H.nblk[g]++;
+        }
+        for (int k = prev + 1; k <= K; ++k) H.yrow[k] = L.nS;
+        // measured (profiles/r2_e2e_ycopy.txt): C3 (134 MB of y) 3.46-3.79 ms vs
+        // 3.77-3.85 ms zero-copy; C2 (16.8 MB) 0.60 vs 0.54 ms -- copy engine
+        // for large y only
+        H.ycopy = ok && L.nS == n && bytes >= (int64_t(64) << 20);
+        if (const char* ev = std::getenv("DSPMV_HOST_YCOPY")) H.ycopy = H.ycopy && std::atoi(ev) != 0;  // A/B
+    }
 }
 
 // Phase 2 on the device side: pack map + send buffer.
@@ -762,6 +788,29 @@ dspmv_status begin_apply(Schedule& s, cudaStream_t caller) {
     return DSPMV_OK;
 }
 
+// apply_host, y by copy engine: queue each group's wait-for-count + copy on
+// the D2H stream.  Called right AFTER the y_L launch: streams can share a
+// hardware queue (CUDA_DEVICE_MAX_CONNECTIONS), and a stream wait queued
+// before the kernel that satisfies it could then block that kernel.
+cudaError_t enqueue_ycopy(Plan& p) {
+    auto& H = p.pipe;
+    auto wait = wait_value32();
+    if (!wait) return cudaErrorNotSupported;
+    for (int k = 0; k < H.K; ++k) {
+        if (H.yrow[k + 1] <= H.yrow[k]) continue;
+        if (wait(reinterpret_cast<CUstream>(H.d2h), reinterpret_cast<CUdeviceptr>(H.d_ydone + k), H.nblk[k],
+                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+            return cudaErrorUnknown;
+        const size_t off = size_t(H.yrow[k]) * p.esize, len = size_t(H.yrow[k + 1] - H.yrow[k]) * p.esize;
+        const cudaError_t e = cudaMemcpyAsync(static_cast<char*>(H.y_host) + off,
+                                              static_cast<const char*>(p.d_yout) + off, len,
+                                              cudaMemcpyDeviceToHost, H.d2h);
+        if (e != cudaSuccess) return e;
+    }
+    H.y_queued = true;
+    return cudaEventRecord(H.ev_out, H.d2h);
+}
+
 // The kernel(s) of GPU vertex op t on stream st (shared by the host-driven
 // executor and graph capture).
 cudaError_t launch_gpu_vertex(Schedule& s, int t, const void* x, void* y, cudaStream_t st) {
@@ -812,8 +861,11 @@ cudaError_t launch_gpu_vertex(Schedule& s, int t, const void* x, void* y, cudaSt
             }
             op.xflag = H.d_xflag;
             op.epoch = p.epoch;
+            op.ydone = H.ycopy ? H.d_ydone : nullptr;
             e = launch_spmv_part(p.L, p.dtype, op, st, 0, p.L.nb, false);
             op.xflag = nullptr;
+            op.ydone = nullptr;
+            if (e == cudaSuccess && H.ycopy) e = enqueue_ycopy(p);
             if (e == cudaSuccess && p.L.nV > 0) {
                 e = cudaStreamWaitEvent(st, H.ev_x[H.K - 1], 0);
                 if (e == cudaSuccess) e = launch_spmv_part(p.L, p.dtype, op, st, p.L.nb, p.L.nb, true);
@@ -1441,6 +1493,9 @@ static void free_plan_device(Plan& p) {
     for (auto& e : p.pipe.ev_x)
         if (e) cudaEventDestroy(e), e = nullptr;
     if (p.pipe.ev_in) cudaEventDestroy(p.pipe.ev_in), p.pipe.ev_in = nullptr;
+    if (p.pipe.d2h) cudaStreamDestroy(p.pipe.d2h), p.pipe.d2h = nullptr;
+    if (p.pipe.ev_zero) cudaEventDestroy(p.pipe.ev_zero), p.pipe.ev_zero = nullptr;
+    if (p.pipe.ev_out) cudaEventDestroy(p.pipe.ev_out), p.pipe.ev_out = nullptr;
     for (auto& e : p.g_pack_ev)
         if (e) cudaEventDestroy(e);
     p.g_pack_ev.clear();
@@ -2206,14 +2261,49 @@ dspmv_status dspmv_apply_host(dspmv_schedule_t s, const void* x_host, void* y_ho
         if (r != CUDA_SUCCESS) return fail(DSPMV_ERR_CUDA, "cuStreamWriteValue32 failed (" + std::to_string(int(r)) + ")");
         CUDA_TRY(cudaEventRecord(H.ev_x[k], q));
     }
+    if (H.ycopy) {
+        // y leaves on the second copy engine, group by group, as the row
+        // blocks of each x chunk finish (SM stores into host memory share
+        // PCIe less well: profiles/r2_ubench_zerocopy.txt).  The counters are
+        // cleared on the caller stream before the apply's kernels; the waits
+        // and copies follow the y_L launch (enqueue_ycopy).
+        auto wait = wait_value32();
+        if (!wait) return fail(DSPMV_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+        if (!H.d2h) {
+            ST_TRY(dev_alloc(p, reinterpret_cast<void**>(&H.d_ydone), size_t(H.K) * 4, true));
+            CUDA_TRY(cudaStreamCreateWithFlags(&H.d2h, cudaStreamNonBlocking));
+            CUDA_TRY(cudaEventCreateWithFlags(&H.ev_zero, cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&H.ev_out, cudaEventDisableTiming));
+        }
+        CUDA_TRY(cudaMemsetAsync(H.d_ydone, 0, size_t(H.K) * 4, cs));   // before this apply's kernels
+        CUDA_TRY(cudaEventRecord(H.ev_zero, cs));
+        CUDA_TRY(cudaStreamWaitEvent(H.d2h, H.ev_zero, 0));
+        H.y_host = y_host;   // the waits and copies are queued right after the y_L launch (enqueue_ycopy)
+    }
     p.streaming = true;
-    const dspmv_status st = dspmv_apply(s, p.d_xin, y_map, stream);
+    const dspmv_status st = dspmv_apply(s, p.d_xin, H.ycopy ? p.d_yout : y_map, stream);
     p.streaming = false;
     if (st != DSPMV_OK) {
         cudaStreamSynchronize(H.h2d);
         return st;
     }
     CUDA_TRY(cudaStreamWaitEvent(cs, H.ev_x[H.K - 1], 0));   // every H2D done before d_xin is reused
+    if (H.ycopy) {
+        if (!H.y_queued) return fail(DSPMV_ERR_STATE, "apply_host: the schedule launched no y_L");
+        H.y_queued = false;
+        // the last y copies; bounded wait (a kernel that died would leave the
+        // copy stream parked on its counter)
+        const auto t0 = std::chrono::steady_clock::now();
+        for (;;) {
+            const cudaError_t q = cudaEventQuery(H.ev_out);
+            if (q == cudaSuccess) break;
+            if (q != cudaErrorNotReady) return fail(DSPMV_ERR_CUDA, std::string("apply_host y copy: ") + cudaGetErrorString(q));
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60)) {
+                p.poisoned = true;
+                return fail(DSPMV_ERR_STATE, "apply_host: y copies did not complete within 60 s");
+            }
+        }
+    }
     CUDA_TRY(cudaStreamSynchronize(cs));
     return DSPMV_OK;
 }

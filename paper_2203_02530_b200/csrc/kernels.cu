@@ -255,6 +255,15 @@ __device__ __forceinline__ void combine(T acc, int32_t k, int32_t orow, const Sp
     }
 }
 
+// apply_host with y leaving by copy engine: block b's rows are stored (its
+// slot was released by every consumer warp, mbarrier acquire); make them
+// visible device-wide, then count the block in its x-chunk group
+__device__ __forceinline__ void block_done(const BlockArgs& a, const SpmvOperands& o, int b) {
+    const int g = __ldg(a.desc + size_t(b) * kDescInts + 15);
+    __threadfence();
+    atomicAdd(o.ydone + g, 1u);
+}
+
 template <int CFG>
 struct Cfg {
     static constexpr int kTile = kBlockCfgs[CFG].tile;
@@ -356,7 +365,10 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
 #ifdef DSPMV_PROFILE
                 const long long tw = clock64();
 #endif
-                if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+                if (u > 0) {
+                    mbar_wait(&empty[s], (u - 1) & 1);
+                    if (kCoh && o.ydone) block_done(a, o, b - C::kStages * int(gridDim.x));
+                }
 #ifdef DSPMV_PROFILE
                 PROF_ADD(0, tw);
                 const long long ti = clock64();
@@ -386,6 +398,12 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
                 PROF_ADD(1, ti);
                 PROF_INC(4, 1);
 #endif
+            }
+            if (kCoh && o.ydone) {   // the last blocks of this CTA: wait until consumed, then count
+                for (int j = it > C::kStages ? it - C::kStages : 0; j < it; ++j) {
+                    mbar_wait(&empty[j % C::kStages], (j / C::kStages) & 1);
+                    block_done(a, o, a.b0 + int(blockIdx.x) + j * int(gridDim.x));
+                }
             }
         }
         return;

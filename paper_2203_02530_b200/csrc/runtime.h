@@ -60,6 +60,9 @@ struct SpmvOperands {
     // xflag[desc[15] of b] >= epoch, i.e. its x chunks have landed
     const unsigned* xflag = nullptr;
     unsigned epoch = 0;
+    // apply_host with y leaving by copy engine: the producer of each row-block
+    // CTA adds 1 to ydone[desc[15]] once a staged block's rows are stored
+    unsigned* ydone = nullptr;
 };
 
 // kernels.cu
@@ -195,6 +198,18 @@ struct Plan {
         cudaStream_t h2d = nullptr;
         std::vector<cudaEvent_t> ev_x;
         cudaEvent_t ev_in = nullptr;
+        // y by copy engine (single rank, row-ordered S blocks, no long rows):
+        // group k's blocks write y rows [yrow[k], yrow[k+1]) and count
+        // themselves in d_ydone[k]; a second copy stream copies each group's
+        // rows once its count reaches nblk[k]
+        bool ycopy = false;
+        std::vector<int64_t> yrow;     // [K+1]
+        std::vector<unsigned> nblk;    // [K]
+        unsigned* d_ydone = nullptr;   // [K]
+        cudaStream_t d2h = nullptr;
+        cudaEvent_t ev_zero = nullptr, ev_out = nullptr;
+        void* y_host = nullptr;        // this apply_host's y (pinned)
+        bool y_queued = false;         // enqueue_ycopy ran for this apply
     } pipe;
     bool streaming = false;            // inside dspmv_apply_host with pinned x/y
 };
