@@ -70,10 +70,13 @@ def xvals(lo, hi):
     return gen.x_values((lo, hi), seed=X_SEED, exact=EXACT)
 
 
-# measured random-gather ceiling of the x operand (scripts/ubench_gather_scope.cu,
-# profiles/r1_ubench_gather_scope.txt: 67 MB x, ld.global.nc.L1::no_allocate +
-# L2 evict_last hint, 148 SMs): the second roofline of irregular matrices
-GATHER_CEILING_GPS = 256.3
+# measured random-gather ceiling of the x operand: the best LSU rate measured
+# for random fp64 gathers from a 64 MB x (ld.global.nc.L1::no_allocate + L2
+# evict_last, 8 gathers in flight per thread, 148 SMs): 271.4 G/s
+# (scripts/ubench_tma_gather4.cu, profiles/r2_ubench_tma_gather4.txt; round 1's
+# scripts/ubench_gather_scope.cu gave 256.3 at 67 MB) -- the second roofline
+# of irregular matrices
+GATHER_CEILING_GPS = 271.4
 
 
 def parse():
@@ -578,8 +581,8 @@ def measure(ctx, wname, headline, clocks=None, sched_from=None):
         roof["gather_roofline"] = {
             "gathers_per_launch": int(info["nnz_local"]), "achieved_G_per_s": round(gps, 1),
             "ceiling_G_per_s": GATHER_CEILING_GPS, "frac": round(gps / GATHER_CEILING_GPS, 4),
-            "ceiling_source": "random fp64 gathers from a 67 MB L2-resident x, 148 SMs "
-                              "(profiles/r1_ubench_gather_scope.txt)"}
+            "ceiling_source": "best measured random fp64 LSU gather rate from a 64 MB x, 148 SMs "
+                              "(profiles/r2_ubench_tma_gather4.txt)"}
     step_bytes = ctx.allsum(float(alg_bytes_rank(info, ctx.v)))
     rec = {
         "workload": workload_desc(wname, world), "value": round(gflops, 3), "unit": "GFLOP/s",
