@@ -67,6 +67,13 @@ def test_binding_marshalling_without_gpu():
         lambda: D.dspmv_comm_destroy(None),
         lambda: D.dspmv_comm_info(None),
         lambda: D.dspmv_host_plan_destroy(None),
+        lambda: D.dspmv_schedule_set_caller_stream0(None, 1),
+        lambda: D.dspmv_apply_graph(None, 0, 0, 1),
+        lambda: D.dspmv_apply_graph_prepare(None, 0, 0, 1),
+        lambda: D.dspmv_apply_graph_group([], [], [], 1),
+        lambda: D.dspmv_apply_group([], [], []),
+        lambda: D.dspmv_plan_create(None, 1, rp, col, val, pack_mode=D.DSPMV_PACK_ALIAS_IF_CONTIGUOUS,
+                                    accumulate_mode=D.DSPMV_ACC_EXPLICIT_IN_END, debug_checks=True),
     ]
     for c in calls:
         with pytest.raises(D.DspmvError) as e:
