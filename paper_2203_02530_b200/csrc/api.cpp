@@ -1322,9 +1322,12 @@ dspmv_status capture_graph(const std::vector<Schedule*>& ss, const std::vector<c
     if (ie != cudaSuccess) return fail(DSPMV_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie));
     s0.gx = xs[0];
     s0.gy = ys[0];
+    for (Schedule* m : s0.g_group)
+        if (m != &s0) m->g_leader = nullptr;
     s0.g_group.clear();
     if (group)
         for (int r = 0; r < R; ++r) {
+            if (r > 0) ss[r]->g_leader = &s0;
             s0.g_group.push_back(ss[r]);
             s0.g_group_ptrs.push_back(xs[r]);
             s0.g_group_ptrs.push_back(ys[r]);
@@ -1987,6 +1990,18 @@ static void destroy_timing(Schedule& s) {
 dspmv_status dspmv_schedule_destroy(dspmv_schedule_t s) {
     if (!s) return fail(DSPMV_ERR_ARG, "null schedule");
     cudaSetDevice(s->plan->device);
+    // a group graph references every member's events: a member going away
+    // drops the leader's graph (re-captured on the next group apply), a
+    // leader going away releases its members
+    if (Schedule* L = s->g_leader) {
+        if (L->gexec) cudaGraphExecDestroy(L->gexec), L->gexec = nullptr;
+        for (Schedule* m : L->g_group)
+            if (m != L) m->g_leader = nullptr;
+        L->g_group.clear();
+        L->g_group_ptrs.clear();
+    }
+    for (Schedule* m : s->g_group)
+        if (m != s) m->g_leader = nullptr;
     if (s->gexec) cudaGraphExecDestroy(s->gexec);
     for (auto& e : s->gev)
         if (e) cudaEventDestroy(e);

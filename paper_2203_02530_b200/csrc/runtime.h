@@ -250,6 +250,7 @@ struct Schedule {
     cudaGraphExec_t gexec = nullptr;
     std::vector<struct Schedule*> g_group;     // LOCAL group graph: the ranks' schedules (on rank 0's)
     std::vector<const void*> g_group_ptrs;     // x_r, y_r the group graph was captured for
+    struct Schedule* g_leader = nullptr;       // member of a group graph held by this schedule
     const void* gx = nullptr;
     void* gy = nullptr;
     bool g_timing = false;

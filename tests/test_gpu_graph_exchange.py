@@ -227,3 +227,30 @@ def test_full_size_group_graph_vs_o1(cfg, P, exchange, pack_mode):
             assert np.all(np.abs(y - yref) <= 1e-12 * scale) and np.isfinite(y).all()
     finally:
         run.close()
+
+
+def test_group_graph_survives_member_replacement():
+    """Destroying one rank's schedule drops the group graph its leader holds
+    (it references that schedule's events); the next group apply with a new
+    schedule re-captures and is still exact."""
+    n, rp, col, val, P = _case("c1")
+    x = gen.x_values((0, n), exact=True)
+    plans = O2.plan_all(rp, col, n, P)
+    yref = O2.simulate(plans, val, x, [(v,) for v in S.topological_orders(S.EDGES)[0]])
+    run = LocalRun(n, rp, col, val, P)
+    xs, ys = run.xy(x)
+    stream = torch.cuda.Stream()
+    try:
+        ops = derive_ops()
+        ss = run.schedule(ops)
+        D.dspmv_apply_graph_group(ss, xs, ys, stream)
+        torch.cuda.synchronize()
+        D.dspmv_schedule_destroy(ss[1])
+        ss[1] = D.dspmv_schedule_create(run.plans[1], ops, 2)
+        for y in ys:
+            y.fill_(float("nan"))
+        D.dspmv_apply_graph_group(ss, xs, ys, stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(np.concatenate([t.cpu().numpy() for t in ys]), yref)
+    finally:
+        run.close()
