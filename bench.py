@@ -559,7 +559,7 @@ def measure(ctx, wname, headline, clocks=None, sched_from=None):
     torch.cuda.synchronize()
     ok, worst = check_parity(sample, y, 0.0 if EXACT else ctx.rel)
     parity = {"ok": ctx.alland(ok), "rows_checked": int(ctx.allsum(float(0 if sample is None else len(sample[0])))),
-              "max_err_over_scale": ctx.allmax(worst), "tolerance": ctx.rel,
+              "max_err_over_scale": ctx.allmax(worst), "tolerance": 0.0 if EXACT else ctx.rel,
               "reference": "numpy fp64 row products of sampled rows (first/last, remote, random) vs the "
                            "north_star bound |y - y_ref| <= tol * sum|a_ij x_j|"}
 
