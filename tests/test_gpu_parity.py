@@ -580,3 +580,41 @@ def test_stream_kernel_edge_cases(skern):
         short = np.diff(rp) <= 256
         assert np.array_equal(y[short], yref[short]) and not np.any(np.signbit(y[np.diff(rp) == 0]))
         assert within_tol(y, yref, O1.o1_absdot(rp, col, val, x), 1e-12)
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c2", "c4"])
+def test_full_size_bench_launch_configuration(cfg):
+    """The launch configuration bench.py times at N = 1: the full BASELINE
+    matrix, a GPU-resident graph with schedule stream 0 bound to the caller's
+    stream, L2 flushed before each apply, two applies -- every row against
+    O1 (C2/C3: bitwise, each row is summed in stored order in one lane; C4:
+    rows <= 256 nnz bitwise, the rest within the R-Q11 tolerance)."""
+    n, (rp, col, val) = gen.config_matrix(cfg)
+    x = gen.x_values((0, n))
+    yref = O1.o1_spmv(rp, col, val, x)
+    comm = D.dspmv_comm_create(D.dspmv_comm_unique_id(), 1, 0, 0)
+    plan = D.dspmv_plan_create(comm, n, rp, col, val)
+    order = ["start", "y_L", "Pack", "PostSend", "PostRecv", "WaitRecv", "Unpack", "y_R", "WaitSend", "end"]
+    s = D.dspmv_schedule_create(plan, derive_ops(order, {"y_L": 0, "Pack": 1, "Unpack": 1, "y_R": 0}), 2)
+    D.dspmv_schedule_set_timing(s, True)
+    D.dspmv_schedule_set_caller_stream0(s, 1)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    st = torch.cuda.Stream()
+    try:
+        for _ in range(2):
+            yd.fill_(float("nan"))
+            D.dspmv_l2_flush(0, st)
+            D.dspmv_apply_graph(s, xd, yd, st)
+            torch.cuda.synchronize()
+            y = yd.cpu().numpy()
+            if cfg in ("c2", "c3"):
+                assert np.array_equal(y, yref)
+            else:
+                short = np.diff(rp) <= 256
+                assert np.array_equal(y[short], yref[short])
+                assert within_tol(y, yref, O1.o1_absdot(rp, col, val, x), 1e-12)
+    finally:
+        D.dspmv_schedule_destroy(s)
+        D.dspmv_plan_destroy(plan)
+        D.dspmv_comm_destroy(comm)
