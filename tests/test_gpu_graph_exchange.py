@@ -202,10 +202,12 @@ def test_multiprocess_put_graph(world):
     ("c5", 4, D.DSPMV_EXCHANGE_PUT, D.DSPMV_PACK_GATHER),
     ("c5", 4, D.DSPMV_EXCHANGE_COPY, D.DSPMV_PACK_ALIAS_IF_CONTIGUOUS),
     ("c4", 8, D.DSPMV_EXCHANGE_PUT, D.DSPMV_PACK_GATHER),
-], ids=["c5-put", "c5-alias", "c4-put-8"])
+    ("c3", 8, D.DSPMV_EXCHANGE_COPY, D.DSPMV_PACK_ALIAS_IF_CONTIGUOUS),
+], ids=["c5-put", "c5-alias", "c4-put-8", "c3-alias-8"])
 def test_full_size_group_graph_vs_o1(cfg, P, exchange, pack_mode):
-    """BASELINE configs[4] (7-pt 192^3 over 4 ranks) and configs[3] (power-law
-    8M over 8 ranks, up to 7 peers) at full size, as ONE GPU-resident graph
+    """BASELINE configs[4] (7-pt 192^3 over 4 ranks), configs[3] (power-law
+    8M over 8 ranks, up to 7 peers) and configs[2] (27-pt 256^3 over 8 ranks,
+    the N = 8 strong-scaling split) at full size, as ONE GPU-resident graph
     per apply with the fused put or aliased sends: every row against the O1
     oracle (the C loop runs the whole matrix in well under a second), over
     both PUT receive-buffer parities."""
