@@ -117,6 +117,9 @@ def parse():
                     help="exact: small-integer matrix values and x (R-Q23), every result exact; the parity "
                          "self-check then requires bitwise equality")
     ap.add_argument("--seed", type=int, default=2530, help="seed of the x values (counter-based, gen/)")
+    ap.add_argument("--plain-exchange", action="store_true",
+                    help="Pack gathers into a send buffer and Unpack copies to x_halo (the DAG's literal "
+                         "kernels) instead of aliased sends and the fused Unpack")
     ap.add_argument("--no-t1", action="store_true",
                     help="N>1: skip the 1-GPU run of the whole matrix on rank 0 (scaling efficiency)")
     return ap.parse_args()
@@ -474,8 +477,13 @@ def measure(ctx, wname, headline, clocks=None, sched_from=None):
     del val
 
     def mk(ex):
+        # stencil send lists are planes: sent straight from x (no Pack kernel)
+        # where possible, and y_R reads the halo where it was received
+        # (profiles/r2_c5_exec_modes.json); --plain-exchange keeps Pack/Unpack
+        extra = {} if a.plain_exchange else dict(pack_mode=D.DSPMV_PACK_ALIAS_IF_CONTIGUOUS,
+                                                  unpack_mode=D.DSPMV_UNPACK_FUSED)
         return D.dspmv_plan_create(ctx.comm, n, rp, col, valn, dtype=ctx.dt,
-                                   caller_stream0=bool(a.caller_stream0), exchange=ex)
+                                   caller_stream0=bool(a.caller_stream0), exchange=ex, **extra)
     exchange_note = None
     if a.comm == "host":
         plan, exchange, ex_mode = mk(D.DSPMV_EXCHANGE_PUT), "put (fused Pack+put over peer memory)", "put"
@@ -588,7 +596,9 @@ def measure(ctx, wname, headline, clocks=None, sched_from=None):
         "workload": workload_desc(wname, world), "value": round(gflops, 3), "unit": "GFLOP/s",
         "ms_per_step": round(ms_per_step, 6), "steps": steps,
         "n_global": n, "nnz_global": int(nnz_total),
-        "parallelism": f"row-partition x{world}, halo exchange: {exchange}",
+        "parallelism": (f"row-partition x{world}, halo exchange: {exchange}"
+                        + ("" if a.plain_exchange else
+                           f", pack: {'aliased sends' if info.get('pack_alias') else 'gather'}, unpack: fused into y_R")),
         "exchange_selection": exchange_note,
         "execution": exec_name(mode), "execution_selection": exec_note, "schedule": sched_desc,
         "step_us_median_min_p90": stats,

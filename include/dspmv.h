@@ -165,7 +165,12 @@ typedef struct {
                                   schedule hashes its ops; a mismatch returns
                                   DSPMV_ERR_ARG / DSPMV_ERR_SCHEDULE on every rank.
                                   Default 0, or the env DSPMV_DEBUG_CHECKS.         */
-    int32_t reserved0;
+    int32_t unpack_mode;       /* DSPMV_UNPACK_COPY (0, default): Unpack copies the
+                                  receive buffer to x_halo (R-Q8).  DSPMV_UNPACK_FUSED:
+                                  Unpack launches nothing and y_R gathers the halo
+                                  straight from the receive buffer (PUT: the half of
+                                  this apply's parity, read from the device epoch) --
+                                  SURVEY 8(d): "the unpack term 2v*h_r is 0 if fused" */
     /* Device memory of the plan (matrix layouts, buffers): alloc(bytes, device,
        ctx) returns device memory on `device` or NULL (-> DSPMV_ERR_OOM);
        free(ptr, bytes, device, ctx) releases it at plan_destroy (after the
@@ -179,6 +184,7 @@ typedef struct {
 
 enum { DSPMV_PACK_GATHER = 0, DSPMV_PACK_ALIAS_IF_CONTIGUOUS = 1 };
 enum { DSPMV_ACC_TICKET = 0, DSPMV_ACC_EXPLICIT_IN_END = 1 };
+enum { DSPMV_UNPACK_COPY = 0, DSPMV_UNPACK_FUSED = 1 };
 
 enum { DSPMV_EXCHANGE_COPY = 0, DSPMV_EXCHANGE_PUT = 1,
        /* timing baseline only (SURVEY 8(d) overlap efficiency, T_noexch): Post/Wait
@@ -222,6 +228,7 @@ typedef struct {
                                         (host plans: 1 if ALIAS_IF_CONTIGUOUS would
                                         alias this rank's send lists)             */
     int32_t accumulate_mode;         /* DSPMV_ACC_* in use                         */
+    int32_t unpack_fused;            /* 1: y_R reads the receive buffer            */
 } dspmv_plan_info;
 dspmv_status dspmv_plan_info_get(dspmv_plan_t plan, dspmv_plan_info* out);
 

@@ -874,7 +874,7 @@ cudaError_t launch_gpu_vertex(Schedule& s, int t, const void* x, void* y, cudaSt
         }
         case DSPMV_OP_UNPACK: {
             const int q = s.op_peer[t];
-            if (q == -1) break;
+            if (q == -1 || p.unpack_fused) break;   // fused: y_R reads the receive buffer
             if (p.put_mode) {   // receive-buffer parity of this apply, from the device epoch
                 const size_t off = q == -2 ? 0 : size_t(p.host.recv_displ[q]) * p.esize;
                 const int64_t cnt = q == -2 ? int64_t(p.host.halo_gid.size()) : p.host.recv_count[q];
@@ -894,6 +894,13 @@ cudaError_t launch_gpu_vertex(Schedule& s, int t, const void* x, void* y, cudaSt
         }
         case DSPMV_OP_SPMV_REMOTE: {
             SpmvOperands op{p.d_xhalo, y, p.d_partR, p.explicit_acc, p.d_partL, p.d_ticket};
+            if (p.unpack_fused) {   // R-Q8 fused: the halo is read where it was received
+                op.x = p.d_recvbuf;
+                if (p.put_mode) {
+                    op.x_epoch = p.d_epoch;
+                    op.x_parity_elems = int64_t(p.recv_stride);
+                }
+            }
             e = launch_spmv(p.R, p.dtype, op, st);
             break;
         }
@@ -1617,6 +1624,9 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
     if ((st = dev_alloc(*p, reinterpret_cast<void**>(&p->d_ticket), size_t(nR) * 4, true)) != DSPMV_OK)
         return bail(st);
     p->explicit_acc = opts.accumulate_mode == DSPMV_ACC_EXPLICIT_IN_END;
+    p->unpack_fused = opts.unpack_mode == DSPMV_UNPACK_FUSED;
+    if (opts.unpack_mode != DSPMV_UNPACK_COPY && !p->unpack_fused)
+        return bail(fail(DSPMV_ERR_ARG, "bad unpack_mode"));
     if (opts.accumulate_mode != DSPMV_ACC_TICKET && !p->explicit_acc)
         return bail(fail(DSPMV_ERR_ARG, "bad accumulate_mode"));
     if (opts.pack_mode != DSPMV_PACK_GATHER && opts.pack_mode != DSPMV_PACK_ALIAS_IF_CONTIGUOUS)
@@ -1720,6 +1730,7 @@ dspmv_status dspmv_plan_info_get(dspmv_plan_t plan, dspmv_plan_info* out) {
     out->s_kernel_local = skern(plan->L);
     out->s_kernel_remote = skern(plan->R);
     out->pack_alias = plan->pack_alias ? 1 : 0;
+    out->unpack_fused = plan->unpack_fused ? 1 : 0;
     out->accumulate_mode = plan->explicit_acc ? DSPMV_ACC_EXPLICIT_IN_END : DSPMV_ACC_TICKET;
     return DSPMV_OK;
 }

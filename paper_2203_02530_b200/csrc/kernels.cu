@@ -213,6 +213,15 @@ __device__ __forceinline__ float load_x(const float* p, uint64_t pol) {
     }
 }
 
+// The x operand of an SpMV op: fixed, or (fused Unpack of a PUT plan inside a
+// graph) the receive-buffer half of this apply's epoch parity.
+template <typename T>
+__device__ __forceinline__ const T* resolve_x(const SpmvOperands& o) {
+    const T* x = static_cast<const T*>(o.x);
+    if (o.x_epoch) x += ((*o.x_epoch) & 1u) * o.x_parity_elems;
+    return x;
+}
+
 template <typename T> __device__ __forceinline__ T mul_rn(T a, T b);
 template <> __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 template <> __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
@@ -410,7 +419,7 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
     }
 
     // ------------------------------------------------------ consumer warps
-    const T* __restrict__ x = static_cast<const T*>(o.x);
+    const T* __restrict__ x = resolve_x<T>(o);
     T* __restrict__ y = static_cast<T*>(o.y);
     const int32_t* __restrict__ out = a.out;
     const int32_t* __restrict__ slot = a.slot;
@@ -459,7 +468,7 @@ template <typename T, bool kCombine>
 __device__ __forceinline__ void vector_rows(const VecArgs& a, const SpmvOperands& o, int w, int nw) {
     const int lane = threadIdx.x & 31;
     const T* __restrict__ val = static_cast<const T*>(a.val);
-    const T* __restrict__ x = static_cast<const T*>(o.x);
+    const T* __restrict__ x = resolve_x<T>(o);
     const uint64_t xpol = policy_evict_last();
     for (int i = w; i < a.nV; i += nw) {
         const int32_t p0 = __ldg(a.rowptr + i), p1 = __ldg(a.rowptr + i + 1);
@@ -521,7 +530,7 @@ __global__ void __launch_bounds__(kStreamCtaWarps * 32) spmv_stream_kernel(Strea
     __shared__ T prod[kStreamCtaWarps][kStreamTile];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const T* __restrict__ val = static_cast<const T*>(a.val);
-    const T* __restrict__ x = static_cast<const T*>(o.x);
+    const T* __restrict__ x = resolve_x<T>(o);
     T* __restrict__ y = static_cast<T*>(o.y);
     T* pr = prod[w];
     // the long rows (> vector_threshold) first, a warp per row, so they do not
@@ -764,7 +773,7 @@ __global__ void __launch_bounds__((kStreamWarps + 1) * 32, kStVariants[V].min_ct
         if (a.v.slot) vector_rows<T, true>(a.v, o, blockIdx.x * kStreamWarps + warp, gridDim.x * kStreamWarps);
         else vector_rows<T, false>(a.v, o, blockIdx.x * kStreamWarps + warp, gridDim.x * kStreamWarps);
     }
-    const T* __restrict__ x = static_cast<const T*>(o.x);
+    const T* __restrict__ x = resolve_x<T>(o);
     T* __restrict__ y = static_cast<T*>(o.y);
     const uint64_t xpol = policy_evict_last();
     constexpr int K = kStreamTile / 32;

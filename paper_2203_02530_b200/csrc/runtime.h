@@ -60,6 +60,10 @@ struct SpmvOperands {
     // xflag[desc[15] of b] >= epoch, i.e. its x chunks have landed
     const unsigned* xflag = nullptr;
     unsigned epoch = 0;
+    // fused Unpack on a PUT plan: y_R reads the receive buffer of this apply's
+    // parity, x + ((*x_epoch) & 1) * x_parity_elems (device epoch, graphs)
+    const unsigned* x_epoch = nullptr;
+    int64_t x_parity_elems = 0;
     // apply_host with y leaving by copy engine: the producer of each row-block
     // CTA adds 1 to ydone[desc[15]] once a staged block's rows are stored
     unsigned* ydone = nullptr;
@@ -168,6 +172,7 @@ struct Plan {
     // DSPMV_PACK_ALIAS_IF_CONTIGUOUS in effect: destination q's send list is
     // x[alias_off[q] .. + send_count[q]), sent straight from x (no Pack kernel)
     bool pack_alias = false;
+    bool unpack_fused = false;         // DSPMV_UNPACK_FUSED: y_R reads the receive buffer
     std::vector<int64_t> alias_off;
     const void* cur_x = nullptr;       // x of the apply being issued / captured
     // DSPMV_ACC_EXPLICIT_IN_END: local row of each combined row (device)

@@ -34,6 +34,7 @@ DSPMV_EXCHANGE_COPY, DSPMV_EXCHANGE_PUT, DSPMV_EXCHANGE_NONE = 0, 1, 2
 DSPMV_SKERNEL_AUTO, DSPMV_SKERNEL_BLOCK, DSPMV_SKERNEL_STREAM, DSPMV_SKERNEL_STREAM_TMA = 0, 1, 2, 3
 DSPMV_PACK_GATHER, DSPMV_PACK_ALIAS_IF_CONTIGUOUS = 0, 1
 DSPMV_ACC_TICKET, DSPMV_ACC_EXPLICIT_IN_END = 0, 1
+DSPMV_UNPACK_COPY, DSPMV_UNPACK_FUSED = 0, 1
 (DSPMV_OP_START, DSPMV_OP_PACK, DSPMV_OP_SPMV_LOCAL, DSPMV_OP_POST_SEND, DSPMV_OP_POST_RECV,
  DSPMV_OP_WAIT_SEND, DSPMV_OP_WAIT_RECV, DSPMV_OP_UNPACK, DSPMV_OP_SPMV_REMOTE, DSPMV_OP_END,
  DSPMV_OP_EVENT_RECORD, DSPMV_OP_EVENT_SYNC, DSPMV_OP_STREAM_WAIT_EVENT) = range(13)
@@ -63,7 +64,7 @@ class dspmv_plan_opts(ctypes.Structure):
                 ("reserve_sms", ctypes.c_int32), ("exchange", ctypes.c_int32),
                 ("s_kernel", ctypes.c_int32), ("pack_mode", ctypes.c_int32),
                 ("accumulate_mode", ctypes.c_int32), ("debug_checks", ctypes.c_int32),
-                ("reserved0", ctypes.c_int32),
+                ("unpack_mode", ctypes.c_int32),
                 ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", ctypes.c_void_p)]
 
 
@@ -80,7 +81,8 @@ class dspmv_plan_info(ctypes.Structure):
                 ("dtype", ctypes.c_int32), ("ready", ctypes.c_int32),
                 ("device_bytes", ctypes.c_int64),
                 ("s_kernel_local", ctypes.c_int32), ("s_kernel_remote", ctypes.c_int32),
-                ("pack_alias", ctypes.c_int32), ("accumulate_mode", ctypes.c_int32)]
+                ("pack_alias", ctypes.c_int32), ("accumulate_mode", ctypes.c_int32),
+                ("unpack_fused", ctypes.c_int32)]
 
 
 class dspmv_op(ctypes.Structure):
@@ -272,7 +274,8 @@ def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_
                       caller_stream0: bool | None = None, reserve_sms: int | None = None,
                       exchange: int = DSPMV_EXCHANGE_COPY, s_kernel: int = DSPMV_SKERNEL_AUTO,
                       pack_mode: int = DSPMV_PACK_GATHER, accumulate_mode: int = DSPMV_ACC_TICKET,
-                      debug_checks: bool | None = None, torch_alloc: bool = True):
+                      debug_checks: bool | None = None, torch_alloc: bool = True,
+                      unpack_mode: int = DSPMV_UNPACK_COPY):
     """rowptr int64[n_local+1], col int32[nnz] (global ids), val float64/32.
     torch_alloc: the plan's device memory comes from torch's caching allocator
     (dspmv_plan_opts.alloc/free); False = cudaMalloc inside the library."""
@@ -294,6 +297,7 @@ def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_
     o.s_kernel = int(s_kernel)
     o.pack_mode = int(pack_mode)
     o.accumulate_mode = int(accumulate_mode)
+    o.unpack_mode = int(unpack_mode)
     if debug_checks is not None:
         o.debug_checks = int(debug_checks)
     if torch_alloc:

@@ -43,8 +43,11 @@ def main():
            "schedule": " ".join(ORDER) + f" streams={STREAMS}", "steps": a.steps, "results": {}}
     ref = None
     for ex_name, ex in (("copy", D.DSPMV_EXCHANGE_COPY), ("put", D.DSPMV_EXCHANGE_PUT)):
-        for pm_name, pm in (("gather", D.DSPMV_PACK_GATHER), ("alias", D.DSPMV_PACK_ALIAS_IF_CONTIGUOUS)):
-            if ex_name == "put" and pm_name == "alias":
+        for pm_name, pm, um in (("gather", D.DSPMV_PACK_GATHER, D.DSPMV_UNPACK_COPY),
+                                ("alias", D.DSPMV_PACK_ALIAS_IF_CONTIGUOUS, D.DSPMV_UNPACK_COPY),
+                                ("alias+fused-unpack", D.DSPMV_PACK_ALIAS_IF_CONTIGUOUS, D.DSPMV_UNPACK_FUSED),
+                                ("gather+fused-unpack", D.DSPMV_PACK_GATHER, D.DSPMV_UNPACK_FUSED)):
+            if ex_name == "put" and pm_name.startswith("alias"):
                 continue   # the put already fuses the gather with the store
             comms = D.dspmv_comm_create_local(P, 0)
             plans, xs, ys = [], [], []
@@ -52,7 +55,7 @@ def main():
                 b, e = int(rb[r]), int(rb[r + 1])
                 lo, hi = int(rp[b]), int(rp[e])
                 plans.append(D.dspmv_plan_create(comms[r], n, rp[b:e + 1], col[lo:hi], val[lo:hi], exchange=ex,
-                                                 pack_mode=pm))
+                                                 pack_mode=pm, unpack_mode=um))
                 xs.append(torch.from_numpy(x[b:e].copy()).cuda())
                 ys.append(torch.empty(e - b, dtype=torch.float64, device="cuda"))
             ss = [D.dspmv_schedule_create(p, ops, 2) for p in plans]

@@ -291,3 +291,34 @@ def test_schedule_caller_stream0_override():
         D.dspmv_schedule_destroy(s)
         D.dspmv_plan_destroy(plan)
         D.dspmv_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("exchange", [D.DSPMV_EXCHANGE_COPY, D.DSPMV_EXCHANGE_PUT], ids=["copy", "put"])
+@pytest.mark.parametrize("name,P", [("c1", 2), ("pl", 3), ("27pt16", 4)])
+def test_fused_unpack_bitwise_oracle(name, P, exchange):
+    """unpack_mode FUSED: Unpack launches nothing and y_R gathers the halo
+    from the receive buffer (PUT: the half of this apply's parity, from the
+    device epoch).  Host lock-step and group graphs, several applies (both
+    parities), a stride of the derived schedules: = O2 bitwise (exact mode)."""
+    n, rp, col, val = _stencil(name, exact=True)
+    x = gen.x_values((0, n), exact=True)
+    plans = O2.plan_all(rp, col, n, P)
+    yref = O2.simulate(plans, val, x, [(v,) for v in S.topological_orders(S.EDGES)[0]])
+    run = LocalRun(n, rp, col, val, P, exchange=exchange, unpack_mode=D.DSPMV_UNPACK_FUSED)
+    xs, ys = run.xy(x)
+    stream = torch.cuda.Stream()
+    try:
+        assert all(D.dspmv_plan_info_get(p)["unpack_fused"] == 1 for p in run.plans)
+        for k, ops in enumerate(S.enumerate_derived(2, S.EDGES)[::128]):
+            ss = run.schedule(oracle_ops_to_lib(ops))
+            for rep in range(3):
+                for y in ys:
+                    y.fill_(float("nan"))
+                if rep == 1:
+                    D.dspmv_apply_group(ss, xs, ys)
+                else:
+                    D.dspmv_apply_graph_group(ss, xs, ys, stream)
+                torch.cuda.synchronize()
+                assert np.array_equal(np.concatenate([t.cpu().numpy() for t in ys]), yref), (k, rep)
+    finally:
+        run.close()
