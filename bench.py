@@ -578,13 +578,14 @@ def measure(ctx, wname, headline, clocks=None, sched_from=None):
     peak, peak_src = peaks()
     sk = info.get("s_kernel_local")
     kname = {D.DSPMV_SKERNEL_STREAM: "spmv_stream_kernel",
-             D.DSPMV_SKERNEL_STREAM_TMA: "spmv_stream_tma_kernel"}.get(sk, "spmv_block_kernel")
+             D.DSPMV_SKERNEL_STREAM_TMA: "spmv_stream_tma_kernel",
+             D.DSPMV_SKERNEL_SELL: "spmv_sell_kernel"}.get(sk, "spmv_block_kernel")
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": ncu_traffic(wname, world),
             "kernel": kname + " (y_L, SPMV_LOCAL op)", "alg_bytes_per_launch": int(yl_bytes),
             "avg_launch_ms": round(yl_ms, 6), "max_rank_launch_ms": round(yl_ms_max, 6),
             "peak_source": peak_src}
-    if sk in (D.DSPMV_SKERNEL_STREAM, D.DSPMV_SKERNEL_STREAM_TMA):
+    if sk in (D.DSPMV_SKERNEL_STREAM, D.DSPMV_SKERNEL_STREAM_TMA, D.DSPMV_SKERNEL_SELL):
         gps = info["nnz_local"] / (yl_ms * 1e-3) / 1e9
         roof["gather_roofline"] = {
             "gathers_per_launch": int(info["nnz_local"]), "achieved_G_per_s": round(gps, 1),

@@ -143,7 +143,12 @@ typedef struct {
                                   per row-aligned tile of <= 256 nnz gathers 8 x values
                                   per lane (coalesced col/val loads), then one lane per
                                   row sums its products in stored order (bitwise the
-                                  serial CSR loop)                              */
+                                  serial CSR loop).  DSPMV_SKERNEL_SELL: the
+                                  plan stores the S rows as 32-row slices (rows sorted
+                                  by length within windows, entry k of the slice's rows
+                                  stored contiguously); one lane per row walks its row
+                                  in stored order with coalesced col/val loads and no
+                                  shared memory (also bitwise the serial loop)         */
     int32_t pack_mode;         /* DSPMV_PACK_GATHER (0, default): Pack gathers
                                   sendbuf[k] = x[pack_map[k]].
                                   DSPMV_PACK_ALIAS_IF_CONTIGUOUS: when every
@@ -191,7 +196,8 @@ enum { DSPMV_EXCHANGE_COPY = 0, DSPMV_EXCHANGE_PUT = 1,
           run their synchronisation but move no data, so y is WRONG on rows with
           remote entries.  Never a product mode. */
        DSPMV_EXCHANGE_NONE = 2 };
-enum { DSPMV_SKERNEL_AUTO = 0, DSPMV_SKERNEL_BLOCK = 1, DSPMV_SKERNEL_STREAM = 2, DSPMV_SKERNEL_STREAM_TMA = 3 };
+enum { DSPMV_SKERNEL_AUTO = 0, DSPMV_SKERNEL_BLOCK = 1, DSPMV_SKERNEL_STREAM = 2, DSPMV_SKERNEL_STREAM_TMA = 3,
+       DSPMV_SKERNEL_SELL = 4 };
 
 void dspmv_plan_opts_default(dspmv_plan_opts* opts);
 

@@ -134,10 +134,12 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
     D.nV = L.nV;
     const int sms = device_sm_count();
     if (L.nb > 0) {
-        ST_TRY(dev_upload(p, &D.s_rowptr, L.s_rowptr.data(), L.s_rowptr.size()));
-        ST_TRY(dev_upload(p, &D.s_col, L.s_col.data(), L.s_col.size()));
-        ST_TRY(dev_upload(p, reinterpret_cast<uint8_t**>(&D.s_val), L.s_val.data(), L.s_val.size()));
-        ST_TRY(dev_upload(p, &D.s_desc, L.s_desc.data(), L.s_desc.size()));
+        if (!L.sell) {   // the sliced form keeps its own copy of the S entries
+            ST_TRY(dev_upload(p, &D.s_rowptr, L.s_rowptr.data(), L.s_rowptr.size()));
+            ST_TRY(dev_upload(p, &D.s_col, L.s_col.data(), L.s_col.size()));
+            ST_TRY(dev_upload(p, reinterpret_cast<uint8_t**>(&D.s_val), L.s_val.data(), L.s_val.size()));
+            ST_TRY(dev_upload(p, &D.s_desc, L.s_desc.data(), L.s_desc.size()));
+        }
         if (L.s_has_slot) ST_TRY(dev_upload(p, &D.s_slot, L.s_slot.data(), L.s_slot.size()));
         if (!L.s_identity) ST_TRY(dev_upload(p, &D.s_out, L.s_out.data(), L.s_out.size()));
         D.cfg = cfg;
@@ -146,7 +148,20 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
         const int reserve = p.opts.reserve_sms >= 0 ? p.opts.reserve_sms : (p.comm->nranks > 1 ? kAutoReserveSms : 0);
         const int usable = std::max(1, sms - reserve);
         D.grid_s = std::max(1, std::min(L.nb, per_sm * usable));
-        if (L.stream) {
+        if (L.sell) {
+            D.stream = true;
+            D.sell = true;
+            D.nslices = int32_t(L.sl_base.size()) - 1;
+            ST_TRY(dev_upload(p, &D.sl_base, L.sl_base.data(), L.sl_base.size()));
+            ST_TRY(dev_upload(p, &D.sl_srow, L.sl_srow.data(), L.sl_srow.size()));
+            ST_TRY(dev_upload(p, &D.sl_len, L.sl_len.data(), L.sl_len.size()));
+            ST_TRY(dev_upload(p, &D.sl_col, L.sl_col.data(), L.sl_col.size()));
+            ST_TRY(dev_upload(p, reinterpret_cast<uint8_t**>(&D.sl_val), L.sl_val.data(), L.sl_val.size()));
+            D.sell_unroll = sell_unroll();
+            int spsm = sell_kernel_ctas_per_sm(p.dtype, D.sell_unroll);
+            if (const char* ev = std::getenv("DSPMV_SELL_CTAS")) spsm = std::max(1, std::min(spsm, std::atoi(ev)));  // sweeps
+            D.grid_sl = std::max(1, std::min((D.nslices + kSellCtaWarps - 1) / kSellCtaWarps, spsm * usable));
+        } else if (L.stream) {
             D.stream = true;
             set_x_persist_limit();
             D.ntiles = int32_t(L.s_tiles.size() / 2);
@@ -190,10 +205,24 @@ static bool stream_tma_default() {
 // S-group kernel of a matrix: forced by opts.s_kernel, else the row-block
 // kernel when a block configuration is forced, else chosen by row lengths.
 bool use_stream(const dspmv_plan_opts& o, const int32_t* rowptr, int32_t nrows, int vthr) {
-    if (o.s_kernel == DSPMV_SKERNEL_STREAM || o.s_kernel == DSPMV_SKERNEL_STREAM_TMA) return true;
+    if (o.s_kernel == DSPMV_SKERNEL_STREAM || o.s_kernel == DSPMV_SKERNEL_STREAM_TMA ||
+        o.s_kernel == DSPMV_SKERNEL_SELL)
+        return true;
     if (o.s_kernel == DSPMV_SKERNEL_BLOCK || o.block_cfg >= 0) return false;
     if (const char* ev = std::getenv("DSPMV_SKERNEL")) return std::atoi(ev) == DSPMV_SKERNEL_STREAM;  // sweeps
     return auto_stream(rowptr, nrows, vthr);
+}
+
+// The sliced form for a CSR-stream S group: forced by opts.s_kernel, else
+// DSPMV_SELL (sweeps), else the default for irregular matrices.
+bool use_sell(const dspmv_plan_opts& o, bool stream) {
+    if (!stream || o.s_kernel == DSPMV_SKERNEL_STREAM || o.s_kernel == DSPMV_SKERNEL_STREAM_TMA) return false;
+    if (o.s_kernel == DSPMV_SKERNEL_SELL) return true;
+    static const int v = [] {
+        const char* ev = std::getenv("DSPMV_SELL");
+        return ev ? std::atoi(ev) : 0;
+    }();
+    return v != 0;
 }
 
 // Streamed host input of dspmv_apply_host (plan time, host only).  x is cut
@@ -1577,9 +1606,9 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
     {
         Layout L;
         const int c = cfg >= 0 ? cfg : auto_block_cfg(h.al_rowptr.data(), int32_t(h.n_local()), vthr, p->esize);
+        const bool sl = use_stream(opts, h.al_rowptr.data(), int32_t(h.n_local()), vthr);
         build_layout(h.al_rowptr.data(), int32_t(h.n_local()), h.al_col.data(), h.al_val.data(), p->esize, nullptr,
-                     nR > 0 ? slotL.data() : nullptr, vthr, kBlockCfgs[c], L,
-                     use_stream(opts, h.al_rowptr.data(), int32_t(h.n_local()), vthr));
+                     nR > 0 ? slotL.data() : nullptr, vthr, kBlockCfgs[c], L, sl, use_sell(opts, sl));
         build_host_pipe(*p, L);   // also stores each block's x chunk in desc[15]
         if ((st = upload_layout(*p, L, c, p->L)) != DSPMV_OK) return bail(st);
         p->L.x_bytes = h.n_local() * p->esize;
@@ -1589,8 +1618,9 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
         for (int32_t k = 0; k < nR; ++k) slotR[k] = k;
         Layout R;
         const int c = cfg >= 0 ? cfg : auto_block_cfg(h.ar_rowptr.data(), nR, vthr, p->esize);
+        const bool sr = use_stream(opts, h.ar_rowptr.data(), nR, vthr);
         build_layout(h.ar_rowptr.data(), nR, h.ar_col.data(), h.ar_val.data(), p->esize, h.ar_rows.data(),
-                     slotR.data(), vthr, kBlockCfgs[c], R, use_stream(opts, h.ar_rowptr.data(), nR, vthr));
+                     slotR.data(), vthr, kBlockCfgs[c], R, sr, use_sell(opts, sr));
         if ((st = upload_layout(*p, R, c, p->R)) != DSPMV_OK) return bail(st);
         p->R.x_bytes = int64_t(h.halo_gid.size()) * p->esize;
     }
@@ -1725,7 +1755,8 @@ dspmv_status dspmv_plan_info_get(dspmv_plan_t plan, dspmv_plan_info* out) {
     out->ready = plan->ready;
     out->device_bytes = plan->device_bytes;
     auto skern = [](const DevLayout& D) {
-        return D.stream ? (D.stream_tma ? DSPMV_SKERNEL_STREAM_TMA : DSPMV_SKERNEL_STREAM) : DSPMV_SKERNEL_BLOCK;
+        return D.sell ? DSPMV_SKERNEL_SELL
+                      : D.stream ? (D.stream_tma ? DSPMV_SKERNEL_STREAM_TMA : DSPMV_SKERNEL_STREAM) : DSPMV_SKERNEL_BLOCK;
     };
     out->s_kernel_local = skern(plan->L);
     out->s_kernel_remote = skern(plan->R);

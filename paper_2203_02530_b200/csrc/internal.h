@@ -58,6 +58,16 @@ constexpr int kStreamCtaWarps = DSPMV_STREAM_CTA_WARPS;   // K1b CTA: warps (one
 // consecutive tiles, staged whole (col, val, rowptr slice) by one producer warp
 constexpr int kSTBlockNnz = kStreamWarps * kStreamTile;    // 2048
 constexpr int kSTBlockRows = kStreamWarps * kStreamRows;   // 512
+// Sliced CSR (spmv_sell_kernel, DSPMV_SKERNEL_SELL): 32-row slices, lane l
+// owns row l; within windows of kSellWindow S rows the rows are sorted by
+// length (descending, stable), so the lanes still active at entry k are a
+// prefix 0..m_k-1 and entry k of the slice is stored as m_k consecutive values
+constexpr int kSellWindow = 256;
+#ifndef DSPMV_SELL_CTA_WARPS
+#define DSPMV_SELL_CTA_WARPS 8
+#endif
+constexpr int kSellCtaWarps = DSPMV_SELL_CTA_WARPS;
+constexpr int kSellUnroll = 8;     // x gathers in flight per lane (DSPMV_SELL_UNROLL: 4 / 8 / 16)
 constexpr int kDefaultStVariant = 2;   // kernels.cu kStVariants: 3 slots, 2 CTAs/SM, pipelined
 constexpr int kDefaultVectorThreshold = 256;  // rows above: warp-per-row kernel
 constexpr int kMaxClass = 5;       // row classes: 2^c lanes per row, c = 0..5
@@ -114,6 +124,13 @@ struct Layout {
     // the same tiles grouped kStreamWarps at a time for the TMA-producer
     // variant: r0 r1 p0 p1 flag tb[0..kStreamWarps] per block (kDescInts)
     std::vector<int32_t> s_tdesc;
+    // sliced form (DSPMV_SKERNEL_SELL): slice s covers lanes 32s..32s+31;
+    // sl_srow = S-row index of the lane (-1: empty lane), sl_len its nnz;
+    // the slice's entries start at sl_base[s] in sl_col / sl_val
+    bool sell = false;
+    std::vector<int32_t> sl_base, sl_srow, sl_col;
+    std::vector<uint16_t> sl_len;
+    std::vector<uint8_t> sl_val;
 };
 // out_row / slot nullable: identity / no combine.
 // Plan-time choice of the row-block configuration for one matrix: measured
@@ -126,7 +143,8 @@ int auto_block_cfg(const int32_t* rowptr, int32_t nrows, int vthr, int esize);
 bool auto_stream(const int32_t* rowptr, int32_t nrows, int vthr);
 void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, const uint8_t* val,
                   int esize, const int32_t* out_row, const int32_t* slot, int vthr,
-                  const BlockCfg& cfg, Layout& L, bool stream = false);
+                  const BlockCfg& cfg, Layout& L, bool stream = false, bool sell = false);
+int sell_window();   // kSellWindow, or DSPMV_SELL_WINDOW (sweeps)
 
 // -------------------------------------------------------------- schedules
 // A DAG vertex instance: kind + peer offset (0 = coarse / not an exchange vertex)

@@ -607,6 +607,76 @@ __global__ void __launch_bounds__(kStreamCtaWarps * 32) spmv_stream_kernel(Strea
 }
 
 
+// Sliced CSR (DSPMV_SKERNEL_SELL, irregular row lengths).  Warp s takes slice
+// s: lane l owns row sl_srow[32s + l] and walks its sl_len entries in CSR
+// order, acc = acc + v*x from +0 with every product and sum rounded (the
+// oracle's loop), so y is bitwise O1 with no shared-memory pass.  The
+// slice's rows are sorted longest first, so the lanes still active at entry
+// k are 0..m_k-1 (m_k = popc of a ballot) and entry k of the slice is m_k
+// consecutive values: every col/val load is coalesced, and the U gathers of
+// a lane are independent, all in flight together.
+struct SellArgs {
+    const int32_t* base;   // per slice: first entry (nslices + 1)
+    const int32_t* srow;   // per lane: S-row index, -1 = empty lane
+    const uint16_t* len;   // per lane: nnz of the row
+    const int32_t* col;
+    const void* val;
+    const int32_t* out;
+    const int32_t* slot;
+    int32_t nslices;
+    VecArgs v;             // rows > vector_threshold (nV = 0: none / launched apart)
+};
+
+template <typename T, bool kCombine, bool kIdentity, int U>
+__global__ void __launch_bounds__(kSellCtaWarps * 32) spmv_sell_kernel(SellArgs a, SpmvOperands o) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const T* __restrict__ val = static_cast<const T*>(a.val);
+    const T* __restrict__ x = resolve_x<T>(o);
+    T* __restrict__ y = static_cast<T*>(o.y);
+    const int gw = blockIdx.x * kSellCtaWarps + w, nw = gridDim.x * kSellCtaWarps;
+    if (a.v.nV > 0) {   // the long rows first, a warp per row, so they do not trail
+        if (a.v.slot) vector_rows<T, true>(a.v, o, gw, nw);
+        else vector_rows<T, false>(a.v, o, gw, nw);
+    }
+    const uint64_t xpol = policy_evict_last();
+    for (int s = gw; s < a.nslices; s += nw) {
+        const int32_t sr = __ldg(a.srow + 32 * s + lane);
+        const int len = __ldg(a.len + 32 * s + lane);
+        int32_t off = __ldg(a.base + s);
+        const int width = __shfl_sync(0xffffffffu, len, 0);
+        T acc = T(0);
+        for (int k0 = 0; k0 < width; k0 += U) {
+            int32_t c[U];
+            T v[U], xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool act = k0 + u < len;
+                const int32_t q = off + lane;
+                off += __popc(__ballot_sync(0xffffffffu, act));
+                c[u] = act ? __ldcs(a.col + q) : 0;
+                v[u] = act ? __ldcs(val + q) : T(0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) xv[u] = k0 + u < len ? ldg_x<true>(x + c[u], xpol) : T(0);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (k0 + u < len) acc = add_rn(acc, mul_rn(v[u], xv[u]));
+        }
+        if (sr >= 0) {
+            const int32_t orow = kIdentity ? sr : __ldg(a.out + sr);
+            if (kCombine) {
+                const int32_t k = __ldg(a.slot + sr);
+                if (k >= 0) {
+                    combine<T>(acc, k, orow, o);
+                    continue;
+                }
+            }
+            __stcs(y + orow, acc);
+        }
+    }
+}
+
+
 // CSR-stream with a TMA producer (irregular row lengths).  The same tiles as
 // spmv_stream_kernel, grouped kStreamWarps to a block: one producer warp
 // stages a whole block (col, val, rowptr slice; 1-D bulk copies with an L2
@@ -1057,6 +1127,29 @@ cudaError_t launch_stream(const DevLayout& L, const SpmvOperands& o, cudaStream_
     return cudaGetLastError();
 }
 
+template <typename T, int U>
+cudaError_t launch_sell_u(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, bool vec) {
+    SellArgs a{L.sl_base, L.sl_srow, L.sl_len, L.sl_col, L.sl_val, L.s_out, L.s_slot, L.nslices,
+               VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}};
+    const bool c = L.s_slot != nullptr, id = L.s_out == nullptr;
+    const dim3 grid(L.grid_sl), block(kSellCtaWarps * 32);
+    if (c && id) spmv_sell_kernel<T, true, true, U><<<grid, block, 0, s>>>(a, o);
+    else if (c) spmv_sell_kernel<T, true, false, U><<<grid, block, 0, s>>>(a, o);
+    else if (id) spmv_sell_kernel<T, false, true, U><<<grid, block, 0, s>>>(a, o);
+    else spmv_sell_kernel<T, false, false, U><<<grid, block, 0, s>>>(a, o);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_sell(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, bool vec) {
+    switch (L.sell_unroll) {
+        case 4: return launch_sell_u<T, 4>(L, o, s, vec);
+        case 16: return launch_sell_u<T, 16>(L, o, s, vec);
+        default: return launch_sell_u<T, 8>(L, o, s, vec);
+    }
+}
+
 int st_variant() {   // DSPMV_STMA_VARIANT (sweeps); default kDefaultStVariant
     static const int v = [] {
         const char* ev = std::getenv("DSPMV_STMA_VARIANT");
@@ -1135,8 +1228,10 @@ template <typename T>
 cudaError_t launch_all(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, int32_t b0, int32_t b1, bool vec) {
     cudaError_t e = cudaSuccess;
     if (L.stream) {  // CSR-stream S group: all tiles (b0 / b1 ignored) and the long rows, one launch
-        if (b1 > b0 && L.ntiles > 0) {
-            e = L.stream_tma ? launch_stream_tma<T>(L, o, s, vec) : launch_stream<T>(L, o, s, vec);
+        if (b1 > b0 && (L.sell ? L.nslices > 0 : L.ntiles > 0)) {
+            e = L.sell         ? launch_sell<T>(L, o, s, vec)
+                : L.stream_tma ? launch_stream_tma<T>(L, o, s, vec)
+                               : launch_stream<T>(L, o, s, vec);
             if (e != cudaSuccess) return e;
             vec = false;
         }
@@ -1203,6 +1298,28 @@ int stream_kernel_ctas_per_sm(int dtype) {
     else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_stream_kernel<double, false, true>, kStreamCtaWarps * 32, 0);
     return n > 0 ? n : 1;
+}
+
+template <typename T, int U>
+int sell_occupancy() {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, spmv_sell_kernel<T, false, false, U>, kSellCtaWarps * 32, 0);
+    return n > 0 ? n : 1;
+}
+
+int sell_kernel_ctas_per_sm(int dtype, int unroll) {
+    const bool f = dtype == DSPMV_F32;
+    switch (unroll) {
+        case 4: return f ? sell_occupancy<float, 4>() : sell_occupancy<double, 4>();
+        case 16: return f ? sell_occupancy<float, 16>() : sell_occupancy<double, 16>();
+        default: return f ? sell_occupancy<float, 8>() : sell_occupancy<double, 8>();
+    }
+}
+
+int sell_unroll() {   // kSellUnroll, or DSPMV_SELL_UNROLL (sweeps; plan time)
+    const char* ev = std::getenv("DSPMV_SELL_UNROLL");
+    const int v = ev ? std::atoi(ev) : kSellUnroll;
+    return v == 4 || v == 16 ? v : 8;
 }
 
 int stream_tma_kernel_ctas_per_sm(int dtype, int variant) {

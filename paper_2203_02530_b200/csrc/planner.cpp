@@ -169,6 +169,57 @@ int auto_block_cfg(const int32_t* rowptr, int32_t nrows, int vthr, int esize) {
     return esize == 4 ? kShortRowBlockCfgF32 : kDefaultBlockCfg;
 }
 
+int sell_window() {   // read at every plan creation (sweeps change it between plans)
+    const char* ev = std::getenv("DSPMV_SELL_WINDOW");
+    const int v = ev ? std::atoi(ev) : kSellWindow;
+    return std::max(32, v - v % 32);
+}
+
+// Sliced form of the S group (DSPMV_SKERNEL_SELL).  Within each window of
+// sell_window() S rows the rows are ordered by length, longest first (ties
+// in row order), and cut into slices of 32 lanes.  Entry k of every row of a
+// slice still longer than k is stored at sl_base[s] + (entries of the slice
+// before k) + lane, so the m_k lanes active at k read m_k consecutive values.
+// Each row's own entries keep their CSR order (the serial loop's).
+static void build_sell(Layout& L, int esize) {
+    const int32_t nS = L.nS, W = sell_window();
+    const int64_t ns = (int64_t(nS) + 31) / 32 + (nS ? (nS / W + 1) : 0);  // upper bound (partial slices per window)
+    L.sl_base.clear();
+    L.sl_srow.clear();
+    L.sl_len.clear();
+    L.sl_base.reserve(size_t(ns) + 1);
+    const int64_t nnz = L.s_rowptr[nS];
+    L.sl_col.assign(size_t(nnz) + kPad, 0);
+    L.sl_val.assign((size_t(nnz) + kPad) * esize, 0);
+    std::vector<int32_t> order;
+    int64_t q = 0;
+    for (int32_t w0 = 0; w0 < nS; w0 += W) {
+        const int32_t w1 = std::min(nS, w0 + W);
+        order.resize(size_t(w1 - w0));
+        for (int32_t r = w0; r < w1; ++r) order[size_t(r - w0)] = r;
+        auto len = [&](int32_t r) { return L.s_rowptr[r + 1] - L.s_rowptr[r]; };
+        std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return len(a) > len(b); });
+        for (size_t s0 = 0; s0 < order.size(); s0 += 32) {
+            const size_t s1 = std::min(order.size(), s0 + 32);
+            L.sl_base.push_back(int32_t(q));
+            for (size_t t = s0; t < s0 + 32; ++t) {
+                L.sl_srow.push_back(t < s1 ? order[t] : -1);
+                L.sl_len.push_back(t < s1 ? uint16_t(len(order[t])) : uint16_t(0));
+            }
+            const int32_t width = len(order[s0]);
+            for (int32_t k = 0; k < width; ++k) {
+                for (size_t t = s0; t < s1 && len(order[t]) > k; ++t) {
+                    const int32_t src = L.s_rowptr[order[t]] + k;
+                    L.sl_col[size_t(q)] = L.s_col[size_t(src)];
+                    std::memcpy(&L.sl_val[size_t(q) * esize], &L.s_val[size_t(src) * esize], size_t(esize));
+                    ++q;
+                }
+            }
+        }
+    }
+    L.sl_base.push_back(int32_t(q));
+}
+
 bool auto_stream(const int32_t* rowptr, int32_t nrows, int vthr) {
     double s1 = 0, s2 = 0;
     int64_t rows = 0;
@@ -186,10 +237,12 @@ bool auto_stream(const int32_t* rowptr, int32_t nrows, int vthr) {
 
 void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, const uint8_t* val,
                   int esize, const int32_t* out_row, const int32_t* slot, int vthr,
-                  const BlockCfg& cfg, Layout& L, bool stream) {
+                  const BlockCfg& cfg, Layout& L, bool stream, bool sell) {
     L = Layout();
     L.nrows = nrows;
-    L.stream = stream;
+    L.stream = stream || sell;
+    L.sell = sell;
+    stream = L.stream;
     if (stream) vthr = std::min(vthr, kStreamTile);   // a CSR-stream tile holds any S row
     std::vector<int32_t> srows, vrows;
     srows.reserve(nrows);
@@ -289,6 +342,7 @@ void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, cons
         L.s_desc.insert(L.s_desc.end(), d, d + kDescInts);
     }
     L.nb = int32_t(L.s_desc.size() / kDescInts);
+    if (sell) build_sell(L, esize);
     if (stream) {
         // CSR-stream tiles: greedy runs of rows with <= kStreamTile nnz and
         // <= kStreamRows rows (every S row has <= vthr <= kStreamTile nnz)

@@ -45,6 +45,16 @@ struct DevLayout {
     int32_t ntblocks = 0;
     int grid_tt = 0;
     int32_t* s_tdesc = nullptr;
+    // sliced form of the S group (Layout::sell, spmv_sell_kernel)
+    bool sell = false;
+    int32_t nslices = 0;
+    int grid_sl = 0;
+    int sell_unroll = 8;
+    int32_t* sl_base = nullptr;
+    int32_t* sl_srow = nullptr;
+    uint16_t* sl_len = nullptr;
+    int32_t* sl_col = nullptr;
+    void* sl_val = nullptr;
     int64_t x_bytes = 0;               // bytes of the x operand (L2 access-policy window)
 };
 
@@ -73,6 +83,8 @@ struct SpmvOperands {
 int block_kernel_smem_bytes(int dtype, int cfg);
 int block_kernel_ctas_per_sm(int dtype, int cfg);
 int stream_kernel_ctas_per_sm(int dtype);
+int sell_kernel_ctas_per_sm(int dtype, int unroll);
+int sell_unroll();   // gathers in flight per lane of spmv_sell_kernel (4 / 8 / 16)
 int stream_tma_kernel_ctas_per_sm(int dtype, int variant);
 int stream_tma_variant();   // kStVariants index in use (DSPMV_STMA_VARIANT)
 void set_x_persist_limit();   // experiment DSPMV_X_PERSIST (plan time)

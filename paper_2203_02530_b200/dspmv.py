@@ -31,7 +31,8 @@ STATUS_NAMES = ["OK", "ERR_ARG", "ERR_RANGE", "ERR_SCHEDULE", "ERR_DEADLOCK", "E
 DSPMV_F64, DSPMV_F32 = 0, 1
 DSPMV_COMM_NCCL, DSPMV_COMM_LOCAL, DSPMV_COMM_HOST = 0, 1, 2
 DSPMV_EXCHANGE_COPY, DSPMV_EXCHANGE_PUT, DSPMV_EXCHANGE_NONE = 0, 1, 2
-DSPMV_SKERNEL_AUTO, DSPMV_SKERNEL_BLOCK, DSPMV_SKERNEL_STREAM, DSPMV_SKERNEL_STREAM_TMA = 0, 1, 2, 3
+DSPMV_SKERNEL_AUTO, DSPMV_SKERNEL_BLOCK, DSPMV_SKERNEL_STREAM, DSPMV_SKERNEL_STREAM_TMA, DSPMV_SKERNEL_SELL = \
+    0, 1, 2, 3, 4
 DSPMV_PACK_GATHER, DSPMV_PACK_ALIAS_IF_CONTIGUOUS = 0, 1
 DSPMV_ACC_TICKET, DSPMV_ACC_EXPLICIT_IN_END = 0, 1
 DSPMV_UNPACK_COPY, DSPMV_UNPACK_FUSED = 0, 1

@@ -34,7 +34,7 @@ profile)
       python bench.py --workload c3 --secondary none --steps 2 --warmup 1 --no-cpu-baseline --no-sweep --execution host > $OUT/ncu_c3.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"spmv_stream_kernel" -s 3 -c 1 -o $OUT/prof_c4 -f \
       python bench.py --workload c4 --secondary none --steps 2 --warmup 1 --no-cpu-baseline --no-sweep --execution host > $OUT/ncu_c4.log 2>&1
-  for tool in memcheck racecheck synccheck; do
+  for tool in memcheck racecheck synccheck; do  # the pool may close compute-sanitizer (exit 86)
     timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/sanitize.py > $OUT/san_$tool.log 2>&1
     echo "$tool exit $?" >> $OUT/sanitizer.txt
   done

@@ -1,0 +1,73 @@
+"""C4 y_L by S-group kernel: the CSR-stream kernel (K1b) against the sliced
+kernel (K1d, DSPMV_SKERNEL_SELL) over its window / unroll settings, on the
+full BASELINE configs[3] matrix at 1 rank (a GPU-resident graph on one
+stream, L2 flushed before every apply, CUDA events around each apply).
+Every variant's y must equal K1b's bit for bit (both are the serial loop on
+rows <= 256 nnz, and the same long-row kernel above).
+
+    python scripts/sell_sweep.py [--reps 30] [--cfgs stream,sell:256:8,...]
+"""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import gen  # noqa: E402
+from paper_2203_02530_b200 import dspmv as D  # noqa: E402
+from tests.gpu_helpers import derive_ops  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--reps", type=int, default=30)
+ap.add_argument("--workload", default="c4")
+ap.add_argument("--cfgs", default="stream,sell:256:8,sell:64:8,sell:1024:8,sell:4096:8,sell:256:4,sell:256:16,stream")
+a = ap.parse_args()
+
+t0 = time.time()
+n, (rp, col, val) = gen.config_matrix(a.workload)
+x = torch.from_numpy(gen.x_values((0, n))).cuda()
+print(f"# {a.workload}: n={n} nnz={rp[-1]} generated in {time.time() - t0:.1f} s", flush=True)
+comm = D.dspmv_comm_create(D.dspmv_comm_unique_id(), 1, 0, 0)
+stream = torch.cuda.Stream()
+ref = None
+for c in a.cfgs.split(","):
+    parts = c.split(":")
+    if parts[0] == "sell":
+        os.environ["DSPMV_SELL_WINDOW"] = parts[1]
+        os.environ["DSPMV_SELL_UNROLL"] = parts[2]
+        sk = D.DSPMV_SKERNEL_SELL
+    else:
+        sk = D.DSPMV_SKERNEL_STREAM
+    t1 = time.time()
+    plan = D.dspmv_plan_create(comm, n, rp, col, val, s_kernel=sk)
+    tp = time.time() - t1
+    info = D.dspmv_plan_info_get(plan)
+    sched = D.dspmv_schedule_create(plan, derive_ops(), 2)
+    D.dspmv_schedule_set_caller_stream0(sched, 1)
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    ts = []
+    with torch.cuda.stream(stream):
+        for i in range(a.reps + 3):
+            D.dspmv_l2_flush(0, stream.cuda_stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            D.dspmv_apply_graph(sched, x, y, stream.cuda_stream)
+            e1.record(stream)
+            e1.synchronize()
+            if i >= 3:
+                ts.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    yh = y.cpu().numpy()
+    if ref is None:
+        ref = yh
+    same = bool(np.array_equal(yh.view(np.int64), ref.view(np.int64)))
+    ms = float(np.median(ts))
+    nnz = int(rp[-1])
+    print(f"{c:16s} kernel={info['s_kernel_local']} yL_ms {ms:.4f} min {min(ts):.4f} "
+          f"G_gathers/s {nnz / ms / 1e6:.1f} plan_s {tp:.1f} bitwise_eq_first {same}", flush=True)
+    D.dspmv_schedule_destroy(sched)
+    D.dspmv_plan_destroy(plan)
+D.dspmv_comm_destroy(comm)

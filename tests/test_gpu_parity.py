@@ -500,7 +500,7 @@ def test_timestamp_aliasing_keeps_times_consistent():
         D.dspmv_comm_destroy(comm)
 
 
-@pytest.mark.parametrize("skern", [D.DSPMV_SKERNEL_STREAM, D.DSPMV_SKERNEL_STREAM_TMA])
+@pytest.mark.parametrize("skern", [D.DSPMV_SKERNEL_STREAM, D.DSPMV_SKERNEL_STREAM_TMA, D.DSPMV_SKERNEL_SELL])
 @pytest.mark.parametrize("name", ["pl20k", "rand300", "7pt32", "27pt20"])
 @pytest.mark.parametrize("P", [1, 3])
 def test_stream_kernel_bitwise_vs_oracle(name, P, skern):
@@ -553,7 +553,7 @@ def test_stream_kernel_auto_choice_and_fp32():
     assert within_tol(y, O1.o1_spmv(rp, col, vr, xr), O1.o1_absdot(rp, col, vr, xr), 1e-5)
 
 
-@pytest.mark.parametrize("skern", [D.DSPMV_SKERNEL_STREAM, D.DSPMV_SKERNEL_STREAM_TMA])
+@pytest.mark.parametrize("skern", [D.DSPMV_SKERNEL_STREAM, D.DSPMV_SKERNEL_STREAM_TMA, D.DSPMV_SKERNEL_SELL])
 def test_stream_kernel_edge_cases(skern):
     """CSR-stream with no S rows at all (every row > 256 nnz: the long-row
     kernel alone), with runs of empty rows (tiles whose rows sum to +0), and
