@@ -152,15 +152,18 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
             D.stream = true;
             D.sell = true;
             D.nslices = int32_t(L.sl_base.size()) - 1;
+            D.nchunks = int32_t(L.sl_chunk.size()) - 1;
+            ST_TRY(dev_upload(p, &D.sl_chunk, L.sl_chunk.data(), L.sl_chunk.size()));
             ST_TRY(dev_upload(p, &D.sl_base, L.sl_base.data(), L.sl_base.size()));
             ST_TRY(dev_upload(p, &D.sl_srow, L.sl_srow.data(), L.sl_srow.size()));
             ST_TRY(dev_upload(p, &D.sl_len, L.sl_len.data(), L.sl_len.size()));
             ST_TRY(dev_upload(p, &D.sl_col, L.sl_col.data(), L.sl_col.size()));
             ST_TRY(dev_upload(p, reinterpret_cast<uint8_t**>(&D.sl_val), L.sl_val.data(), L.sl_val.size()));
             D.sell_unroll = sell_unroll();
+            set_x_persist_limit();
             int spsm = sell_kernel_ctas_per_sm(p.dtype, D.sell_unroll);
             if (const char* ev = std::getenv("DSPMV_SELL_CTAS")) spsm = std::max(1, std::min(spsm, std::atoi(ev)));  // sweeps
-            D.grid_sl = std::max(1, std::min((D.nslices + kSellCtaWarps - 1) / kSellCtaWarps, spsm * usable));
+            D.grid_sl = std::max(1, std::min((D.nchunks + kSellCtaWarps - 1) / kSellCtaWarps, spsm * usable));
         } else if (L.stream) {
             D.stream = true;
             set_x_persist_limit();

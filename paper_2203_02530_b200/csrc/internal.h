@@ -63,6 +63,7 @@ constexpr int kSTBlockRows = kStreamWarps * kStreamRows;   // 512
 // length (descending, stable), so the lanes still active at entry k are a
 // prefix 0..m_k-1 and entry k of the slice is stored as m_k consecutive values
 constexpr int kSellWindow = 256;
+constexpr int kSellChunkCost = 4096;   // work chunk: ~entries (+ overheads) per warp grab
 #ifndef DSPMV_SELL_CTA_WARPS
 #define DSPMV_SELL_CTA_WARPS 8
 #endif
@@ -129,6 +130,7 @@ struct Layout {
     // the slice's entries start at sl_base[s] in sl_col / sl_val
     bool sell = false;
     std::vector<int32_t> sl_base, sl_srow, sl_col;
+    std::vector<int32_t> sl_chunk;     // first slice of each work chunk (+ end)
     std::vector<uint16_t> sl_len;
     std::vector<uint8_t> sl_val;
 };
@@ -145,6 +147,7 @@ void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, cons
                   int esize, const int32_t* out_row, const int32_t* slot, int vthr,
                   const BlockCfg& cfg, Layout& L, bool stream = false, bool sell = false);
 int sell_window();   // kSellWindow, or DSPMV_SELL_WINDOW (sweeps)
+int sell_chunk_cost();   // kSellChunkCost, or DSPMV_SELL_CHUNK (sweeps)
 
 // -------------------------------------------------------------- schedules
 // A DAG vertex instance: kind + peer offset (0 = coarse / not an exchange vertex)

@@ -616,6 +616,7 @@ __global__ void __launch_bounds__(kStreamCtaWarps * 32) spmv_stream_kernel(Strea
 // consecutive values: every col/val load is coalesced, and the U gathers of
 // a lane are independent, all in flight together.
 struct SellArgs {
+    const int32_t* chunk;  // per work chunk: first slice (nchunks + 1)
     const int32_t* base;   // per slice: first entry (nslices + 1)
     const int32_t* srow;   // per lane: S-row index, -1 = empty lane
     const uint16_t* len;   // per lane: nnz of the row
@@ -623,12 +624,15 @@ struct SellArgs {
     const void* val;
     const int32_t* out;
     const int32_t* slot;
-    int32_t nslices;
+    int32_t nchunks;
     VecArgs v;             // rows > vector_threshold (nV = 0: none / launched apart)
 };
 
 template <typename T, bool kCombine, bool kIdentity, int U>
-__global__ void __launch_bounds__(kSellCtaWarps * 32) spmv_sell_kernel(SellArgs a, SpmvOperands o) {
+#ifndef DSPMV_SELL_MINB
+#define DSPMV_SELL_MINB 1   // diagnostic builds: CTAs/SM the register budget must allow
+#endif
+__global__ void __launch_bounds__(kSellCtaWarps * 32, DSPMV_SELL_MINB) spmv_sell_kernel(SellArgs a, SpmvOperands o) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const T* __restrict__ val = static_cast<const T*>(a.val);
     const T* __restrict__ x = resolve_x<T>(o);
@@ -639,7 +643,8 @@ __global__ void __launch_bounds__(kSellCtaWarps * 32) spmv_sell_kernel(SellArgs 
         else vector_rows<T, false>(a.v, o, gw, nw);
     }
     const uint64_t xpol = policy_evict_last();
-    for (int s = gw; s < a.nslices; s += nw) {
+    for (int c = gw; c < a.nchunks; c += nw)
+    for (int s = __ldg(a.chunk + c), se = __ldg(a.chunk + c + 1); s < se; ++s) {
         const int32_t sr = __ldg(a.srow + 32 * s + lane);
         const int len = __ldg(a.len + 32 * s + lane);
         int32_t off = __ldg(a.base + s);
@@ -1129,10 +1134,27 @@ cudaError_t launch_stream(const DevLayout& L, const SpmvOperands& o, cudaStream_
 
 template <typename T, int U>
 cudaError_t launch_sell_u(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, bool vec) {
-    SellArgs a{L.sl_base, L.sl_srow, L.sl_len, L.sl_col, L.sl_val, L.s_out, L.s_slot, L.nslices,
+    SellArgs a{L.sl_chunk, L.sl_base, L.sl_srow, L.sl_len, L.sl_col, L.sl_val, L.s_out, L.s_slot, L.nchunks,
                VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}};
     const bool c = L.s_slot != nullptr, id = L.s_out == nullptr;
     const dim3 grid(L.grid_sl), block(kSellCtaWarps * 32);
+    if (x_persist_fraction() > 0 && L.x_bytes > 0) {   // experiment DSPMV_X_PERSIST
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = block;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        x_window(at[0], o.x, L.x_bytes);
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaError_t e;
+        if (c && id) e = cudaLaunchKernelEx(&cfg, spmv_sell_kernel<T, true, true, U>, a, o);
+        else if (c) e = cudaLaunchKernelEx(&cfg, spmv_sell_kernel<T, true, false, U>, a, o);
+        else if (id) e = cudaLaunchKernelEx(&cfg, spmv_sell_kernel<T, false, true, U>, a, o);
+        else e = cudaLaunchKernelEx(&cfg, spmv_sell_kernel<T, false, false, U>, a, o);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return e != cudaSuccess ? e : cudaGetLastError();
+    }
     if (c && id) spmv_sell_kernel<T, true, true, U><<<grid, block, 0, s>>>(a, o);
     else if (c) spmv_sell_kernel<T, true, false, U><<<grid, block, 0, s>>>(a, o);
     else if (id) spmv_sell_kernel<T, false, true, U><<<grid, block, 0, s>>>(a, o);

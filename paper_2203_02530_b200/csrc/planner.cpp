@@ -175,6 +175,11 @@ int sell_window() {   // read at every plan creation (sweeps change it between p
     return std::max(32, v - v % 32);
 }
 
+int sell_chunk_cost() {   // read at every plan creation (sweeps)
+    const char* ev = std::getenv("DSPMV_SELL_CHUNK");
+    return ev ? std::max(1, std::atoi(ev)) : kSellChunkCost;
+}
+
 // Sliced form of the S group (DSPMV_SKERNEL_SELL).  Within each window of
 // sell_window() S rows the rows are ordered by length, longest first (ties
 // in row order), and cut into slices of 32 lanes.  Entry k of every row of a
@@ -218,6 +223,20 @@ static void build_sell(Layout& L, int esize) {
         }
     }
     L.sl_base.push_back(int32_t(q));
+    // Work chunks: runs of consecutive slices of about equal cost (entries +
+    // per-iteration and per-slice overhead).  Warps stride over chunks, so the
+    // rows in flight stay a moving front (x locality) and a window's wide
+    // first slice does not always land on the same warps.
+    const int64_t target = sell_chunk_cost();
+    L.sl_chunk.clear();
+    int64_t acc = 0;
+    const int32_t nsl = int32_t(L.sl_base.size()) - 1;
+    for (int32_t s = 0; s < nsl; ++s) {
+        if (acc == 0) L.sl_chunk.push_back(s);
+        acc += int64_t(L.sl_base[s + 1] - L.sl_base[s]) + 8 * int64_t(L.sl_len[size_t(32) * s]) + 64;
+        if (acc >= target) acc = 0;
+    }
+    L.sl_chunk.push_back(nsl);
 }
 
 bool auto_stream(const int32_t* rowptr, int32_t nrows, int vthr) {

@@ -50,6 +50,8 @@ struct DevLayout {
     int32_t nslices = 0;
     int grid_sl = 0;
     int sell_unroll = 8;
+    int32_t nchunks = 0;
+    int32_t* sl_chunk = nullptr;
     int32_t* sl_base = nullptr;
     int32_t* sl_srow = nullptr;
     uint16_t* sl_len = nullptr;

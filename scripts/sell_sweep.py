@@ -23,7 +23,9 @@ from tests.gpu_helpers import derive_ops  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=30)
 ap.add_argument("--workload", default="c4")
-ap.add_argument("--cfgs", default="stream,sell:256:8,sell:64:8,sell:1024:8,sell:4096:8,sell:256:4,sell:256:16,stream")
+ap.add_argument("--cfgs", default="stream,sell:256:8:256:4096,sell:1024:8:256:4096,sell:4096:8:256:4096,"
+                "sell:256:8:64:4096,sell:1024:8:64:4096,sell:1024:8:128:4096,sell:1024:8:32:4096,"
+                "sell:1024:4:64:4096,sell:1024:16:64:4096,sell:1024:8:64:16384,sell:1024:8:64:1024,stream")
 a = ap.parse_args()
 
 t0 = time.time()
@@ -34,15 +36,22 @@ comm = D.dspmv_comm_create(D.dspmv_comm_unique_id(), 1, 0, 0)
 stream = torch.cuda.Stream()
 ref = None
 for c in a.cfgs.split(","):
-    parts = c.split(":")
+    parts = c.split(":")   # sell:window:unroll[:vector_threshold[:chunk_cost[:ctas_per_sm]]]
+    vthr = -1
     if parts[0] == "sell":
         os.environ["DSPMV_SELL_WINDOW"] = parts[1]
         os.environ["DSPMV_SELL_UNROLL"] = parts[2]
+        if len(parts) > 3:
+            vthr = int(parts[3])
+        if len(parts) > 4:
+            os.environ["DSPMV_SELL_CHUNK"] = parts[4]
+        if len(parts) > 5:
+            os.environ["DSPMV_SELL_CTAS"] = parts[5]
         sk = D.DSPMV_SKERNEL_SELL
     else:
         sk = D.DSPMV_SKERNEL_STREAM
     t1 = time.time()
-    plan = D.dspmv_plan_create(comm, n, rp, col, val, s_kernel=sk)
+    plan = D.dspmv_plan_create(comm, n, rp, col, val, s_kernel=sk, vector_threshold=vthr)
     tp = time.time() - t1
     info = D.dspmv_plan_info_get(plan)
     sched = D.dspmv_schedule_create(plan, derive_ops(), 2)
@@ -64,10 +73,11 @@ for c in a.cfgs.split(","):
     if ref is None:
         ref = yh
     same = bool(np.array_equal(yh.view(np.int64), ref.view(np.int64)))
+    rel = float(np.max(np.abs(yh - ref)) / max(1e-300, np.max(np.abs(ref))))
     ms = float(np.median(ts))
     nnz = int(rp[-1])
     print(f"{c:16s} kernel={info['s_kernel_local']} yL_ms {ms:.4f} min {min(ts):.4f} "
-          f"G_gathers/s {nnz / ms / 1e6:.1f} plan_s {tp:.1f} bitwise_eq_first {same}", flush=True)
+          f"G_gathers/s {nnz / ms / 1e6:.1f} plan_s {tp:.1f} bitwise_eq_first {same} maxrel {rel:.1e}", flush=True)
     D.dspmv_schedule_destroy(sched)
     D.dspmv_plan_destroy(plan)
 D.dspmv_comm_destroy(comm)
