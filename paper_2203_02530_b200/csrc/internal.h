@@ -68,7 +68,7 @@ constexpr int kSellChunkCost = 4096;   // work chunk: ~entries (+ overheads) per
 #define DSPMV_SELL_CTA_WARPS 8
 #endif
 constexpr int kSellCtaWarps = DSPMV_SELL_CTA_WARPS;
-constexpr int kSellUnroll = 8;     // x gathers in flight per lane (DSPMV_SELL_UNROLL: 4 / 8 / 16)
+constexpr int kSellUnroll = 4;     // x gathers in flight per lane (DSPMV_SELL_UNROLL: 4 / 8 / 16)
 constexpr int kDefaultStVariant = 2;   // kernels.cu kStVariants: 3 slots, 2 CTAs/SM, pipelined
 constexpr int kDefaultVectorThreshold = 256;  // rows above: warp-per-row kernel
 constexpr int kMaxClass = 5;       // row classes: 2^c lanes per row, c = 0..5

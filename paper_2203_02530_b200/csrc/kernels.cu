@@ -643,40 +643,50 @@ __global__ void __launch_bounds__(kSellCtaWarps * 32, DSPMV_SELL_MINB) spmv_sell
         else vector_rows<T, false>(a.v, o, gw, nw);
     }
     const uint64_t xpol = policy_evict_last();
-    for (int c = gw; c < a.nchunks; c += nw)
-    for (int s = __ldg(a.chunk + c), se = __ldg(a.chunk + c + 1); s < se; ++s) {
-        const int32_t sr = __ldg(a.srow + 32 * s + lane);
-        const int len = __ldg(a.len + 32 * s + lane);
+    // Per chunk, slice s+1's lane metadata is loaded while slice s gathers, and
+    // its output row / combine slot at the end of slice s, so neither sits on
+    // the next slice's dependent chain (metadata -> col -> x).
+    for (int c = gw; c < a.nchunks; c += nw) {
+        int s = __ldg(a.chunk + c);
+        const int se = __ldg(a.chunk + c + 1);
+        int32_t sr = __ldg(a.srow + 32 * s + lane);
+        int len = __ldg(a.len + 32 * s + lane);
         int32_t off = __ldg(a.base + s);
-        const int width = __shfl_sync(0xffffffffu, len, 0);
-        T acc = T(0);
-        for (int k0 = 0; k0 < width; k0 += U) {
-            int32_t c[U];
-            T v[U], xv[U];
+        int32_t orow = sr < 0 ? -1 : kIdentity ? sr : __ldg(a.out + sr);
+        int32_t kslot = kCombine && sr >= 0 ? __ldg(a.slot + sr) : -1;
+        for (; s < se; ++s) {
+            const bool more = s + 1 < se;
+            const int32_t sr_n = more ? __ldg(a.srow + 32 * (s + 1) + lane) : -1;
+            const int len_n = more ? __ldg(a.len + 32 * (s + 1) + lane) : 0;
+            const int32_t off_n = more ? __ldg(a.base + s + 1) : 0;
+            const int width = __shfl_sync(0xffffffffu, len, 0);
+            T acc = T(0);
+            for (int k0 = 0; k0 < width; k0 += U) {
+                int32_t cc[U];
+                T v[U], xv[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const bool act = k0 + u < len;
-                const int32_t q = off + lane;
-                off += __popc(__ballot_sync(0xffffffffu, act));
-                c[u] = act ? __ldcs(a.col + q) : 0;
-                v[u] = act ? __ldcs(val + q) : T(0);
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) xv[u] = k0 + u < len ? ldg_x<true>(x + c[u], xpol) : T(0);
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (k0 + u < len) acc = add_rn(acc, mul_rn(v[u], xv[u]));
-        }
-        if (sr >= 0) {
-            const int32_t orow = kIdentity ? sr : __ldg(a.out + sr);
-            if (kCombine) {
-                const int32_t k = __ldg(a.slot + sr);
-                if (k >= 0) {
-                    combine<T>(acc, k, orow, o);
-                    continue;
+                for (int u = 0; u < U; ++u) {
+                    const bool act = k0 + u < len;
+                    const int32_t q = off + lane;
+                    off += __popc(__ballot_sync(0xffffffffu, act));
+                    cc[u] = act ? __ldcs(a.col + q) : 0;
+                    v[u] = act ? __ldcs(val + q) : T(0);
                 }
+#pragma unroll
+                for (int u = 0; u < U; ++u) xv[u] = k0 + u < len ? ldg_x<true>(x + cc[u], xpol) : T(0);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (k0 + u < len) acc = add_rn(acc, mul_rn(v[u], xv[u]));
             }
-            __stcs(y + orow, acc);
+            if (orow >= 0) {
+                if (kCombine && kslot >= 0) combine<T>(acc, kslot, orow, o);
+                else __stcs(y + orow, acc);
+            }
+            orow = sr_n < 0 ? -1 : kIdentity ? sr_n : __ldg(a.out + sr_n);
+            kslot = kCombine && sr_n >= 0 ? __ldg(a.slot + sr_n) : -1;
+            sr = sr_n;
+            len = len_n;
+            off = off_n;
         }
     }
 }
