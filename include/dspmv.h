@@ -304,6 +304,21 @@ dspmv_status dspmv_layout_host(const int64_t* rowptr, int32_t nrows, int dtype, 
  * each; S rows in matrix order) and the V-group rows (int32[nV], rows of
  * more than min(vthr, 256) nnz).  Tiles and V rows are returned whatever
  * *stream_used says.  Pass NULL outputs to get sizes. */
+/* Host-only, test hook: the sliced form (DSPMV_SKERNEL_SELL) of the same
+ * matrix's S rows (rows of <= min(vthr, 256) nnz, -1 = default), with sort
+ * window `window` rows (-1 = default, K1d):
+ *   slice_base int32[n_slices+1]  first stored entry of each slice
+ *   lane_row   int32[32*n_slices] S-row index of each lane (-1: empty lane)
+ *   lane_len   int32[32*n_slices] nnz of the lane's row
+ *   entry_src  int32[nnz_S]       position, in the S group's CSR order (the
+ *                                 rows' entries back to back in S-row order),
+ *                                 of each stored entry
+ *   chunks     int32[n_chunks+1]  first slice of each work chunk
+ * Pass NULL outputs to get the sizes (*n_slices, *n_entries, *n_chunks). */
+dspmv_status dspmv_sell_layout_host(const int64_t* rowptr, int32_t nrows, int vthr, int window,
+                                    int32_t* slice_base, int32_t* lane_row, int32_t* lane_len,
+                                    int32_t* entry_src, int32_t* chunks, int32_t* n_slices,
+                                    int64_t* n_entries, int32_t* n_chunks);
 dspmv_status dspmv_stream_layout_host(const int64_t* rowptr, int32_t nrows, int vthr, int s_kernel,
                                       int32_t* tiles, int32_t* n_tiles, int32_t* v_rows, int32_t* n_v,
                                       int32_t* stream_used);

@@ -1942,6 +1942,50 @@ dspmv_status dspmv_layout_host(const int64_t* rowptr, int32_t nrows, int dtype, 
     return DSPMV_OK;
 }
 
+dspmv_status dspmv_sell_layout_host(const int64_t* rowptr, int32_t nrows, int vthr, int window,
+                                    int32_t* slice_base, int32_t* lane_row, int32_t* lane_len,
+                                    int32_t* entry_src, int32_t* chunks, int32_t* n_slices,
+                                    int64_t* n_entries, int32_t* n_chunks) {
+    if (!rowptr || nrows < 0 || !n_slices || !n_entries || !n_chunks) return fail(DSPMV_ERR_ARG, "null argument");
+    if (vthr < 0) vthr = kDefaultVectorThreshold;
+    if (window == 0 || window < -1) return fail(DSPMV_ERR_ARG, "window must be -1 or > 0");
+    std::vector<int32_t> rp(static_cast<size_t>(nrows) + 1);
+    for (int32_t i = 0; i <= nrows; ++i) {
+        const int64_t v = rowptr[i] - rowptr[0];
+        if (v >= (int64_t(1) << 31)) return fail(DSPMV_ERR_RANGE, "nnz >= 2^31");
+        rp[i] = int32_t(v);
+    }
+    // col[q] = q: the stored col array then is each entry's CSR position
+    std::vector<int32_t> col(size_t(rp[nrows])), ident(static_cast<size_t>(nrows));
+    for (size_t q = 0; q < col.size(); ++q) col[q] = int32_t(q);
+    for (int32_t i = 0; i < nrows; ++i) ident[i] = i;
+    Layout L;
+    g_sell_window_override = window > 0 ? std::max(32, window - window % 32) : 0;
+    build_layout(rp.data(), nrows, col.data(), nullptr, 8, ident.data(), nullptr, vthr,
+                 kBlockCfgs[kDefaultBlockCfg], L, true, true);
+    g_sell_window_override = 0;
+    const int32_t ns = int32_t(L.sl_base.size()) - 1, nc = int32_t(L.sl_chunk.size()) - 1;
+    const int64_t ne = L.sl_base.back();
+    const bool fit = !slice_base || (*n_slices >= ns && *n_entries >= ne && *n_chunks >= nc);
+    if (slice_base && fit) {
+        std::copy(L.sl_base.begin(), L.sl_base.end(), slice_base);
+        if (lane_row) std::copy(L.sl_srow.begin(), L.sl_srow.end(), lane_row);
+        if (lane_len) std::copy(L.sl_len.begin(), L.sl_len.end(), lane_len);
+        // S-group CSR position of each stored entry: the S rows' entries back to back
+        if (entry_src) {
+            std::vector<int32_t> spos(col.size(), -1);
+            for (int64_t q = 0; q < int64_t(L.s_rowptr[L.nS]); ++q) spos[size_t(L.s_col[size_t(q)])] = int32_t(q);
+            for (int64_t q = 0; q < ne; ++q) entry_src[q] = spos[size_t(L.sl_col[size_t(q)])];
+        }
+        if (chunks) std::copy(L.sl_chunk.begin(), L.sl_chunk.end(), chunks);
+    }
+    *n_slices = ns;
+    *n_entries = ne;
+    *n_chunks = nc;
+    if (!fit) return fail(DSPMV_ERR_ARG, "output arrays too small");
+    return DSPMV_OK;
+}
+
 dspmv_status dspmv_stream_layout_host(const int64_t* rowptr, int32_t nrows, int vthr, int s_kernel,
                                       int32_t* tiles, int32_t* n_tiles, int32_t* v_rows, int32_t* n_v,
                                       int32_t* stream_used) {

@@ -147,6 +147,7 @@ void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, cons
                   int esize, const int32_t* out_row, const int32_t* slot, int vthr,
                   const BlockCfg& cfg, Layout& L, bool stream = false, bool sell = false);
 int sell_window();   // kSellWindow, or DSPMV_SELL_WINDOW (sweeps)
+extern int g_sell_window_override;   // > 0: sell_window() (host test hook only)
 int sell_chunk_cost();   // kSellChunkCost, or DSPMV_SELL_CHUNK (sweeps)
 
 // -------------------------------------------------------------- schedules

@@ -169,7 +169,10 @@ int auto_block_cfg(const int32_t* rowptr, int32_t nrows, int vthr, int esize) {
     return esize == 4 ? kShortRowBlockCfgF32 : kDefaultBlockCfg;
 }
 
+int g_sell_window_override = 0;   // dspmv_sell_layout_host (host tests)
+
 int sell_window() {   // read at every plan creation (sweeps change it between plans)
+    if (g_sell_window_override > 0) return g_sell_window_override;
     const char* ev = std::getenv("DSPMV_SELL_WINDOW");
     const int v = ev ? std::atoi(ev) : kSellWindow;
     return std::max(32, v - v % 32);

@@ -128,6 +128,7 @@ _sig("dspmv_host_plan_requests", [_P, _I, _P, ctypes.c_size_t, _P])
 _sig("dspmv_host_plan_set_requests", [_P, _P, _P])
 _sig("dspmv_layout_host", [_P, ctypes.c_int32, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P])
 _sig("dspmv_stream_layout_host", [_P, ctypes.c_int32, _I, _I, _P, _P, _P, _P, _P])
+_sig("dspmv_sell_layout_host", [_P, ctypes.c_int32, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P])
 _sig("dspmv_schedule_validate", [_P, _I, _I])
 _sig("dspmv_schedule_derive", [_P, _P, _I, _P, _I, _P])
 _sig("dspmv_schedule_derive_peers", [_P, _P, _P, _I, _I, _P, _I, _P])
@@ -434,6 +435,27 @@ def dspmv_stream_layout_host(rowptr, vthr: int = -1, s_kernel: int = DSPMV_SKERN
     _check(lib.dspmv_stream_layout_host(rowptr.ctypes.data, nr, vthr, s_kernel, tiles.ctypes.data, ctypes.byref(nt),
                                         v_rows.ctypes.data, ctypes.byref(nv), ctypes.byref(su)))
     return tiles[:2 * nt.value].reshape(-1, 2), v_rows[:nv.value], bool(su.value)
+
+
+def dspmv_sell_layout_host(rowptr, vthr: int = -1, window: int = -1):
+    """The planner's sliced (DSPMV_SKERNEL_SELL) form of the S rows:
+    dict(base[ns+1], lane_row[ns,32], lane_len[ns,32], entry_src[nnz_S], chunks[nc+1])."""
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    nr = len(rowptr) - 1
+    ns, ne, nc = ctypes.c_int32(0), ctypes.c_int64(0), ctypes.c_int32(0)
+    _check(lib.dspmv_sell_layout_host(rowptr.ctypes.data, nr, vthr, window, None, None, None, None, None,
+                                      ctypes.byref(ns), ctypes.byref(ne), ctypes.byref(nc)))
+    base = np.zeros(ns.value + 1, np.int32)
+    lane_row = np.zeros(max(1, 32 * ns.value), np.int32)
+    lane_len = np.zeros(max(1, 32 * ns.value), np.int32)
+    src = np.zeros(max(1, ne.value), np.int32)
+    chunks = np.zeros(nc.value + 1, np.int32)
+    _check(lib.dspmv_sell_layout_host(rowptr.ctypes.data, nr, vthr, window, base.ctypes.data, lane_row.ctypes.data,
+                                      lane_len.ctypes.data, src.ctypes.data, chunks.ctypes.data,
+                                      ctypes.byref(ns), ctypes.byref(ne), ctypes.byref(nc)))
+    n = ns.value
+    return dict(base=base, lane_row=lane_row[:32 * n].reshape(n, 32), lane_len=lane_len[:32 * n].reshape(n, 32),
+                entry_src=src[:ne.value], chunks=chunks)
 
 
 def dspmv_schedule_validate(ops, n_streams: int):

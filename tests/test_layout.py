@@ -121,3 +121,46 @@ def test_stream_kernel_auto_choice_host():
     lens = np.diff(pl).astype(float)
     lens = lens[lens <= 256]
     assert lens.std() > 0.5 * lens.mean()   # the criterion, computed independently
+
+
+@pytest.mark.parametrize("name", ["pl", "7pt", "27pt"])
+@pytest.mark.parametrize("window", [-1, 32, 96, 4096])
+def test_sell_layout_invariants(name, window):
+    """Sliced form (DSPMV_SKERNEL_SELL, K1d): every S row (<= 256
+    nnz) sits in exactly one lane; within a sort window rows are longest
+    first; the lanes active at entry k are a prefix 0..m_k-1 and entry k of
+    the slice is stored as their m_k consecutive values, each lane's entries
+    in its row's CSR order; the stored entries are a permutation of the S
+    group's; the work chunks cover the slices in order."""
+    rp = MATS[name]()
+    lens = np.diff(rp)
+    s_rows = np.nonzero(lens <= 256)[0]
+    L = D.dspmv_sell_layout_host(rp, window=window)
+    base, row, ln, src, ch = L["base"], L["lane_row"], L["lane_len"], L["entry_src"], L["chunks"]
+    ns = len(base) - 1
+    sl = lens[s_rows]
+    s_start = np.concatenate([[0], np.cumsum(sl)])
+    assert sorted(row[row >= 0].tolist()) == list(range(len(s_rows)))
+    assert np.array_equal(ln[row >= 0], sl[row[row >= 0]]) and np.all(ln[row < 0] == 0)
+    assert np.all(np.diff(ln, axis=1) <= 0)                     # longest first within a slice
+    assert base[0] == 0 and base[-1] == len(src) == sl.sum()
+    assert np.array_equal(np.sort(src), np.arange(len(src)))    # a permutation of the S entries
+    w = 256 if window == -1 else window
+    for s in range(ns):
+        q = base[s]
+        for k in range(int(ln[s, 0])):
+            act = ln[s] > k
+            m = int(act.sum())
+            assert np.all(act[:m]) and not np.any(act[m:])
+            want = s_start[row[s, :m]] + k                      # entry k of each active lane's row
+            assert np.array_equal(src[q:q + m], want)
+            q += m
+        assert q == base[s + 1]
+    # window order: the S rows of window j are exactly S rows [j*w, (j+1)*w)
+    win_of_slice = []
+    for s in range(ns):
+        r = row[s][row[s] >= 0]
+        assert len(set((r // w).tolist())) == 1
+        win_of_slice.append(int(r[0] // w))
+    assert win_of_slice == sorted(win_of_slice)
+    assert ch[0] == 0 and ch[-1] == ns and np.all(np.diff(ch) > 0)
