@@ -143,6 +143,8 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
         if (L.s_has_slot) ST_TRY(dev_upload(p, &D.s_slot, L.s_slot.data(), L.s_slot.size()));
         if (!L.s_identity) ST_TRY(dev_upload(p, &D.s_out, L.s_out.data(), L.s_out.size()));
         D.cfg = cfg;
+        if (const char* ev = std::getenv("DSPMV_L2PF")) D.l2pf = std::max(0, std::atoi(ev));   // sweeps
+        if (const char* ev = std::getenv("DSPMV_ST_L2PF")) D.st_l2pf = std::max(0, std::atoi(ev));   // sweeps
         const int per_sm = block_kernel_ctas_per_sm(p.dtype, cfg);
         // optionally leave SMs free for concurrent NCCL / pack kernels
         const int reserve = p.opts.reserve_sms >= 0 ? p.opts.reserve_sms : (p.comm->nranks > 1 ? kAutoReserveSms : 0);
@@ -160,6 +162,7 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
             ST_TRY(dev_upload(p, &D.sl_col, L.sl_col.data(), L.sl_col.size()));
             ST_TRY(dev_upload(p, reinterpret_cast<uint8_t**>(&D.sl_val), L.sl_val.data(), L.sl_val.size()));
             D.sell_unroll = sell_unroll();
+            if (const char* ev = std::getenv("DSPMV_SELL_L1")) D.sell_l1 = std::atoi(ev) != 0;
             set_x_persist_limit();
             int spsm = sell_kernel_ctas_per_sm(p.dtype, D.sell_unroll);
             if (const char* ev = std::getenv("DSPMV_SELL_CTAS")) spsm = std::max(1, std::min(spsm, std::atoi(ev)));  // sweeps

@@ -119,6 +119,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// 1-D bulk prefetch global -> L2 (no shared memory, no completion)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -240,6 +245,7 @@ struct BlockArgs {
     const int32_t* out;
     const int32_t* slot;
     int32_t b0, nb;     // row blocks [b0, nb)
+    int32_t l2pf;       // > 0: the producer also prefetches block b + l2pf*grid into L2
 };
 
 struct VecArgs {
@@ -403,6 +409,17 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
                     bulk_g2s(S.col, a.col + a0, bc, &full[s], pol);
                 }
                 bulk_g2s(S.rp, a.rowptr + ra0, br, &full[s], pol);
+                if (a.l2pf > 0) {   // a later block of this CTA: HBM -> L2 now, so its TMA load hits L2
+                    const int bn = b + a.l2pf * int(gridDim.x);
+                    if (bn < a.nb) {
+                        const int4 e0 = __ldg(reinterpret_cast<const int4*>(a.desc + size_t(bn) * kDescInts));
+                        const int32_t c0 = e0.z & ~3, c1 = (e0.w + 3) & ~3;
+                        if (c1 > c0) {
+                            bulk_prefetch_l2(static_cast<const T*>(a.val) + c0, uint32_t(c1 - c0) * sizeof(T));
+                            bulk_prefetch_l2(a.col + c0, uint32_t(c1 - c0) * 4u);
+                        }
+                    }
+                }
 #ifdef DSPMV_PROFILE
                 PROF_ADD(1, ti);
                 PROF_INC(4, 1);
@@ -516,6 +533,7 @@ struct StreamArgs {
     const int32_t* tiles;   // [r0, r1) per tile, S-row indices
     int32_t ntiles;
     VecArgs v;              // rows > vector_threshold (nV = 0: none / launched apart)
+    int32_t l2pf;           // > 0: lane 0 prefetches tile t + l2pf*warps into L2
 };
 
 // CSR-stream (irregular row lengths).  Lane l of a warp takes entries
@@ -546,6 +564,17 @@ __global__ void __launch_bounds__(kStreamCtaWarps * 32) spmv_stream_kernel(Strea
     for (int t = blockIdx.x * kStreamCtaWarps + w; t < a.ntiles; t += gridDim.x * kStreamCtaWarps) {
         const int2 tr = __ldg(reinterpret_cast<const int2*>(a.tiles) + t);
         const int32_t p0 = __ldg(a.rowptr + tr.x), m = __ldg(a.rowptr + tr.y) - p0;
+        if (a.l2pf > 0 && lane == 0) {   // a later tile of this warp: HBM -> L2 while this one gathers
+            const int tn = t + a.l2pf * gridDim.x * kStreamCtaWarps;
+            if (tn < a.ntiles) {
+                const int2 trn = __ldg(reinterpret_cast<const int2*>(a.tiles) + tn);
+                const int32_t c0 = __ldg(a.rowptr + trn.x) & ~3, c1 = (__ldg(a.rowptr + trn.y) + 3) & ~3;
+                if (c1 > c0) {
+                    bulk_prefetch_l2(val + c0, uint32_t(c1 - c0) * sizeof(T));
+                    bulk_prefetch_l2(a.col + c0, uint32_t(c1 - c0) * 4u);
+                }
+            }
+        }
         int32_t c[kStreamTile / 32];
         T v[kStreamTile / 32], xv[kStreamTile / 32];
 #pragma unroll
@@ -626,12 +655,13 @@ struct SellArgs {
     const int32_t* slot;
     int32_t nchunks;
     VecArgs v;             // rows > vector_threshold (nV = 0: none / launched apart)
+    int32_t l2pf;          // > 0: lane 0 prefetches chunk c + l2pf*warps into L2
 };
 
-template <typename T, bool kCombine, bool kIdentity, int U>
 #ifndef DSPMV_SELL_MINB
 #define DSPMV_SELL_MINB 1   // diagnostic builds: CTAs/SM the register budget must allow
 #endif
+template <typename T, bool kCombine, bool kIdentity, int U, bool kNoL1 = true>
 __global__ void __launch_bounds__(kSellCtaWarps * 32, DSPMV_SELL_MINB) spmv_sell_kernel(SellArgs a, SpmvOperands o) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const T* __restrict__ val = static_cast<const T*>(a.val);
@@ -649,6 +679,17 @@ __global__ void __launch_bounds__(kSellCtaWarps * 32, DSPMV_SELL_MINB) spmv_sell
     for (int c = gw; c < a.nchunks; c += nw) {
         int s = __ldg(a.chunk + c);
         const int se = __ldg(a.chunk + c + 1);
+        if (a.l2pf > 0 && lane == 0) {   // a later chunk of this warp: HBM -> L2 while this one gathers
+            const int cn = c + a.l2pf * nw;
+            if (cn < a.nchunks) {
+                const int32_t e0 = __ldg(a.base + __ldg(a.chunk + cn)) & ~3;
+                const int32_t e1 = (__ldg(a.base + __ldg(a.chunk + cn + 1)) + 3) & ~3;
+                if (e1 > e0) {
+                    bulk_prefetch_l2(val + e0, uint32_t(e1 - e0) * sizeof(T));
+                    bulk_prefetch_l2(a.col + e0, uint32_t(e1 - e0) * 4u);
+                }
+            }
+        }
         int32_t sr = __ldg(a.srow + 32 * s + lane);
         int len = __ldg(a.len + 32 * s + lane);
         int32_t off = __ldg(a.base + s);
@@ -673,7 +714,7 @@ __global__ void __launch_bounds__(kSellCtaWarps * 32, DSPMV_SELL_MINB) spmv_sell
                     v[u] = act ? __ldcs(val + q) : T(0);
                 }
 #pragma unroll
-                for (int u = 0; u < U; ++u) xv[u] = k0 + u < len ? ldg_x<true>(x + cc[u], xpol) : T(0);
+                for (int u = 0; u < U; ++u) xv[u] = k0 + u < len ? ldg_x<kNoL1>(x + cc[u], xpol) : T(0);
 #pragma unroll
                 for (int u = 0; u < U; ++u)
                     if (k0 + u < len) acc = add_rn(acc, mul_rn(v[u], xv[u]));
@@ -1048,7 +1089,7 @@ cudaError_t prep_block_kernel() {
 
 template <typename T, int CFG, bool C, bool I>
 cudaError_t launch_block(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, int32_t b0, int32_t b1) {
-    BlockArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_desc, L.s_out, L.s_slot, b0, b1};
+    BlockArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_desc, L.s_out, L.s_slot, b0, b1, L.l2pf};
     const int grid = std::min(L.grid_s, b1 - b0);
     cudaError_t e;
     if (o.xflag) {   // x streamed in: the coherent-load instantiation
@@ -1114,7 +1155,7 @@ void x_window(cudaLaunchAttribute& at, const void* x, int64_t bytes) {
 template <typename T>
 cudaError_t launch_stream(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, bool vec) {
     StreamArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_out, L.s_slot, L.s_tiles, L.ntiles,
-                 VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}};
+                 VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}, L.st_l2pf};
     const bool c = L.s_slot != nullptr, id = L.s_out == nullptr;
     const dim3 grid(L.grid_t), block(kStreamCtaWarps * 32);
     if (x_persist_fraction() > 0 && L.x_bytes > 0) {
@@ -1142,10 +1183,10 @@ cudaError_t launch_stream(const DevLayout& L, const SpmvOperands& o, cudaStream_
     return cudaGetLastError();
 }
 
-template <typename T, int U>
+template <typename T, int U, bool kNoL1>
 cudaError_t launch_sell_u(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, bool vec) {
     SellArgs a{L.sl_chunk, L.sl_base, L.sl_srow, L.sl_len, L.sl_col, L.sl_val, L.s_out, L.s_slot, L.nchunks,
-               VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}};
+               VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}, L.st_l2pf};
     const bool c = L.s_slot != nullptr, id = L.s_out == nullptr;
     const dim3 grid(L.grid_sl), block(kSellCtaWarps * 32);
     if (x_persist_fraction() > 0 && L.x_bytes > 0) {   // experiment DSPMV_X_PERSIST
@@ -1158,27 +1199,34 @@ cudaError_t launch_sell_u(const DevLayout& L, const SpmvOperands& o, cudaStream_
         cfg.attrs = at;
         cfg.numAttrs = 1;
         cudaError_t e;
-        if (c && id) e = cudaLaunchKernelEx(&cfg, spmv_sell_kernel<T, true, true, U>, a, o);
-        else if (c) e = cudaLaunchKernelEx(&cfg, spmv_sell_kernel<T, true, false, U>, a, o);
-        else if (id) e = cudaLaunchKernelEx(&cfg, spmv_sell_kernel<T, false, true, U>, a, o);
-        else e = cudaLaunchKernelEx(&cfg, spmv_sell_kernel<T, false, false, U>, a, o);
+        if (c && id) e = cudaLaunchKernelEx(&cfg, spmv_sell_kernel<T, true, true, U, kNoL1>, a, o);
+        else if (c) e = cudaLaunchKernelEx(&cfg, spmv_sell_kernel<T, true, false, U, kNoL1>, a, o);
+        else if (id) e = cudaLaunchKernelEx(&cfg, spmv_sell_kernel<T, false, true, U, kNoL1>, a, o);
+        else e = cudaLaunchKernelEx(&cfg, spmv_sell_kernel<T, false, false, U, kNoL1>, a, o);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return e != cudaSuccess ? e : cudaGetLastError();
     }
-    if (c && id) spmv_sell_kernel<T, true, true, U><<<grid, block, 0, s>>>(a, o);
-    else if (c) spmv_sell_kernel<T, true, false, U><<<grid, block, 0, s>>>(a, o);
-    else if (id) spmv_sell_kernel<T, false, true, U><<<grid, block, 0, s>>>(a, o);
-    else spmv_sell_kernel<T, false, false, U><<<grid, block, 0, s>>>(a, o);
+    if (c && id) spmv_sell_kernel<T, true, true, U, kNoL1><<<grid, block, 0, s>>>(a, o);
+    else if (c) spmv_sell_kernel<T, true, false, U, kNoL1><<<grid, block, 0, s>>>(a, o);
+    else if (id) spmv_sell_kernel<T, false, true, U, kNoL1><<<grid, block, 0, s>>>(a, o);
+    else spmv_sell_kernel<T, false, false, U, kNoL1><<<grid, block, 0, s>>>(a, o);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_sell(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, bool vec) {
+    if (L.sell_l1) {   // uniform (banded) rows: neighbouring rows share x lines in L1
+        switch (L.sell_unroll) {
+            case 4: return launch_sell_u<T, 4, false>(L, o, s, vec);
+            case 16: return launch_sell_u<T, 16, false>(L, o, s, vec);
+            default: return launch_sell_u<T, 8, false>(L, o, s, vec);
+        }
+    }
     switch (L.sell_unroll) {
-        case 4: return launch_sell_u<T, 4>(L, o, s, vec);
-        case 16: return launch_sell_u<T, 16>(L, o, s, vec);
-        default: return launch_sell_u<T, 8>(L, o, s, vec);
+        case 4: return launch_sell_u<T, 4, true>(L, o, s, vec);
+        case 16: return launch_sell_u<T, 16, true>(L, o, s, vec);
+        default: return launch_sell_u<T, 8, true>(L, o, s, vec);
     }
 }
 

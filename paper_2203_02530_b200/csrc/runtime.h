@@ -22,6 +22,8 @@ struct DevLayout {
     int32_t nS = 0, nb = 0, nV = 0;
     int grid_s = 0, grid_v = 0;
     int cfg = 0;                       // kBlockCfgs index of the row-block kernel
+    int l2pf = kBlockL2Prefetch;       // row-block producer's L2 prefetch distance (blocks of this CTA)
+    int st_l2pf = 0;                   // CSR-stream / sliced kernels: L2 prefetch distance (tiles / chunks)
     bool combine = false;              // any row of this matrix needs the ticket combine
     int32_t* s_rowptr = nullptr;
     int32_t* s_col = nullptr;
@@ -50,6 +52,7 @@ struct DevLayout {
     int32_t nslices = 0;
     int grid_sl = 0;
     int sell_unroll = 8;
+    bool sell_l1 = false;              // x gathers allocate in L1 (DSPMV_SELL_L1, sweeps)
     int32_t nchunks = 0;
     int32_t* sl_chunk = nullptr;
     int32_t* sl_base = nullptr;

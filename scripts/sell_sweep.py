@@ -36,7 +36,7 @@ comm = D.dspmv_comm_create(D.dspmv_comm_unique_id(), 1, 0, 0)
 stream = torch.cuda.Stream()
 ref = None
 for c in a.cfgs.split(","):
-    parts = c.split(":")   # sell:window:unroll[:vector_threshold[:chunk_cost[:ctas_per_sm]]]
+    parts = c.split(":")   # sell:window:unroll[:vector_threshold[:chunk_cost[:ctas_per_sm[:x_in_L1]]]]
     vthr = -1
     if parts[0] == "sell":
         os.environ["DSPMV_SELL_WINDOW"] = parts[1]
@@ -47,7 +47,12 @@ for c in a.cfgs.split(","):
             os.environ["DSPMV_SELL_CHUNK"] = parts[4]
         if len(parts) > 5:
             os.environ["DSPMV_SELL_CTAS"] = parts[5]
+        if len(parts) > 6:
+            os.environ["DSPMV_SELL_L1"] = parts[6]
         sk = D.DSPMV_SKERNEL_SELL
+    elif parts[0] == "auto":   # auto[:l2_prefetch_distance]
+        sk = D.DSPMV_SKERNEL_AUTO
+        os.environ["DSPMV_L2PF"] = parts[1] if len(parts) > 1 else "0"
     else:
         sk = D.DSPMV_SKERNEL_STREAM
     t1 = time.time()
@@ -57,6 +62,7 @@ for c in a.cfgs.split(","):
     sched = D.dspmv_schedule_create(plan, derive_ops(), 2)
     D.dspmv_schedule_set_caller_stream0(sched, 1)
     y = torch.empty(n, dtype=torch.float64, device="cuda")
+    gbytes = (12 * int(rp[-1]) + 4 * (n + 1) + 16 * n) / 1e9   # SURVEY 8(d) algorithmic bytes
     ts = []
     with torch.cuda.stream(stream):
         for i in range(a.reps + 3):
@@ -77,7 +83,7 @@ for c in a.cfgs.split(","):
     ms = float(np.median(ts))
     nnz = int(rp[-1])
     print(f"{c:16s} kernel={info['s_kernel_local']} yL_ms {ms:.4f} min {min(ts):.4f} "
-          f"G_gathers/s {nnz / ms / 1e6:.1f} plan_s {tp:.1f} bitwise_eq_first {same} maxrel {rel:.1e}", flush=True)
+          f"G_gathers/s {nnz / ms / 1e6:.1f} TB/s {gbytes / ms:.3f} plan_s {tp:.1f} bitwise_eq_first {same} maxrel {rel:.1e}", flush=True)
     D.dspmv_schedule_destroy(sched)
     D.dspmv_plan_destroy(plan)
 D.dspmv_comm_destroy(comm)
