@@ -38,6 +38,7 @@ ref = None
 for c in a.cfgs.split(","):
     parts = c.split(":")   # sell:window:unroll[:vector_threshold[:chunk_cost[:ctas_per_sm[:x_in_L1]]]]
     vthr = -1
+    bcfg = -1
     if parts[0] == "sell":
         os.environ["DSPMV_SELL_WINDOW"] = parts[1]
         os.environ["DSPMV_SELL_UNROLL"] = parts[2]
@@ -50,13 +51,16 @@ for c in a.cfgs.split(","):
         if len(parts) > 6:
             os.environ["DSPMV_SELL_L1"] = parts[6]
         sk = D.DSPMV_SKERNEL_SELL
-    elif parts[0] == "auto":   # auto[:l2_prefetch_distance]
+    elif parts[0] in ("auto", "cfg"):   # auto[:l2_prefetch_distance] / cfg:block_cfg[:l2_prefetch_distance]
         sk = D.DSPMV_SKERNEL_AUTO
-        os.environ["DSPMV_L2PF"] = parts[1] if len(parts) > 1 else "0"
+        if parts[0] == "cfg":
+            bcfg = int(parts[1])
+            parts = parts[1:]
+        os.environ["DSPMV_L2PF"] = parts[1] if len(parts) > 1 else "1"
     else:
         sk = D.DSPMV_SKERNEL_STREAM
     t1 = time.time()
-    plan = D.dspmv_plan_create(comm, n, rp, col, val, s_kernel=sk, vector_threshold=vthr)
+    plan = D.dspmv_plan_create(comm, n, rp, col, val, s_kernel=sk, vector_threshold=vthr, block_cfg=bcfg)
     tp = time.time() - t1
     info = D.dspmv_plan_info_get(plan)
     sched = D.dspmv_schedule_create(plan, derive_ops(), 2)
