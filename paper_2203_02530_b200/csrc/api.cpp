@@ -143,8 +143,8 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
         if (L.s_has_slot) ST_TRY(dev_upload(p, &D.s_slot, L.s_slot.data(), L.s_slot.size()));
         if (!L.s_identity) ST_TRY(dev_upload(p, &D.s_out, L.s_out.data(), L.s_out.size()));
         D.cfg = cfg;
-        if (const char* ev = std::getenv("DSPMV_L2PF")) D.l2pf = std::max(0, std::atoi(ev));   // sweeps
-        if (const char* ev = std::getenv("DSPMV_ST_L2PF")) D.st_l2pf = std::max(0, std::atoi(ev));   // sweeps
+        if (const char* ev = std::getenv("DSPMV_L2PF")) D.l2pf = std::atoi(ev);   // sweeps (< 0: evict_first hint)
+        if (const char* ev = std::getenv("DSPMV_ST_L2PF")) D.st_l2pf = std::atoi(ev);   // sweeps (< 0: col only)
         const int per_sm = block_kernel_ctas_per_sm(p.dtype, cfg);
         // optionally leave SMs free for concurrent NCCL / pack kernels
         const int reserve = p.opts.reserve_sms >= 0 ? p.opts.reserve_sms : (p.comm->nranks > 1 ? kAutoReserveSms : 0);

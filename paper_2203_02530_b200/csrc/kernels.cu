@@ -123,6 +123,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes, uint64_t pol) {
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src), "r"(bytes), "l"(pol)
+                 : "memory");
+}
 
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
     unsigned v;
@@ -409,14 +413,17 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
                     bulk_g2s(S.col, a.col + a0, bc, &full[s], pol);
                 }
                 bulk_g2s(S.rp, a.rowptr + ra0, br, &full[s], pol);
-                if (a.l2pf > 0) {   // a later block of this CTA: HBM -> L2 now, so its TMA load hits L2
-                    const int bn = b + a.l2pf * int(gridDim.x);
+                if (a.l2pf != 0) {   // a later block of this CTA: HBM -> L2 now, so its TMA load hits L2
+                    const int bn = b + (a.l2pf > 0 ? a.l2pf : -a.l2pf) * int(gridDim.x);
                     if (bn < a.nb) {
                         const int4 e0 = __ldg(reinterpret_cast<const int4*>(a.desc + size_t(bn) * kDescInts));
                         const int32_t c0 = e0.z & ~3, c1 = (e0.w + 3) & ~3;
-                        if (c1 > c0) {
+                        if (c1 > c0 && a.l2pf > 0) {
                             bulk_prefetch_l2(static_cast<const T*>(a.val) + c0, uint32_t(c1 - c0) * sizeof(T));
                             bulk_prefetch_l2(a.col + c0, uint32_t(c1 - c0) * 4u);
+                        } else if (c1 > c0) {   // l2pf < 0 (sweeps): with the evict_first policy
+                            bulk_prefetch_l2(static_cast<const T*>(a.val) + c0, uint32_t(c1 - c0) * sizeof(T), pol);
+                            bulk_prefetch_l2(a.col + c0, uint32_t(c1 - c0) * 4u, pol);
                         }
                     }
                 }
@@ -564,14 +571,15 @@ __global__ void __launch_bounds__(kStreamCtaWarps * 32) spmv_stream_kernel(Strea
     for (int t = blockIdx.x * kStreamCtaWarps + w; t < a.ntiles; t += gridDim.x * kStreamCtaWarps) {
         const int2 tr = __ldg(reinterpret_cast<const int2*>(a.tiles) + t);
         const int32_t p0 = __ldg(a.rowptr + tr.x), m = __ldg(a.rowptr + tr.y) - p0;
-        if (a.l2pf > 0 && lane == 0) {   // a later tile of this warp: HBM -> L2 while this one gathers
-            const int tn = t + a.l2pf * gridDim.x * kStreamCtaWarps;
+        if (a.l2pf != 0 && lane == 0) {   // a later tile of this warp: HBM -> L2 (evict_first) while this one gathers
+            const int tn = t + (a.l2pf > 0 ? a.l2pf : -a.l2pf) * gridDim.x * kStreamCtaWarps;
             if (tn < a.ntiles) {
                 const int2 trn = __ldg(reinterpret_cast<const int2*>(a.tiles) + tn);
                 const int32_t c0 = __ldg(a.rowptr + trn.x) & ~3, c1 = (__ldg(a.rowptr + trn.y) + 3) & ~3;
                 if (c1 > c0) {
-                    bulk_prefetch_l2(val + c0, uint32_t(c1 - c0) * sizeof(T));
-                    bulk_prefetch_l2(a.col + c0, uint32_t(c1 - c0) * 4u);
+                    const uint64_t pf = policy_evict_first();
+                    if (a.l2pf > 0) bulk_prefetch_l2(val + c0, uint32_t(c1 - c0) * sizeof(T), pf);
+                    bulk_prefetch_l2(a.col + c0, uint32_t(c1 - c0) * 4u, pf);   // l2pf < 0: col only
                 }
             }
         }
@@ -679,14 +687,15 @@ __global__ void __launch_bounds__(kSellCtaWarps * 32, DSPMV_SELL_MINB) spmv_sell
     for (int c = gw; c < a.nchunks; c += nw) {
         int s = __ldg(a.chunk + c);
         const int se = __ldg(a.chunk + c + 1);
-        if (a.l2pf > 0 && lane == 0) {   // a later chunk of this warp: HBM -> L2 while this one gathers
-            const int cn = c + a.l2pf * nw;
+        if (a.l2pf != 0 && lane == 0) {   // a later chunk of this warp: HBM -> L2 (evict_first) while this one gathers
+            const int cn = c + (a.l2pf > 0 ? a.l2pf : -a.l2pf) * nw;
             if (cn < a.nchunks) {
                 const int32_t e0 = __ldg(a.base + __ldg(a.chunk + cn)) & ~3;
                 const int32_t e1 = (__ldg(a.base + __ldg(a.chunk + cn + 1)) + 3) & ~3;
                 if (e1 > e0) {
-                    bulk_prefetch_l2(val + e0, uint32_t(e1 - e0) * sizeof(T));
-                    bulk_prefetch_l2(a.col + e0, uint32_t(e1 - e0) * 4u);
+                    const uint64_t pf = policy_evict_first();
+                    if (a.l2pf > 0) bulk_prefetch_l2(val + e0, uint32_t(e1 - e0) * sizeof(T), pf);
+                    bulk_prefetch_l2(a.col + e0, uint32_t(e1 - e0) * 4u, pf);   // l2pf < 0: col only
                 }
             }
         }
