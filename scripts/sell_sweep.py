@@ -23,6 +23,7 @@ from tests.gpu_helpers import derive_ops  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=30)
 ap.add_argument("--workload", default="c4")
+ap.add_argument("--flush", type=int, default=1, help="flush L2 before each apply (0: back-to-back applies)")
 ap.add_argument("--cfgs", default="stream,sell:256:8:256:4096,sell:1024:8:256:4096,sell:4096:8:256:4096,"
                 "sell:256:8:64:4096,sell:1024:8:64:4096,sell:1024:8:128:4096,sell:1024:8:32:4096,"
                 "sell:1024:4:64:4096,sell:1024:16:64:4096,sell:1024:8:64:16384,sell:1024:8:64:1024,stream")
@@ -70,7 +71,8 @@ for c in a.cfgs.split(","):
     ts = []
     with torch.cuda.stream(stream):
         for i in range(a.reps + 3):
-            D.dspmv_l2_flush(0, stream.cuda_stream)
+            if a.flush:
+                D.dspmv_l2_flush(0, stream.cuda_stream)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             D.dspmv_apply_graph(sched, x, y, stream.cuda_stream)
