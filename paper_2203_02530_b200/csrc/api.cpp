@@ -1963,10 +1963,8 @@ dspmv_status dspmv_sell_layout_host(const int64_t* rowptr, int32_t nrows, int vt
     for (size_t q = 0; q < col.size(); ++q) col[q] = int32_t(q);
     for (int32_t i = 0; i < nrows; ++i) ident[i] = i;
     Layout L;
-    g_sell_window_override = window > 0 ? std::max(32, window - window % 32) : 0;
     build_layout(rp.data(), nrows, col.data(), nullptr, 8, ident.data(), nullptr, vthr,
-                 kBlockCfgs[kDefaultBlockCfg], L, true, true);
-    g_sell_window_override = 0;
+                 kBlockCfgs[kDefaultBlockCfg], L, true, true, window > 0 ? window : 0);
     const int32_t ns = int32_t(L.sl_base.size()) - 1, nc = int32_t(L.sl_chunk.size()) - 1;
     const int64_t ne = L.sl_base.back();
     const bool fit = !slice_base || (*n_slices >= ns && *n_entries >= ne && *n_chunks >= nc);

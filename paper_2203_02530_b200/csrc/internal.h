@@ -149,9 +149,8 @@ int auto_block_cfg(const int32_t* rowptr, int32_t nrows, int vthr, int esize);
 bool auto_stream(const int32_t* rowptr, int32_t nrows, int vthr);
 void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, const uint8_t* val,
                   int esize, const int32_t* out_row, const int32_t* slot, int vthr,
-                  const BlockCfg& cfg, Layout& L, bool stream = false, bool sell = false);
-int sell_window();   // kSellWindow, or DSPMV_SELL_WINDOW (sweeps)
-extern int g_sell_window_override;   // > 0: sell_window() (host test hook only)
+                  const BlockCfg& cfg, Layout& L, bool stream = false, bool sell = false, int sell_win = 0);
+int sell_window();   // kSellWindow, or DSPMV_SELL_WINDOW (sweeps); sell_win > 0 overrides
 int sell_chunk_cost();   // kSellChunkCost, or DSPMV_SELL_CHUNK (sweeps)
 
 // -------------------------------------------------------------- schedules

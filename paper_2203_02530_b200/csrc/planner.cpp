@@ -169,10 +169,7 @@ int auto_block_cfg(const int32_t* rowptr, int32_t nrows, int vthr, int esize) {
     return esize == 4 ? kShortRowBlockCfgF32 : kDefaultBlockCfg;
 }
 
-int g_sell_window_override = 0;   // dspmv_sell_layout_host (host tests)
-
 int sell_window() {   // read at every plan creation (sweeps change it between plans)
-    if (g_sell_window_override > 0) return g_sell_window_override;
     const char* ev = std::getenv("DSPMV_SELL_WINDOW");
     const int v = ev ? std::atoi(ev) : kSellWindow;
     return std::max(32, v - v % 32);
@@ -189,8 +186,8 @@ int sell_chunk_cost() {   // read at every plan creation (sweeps)
 // slice still longer than k is stored at sl_base[s] + (entries of the slice
 // before k) + lane, so the m_k lanes active at k read m_k consecutive values.
 // Each row's own entries keep their CSR order (the serial loop's).
-static void build_sell(Layout& L, int esize) {
-    const int32_t nS = L.nS, W = sell_window();
+static void build_sell(Layout& L, int esize, int window) {
+    const int32_t nS = L.nS, W = window > 0 ? std::max(32, window - window % 32) : sell_window();
     const int64_t ns = (int64_t(nS) + 31) / 32 + (nS ? (nS / W + 1) : 0);  // upper bound (partial slices per window)
     L.sl_base.clear();
     L.sl_srow.clear();
@@ -259,7 +256,7 @@ bool auto_stream(const int32_t* rowptr, int32_t nrows, int vthr) {
 
 void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, const uint8_t* val,
                   int esize, const int32_t* out_row, const int32_t* slot, int vthr,
-                  const BlockCfg& cfg, Layout& L, bool stream, bool sell) {
+                  const BlockCfg& cfg, Layout& L, bool stream, bool sell, int sell_win) {
     L = Layout();
     L.nrows = nrows;
     L.stream = stream || sell;
@@ -364,7 +361,7 @@ void build_layout(const int32_t* rowptr, int32_t nrows, const int32_t* col, cons
         L.s_desc.insert(L.s_desc.end(), d, d + kDescInts);
     }
     L.nb = int32_t(L.s_desc.size() / kDescInts);
-    if (sell) build_sell(L, esize);
+    if (sell) build_sell(L, esize, sell_win);
     if (stream) {
         // CSR-stream tiles: greedy runs of rows with <= kStreamTile nnz and
         // <= kStreamRows rows (every S row has <= vthr <= kStreamTile nnz)
