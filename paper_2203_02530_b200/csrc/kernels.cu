@@ -667,7 +667,7 @@ struct SellArgs {
 };
 
 #ifndef DSPMV_SELL_MINB
-#define DSPMV_SELL_MINB 1   // diagnostic builds: CTAs/SM the register budget must allow
+#define DSPMV_SELL_MINB 6   // 48 resident warps at 40 registers (measured best, profiles/r2_c4_sell.txt)
 #endif
 template <typename T, bool kCombine, bool kIdentity, int U, bool kNoL1 = true>
 __global__ void __launch_bounds__(kSellCtaWarps * 32, DSPMV_SELL_MINB) spmv_sell_kernel(SellArgs a, SpmvOperands o) {
