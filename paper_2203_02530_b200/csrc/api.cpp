@@ -172,6 +172,10 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
             set_x_persist_limit();
             D.ntiles = int32_t(L.s_tiles.size() / 2);
             ST_TRY(dev_upload(p, &D.s_tiles, L.s_tiles.data(), L.s_tiles.size()));
+            D.st_dynamic = kStreamDynamic;
+            if (const char* ev = std::getenv("DSPMV_ST_DYNAMIC")) D.st_dynamic = std::atoi(ev) != 0;   // A/B
+            if (const char* ev = std::getenv("DSPMV_ST_GRAB")) D.st_grab = std::max(1, std::atoi(ev));   // sweeps
+            if (D.st_dynamic) ST_TRY(dev_alloc(p, reinterpret_cast<void**>(&D.d_work), 2 * sizeof(unsigned), true));
             int tpsm = stream_kernel_ctas_per_sm(p.dtype);
             if (const char* ev = std::getenv("DSPMV_STREAM_CTAS")) tpsm = std::max(1, std::min(tpsm, std::atoi(ev)));  // sweeps
             D.grid_t = std::max(1, std::min((D.ntiles + kStreamCtaWarps - 1) / kStreamCtaWarps, tpsm * usable));

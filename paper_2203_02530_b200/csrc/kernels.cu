@@ -541,6 +541,8 @@ struct StreamArgs {
     int32_t ntiles;
     VecArgs v;              // rows > vector_threshold (nV = 0: none / launched apart)
     int32_t l2pf;           // > 0: lane 0 prefetches tile t + l2pf*warps into L2
+    unsigned* work;         // non-null: tiles handed out in batches from work[0] (work[1]: warps done)
+    int32_t grab;           // tiles per batch
 };
 
 // CSR-stream (irregular row lengths).  Lane l of a warp takes entries
@@ -568,7 +570,13 @@ __global__ void __launch_bounds__(kStreamCtaWarps * 32) spmv_stream_kernel(Strea
 #if defined(DSPMV_K1B_EF)
     const uint64_t mpol = policy_evict_first();
 #endif
-    for (int t = blockIdx.x * kStreamCtaWarps + w; t < a.ntiles; t += gridDim.x * kStreamCtaWarps) {
+    // Tiles go out in batches of a.grab: batch gw first, then (dynamic,
+    // a.work) the next free batch from an atomic counter -- fetched one batch
+    // ahead so its latency hides -- or (static) batch gw + nw, ...
+    const int gw = blockIdx.x * kStreamCtaWarps + w, nw = gridDim.x * kStreamCtaWarps;
+    int bnext = a.work && lane == 0 ? int(atomicAdd(a.work, 1u)) + nw : 0;
+    for (int bt = gw; bt * a.grab < a.ntiles;) {
+    for (int t = bt * a.grab, te = min(a.ntiles, t + a.grab); t < te; ++t) {
         const int2 tr = __ldg(reinterpret_cast<const int2*>(a.tiles) + t);
         const int32_t p0 = __ldg(a.rowptr + tr.x), m = __ldg(a.rowptr + tr.y) - p0;
         if (a.l2pf != 0 && lane == 0) {   // a later tile of this warp: HBM -> L2 (evict_first) while this one gathers
@@ -640,6 +648,23 @@ __global__ void __launch_bounds__(kStreamCtaWarps * 32) spmv_stream_kernel(Strea
             __stcs(y + orow, acc);
         }
         __syncwarp();
+    }
+        if (a.work) {
+            bt = __shfl_sync(0xffffffffu, bnext, 0);
+            if (lane == 0) bnext = int(atomicAdd(a.work, 1u)) + nw;
+        } else {
+            bt += nw;
+        }
+    }
+    if (a.work && lane == 0) {
+        // the last warp out resets the counters for the next launch (stream
+        // order publishes them); every fetch of this warp completed first
+        if (bnext < 0) __trap();
+        __threadfence();
+        if (atomicAdd(a.work + 1, 1u) == unsigned(nw) - 1u) {
+            atomicExch(a.work, 0u);
+            atomicExch(a.work + 1, 0u);
+        }
     }
 }
 
@@ -1164,7 +1189,8 @@ void x_window(cudaLaunchAttribute& at, const void* x, int64_t bytes) {
 template <typename T>
 cudaError_t launch_stream(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, bool vec) {
     StreamArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_out, L.s_slot, L.s_tiles, L.ntiles,
-                 VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}, L.st_l2pf};
+                 VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}, L.st_l2pf,
+                 L.st_dynamic ? L.d_work : nullptr, L.st_grab};
     const bool c = L.s_slot != nullptr, id = L.s_out == nullptr;
     const dim3 grid(L.grid_t), block(kStreamCtaWarps * 32);
     if (x_persist_fraction() > 0 && L.x_bytes > 0) {

@@ -24,6 +24,9 @@ struct DevLayout {
     int cfg = 0;                       // kBlockCfgs index of the row-block kernel
     int l2pf = kBlockL2Prefetch;       // row-block producer's L2 prefetch distance (blocks of this CTA)
     int st_l2pf = 0;                   // CSR-stream / sliced kernels: L2 prefetch distance (tiles / chunks)
+    bool st_dynamic = false;           // CSR-stream: tile batches from an atomic counter (d_work)
+    int st_grab = kStreamGrab;         // CSR-stream: tiles per batch
+    unsigned* d_work = nullptr;        // [2] zeroed; reset by the last warp of each launch
     bool combine = false;              // any row of this matrix needs the ticket combine
     int32_t* s_rowptr = nullptr;
     int32_t* s_col = nullptr;
