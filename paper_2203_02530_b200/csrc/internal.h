@@ -53,9 +53,9 @@ constexpr int kStreamWarps = 8;    // CSR-stream tiles per TMA-fed block (K1c)
 #ifndef DSPMV_STREAM_CTA_WARPS
 #define DSPMV_STREAM_CTA_WARPS 20
 #endif
-constexpr int kStreamCtaWarps = DSPMV_STREAM_CTA_WARPS;
-constexpr int kStreamGrab = 4;
-constexpr bool kStreamDynamic = true;   // K1b: batches from an atomic counter (C4 0.700-0.703 ms vs 0.709-0.716 static)      // K1b: tiles per work batch (static or from the atomic counter)   // K1b CTA: warps (one tile each); 20 x 2 CTAs/SM measured 1 % faster than 8 x 5 on C4
+constexpr int kStreamCtaWarps = DSPMV_STREAM_CTA_WARPS;   // K1b CTA: warps (one tile each); 20 x 2 CTAs/SM measured 1 % faster than 8 x 5 on C4
+constexpr int kStreamGrab = 8;          // K1b: consecutive tiles per work batch (4-8 measured best; 1: 0.77-0.81 ms)
+constexpr bool kStreamDynamic = true;   // K1b: batches from an atomic counter (C4 0.700-0.703 ms vs 0.709-0.716 static)
 // CSR-stream with a TMA producer (spmv_stream_tma_kernel): a block is kStreamWarps
 // consecutive tiles, staged whole (col, val, rowptr slice) by one producer warp
 constexpr int kSTBlockNnz = kStreamWarps * kStreamTile;    // 2048
