@@ -176,6 +176,14 @@ typedef struct {
                                   straight from the receive buffer (PUT: the half of
                                   this apply's parity, read from the device epoch) --
                                   SURVEY 8(d): "the unpack term 2v*h_r is 0 if fused" */
+    int32_t long_row_sum;      /* rows of more than vector_threshold nnz (a warp per
+                                  row): DSPMV_LONG_ROW_TREE (0, default): each lane
+                                  accumulates every 32nd product with a fused
+                                  multiply-add, then a shuffle tree (within the R-Q11
+                                  tolerance).  DSPMV_LONG_ROW_STORED: rounded products
+                                  added in stored order from +0 (the serial CSR loop,
+                                  P:273), so EVERY row is bitwise the oracle's; the
+                                  sum is a serial chain per row (C4: +2 %, DESIGN K2) */
     /* Device memory of the plan (matrix layouts, buffers): alloc(bytes, device,
        ctx) returns device memory on `device` or NULL (-> DSPMV_ERR_OOM);
        free(ptr, bytes, device, ctx) releases it at plan_destroy (after the
@@ -190,6 +198,7 @@ typedef struct {
 enum { DSPMV_PACK_GATHER = 0, DSPMV_PACK_ALIAS_IF_CONTIGUOUS = 1 };
 enum { DSPMV_ACC_TICKET = 0, DSPMV_ACC_EXPLICIT_IN_END = 1 };
 enum { DSPMV_UNPACK_COPY = 0, DSPMV_UNPACK_FUSED = 1 };
+enum { DSPMV_LONG_ROW_TREE = 0, DSPMV_LONG_ROW_STORED = 1 };
 
 enum { DSPMV_EXCHANGE_COPY = 0, DSPMV_EXCHANGE_PUT = 1,
        /* timing baseline only (SURVEY 8(d) overlap efficiency, T_noexch): Post/Wait

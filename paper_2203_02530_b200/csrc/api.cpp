@@ -197,6 +197,7 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
         ST_TRY(dev_upload(p, &D.v_out, L.v_out.data(), L.v_out.size()));
         if (L.v_has_slot) ST_TRY(dev_upload(p, &D.v_slot, L.v_slot.data(), L.v_slot.size()));
         D.grid_v = int(std::min<int64_t>((int64_t(L.nV) + 7) / 8, int64_t(sms) * 8));
+        D.v_ordered = p.opts.long_row_sum == DSPMV_LONG_ROW_STORED;
     }
     D.combine = L.s_has_slot || L.v_has_slot;
     return DSPMV_OK;
@@ -1560,6 +1561,8 @@ dspmv_status dspmv_plan_create(dspmv_comm_t comm, int64_t n_global, int64_t n_lo
     dspmv_plan_opts_default(&opts);
     if (opts_in) opts = *opts_in;
     if (opts.dtype != DSPMV_F64 && opts.dtype != DSPMV_F32) return fail(DSPMV_ERR_ARG, "bad dtype");
+    if (opts.long_row_sum != DSPMV_LONG_ROW_TREE && opts.long_row_sum != DSPMV_LONG_ROW_STORED)
+        return fail(DSPMV_ERR_ARG, "bad long_row_sum");
     int vthr = opts.vector_threshold < 0 ? kDefaultVectorThreshold : opts.vector_threshold;
     int cfg = opts.block_cfg;  // -1: chosen per layout (auto_block_cfg)
     if (const char* ev = std::getenv("DSPMV_BLOCK_CFG")) cfg = std::atoi(ev);  // tuning sweeps

@@ -259,6 +259,7 @@ struct VecArgs {
     const int32_t* out;
     const int32_t* slot;
     int32_t nV;
+    int32_t ordered;     // 1: products summed in stored order (bitwise O1), 0: FMA lanes + shuffle tree
 };
 
 // Deposit a partial of a combined row; the second arriver writes y (R-Q9).
@@ -483,13 +484,63 @@ __global__ void __launch_bounds__(Cfg<CFG>::kThreadsPerCta, kBlockCfgs[CFG].min_
     }
 }
 
-// Rows > vector_threshold: warp w of nw takes rows w, w + nw, ...  Each lane
-// accumulates every 32nd product with a fused multiply-add (one rounding per
-// term, __fma_rn), then a shuffle tree adds the 32 lane sums: a different
-// summation order and rounding than the oracle's loop, checked by the R-Q11
-// tolerance (DESIGN.md R-Q10).
+// Rows > vector_threshold: warp w of nw takes rows w, w + nw, ...
+// Ordered (a.ordered): lane l forms the rounded products of entries l, l+32,
+// .. (4 chunks of 32 in flight), then the warp adds them to acc in stored
+// order through shuffles -- acc = acc + p from +0, the oracle's loop,
+// so these rows are bitwise O1 too (the chain is serial: a 4,096-nnz row takes
+// tens of microseconds, which the dynamic tile hand-out of K1b absorbs).
+// Otherwise each lane accumulates every 32nd product with a fused
+// multiply-add (__fma_rn), then a shuffle tree adds the 32 lane sums: a
+// different order and rounding, checked by the R-Q11 tolerance (R-Q10).
+template <typename T, bool kCombine>
+__device__ __forceinline__ void vector_rows_ordered(const VecArgs& a, const SpmvOperands& o, int w, int nw) {
+    const int lane = threadIdx.x & 31;
+    const T* __restrict__ val = static_cast<const T*>(a.val);
+    const T* __restrict__ x = resolve_x<T>(o);
+    const uint64_t xpol = policy_evict_last();
+    for (int i = w; i < a.nV; i += nw) {
+        const int32_t p0 = __ldg(a.rowptr + i), p1 = __ldg(a.rowptr + i + 1);
+        T acc = T(0);
+        for (int32_t b = p0; b < p1; b += 128) {
+            int32_t c[4];
+            T v[4], pr[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int32_t q = b + 32 * u + lane;
+                c[u] = q < p1 ? __ldcs(a.col + q) : 0;
+                v[u] = q < p1 ? __ldcs(val + q) : T(0);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                pr[u] = b + 32 * u + lane < p1 ? mul_rn(v[u], ldg_x<true>(x + c[u], xpol)) : T(0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int m = min(32, p1 - (b + 32 * u));   // warp-uniform
+#pragma unroll 8
+                for (int k = 0; k < m; ++k) acc = add_rn(acc, __shfl_sync(0xffffffffu, pr[u], k));
+            }
+        }
+        if (lane == 0) {
+            const int32_t orow = a.out[i];
+            if (kCombine) {
+                const int32_t k = a.slot[i];
+                if (k >= 0) {
+                    combine<T>(acc, k, orow, o);
+                    continue;
+                }
+            }
+            static_cast<T*>(o.y)[orow] = acc;
+        }
+    }
+}
+
 template <typename T, bool kCombine>
 __device__ __forceinline__ void vector_rows(const VecArgs& a, const SpmvOperands& o, int w, int nw) {
+    if (a.ordered) {
+        vector_rows_ordered<T, kCombine>(a, o, w, nw);
+        return;
+    }
     const int lane = threadIdx.x & 31;
     const T* __restrict__ val = static_cast<const T*>(a.val);
     const T* __restrict__ x = resolve_x<T>(o);
@@ -1189,7 +1240,7 @@ void x_window(cudaLaunchAttribute& at, const void* x, int64_t bytes) {
 template <typename T>
 cudaError_t launch_stream(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, bool vec) {
     StreamArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_out, L.s_slot, L.s_tiles, L.ntiles,
-                 VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}, L.st_l2pf,
+                 VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0, L.v_ordered}, L.st_l2pf,
                  L.st_dynamic ? L.d_work : nullptr, L.st_grab};
     const bool c = L.s_slot != nullptr, id = L.s_out == nullptr;
     const dim3 grid(L.grid_t), block(kStreamCtaWarps * 32);
@@ -1221,7 +1272,7 @@ cudaError_t launch_stream(const DevLayout& L, const SpmvOperands& o, cudaStream_
 template <typename T, int U, bool kNoL1>
 cudaError_t launch_sell_u(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, bool vec) {
     SellArgs a{L.sl_chunk, L.sl_base, L.sl_srow, L.sl_len, L.sl_col, L.sl_val, L.s_out, L.s_slot, L.nchunks,
-               VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}, L.st_l2pf};
+               VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0, L.v_ordered}, L.st_l2pf};
     const bool c = L.s_slot != nullptr, id = L.s_out == nullptr;
     const dim3 grid(L.grid_sl), block(kSellCtaWarps * 32);
     if (x_persist_fraction() > 0 && L.x_bytes > 0) {   // experiment DSPMV_X_PERSIST
@@ -1293,7 +1344,7 @@ cudaError_t launch_stream_tma_v(const DevLayout& L, const SpmvOperands& o, cudaS
     cudaError_t e = prep_stream_tma<T, C, I, V>();
     if (e != cudaSuccess) return e;
     StreamTmaArgs a{L.s_rowptr, L.s_col, L.s_val, L.s_tdesc, L.s_out, L.s_slot, L.ntblocks,
-                    VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0}};
+                    VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0, L.v_ordered}};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(L.grid_tt);
     cfg.blockDim = dim3((kStreamWarps + 1) * 32);
@@ -1355,7 +1406,7 @@ cudaError_t launch_all(const DevLayout& L, const SpmvOperands& o, cudaStream_t s
         if (e != cudaSuccess) return e;
     }
     if (vec && L.nV > 0) {
-        VecArgs a{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, L.nV};
+        VecArgs a{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, L.nV, L.v_ordered};
         if (L.v_slot) spmv_vector_kernel<T, true><<<L.grid_v, kThreads, 0, s>>>(a, o);
         else spmv_vector_kernel<T, false><<<L.grid_v, kThreads, 0, s>>>(a, o);
         g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -39,6 +39,7 @@ struct DevLayout {
     void* v_val = nullptr;
     int32_t* v_out = nullptr;
     int32_t* v_slot = nullptr;
+    int32_t v_ordered = 0;             // V rows summed in stored order (long_row_sum STORED: bitwise O1)
     // CSR-stream S group (Layout::stream): tiles instead of TMA row blocks
     bool stream = false;
     int32_t ntiles = 0;

@@ -36,6 +36,7 @@ DSPMV_SKERNEL_AUTO, DSPMV_SKERNEL_BLOCK, DSPMV_SKERNEL_STREAM, DSPMV_SKERNEL_STR
 DSPMV_PACK_GATHER, DSPMV_PACK_ALIAS_IF_CONTIGUOUS = 0, 1
 DSPMV_ACC_TICKET, DSPMV_ACC_EXPLICIT_IN_END = 0, 1
 DSPMV_UNPACK_COPY, DSPMV_UNPACK_FUSED = 0, 1
+DSPMV_LONG_ROW_TREE, DSPMV_LONG_ROW_STORED = 0, 1
 (DSPMV_OP_START, DSPMV_OP_PACK, DSPMV_OP_SPMV_LOCAL, DSPMV_OP_POST_SEND, DSPMV_OP_POST_RECV,
  DSPMV_OP_WAIT_SEND, DSPMV_OP_WAIT_RECV, DSPMV_OP_UNPACK, DSPMV_OP_SPMV_REMOTE, DSPMV_OP_END,
  DSPMV_OP_EVENT_RECORD, DSPMV_OP_EVENT_SYNC, DSPMV_OP_STREAM_WAIT_EVENT) = range(13)
@@ -65,7 +66,7 @@ class dspmv_plan_opts(ctypes.Structure):
                 ("reserve_sms", ctypes.c_int32), ("exchange", ctypes.c_int32),
                 ("s_kernel", ctypes.c_int32), ("pack_mode", ctypes.c_int32),
                 ("accumulate_mode", ctypes.c_int32), ("debug_checks", ctypes.c_int32),
-                ("unpack_mode", ctypes.c_int32),
+                ("unpack_mode", ctypes.c_int32), ("long_row_sum", ctypes.c_int32),
                 ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", ctypes.c_void_p)]
 
 
@@ -277,7 +278,7 @@ def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_
                       exchange: int = DSPMV_EXCHANGE_COPY, s_kernel: int = DSPMV_SKERNEL_AUTO,
                       pack_mode: int = DSPMV_PACK_GATHER, accumulate_mode: int = DSPMV_ACC_TICKET,
                       debug_checks: bool | None = None, torch_alloc: bool = True,
-                      unpack_mode: int = DSPMV_UNPACK_COPY):
+                      unpack_mode: int = DSPMV_UNPACK_COPY, long_row_sum: int = DSPMV_LONG_ROW_TREE):
     """rowptr int64[n_local+1], col int32[nnz] (global ids), val float64/32.
     torch_alloc: the plan's device memory comes from torch's caching allocator
     (dspmv_plan_opts.alloc/free); False = cudaMalloc inside the library."""
@@ -300,6 +301,7 @@ def dspmv_plan_create(comm, n_global: int, rowptr, col_global, val, dtype=DSPMV_
     o.pack_mode = int(pack_mode)
     o.accumulate_mode = int(accumulate_mode)
     o.unpack_mode = int(unpack_mode)
+    o.long_row_sum = int(long_row_sum)
     if debug_checks is not None:
         o.debug_checks = int(debug_checks)
     if torch_alloc:

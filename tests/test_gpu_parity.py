@@ -618,3 +618,29 @@ def test_full_size_bench_launch_configuration(cfg):
         D.dspmv_schedule_destroy(s)
         D.dspmv_plan_destroy(plan)
         D.dspmv_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("skern", [D.DSPMV_SKERNEL_STREAM, D.DSPMV_SKERNEL_SELL, D.DSPMV_SKERNEL_BLOCK])
+@pytest.mark.parametrize("name,vthr", [("pl20k", -1), ("pl20k", 64), ("rand300", 8)])
+@pytest.mark.parametrize("P", [1, 3])
+def test_long_row_sum_stored_bitwise_every_row(name, vthr, P, skern):
+    """long_row_sum = DSPMV_LONG_ROW_STORED: the warp-per-row rows (more than
+    vector_threshold nnz, up to 4,096 on the power-law matrix) add their
+    rounded products in stored order, so y equals the oracle's O2 loops bit
+    for bit on EVERY row when the S-group kernel sums its rows in one lane
+    (CSR-stream, sliced; the row-block kernel with rows of <= 8 nnz)."""
+    n, (rp, col, val) = _mat(name)
+    if skern == D.DSPMV_SKERNEL_BLOCK and name == "pl20k":
+        pytest.skip("the row-block kernel sums rows of 9..256 nnz with several lanes (tolerance)")
+    x = gen.x_values((0, n))
+    run = LocalRun(n, rp, col, val, P, s_kernel=skern, vector_threshold=vthr,
+                   long_row_sum=D.DSPMV_LONG_ROW_STORED)
+    try:
+        y = run.apply(run.schedule(derive_ops()), x, reps=2)
+    finally:
+        run.close()
+    plans = O2.plan_all(rp, col, n, P)
+    yref = O2.simulate(plans, val, x, [(v,) for v in S.topological_orders(S.EDGES)[0]])
+    long_rows = np.diff(rp) > (256 if vthr < 0 else vthr)
+    assert long_rows.any()
+    assert np.array_equal(y.view(np.int64), yref.view(np.int64))
