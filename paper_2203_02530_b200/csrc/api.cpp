@@ -162,6 +162,9 @@ dspmv_status upload_layout(Plan& p, const Layout& L, int cfg, DevLayout& D) {
             ST_TRY(dev_upload(p, &D.sl_col, L.sl_col.data(), L.sl_col.size()));
             ST_TRY(dev_upload(p, reinterpret_cast<uint8_t**>(&D.sl_val), L.sl_val.data(), L.sl_val.size()));
             D.sell_unroll = sell_unroll();
+            D.st_dynamic = kStreamDynamic;
+            if (const char* ev = std::getenv("DSPMV_ST_DYNAMIC")) D.st_dynamic = std::atoi(ev) != 0;   // A/B
+            if (D.st_dynamic) ST_TRY(dev_alloc(p, reinterpret_cast<void**>(&D.d_work), 2 * sizeof(unsigned), true));
             if (const char* ev = std::getenv("DSPMV_SELL_L1")) D.sell_l1 = std::atoi(ev) != 0;
             set_x_persist_limit();
             int spsm = sell_kernel_ctas_per_sm(p.dtype, D.sell_unroll);

@@ -69,7 +69,7 @@ constexpr int kSTBlockRows = kStreamWarps * kStreamRows;   // 512
 // stages block b (C3 y_L 0.953 -> 0.875 ms at d = 1 or 2, C2 unchanged at 1)
 constexpr int kBlockL2Prefetch = 1;
 constexpr int kSellWindow = 256;
-constexpr int kSellChunkCost = 4096;   // work chunk: ~entries (+ overheads) per warp grab
+constexpr int kSellChunkCost = 2048;   // work chunk: ~entries (+ overheads) per warp grab (dynamic: 2048 best)
 #ifndef DSPMV_SELL_CTA_WARPS
 #define DSPMV_SELL_CTA_WARPS 8
 #endif

@@ -740,6 +740,7 @@ struct SellArgs {
     int32_t nchunks;
     VecArgs v;             // rows > vector_threshold (nV = 0: none / launched apart)
     int32_t l2pf;          // > 0: lane 0 prefetches chunk c + l2pf*warps into L2
+    unsigned* work;        // non-null: chunks handed out from work[0] (work[1]: warps done)
 };
 
 #ifndef DSPMV_SELL_MINB
@@ -760,7 +761,10 @@ __global__ void __launch_bounds__(kSellCtaWarps * 32, DSPMV_SELL_MINB) spmv_sell
     // Per chunk, slice s+1's lane metadata is loaded while slice s gathers, and
     // its output row / combine slot at the end of slice s, so neither sits on
     // the next slice's dependent chain (metadata -> col -> x).
-    for (int c = gw; c < a.nchunks; c += nw) {
+    // chunk gw first, then (a.work) the next free chunk from an atomic
+    // counter, fetched one chunk ahead, or (static) chunk gw + nw, ...
+    int cnext = a.work && lane == 0 ? int(atomicAdd(a.work, 1u)) + nw : 0;
+    for (int c = gw; c < a.nchunks;) {
         int s = __ldg(a.chunk + c);
         const int se = __ldg(a.chunk + c + 1);
         if (a.l2pf != 0 && lane == 0) {   // a later chunk of this warp: HBM -> L2 (evict_first) while this one gathers
@@ -813,6 +817,20 @@ __global__ void __launch_bounds__(kSellCtaWarps * 32, DSPMV_SELL_MINB) spmv_sell
             sr = sr_n;
             len = len_n;
             off = off_n;
+        }
+        if (a.work) {
+            c = __shfl_sync(0xffffffffu, cnext, 0);
+            if (lane == 0) cnext = int(atomicAdd(a.work, 1u)) + nw;
+        } else {
+            c += nw;
+        }
+    }
+    if (a.work && lane == 0) {   // the last warp out resets the counters (as in spmv_stream_kernel)
+        if (cnext < 0) __trap();
+        __threadfence();
+        if (atomicAdd(a.work + 1, 1u) == unsigned(nw) - 1u) {
+            atomicExch(a.work, 0u);
+            atomicExch(a.work + 1, 0u);
         }
     }
 }
@@ -1272,7 +1290,8 @@ cudaError_t launch_stream(const DevLayout& L, const SpmvOperands& o, cudaStream_
 template <typename T, int U, bool kNoL1>
 cudaError_t launch_sell_u(const DevLayout& L, const SpmvOperands& o, cudaStream_t s, bool vec) {
     SellArgs a{L.sl_chunk, L.sl_base, L.sl_srow, L.sl_len, L.sl_col, L.sl_val, L.s_out, L.s_slot, L.nchunks,
-               VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0, L.v_ordered}, L.st_l2pf};
+               VecArgs{L.v_rowptr, L.v_col, L.v_val, L.v_out, L.v_slot, vec ? L.nV : 0, L.v_ordered}, L.st_l2pf,
+               L.st_dynamic ? L.d_work : nullptr};
     const bool c = L.s_slot != nullptr, id = L.s_out == nullptr;
     const dim3 grid(L.grid_sl), block(kSellCtaWarps * 32);
     if (x_persist_fraction() > 0 && L.x_bytes > 0) {   // experiment DSPMV_X_PERSIST

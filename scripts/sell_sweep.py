@@ -23,6 +23,7 @@ from tests.gpu_helpers import derive_ops  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=30)
 ap.add_argument("--workload", default="c4")
+ap.add_argument("--long-row-sum", type=int, default=0, help="1: DSPMV_LONG_ROW_STORED")
 ap.add_argument("--flush", type=int, default=1, help="flush L2 before each apply (0: back-to-back applies)")
 ap.add_argument("--cfgs", default="stream,sell:256:8:256:4096,sell:1024:8:256:4096,sell:4096:8:256:4096,"
                 "sell:256:8:64:4096,sell:1024:8:64:4096,sell:1024:8:128:4096,sell:1024:8:32:4096,"
@@ -61,7 +62,8 @@ for c in a.cfgs.split(","):
     else:
         sk = D.DSPMV_SKERNEL_STREAM
     t1 = time.time()
-    plan = D.dspmv_plan_create(comm, n, rp, col, val, s_kernel=sk, vector_threshold=vthr, block_cfg=bcfg)
+    plan = D.dspmv_plan_create(comm, n, rp, col, val, s_kernel=sk, vector_threshold=vthr, block_cfg=bcfg,
+                                 long_row_sum=a.long_row_sum)
     tp = time.time() - t1
     info = D.dspmv_plan_info_get(plan)
     sched = D.dspmv_schedule_create(plan, derive_ops(), 2)
