@@ -604,7 +604,10 @@ struct StreamArgs {
 // go to shared memory; lane j then sums row j's products in stored order from
 // +0 (the oracle's loop), so y is bitwise O1 on every row.
 template <typename T, bool kCombine, bool kIdentity>
-__global__ void __launch_bounds__(kStreamCtaWarps * 32) spmv_stream_kernel(StreamArgs a, SpmvOperands o) {
+#ifndef DSPMV_STREAM_MINB
+#define DSPMV_STREAM_MINB 2   // 2 CTAs of 20 warps (48 registers); without a minimum ptxas takes 64 and fits one
+#endif
+__global__ void __launch_bounds__(kStreamCtaWarps * 32, DSPMV_STREAM_MINB) spmv_stream_kernel(StreamArgs a, SpmvOperands o) {
     __shared__ T prod[kStreamCtaWarps][kStreamTile];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const T* __restrict__ val = static_cast<const T*>(a.val);
