@@ -6,6 +6,8 @@
 #   profile  ncu launch list of the default bench, full captures of the C3 / C4 y_L kernels,
 #            compute-sanitizer over scripts/sanitize.py
 #   ubench   PCIe peak, zero-copy stores, LSU vs TMA random gathers
+#   kernels  the round-2 y_L sweeps: L2 prefetch distance (C3, C2), K1b hand-out and K1d settings (C4),
+#            column panels (C4) -- profiles/r2_l2_prefetch.txt, r2_c4_sell.txt
 # Outputs land in gpurun_out/ (summaries are copied to profiles/ by hand).
 set -u
 OUT=gpurun_out; mkdir -p $OUT
@@ -44,6 +46,14 @@ ubench)
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/uz scripts/ubench_zerocopy.cu && timeout 120 /tmp/uz 134 > $OUT/uz.txt 2>&1
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/ug scripts/ubench_tma_gather4.cu -lcuda && \
       { timeout 60 /tmp/ug 134 64 2 1 0; timeout 60 /tmp/ug 134 64 2 1 3; timeout 60 /tmp/ug 134 64 2 1 1; } > $OUT/ug.txt 2>&1
+  ;;
+kernels)
+  S="timeout 600 python scripts/sell_sweep.py --reps 30"
+  for w in c3 c2; do $S --workload $w --cfgs auto:0,auto:1,auto:2,auto:4 > $OUT/l2pf_$w.txt 2>&1; done
+  for d in 0 1; do DSPMV_ST_DYNAMIC=$d $S --workload c4 --cfgs stream,stream > $OUT/c4_dyn$d.txt 2>&1; done
+  $S --workload c4 --cfgs stream,sell:256:4:64:2048:6,sell:256:4:256:2048:6,sell:256:4:64:4096:6 > $OUT/c4_sell.txt 2>&1
+  $S --workload c4 --long-row-sum 1 --cfgs stream,sell:256:4:64:2048:6 > $OUT/c4_stored.txt 2>&1
+  timeout 900 python scripts/c4_panels.py > $OUT/c4_panels.txt 2>&1
   ;;
 esac
 echo done
