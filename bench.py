@@ -1030,7 +1030,7 @@ def run_ours(a):
             out["parity_ok"] = out["parity_ok"] and all(s["parity"]["ok"] for s in secs.values())
         if cpu is not None:
             out["cpu_baseline"] = cpu
-        print(json.dumps(out), flush=True)
+        emit(json.dumps(out))
     ctx.close()
 
 
@@ -1110,7 +1110,7 @@ def run_reference(a, budget_s=90.0):
     desc = workload_desc(a.workload, world)
     sample = (f"rows [0,{rows}) of {n} ({nnz} nnz) per step, O1 serial, 1 thread"
               + (" (the whole matrix)" if rows == n else " (bounded sample)"))
-    print(json.dumps({
+    emit(json.dumps({
         "metric": METRIC, "value": round(gflops, 4), "unit": "GFLOP/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(dt / a.steps * 1e3, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": a.dtype,
@@ -1120,10 +1120,27 @@ def run_reference(a, budget_s=90.0):
                          "kind": "oracle", "sample": sample, "cpu": _cpu_model()},
         "e2e": {"value": round(gflops, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-    }), flush=True)
+    }))
+
+
+_JSON_OUT = None   # the process's real stdout while fd 1 points at stderr
+
+
+def emit(line: str):
+    """The one JSON line on stdout (libraries' own prints, e.g. NCCL's version
+    banner under NCCL_DEBUG, go to stderr while the bench runs)."""
+    if _JSON_OUT is not None:
+        _JSON_OUT.write(line + "\n")
+        _JSON_OUT.flush()
+    else:
+        print(line, flush=True)
 
 
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)   # everything else written to fd 1 (C libraries included) -> stderr
     a = parse()
     global X_SEED, EXACT
     X_SEED, EXACT = a.seed, a.value_mode == "exact"
