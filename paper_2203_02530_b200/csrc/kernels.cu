@@ -630,79 +630,79 @@ __global__ void __launch_bounds__(kStreamCtaWarps * 32, DSPMV_STREAM_MINB) spmv_
     const int gw = blockIdx.x * kStreamCtaWarps + w, nw = gridDim.x * kStreamCtaWarps;
     int bnext = a.work && lane == 0 ? int(atomicAdd(a.work, 1u)) + nw : 0;
     for (int bt = gw; bt * a.grab < a.ntiles;) {
-    for (int t = bt * a.grab, te = min(a.ntiles, t + a.grab); t < te; ++t) {
-        const int2 tr = __ldg(reinterpret_cast<const int2*>(a.tiles) + t);
-        const int32_t p0 = __ldg(a.rowptr + tr.x), m = __ldg(a.rowptr + tr.y) - p0;
-        if (a.l2pf != 0 && lane == 0) {   // a later tile of this warp: HBM -> L2 (evict_first) while this one gathers
-            const int tn = t + (a.l2pf > 0 ? a.l2pf : -a.l2pf) * gridDim.x * kStreamCtaWarps;
-            if (tn < a.ntiles) {
-                const int2 trn = __ldg(reinterpret_cast<const int2*>(a.tiles) + tn);
-                const int32_t c0 = __ldg(a.rowptr + trn.x) & ~3, c1 = (__ldg(a.rowptr + trn.y) + 3) & ~3;
-                if (c1 > c0) {
-                    const uint64_t pf = policy_evict_first();
-                    if (a.l2pf > 0) bulk_prefetch_l2(val + c0, uint32_t(c1 - c0) * sizeof(T), pf);
-                    bulk_prefetch_l2(a.col + c0, uint32_t(c1 - c0) * 4u, pf);   // l2pf < 0: col only
+        for (int t = bt * a.grab, te = min(a.ntiles, t + a.grab); t < te; ++t) {
+            const int2 tr = __ldg(reinterpret_cast<const int2*>(a.tiles) + t);
+            const int32_t p0 = __ldg(a.rowptr + tr.x), m = __ldg(a.rowptr + tr.y) - p0;
+            if (a.l2pf != 0 && lane == 0) {   // a later tile of this warp: HBM -> L2 (evict_first) while this one gathers
+                const int tn = t + (a.l2pf > 0 ? a.l2pf : -a.l2pf) * gridDim.x * kStreamCtaWarps;
+                if (tn < a.ntiles) {
+                    const int2 trn = __ldg(reinterpret_cast<const int2*>(a.tiles) + tn);
+                    const int32_t c0 = __ldg(a.rowptr + trn.x) & ~3, c1 = (__ldg(a.rowptr + trn.y) + 3) & ~3;
+                    if (c1 > c0) {
+                        const uint64_t pf = policy_evict_first();
+                        if (a.l2pf > 0) bulk_prefetch_l2(val + c0, uint32_t(c1 - c0) * sizeof(T), pf);
+                        bulk_prefetch_l2(a.col + c0, uint32_t(c1 - c0) * 4u, pf);   // l2pf < 0: col only
+                    }
                 }
             }
-        }
-        int32_t c[kStreamTile / 32];
-        T v[kStreamTile / 32], xv[kStreamTile / 32];
+            int32_t c[kStreamTile / 32];
+            T v[kStreamTile / 32], xv[kStreamTile / 32];
 #pragma unroll
-        for (int k = 0; k < kStreamTile / 32; ++k) {
-            const int q = lane + 32 * k;
+            for (int k = 0; k < kStreamTile / 32; ++k) {
+                const int q = lane + 32 * k;
 #if defined(DSPMV_K1B_EF)
-            // experiment: the matrix stream with an explicit L2 evict_first policy
-            c[k] = q < m ? ld_stream_ef(a.col + p0 + q, mpol) : 0;
-            v[k] = q < m ? ld_stream_ef(val + p0 + q, mpol) : T(0);
+                // experiment: the matrix stream with an explicit L2 evict_first policy
+                c[k] = q < m ? ld_stream_ef(a.col + p0 + q, mpol) : 0;
+                v[k] = q < m ? ld_stream_ef(val + p0 + q, mpol) : T(0);
 #else
-            c[k] = q < m ? __ldcs(a.col + p0 + q) : 0;
-            v[k] = q < m ? __ldcs(val + p0 + q) : T(0);
+                c[k] = q < m ? __ldcs(a.col + p0 + q) : 0;
+                v[k] = q < m ? __ldcs(val + p0 + q) : T(0);
 #endif
-        }
-#pragma unroll
-        for (int k = 0; k < kStreamTile / 32; ++k) {
-#if defined(DSPMV_DIAG_GATHER) && DSPMV_DIAG_GATHER == 4
-            xv[k] = T(c[k]);  // diagnostic build 4: no gathers (cost of the streaming + row sums)
-#else
-            xv[k] = lane + 32 * k < m ? ldg_x<true>(x + c[k], xpol) : T(0);
-#endif
-        }
-        __syncwarp();  // keeps ptxas from pairing each gather with its multiply: all 8 stay in flight
-#if defined(DSPMV_DIAG_GATHER) && DSPMV_DIAG_GATHER == 5
-        // diagnostic build 5: no shared memory at all (each lane sums its 8
-        // products and stores one value per row slot): gathers + streaming only
-        {
-            T acc5 = T(0);
-#pragma unroll
-            for (int k = 0; k < kStreamTile / 32; ++k) acc5 = add_rn(acc5, mul_rn(v[k], xv[k]));
-            if (tr.x + lane < tr.y) __stcs(y + (kIdentity ? tr.x + lane : a.out[tr.x + lane]), acc5);
-            continue;
-        }
-#endif
-#pragma unroll
-        for (int k = 0; k < kStreamTile / 32; ++k) pr[lane + 32 * k] = mul_rn(v[k], xv[k]);
-        __syncwarp();
-        for (int32_t r = tr.x + lane; r < tr.y; r += 32) {
-#if defined(DSPMV_DIAG_GATHER) && DSPMV_DIAG_GATHER == 3
-            // diagnostic build 3: no row sums (cost of the gather phase alone)
-            const T acc = pr[r - tr.x];
-#else
-            const int32_t e0 = __ldg(a.rowptr + r) - p0, e1 = __ldg(a.rowptr + r + 1) - p0;
-            T acc = T(0);
-            for (int32_t q = e0; q < e1; ++q) acc = add_rn(acc, pr[q]);
-#endif
-            const int32_t orow = kIdentity ? r : a.out[r];
-            if (kCombine) {
-                const int32_t k = a.slot[r];
-                if (k >= 0) {
-                    combine<T>(acc, k, orow, o);
-                    continue;
-                }
             }
-            __stcs(y + orow, acc);
+#pragma unroll
+            for (int k = 0; k < kStreamTile / 32; ++k) {
+#if defined(DSPMV_DIAG_GATHER) && DSPMV_DIAG_GATHER == 4
+                xv[k] = T(c[k]);  // diagnostic build 4: no gathers (cost of the streaming + row sums)
+#else
+                xv[k] = lane + 32 * k < m ? ldg_x<true>(x + c[k], xpol) : T(0);
+#endif
+            }
+            __syncwarp();  // keeps ptxas from pairing each gather with its multiply: all 8 stay in flight
+#if defined(DSPMV_DIAG_GATHER) && DSPMV_DIAG_GATHER == 5
+            // diagnostic build 5: no shared memory at all (each lane sums its 8
+            // products and stores one value per row slot): gathers + streaming only
+            {
+                T acc5 = T(0);
+#pragma unroll
+                for (int k = 0; k < kStreamTile / 32; ++k) acc5 = add_rn(acc5, mul_rn(v[k], xv[k]));
+                if (tr.x + lane < tr.y) __stcs(y + (kIdentity ? tr.x + lane : a.out[tr.x + lane]), acc5);
+                continue;
+            }
+#endif
+#pragma unroll
+            for (int k = 0; k < kStreamTile / 32; ++k) pr[lane + 32 * k] = mul_rn(v[k], xv[k]);
+            __syncwarp();
+            for (int32_t r = tr.x + lane; r < tr.y; r += 32) {
+#if defined(DSPMV_DIAG_GATHER) && DSPMV_DIAG_GATHER == 3
+                // diagnostic build 3: no row sums (cost of the gather phase alone)
+                const T acc = pr[r - tr.x];
+#else
+                const int32_t e0 = __ldg(a.rowptr + r) - p0, e1 = __ldg(a.rowptr + r + 1) - p0;
+                T acc = T(0);
+                for (int32_t q = e0; q < e1; ++q) acc = add_rn(acc, pr[q]);
+#endif
+                const int32_t orow = kIdentity ? r : a.out[r];
+                if (kCombine) {
+                    const int32_t k = a.slot[r];
+                    if (k >= 0) {
+                        combine<T>(acc, k, orow, o);
+                        continue;
+                    }
+                }
+                __stcs(y + orow, acc);
+            }
+            __syncwarp();
         }
-        __syncwarp();
-    }
         if (a.work) {
             bt = __shfl_sync(0xffffffffu, bnext, 0);
             if (lane == 0) bnext = int(atomicAdd(a.work, 1u)) + nw;
