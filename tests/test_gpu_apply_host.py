@@ -35,14 +35,15 @@ def _case(name):
 
 
 @pytest.mark.parametrize("dtype", [D.DSPMV_F64, D.DSPMV_F32], ids=["f64", "f32"])
-@pytest.mark.parametrize("name", ["7pt96", "7pt97", "pl400k"])
+@pytest.mark.parametrize("name", ["7pt96", "7pt97", "pl400k", "pl400k-sell"])
 def test_apply_host_pipelined_equals_device_apply(name, dtype):
-    n, (rp, col, val) = _case(name)
+    skern = D.DSPMV_SKERNEL_SELL if name.endswith("-sell") else D.DSPMV_SKERNEL_AUTO
+    n, (rp, col, val) = _case(name.replace("-sell", ""))
     tdt = torch.float32 if dtype == D.DSPMV_F32 else torch.float64
     npdt = np.float32 if dtype == D.DSPMV_F32 else np.float64
     v = val.astype(npdt)
     comm = D.dspmv_comm_create(D.dspmv_comm_unique_id(), 1, 0, 0)
-    plan = D.dspmv_plan_create(comm, n, rp, col, v, dtype=dtype, vector_threshold=64)
+    plan = D.dspmv_plan_create(comm, n, rp, col, v, dtype=dtype, vector_threshold=64, s_kernel=skern)
     x = gen.x_values((0, n)).astype(npdt)
     xd = torch.from_numpy(x).cuda()
     try:
