@@ -122,6 +122,10 @@ def parse():
     ap.add_argument("--plain-exchange", action="store_true",
                     help="Pack gathers into a send buffer and Unpack copies to x_halo (the DAG's literal "
                          "kernels) instead of aliased sends and the fused Unpack")
+    ap.add_argument("--settle-s", type=float, default=2.0,
+                    help="idle seconds before each workload's warm-up + timed region, so the board's power "
+                         "controller does not carry the schedule sweep's draw into it (C3 runs at ~1 kW; "
+                         "sustained, power-capped figures: DESIGN.md section 6)")
     ap.add_argument("--no-t1", action="store_true",
                     help="N>1: skip the 1-GPU run of the whole matrix on rank 0 (scaling efficiency)")
     return ap.parse_args()
@@ -564,6 +568,10 @@ def measure(ctx, wname, headline, clocks=None, sched_from=None):
     apply_fn, mode, exec_note = pick_mode(ctx, sched, x, y, mode_pref, ex_mode)
 
     # ---- warmup + timed region
+    if a.settle_s > 0:
+        torch.cuda.synchronize()
+        time.sleep(a.settle_s)
+        ctx.barrier()
     for _ in range(a.warmup):
         if flush_steps:
             D.dspmv_l2_flush(ctx.device, ctx.stream)
@@ -1026,7 +1034,8 @@ def run_ours(a):
                 "schedule": head.pop("schedule"),
                 "l2": head.pop("l2"),
                 "step_timing": ("CUDA events recorded by dspmv_apply on the caller stream at START "
-                                "and END (the whole schedule incl. host syncs); max over ranks"),
+                                "and END (the whole schedule incl. host syncs); max over ranks; "
+                                f"{a.settle_s:g} s idle before the warm-up (power controller)"),
                 "step_us_median_min_p90": head.pop("step_us_median_min_p90"),
                 **{k: head.pop(k) for k in ("step_us_median_warm_l2", "step_us_median_flushed_l2") if k in head},
                 "step_hbm_gbs_algorithmic": head.pop("step_hbm_gbs_algorithmic"),
